@@ -1,0 +1,200 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle/crvpinn_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` leg. The product package never imports it.
+
+Every function follows the paper step by step; see the header of crvpinn_oracle.c for the
+passage each step cites and DESIGN.md §4 for the pins (P1..P13) in tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "crvpinn_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+MOBILITY_RATIO = 25.35 / 3.95   # Table 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        D = ctypes.POINTER(ctypes.c_double)
+        F = ctypes.POINTER(ctypes.c_float)
+        I = ctypes.POINTER(ctypes.c_int)
+        L.orc_create.restype = P
+        L.orc_create.argtypes = [ctypes.c_int, ctypes.c_int, I, F, F, F, F, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_int]
+        L.orc_destroy.argtypes = [P]
+        L.orc_num_params.restype = ctypes.c_long
+        L.orc_num_params.argtypes = [P]
+        L.orc_get_theta.argtypes = [P, D]
+        L.orc_set_theta.argtypes = [P, D]
+        L.orc_get_adam.argtypes = [P, D, D, ctypes.POINTER(ctypes.c_long)]
+        L.orc_get_alpha.argtypes = [P, D]
+        L.orc_set_saturation.argtypes = [P, F, F]
+        L.orc_forward.argtypes = [P, D, D]
+        L.orc_residual.argtypes = [P, D, D]
+        L.orc_residual_adjoint.argtypes = [P, D, D]
+        L.orc_gram_solve.argtypes = [P, D, D]
+        L.orc_gram_matvec.argtypes = [P, D, D]
+        L.orc_loss_u.restype = ctypes.c_double
+        L.orc_loss_u.argtypes = [P, D, D, D]
+        L.orc_loss_grad.restype = ctypes.c_double
+        L.orc_loss_grad.argtypes = [P, D, D, D, D, D, D]
+        L.orc_adam_step.argtypes = [P, D]
+        L.orc_train.restype = ctypes.c_int
+        L.orc_train.argtypes = [P, ctypes.c_int, D]
+        L.orc_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _fp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+class Oracle:
+    """One CRVPINN problem: grid N, widths, inputs K, S, f, parameters and Adam state."""
+
+    def __init__(self, N: int, widths, K, S, f, theta0=None, *, mobility: float = MOBILITY_RATIO,
+                 lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 factor_gram: bool = True):
+        L = lib()
+        self.N, self.n = int(N), int(N) - 1
+        self.widths = tuple(int(w) for w in widths)
+        w = (ctypes.c_int * len(self.widths))(*self.widths)
+        self._K, self._S, self._f = _f32(K), _f32(S), _f32(f)
+        th = None if theta0 is None else _f32(theta0)
+        self._h = L.orc_create(self.N, len(self.widths) - 1, w, _fp(self._K), _fp(self._S),
+                               _fp(self._f), None if th is None else _fp(th), mobility, lr,
+                               beta1, beta2, eps, 1 if factor_gram else 0)
+        if not self._h:
+            raise MemoryError("orc_create failed")
+        self.np = int(L.orc_num_params(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_destroy(self._h)
+            self._h = None
+
+    # -- state
+    @property
+    def theta(self) -> np.ndarray:
+        out = np.empty(self.np)
+        lib().orc_get_theta(self._h, _dp(out))
+        return out
+
+    @theta.setter
+    def theta(self, th):
+        th = np.ascontiguousarray(th, dtype=np.float64)
+        lib().orc_set_theta(self._h, _dp(th))
+
+    def adam_state(self):
+        m, v, t = np.empty(self.np), np.empty(self.np), ctypes.c_long(0)
+        lib().orc_get_adam(self._h, _dp(m), _dp(v), ctypes.byref(t))
+        return m, v, int(t.value)
+
+    def alpha(self) -> np.ndarray:
+        out = np.empty((self.N + 1) ** 2)
+        lib().orc_get_alpha(self._h, _dp(out))
+        return out
+
+    def set_saturation(self, S, K=None):
+        self._S = _f32(S)
+        if K is not None:
+            self._K = _f32(K)
+        lib().orc_set_saturation(self._h, _fp(self._K), _fp(self._S))
+
+    # -- steps
+    def forward(self, theta=None) -> np.ndarray:
+        th = self.theta if theta is None else np.ascontiguousarray(theta, dtype=np.float64)
+        u = np.empty((self.N + 1) ** 2)
+        lib().orc_forward(self._h, _dp(th), _dp(u))
+        return u
+
+    def residual(self, u) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        r = np.empty(self.n * self.n)
+        lib().orc_residual(self._h, _dp(u), _dp(r))
+        return r
+
+    def residual_adjoint(self, w) -> np.ndarray:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        g = np.empty((self.N + 1) ** 2)
+        lib().orc_residual_adjoint(self._h, _dp(w), _dp(g))
+        return g
+
+    def gram_solve(self, rhs) -> np.ndarray:
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        q = np.empty(self.n * self.n)
+        lib().orc_gram_solve(self._h, _dp(rhs), _dp(q))
+        return q
+
+    def gram_matvec(self, v) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty(self.n * self.n)
+        lib().orc_gram_matvec(self._h, _dp(v), _dp(out))
+        return out
+
+    def loss_u(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        r, q = np.empty(self.n * self.n), np.empty(self.n * self.n)
+        loss = lib().orc_loss_u(self._h, _dp(u), _dp(r), _dp(q))
+        return loss, r, q
+
+    def loss_grad(self, theta=None, intermediates: bool = False):
+        th = None if theta is None else np.ascontiguousarray(theta, dtype=np.float64)
+        g = np.empty(self.np)
+        nn, n2 = (self.N + 1) ** 2, self.n * self.n
+        if intermediates:
+            u, r, q, gu = np.empty(nn), np.empty(n2), np.empty(n2), np.empty(nn)
+            loss = lib().orc_loss_grad(self._h, None if th is None else _dp(th), _dp(g),
+                                       _dp(u), _dp(r), _dp(q), _dp(gu))
+            return loss, g, dict(u=u, res=r, q=q, gu=gu)
+        loss = lib().orc_loss_grad(self._h, None if th is None else _dp(th), _dp(g),
+                                   None, None, None, None)
+        return loss, g
+
+    def adam_step(self, grad):
+        grad = np.ascontiguousarray(grad, dtype=np.float64)
+        lib().orc_adam_step(self._h, _dp(grad))
+
+    def train(self, n_iters: int) -> np.ndarray:
+        hist = np.empty(n_iters)
+        rc = lib().orc_train(self._h, int(n_iters), _dp(hist))
+        if rc != 0:
+            raise FloatingPointError("oracle loss became non-finite")
+        return hist
+
+
+def max_threads() -> int:
+    return int(lib().orc_max_threads())

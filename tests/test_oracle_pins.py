@@ -1,0 +1,463 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix.
+
+Each test names the pin (P1..P13) and the passage it follows. None of these re-calls the
+oracle's own formula as its reference: the references are closed forms, brute-force literal
+definitions, finite differences, eigen-decompositions, or independent library routines
+(numpy/scipy dense solves, torch autograd, torch.optim.Adam).
+
+Inputs are fp32 (the ABI's input type) promoted to fp64, so closed forms that involve the
+source f hold to fp32 input rounding (~1e-7 relative), not to 1e-15.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _ctx(N, widths=(2, 8, 1), K=None, S=None, f=None, theta=None, **kw):
+    nn = (N + 1) ** 2
+    K = np.ones(nn, np.float32) if K is None else K
+    S = np.zeros(nn, np.float32) if S is None else S
+    f = np.zeros(nn, np.float32) if f is None else f
+    return oracle.Oracle(N, widths, K, S, f, theta, **kw)
+
+
+def _dst_matrix(N):
+    n = N - 1
+    i = np.arange(1, n + 1)
+    S = math.sqrt(2.0 / N) * np.sin(math.pi * np.outer(i, i) / N)
+    lam = 4.0 * np.sin(math.pi * i / (2.0 * N)) ** 2
+    return S, lam
+
+
+def _gram_inv_dst(N, R):
+    """G^-1 R via the 2-D sine eigenbasis of the 5-point matrix (independent of the LU)."""
+    S, lam = _dst_matrix(N)
+    h = 1.0 / N
+    n = N - 1
+    Rm = R.reshape(n, n)
+    Z = (S @ Rm @ S) / (lam[:, None] + lam[None, :])
+    return (h * h * (S @ Z @ S)).reshape(-1)
+
+
+# --------------------------------------------------------------------------- P0: Table 1
+def test_table1_golden_mobility_ratio():
+    """Reading R10: M = mu_w/mu_g from Table 1 (golden fixture)."""
+    with open(os.path.join(GOLDEN, "table1.json")) as fh:
+        t1 = json.load(fh)
+    assert t1["mu_w"] == 25.35e-5 and t1["mu_g"] == 3.95e-5
+    assert abs(oracle.MOBILITY_RATIO - t1["mu_w"] / t1["mu_g"]) < 1e-15
+    assert abs(W.MOBILITY_RATIO - 6.417721518987342) < 1e-12
+
+
+def test_alpha_A0_special_cases():
+    """alpha = K((1-S) + M S): S=0 -> K, S=1 -> M K, clamping of S."""
+    N = 4
+    nn = (N + 1) ** 2
+    rng = np.random.default_rng(3)
+    K = rng.uniform(0.5, 2.0, nn).astype(np.float32)
+    for s, factor in [(0.0, 1.0), (1.0, oracle.MOBILITY_RATIO), (-0.3, 1.0), (1.7, oracle.MOBILITY_RATIO)]:
+        o = _ctx(N, K=K, S=np.full(nn, s, np.float32))
+        np.testing.assert_allclose(o.alpha(), K.astype(np.float64) * factor, rtol=1e-15)
+    # monotone in S when mu_g < mu_w
+    Ss = np.linspace(0, 1, 100).astype(np.float32)
+    o = _ctx(N, K=np.ones(nn, np.float32), S=np.resize(Ss, nn))
+    a = o.alpha()[:100]
+    assert np.all(np.diff(a) > 0)
+
+
+# --------------------------------------------------------------------------- P1, P2: Gram
+@pytest.mark.parametrize("N", [3, 4, 7, 10])
+def test_P1_gram_matrix_entries(N):
+    """G entries (Eq. 26): 4h^-2 diagonal, -h^-2 for 4-neighbours, 0 else.
+
+    Probed through the oracle's matvec on unit vectors; the reference is the neighbour rule
+    in (i,j) lattice coordinates, not the oracle's row-offset arithmetic.
+    """
+    o = _ctx(N, factor_gram=False)
+    n, h2i = N - 1, float(N * N)
+    for col in range(n * n):
+        e = np.zeros(n * n)
+        e[col] = 1.0
+        g = o.gram_matvec(e)
+        ci, cj = col % n, col // n
+        for row in range(n * n):
+            ri, rj = row % n, row // n
+            d = abs(ri - ci) + abs(rj - cj)
+            want = 4 * h2i if d == 0 else (-h2i if d == 1 else 0.0)
+            assert abs(g[row] - want) <= 1e-14 * h2i
+
+
+@pytest.mark.parametrize("N", [4, 6, 8])
+def test_P2_gram_solve_vs_dense_lapack(N):
+    """LU substitution (Eq. 28) == dense LAPACK solve of G at N<=8 to 1e-12."""
+    o = _ctx(N)
+    n = N - 1
+    G = np.column_stack([o.gram_matvec(np.eye(n * n)[:, c]) for c in range(n * n)])
+    rng = np.random.default_rng(N)
+    for _ in range(3):
+        r = rng.standard_normal(n * n)
+        np.testing.assert_allclose(o.gram_solve(r), np.linalg.solve(G, r), rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("N", [8, 16, 33])
+def test_P2_gram_solve_eigenpairs(N):
+    """G^-1 phi_ab = h^2/(lam_a+lam_b) phi_ab, phi_ab = sin(pi a i/N) sin(pi b j/N) (closed form)."""
+    o = _ctx(N)
+    n, h = N - 1, 1.0 / N
+    i = np.arange(1, n + 1)
+    for a, b in [(1, 1), (2, 5), (n, 1), (n // 2, n)]:
+        phi = np.outer(np.sin(math.pi * b * i / N), np.sin(math.pi * a * i / N)).reshape(-1)
+        lam = 4 * math.sin(math.pi * a / (2 * N)) ** 2 + 4 * math.sin(math.pi * b / (2 * N)) ** 2
+        np.testing.assert_allclose(o.gram_solve(phi), h * h / lam * phi, rtol=1e-11, atol=1e-13)
+
+
+def test_P2_gram_solve_vs_dst_random():
+    """Band LU solve == 2-D sine-transform solve on random RES (N=32)."""
+    N = 32
+    o = _ctx(N)
+    r = np.random.default_rng(0).standard_normal((N - 1) ** 2)
+    np.testing.assert_allclose(o.gram_solve(r), _gram_inv_dst(N, r), rtol=1e-11, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- P3: stencil
+def _literal_residual(N, alpha, u, f):
+    """Eq. 25 by brute force: h^2 sum_{p in Omega_h} alpha_p grad+u_p . grad+delta_kl(p) - h^2 f_kl.
+
+    Full sums over every lattice node p (no use of the delta's support); grad+ (Eq. 22) of any
+    lattice function is taken as 0 where the forward neighbour leaves the lattice.
+    """
+    h = 1.0 / N
+    A = alpha.reshape(N + 1, N + 1)
+    U = u.reshape(N + 1, N + 1)
+
+    def grad_plus(F):
+        gx = np.zeros_like(F)
+        gy = np.zeros_like(F)
+        gx[:, :-1] = (F[:, 1:] - F[:, :-1]) / h
+        gy[:-1, :] = (F[1:, :] - F[:-1, :]) / h
+        return gx, gy
+
+    ux, uy = grad_plus(U)
+    # grad+ u at i=N or j=N is never paired with a non-zero grad+ delta for interior tests
+    out = np.zeros((N - 1) * (N - 1))
+    for l in range(1, N):
+        for k in range(1, N):
+            D = np.zeros((N + 1, N + 1))
+            D[l, k] = 1.0
+            dx, dy = grad_plus(D)
+            lhs = h * h * np.sum(A * (ux * dx + uy * dy))
+            rhs = h * h * np.sum(f.reshape(N + 1, N + 1) * D)
+            out[(l - 1) * (N - 1) + (k - 1)] = lhs - rhs
+    return out
+
+
+@pytest.mark.parametrize("N", [4, 7, 8])
+def test_P3_residual_vs_literal_inner_product(N):
+    K, S, f = W.random_fields(N, seed=N)
+    o = _ctx(N, K=K, S=S, f=f, factor_gram=False)
+    u = np.random.default_rng(N + 1).standard_normal((N + 1) ** 2)
+    u = u.reshape(N + 1, N + 1)
+    u[0, :] = u[-1, :] = u[:, 0] = u[:, -1] = 0.0
+    u = u.reshape(-1)
+    want = _literal_residual(N, o.alpha(), u, f.astype(np.float64))
+    np.testing.assert_allclose(o.residual(u), want, rtol=1e-12, atol=1e-13)
+
+
+def test_residual_special_cases():
+    """alpha=1 collapses to the 5-point Laplacian; u=0, f=1 gives RES = -h^2."""
+    N = 8
+    nn = (N + 1) ** 2
+    o = _ctx(N, f=np.ones(nn, np.float32), factor_gram=False)
+    np.testing.assert_array_equal(o.residual(np.zeros(nn)), np.full((N - 1) ** 2, -1.0 / N ** 2))
+    o0 = _ctx(N, factor_gram=False)
+    u = np.random.default_rng(1).standard_normal((N + 1, N + 1))
+    u[0, :] = u[-1, :] = u[:, 0] = u[:, -1] = 0.0
+    lap = 4 * u[1:-1, 1:-1] - u[1:-1, :-2] - u[1:-1, 2:] - u[:-2, 1:-1] - u[2:, 1:-1]
+    np.testing.assert_allclose(o0.residual(u.reshape(-1)), lap.reshape(-1), rtol=1e-13, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- P4, P5: closed forms
+def test_P4_residual_zero_manufactured_sine():
+    """alpha=1, f=2 pi^2 sin sin: u = c_h sin sin solves the discrete equation exactly (reading R1)."""
+    N = 32
+    h = 1.0 / N
+    X, Y = W.grid_xy(N)
+    f = (2 * math.pi ** 2 * np.sin(math.pi * X) * np.sin(math.pi * Y)).astype(np.float32)
+    o = _ctx(N, f=f.reshape(-1))
+    ch = (math.pi * h / 2) ** 2 / math.sin(math.pi * h / 2) ** 2
+    assert abs(ch - 1.000803577679372) < 1e-14
+    # exact in fp64 for the fp32-rounded f: compare with h^2 (f32 - f64) scale
+    u = (ch * np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)
+    res = o.residual(u)
+    assert np.max(np.abs(res)) < 4 * h * h * 2 * math.pi ** 2 * 2 ** -24
+    # the sign reading: -div(grad p) = f  ->  p = +sin sin (not -sin sin)
+    assert np.max(np.abs(o.residual(-u))) > 1e-3
+
+
+def test_P4_residual_zero_polynomial():
+    """u = x(1-x)y(1-y), f = 2[x(1-x)+y(1-y)]: the 5-point stencil is exact on quadratics."""
+    N = 16
+    h = 1.0 / N
+    X, Y = W.grid_xy(N)
+    f = (2 * (X * (1 - X) + Y * (1 - Y))).astype(np.float32)
+    o = _ctx(N, f=f.reshape(-1))
+    u = (X * (1 - X) * Y * (1 - Y)).reshape(-1)
+    assert np.max(np.abs(o.residual(u))) < 8 * h * h * 2 ** -24
+
+
+def test_P4_direct_solve_variable_alpha_gives_zero_loss():
+    """u* = dense solve of the assembled discrete system (variable alpha) -> LOSS <= 1e-18."""
+    N = 12
+    K, S, f = W.random_fields(N, seed=11)
+    o = _ctx(N, K=K, S=S, f=f)
+    n, nn = N - 1, (N + 1) ** 2
+    interior = [(j * (N + 1) + i) for j in range(1, N) for i in range(1, N)]
+    # assemble the discrete operator from the brute-force literal Eq. 25 (P3's reference)
+    alpha = o.alpha()
+    zero_f = np.zeros(nn)
+    cols = []
+    for p in interior:
+        e = np.zeros(nn)
+        e[p] = 1.0
+        cols.append(_literal_residual(N, alpha, e, zero_f))
+    A = np.column_stack(cols)
+    b = (f.astype(np.float64).reshape(N + 1, N + 1)[1:-1, 1:-1] / N ** 2).reshape(-1)
+    ustar = np.zeros(nn)
+    ustar[interior] = np.linalg.solve(A, b)
+    loss, res, _ = o.loss_u(ustar)
+    assert np.max(np.abs(res)) < 1e-12 and loss <= 1e-18
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 2.0])
+def test_P5_loss_closed_form(beta):
+    """alpha=1, f=2 pi^2 sin sin: LOSS(beta sin sin) = 2 sin^2(pi h/2) (c_h - beta)^2 [derived]."""
+    N = 32
+    h = 1.0 / N
+    X, Y = W.grid_xy(N)
+    f = (2 * math.pi ** 2 * np.sin(math.pi * X) * np.sin(math.pi * Y)).astype(np.float32)
+    o = _ctx(N, f=f.reshape(-1))
+    ch = (math.pi * h / 2) ** 2 / math.sin(math.pi * h / 2) ** 2
+    want = 2 * math.sin(math.pi * h / 2) ** 2 * (ch - beta) ** 2
+    loss, _, _ = o.loss_u((beta * np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1))
+    assert abs(loss - want) <= 1e-6 * max(want, 1e-3)
+    if beta == 0.0:
+        assert abs(loss - 4.823015329536e-3) < 1e-8
+
+
+# --------------------------------------------------------------------------- P6: inf-sup bounds
+def test_P6_robust_loss_bounds():
+    """gamma^2 h^2 e^T T e <= LOSS <= C^2 h^2 e^T T e, e = u - u*, gamma/C = min/max alpha."""
+    N = 10
+    K, S, f = W.random_fields(N, seed=5, kmin=0.3, kmax=3.0)
+    o = _ctx(N, K=K, S=S, f=f)
+    nn, n = (N + 1) ** 2, N - 1
+    interior = [(j * (N + 1) + i) for j in range(1, N) for i in range(1, N)]
+    A = np.column_stack([o.residual(np.eye(nn)[:, p]) - o.residual(np.zeros(nn)) for p in interior])
+    b = -o.residual(np.zeros(nn))
+    ustar = np.zeros(nn)
+    ustar[interior] = np.linalg.solve(A, b)
+    used = o.alpha().reshape(N + 1, N + 1)[:N, :N]     # nodes whose grad+ enters Eq. 25
+    gamma, C = used.min(), used.max()
+    T1 = 2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    T = np.kron(np.eye(n), T1) + np.kron(T1, np.eye(n))
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        u = ustar.copy()
+        u[interior] += rng.standard_normal(n * n)
+        e = (u - ustar)[interior]
+        loss, _, _ = o.loss_u(u)
+        eTe = e @ T @ e / N ** 2
+        assert gamma ** 2 * eTe * (1 - 1e-10) <= loss <= C ** 2 * eTe * (1 + 1e-10)
+
+
+# --------------------------------------------------------------------------- P7: adjoint
+def test_P7_adjoint_and_symmetry():
+    """<A u, w> = <u, A^T w>; A symmetric; alpha=1: g_u = 2 h^2 RES [derived]."""
+    N = 9
+    K, S, f = W.random_fields(N, seed=9)
+    o = _ctx(N, K=K, S=S, f=f)
+    nn, n = (N + 1) ** 2, N - 1
+    rng = np.random.default_rng(4)
+    mask = np.zeros((N + 1, N + 1))
+    mask[1:-1, 1:-1] = 1
+    mask = mask.reshape(-1)
+    r0 = o.residual(np.zeros(nn))
+    u = rng.standard_normal(nn) * mask
+    v = rng.standard_normal(nn) * mask
+    w = rng.standard_normal(n * n)
+    Au = o.residual(u) - r0
+    Av = o.residual(v) - r0
+    assert abs(Au @ w - u @ o.residual_adjoint(w)) < 1e-12 * np.abs(Au).sum() * np.abs(w).max()
+    def interior(x):
+        return x.reshape(N + 1, N + 1)[1:-1, 1:-1].reshape(-1)
+    assert abs(Au @ interior(v) - Av @ interior(u)) < 1e-12 * (np.abs(Au).sum() + np.abs(Av).sum())
+    # alpha = 1: the Gram cancels
+    X, Y = W.grid_xy(N)
+    o1 = _ctx(N, f=f, theta=W.random_theta((2, 8, 1), 1))
+    loss, g, it = o1.loss_grad(intermediates=True)
+    np.testing.assert_allclose(interior(it["gu"]), 2 * it["res"] / N ** 2, rtol=1e-10, atol=1e-16)
+
+
+# --------------------------------------------------------------------------- P8: gradient vs FD
+@pytest.mark.parametrize("widths,N,seed", [((2, 8, 1), 8, 0), ((2, 16, 16, 1), 8, 1),
+                                           ((2, 32, 32, 1), 10, 2), ((2, 64, 64, 64, 1), 8, 3)])
+def test_P8_gradient_vs_central_fd(widths, N, seed):
+    K, S, f = W.random_fields(N, seed=seed)
+    th = W.random_theta(widths, seed).astype(np.float64)
+    o = _ctx(N, widths, K, S, f, th)
+    loss, g = o.loss_grad(th)
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(len(th), size=min(len(th), 40), replace=False)
+    for k in idx:
+        step = 1e-6 * max(1.0, abs(th[k]))
+        tp, tm = th.copy(), th.copy()
+        tp[k] += step
+        tm[k] -= step
+        fd = (o.loss_grad(tp)[0] - o.loss_grad(tm)[0]) / (2 * step)
+        assert abs(fd - g[k]) <= 1e-6 * max(abs(g[k]), 1e-3 * np.abs(g).max()), (k, fd, g[k])
+
+
+# --------------------------------------------------------------------------- P9: Adam
+def test_P9_adam_first_step_closed_form():
+    """Step 1: m_hat = g, v_hat = g^2  ->  theta_1 = theta_0 - lr g/(|g| + eps)."""
+    N = 8
+    K, S, f = W.random_fields(N, seed=2)
+    th0 = W.random_theta((2, 8, 1), 2)
+    o = _ctx(N, (2, 8, 1), K, S, f, th0, lr=1e-2)
+    _, g = o.loss_grad()
+    o.adam_step(g)
+    want = th0.astype(np.float64) - 1e-2 * g / (np.abs(g) + 1e-8)
+    np.testing.assert_allclose(o.theta, want, rtol=1e-14, atol=1e-16)
+
+
+def test_P9_adam_vs_torch_optim():
+    torch = pytest.importorskip("torch")
+    N = 8
+    K, S, f = W.random_fields(N, seed=3)
+    th0 = W.random_theta((2, 16, 16, 1), 3)
+    o = _ctx(N, (2, 16, 16, 1), K, S, f, th0, lr=3e-3)
+    p = torch.nn.Parameter(torch.tensor(th0.astype(np.float64)))
+    opt = torch.optim.Adam([p], lr=3e-3, betas=(0.9, 0.999), eps=1e-8)
+    for _ in range(10):
+        _, g = o.loss_grad(p.detach().numpy())
+        p.grad = torch.tensor(g)
+        opt.step()
+        o.adam_step(g)
+    np.testing.assert_allclose(o.theta, p.detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- P10: torch autograd
+def _torch_loss(torch, N, widths, theta, alpha, f):
+    """Independent implementation: torch MLP + shifted-slice stencil + eigenbasis Gram inverse."""
+    h = 1.0 / N
+    n = N - 1
+    th = theta
+    c = torch.arange(N + 1, dtype=torch.float64) / N
+    Y, X = torch.meshgrid(c, c, indexing="ij")
+    z = torch.stack([X[1:-1, 1:-1].reshape(-1), Y[1:-1, 1:-1].reshape(-1)], 1)
+    off = 0
+    a = z
+    for l in range(len(widths) - 1):
+        fin, fout = widths[l], widths[l + 1]
+        Wm = th[off:off + fin * fout].reshape(fout, fin)
+        off += fin * fout
+        bb = th[off:off + fout]
+        off += fout
+        a = a @ Wm.T + bb
+        if l < len(widths) - 2:
+            a = torch.tanh(a)
+    cut = 16 * X * (1 - X) * Y * (1 - Y)
+    U = torch.zeros(N + 1, N + 1, dtype=torch.float64)
+    U = U.index_put((torch.arange(1, N).repeat_interleave(n), torch.arange(1, N).repeat(n)),
+                    a[:, 0] * cut[1:-1, 1:-1].reshape(-1))
+    A = torch.tensor(alpha.reshape(N + 1, N + 1))
+    c0 = U[1:-1, 1:-1]
+    res = (A[1:-1, 0:-2] * (c0 - U[1:-1, 0:-2]) + A[0:-2, 1:-1] * (c0 - U[0:-2, 1:-1])
+           + A[1:-1, 1:-1] * (c0 - U[1:-1, 2:]) + A[1:-1, 1:-1] * (c0 - U[2:, 1:-1])
+           - h * h * torch.tensor(f.reshape(N + 1, N + 1)[1:-1, 1:-1].astype(np.float64)))
+    S, lam = _dst_matrix(N)
+    S = torch.tensor(S)
+    lam = torch.tensor(lam)
+    Z = (S @ res @ S) / (lam[:, None] + lam[None, :])
+    q = h * h * (S @ Z @ S)
+    return (res * q).sum()
+
+
+@pytest.mark.parametrize("name,Nred", [("C1", None), ("C2", None), ("C3", 32), ("C4", 16), ("C5", 16)])
+def test_P10_loss_grad_vs_torch_autograd(name, Nred):
+    torch = pytest.importorskip("torch")
+    F = W.make_fields(name)
+    w = F.workload
+    N = w.N if Nred is None else Nred
+    if Nred is None:
+        K, S, f = F.K, F.S, F.f
+    else:
+        K, S, f = W.random_fields(N, seed=w.N)
+    th = W.random_theta(w.widths, 7).astype(np.float64)
+    o = _ctx(N, w.widths, K, S, f, th)
+    loss, g = o.loss_grad()
+    p = torch.tensor(th, requires_grad=True)
+    tl = _torch_loss(torch, N, w.widths, p, o.alpha(), f)
+    tl.backward()
+    assert abs(loss - tl.item()) <= 1e-10 * abs(tl.item())
+    np.testing.assert_allclose(g, p.grad.numpy(), rtol=1e-8, atol=1e-10 * np.abs(g).max())
+
+
+# --------------------------------------------------------------------------- P11: convergence
+def test_P11_training_converges_to_closed_form():
+    """C1 (BASELINE.json configs[0]): 2000 Adam steps, lr 1e-3 -> rel-L2(u, c_h sin sin) <= 1e-2."""
+    F = W.make_fields("C1")
+    w = F.workload
+    o = oracle.Oracle(w.N, w.widths, F.K, F.S, F.f, F.theta0, lr=w.lr)
+    hist = o.train(2000)
+    N = w.N
+    h = 1.0 / N
+    X, Y = W.grid_xy(N)
+    ch = (math.pi * h / 2) ** 2 / math.sin(math.pi * h / 2) ** 2
+    ustar = (ch * np.sin(math.pi * X) * np.sin(math.pi * Y)).reshape(-1)
+    u = o.forward()
+    assert np.linalg.norm(u - ustar) / np.linalg.norm(ustar) <= 1e-2
+    assert hist[-1] < 1e-2 * hist[0]   # SPEC.md:441 asks >= 1000x for its own init; see DESIGN.md
+
+
+# --------------------------------------------------------------------------- P12, P13
+def test_P12_cutoff_boundary_exact_zero():
+    N = 16
+    o = _ctx(N, (2, 8, 8, 1), theta=W.random_theta((2, 8, 8, 1), 0))
+    U = o.forward().reshape(N + 1, N + 1)
+    assert np.all(U[0, :] == 0) and np.all(U[-1, :] == 0) and np.all(U[:, 0] == 0) and np.all(U[:, -1] == 0)
+    assert np.count_nonzero(U[1:-1, 1:-1]) == (N - 1) ** 2
+
+
+def test_P12_cutoff_normalisation():
+    """cutoff(1/2,1/2) = 1: a net that outputs the constant 1 gives u(1/2,1/2) = 1."""
+    N = 8
+    widths = (2, 4, 1)
+    th = np.zeros(2 * 4 + 4 + 4 * 1 + 1)
+    th[-1] = 1.0      # output bias
+    o = _ctx(N, widths, theta=th.astype(np.float32))
+    U = o.forward().reshape(N + 1, N + 1)
+    assert U[N // 2, N // 2] == 1.0
+
+
+def test_P13_zero_output_layer():
+    """Zero output layer => u = 0, RES = -b, LOSS = b^T G^-1 b."""
+    N = 16
+    K, S, f = W.random_fields(N, seed=13)
+    widths = (2, 16, 1)
+    th = W.random_theta(widths, 13)
+    th[-(16 + 1):] = 0.0
+    o = _ctx(N, widths, K, S, f, th)
+    loss, g, it = o.loss_grad(intermediates=True)
+    assert np.all(it["u"] == 0.0)
+    b = f.astype(np.float64).reshape(N + 1, N + 1)[1:-1, 1:-1].reshape(-1) / N ** 2
+    np.testing.assert_allclose(it["res"], -b, rtol=1e-15)
+    assert abs(loss - b @ _gram_inv_dst(N, b)) <= 1e-11 * loss
