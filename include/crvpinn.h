@@ -1,0 +1,150 @@
+/*
+ * crvpinn.h -- C ABI of the B200 (sm_100a) CRVPINN pressure-update library.
+ *
+ * The library implements the hot path of arXiv 2604.20731 §5-§6: the robust-loss training
+ * of the pressure network p_theta that replaces the MUMPS pressure solve. One Adam iteration
+ * is, in the paper's notation:
+ *
+ *   A1 PINN_ij = 16 x(1-x) y(1-y) net_theta(x_i, y_j)            PAPER.md:373 (readings R5, R6)
+ *   A2 RES_kl  = (alpha grad+ PINN, grad+ delta_kl)_h - (RHS, delta_kl)_h   Eq. 25
+ *   A3 q       = G^-1 RES, G = h^-2 (4 / -1 five-point)           Eq. 26-28
+ *   A4 LOSS    = RES^T q                                          Eq. 27
+ *   A5-A7 dLOSS/dtheta by reverse mode (u-adjoint 2 A(alpha) q, MLP backward, reduction)
+ *   A8 Adam step ("Adam optimizer")
+ *
+ * alpha_ij = K_ij ((1 - S_ij) + M S_ij), M = mu_w/mu_g (Eq. 23 first line, PAPER.md:369,
+ * non-dimensional reading R10), and b = h^2 f with f the right side of -div(alpha grad p) = f
+ * (reading R1; for an injection well f > 0). All readings are listed in DESIGN.md §2.
+ *
+ * Conventions (apply to every entry point):
+ *  - N is the number of grid intervals per axis, h = 1/N, nodes (x_i, y_j) = (i/N, j/N),
+ *    0 <= i,j <= N (Eq. 21, reading R9). Unknowns are the (N-1)^2 interior nodes.
+ *  - Host fields are float32, row-major (N+1) x (N+1): F[j*(N+1) + i] at (x_i, y_j).
+ *  - theta is float32, flattened W1 (row-major out x in), b1, W2, b2, ..., W_{L+1}, b_{L+1}.
+ *  - All pointer arguments are caller-owned; inputs are copied before the call returns
+ *    (unless documented as device pointers), outputs are written into caller buffers.
+ *  - A context owns all of its device memory, its CUDA stream (or uses the one given in
+ *    opts.stream) and its captured CUDA graphs. A context is NOT thread-safe; several
+ *    contexts may coexist (one per GPU / per independent problem).
+ *  - Return value: CRVPINN_OK (0) or a negative code; crvpinn_last_error() explains it.
+ *  - The library never falls back to a CPU path: without a usable sm_100 device every
+ *    call that needs one returns CRVPINN_ECUDA.
+ */
+#ifndef CRVPINN_H
+#define CRVPINN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct crvpinn_ctx crvpinn_ctx;   /* opaque */
+
+enum {
+    CRVPINN_OK = 0,
+    CRVPINN_EINVAL = -1,      /* bad argument: N, widths, null required pointer, n < 1 */
+    CRVPINN_ENOMEM = -2,      /* device allocation failed */
+    CRVPINN_ECUDA = -3,       /* CUDA runtime error / no sm_100 device */
+    CRVPINN_ENONFINITE = -4,  /* loss or gradient became non-finite; theta restored */
+    CRVPINN_EDOMAIN = -5      /* K <= 0 or a non-finite input field */
+};
+
+/* Arithmetic of the MLP contractions (A1, A6). The stencil, Gram solve, reductions and
+ * Adam are fp32 (reductions of the loss in fp64) in every mode. */
+enum {
+    CRVPINN_PREC_TENSOR = 0,  /* tcgen05 tensor cores, fp16 operands (10-bit mantissa, same as
+                                 TF32): forward activations split hi+lo (2 MMAs), backward 1 MMA
+                                 with power-of-two gradient scaling; fp32 accumulate in TMEM.
+                                 Parity class: north_star's "TF32" tolerances. */
+    CRVPINN_PREC_FP32 = 1     /* SIMT FFMA fp32 everywhere. Parity class: "fp32" tolerances. */
+};
+
+typedef struct {
+    double lr;              /* Adam learning rate (default 1e-3, BASELINE.json configs[0]) */
+    double beta1, beta2;    /* default 0.9, 0.999 (reading R7) */
+    double eps;             /* default 1e-8 */
+    double mobility_ratio;  /* M = mu_w/mu_g, default 25.35/3.95 (Table 1) */
+    int precision;          /* CRVPINN_PREC_*, default CRVPINN_PREC_TENSOR */
+    uint64_t seed;          /* Xavier init seed when theta0 == NULL */
+    void *stream;           /* cudaStream_t to run on; NULL = the context creates its own */
+    int device;             /* CUDA device ordinal, default 0 */
+} crvpinn_opts;
+
+/* Fill *o with the defaults listed above. */
+void crvpinn_default_opts(crvpinn_opts *o);
+
+/* Create a problem on grid N (power of two, 16 <= N <= 2048) with layer widths
+ * widths[0..n_widths-1] = {2, w, ..., w, 1} (hidden widths multiples of 32, <= 256).
+ * K, S, f: host (N+1)^2 float32 fields (K > 0; S is clamped to [0,1]).
+ * theta0: host float32 of crvpinn_num_params entries, or NULL for Xavier-uniform (biases 0).
+ * Runs step A0 (alpha, b) and builds the Gram-solve constants (Eq. 28 "factorization performed
+ * only once", realised as the sine basis of G). Adam state starts at zero. */
+int crvpinn_create(crvpinn_ctx **out, int N, int n_widths, const int *widths,
+                   const float *K, const float *S, const float *f,
+                   const float *theta0, const crvpinn_opts *opts);
+
+/* Replace the saturation field (host, (N+1)^2) and recompute alpha (step A0).
+ * PAPER.md:447-452 (§6 step 7: "including the actual saturation S_g^n"). */
+int crvpinn_set_saturation(crvpinn_ctx *ctx, const float *S);
+
+/* Same, with S a DEVICE pointer (float32, (N+1)^2) on the context's device; the copy is
+ * stream-ordered on the context stream. Used when the saturation is already resident. */
+int crvpinn_set_saturation_device(crvpinn_ctx *ctx, const void *S_dev);
+
+/* Pretraining: n_iters Adam iterations on the current fields (§6 step 2).
+ * loss_hist (nullable, n_iters doubles): loss_hist[k] = LOSS(theta_k) before update k+1. */
+int crvpinn_pretrain(crvpinn_ctx *ctx, int n_iters, double *loss_hist);
+
+/* One pressure update: n_adam Adam iterations (§6 step 7; 100 in the paper).
+ * Same semantics as crvpinn_pretrain; theta and the Adam state (m, v, t) persist across calls
+ * (reading R8). All n_adam iterations run as one CUDA graph (captured on first use per n).
+ * On a non-finite loss/gradient returns CRVPINN_ENONFINITE and restores theta and the Adam
+ * state to their values at call entry. */
+int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist);
+
+/* Evaluate the network on the lattice: p_out (host, (N+1)^2 float32) = PINN_ij, exactly 0 on
+ * the boundary (the hand-off to the IGA projection). */
+int crvpinn_eval(crvpinn_ctx *ctx, float *p_out);
+
+/* LOSS (Eq. 27) and dLOSS/dtheta at the current theta, no update. grad nullable. */
+int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad);
+
+/* Intermediates of the last crvpinn_loss_grad (test hook, host float32; each nullable):
+ * u (N+1)^2 lattice, res (N-1)^2, q (N-1)^2, gu (N+1)^2 lattice = dLOSS/du (0 on boundary). */
+int crvpinn_get_intermediates(crvpinn_ctx *ctx, float *u, float *res, float *q, float *gu);
+
+size_t crvpinn_num_params(const crvpinn_ctx *ctx);
+
+/* theta (float32, num_params). get is stream-ordered and synchronising. */
+int crvpinn_get_params(crvpinn_ctx *ctx, float *theta);
+int crvpinn_set_params(crvpinn_ctx *ctx, const float *theta);
+
+/* Checkpoint / resume of the Adam state (m, v: float32 num_params each; t: step count). */
+int crvpinn_get_adam(crvpinn_ctx *ctx, float *m, float *v, int64_t *t);
+int crvpinn_set_adam(crvpinn_ctx *ctx, const float *m, const float *v, int64_t t);
+
+/* Per-stage device timing of the iterations run by crvpinn_step while profiling is on:
+ * CUDA events recorded on the context stream around each stage INSIDE the captured graph.
+ * Stages: 0 = MLP forward (A1), 1 = stencil + Gram + loss + adjoint (A2-A5),
+ * 2 = MLP backward + weight-gradient reduction (A6-A7), 3 = Adam (A8).
+ * Enabling/disabling drops cached graphs. ms_sum[s] accumulates milliseconds over all
+ * profiled iterations since the last reset; *n_iters receives their count. */
+int crvpinn_set_profiling(crvpinn_ctx *ctx, int on);
+int crvpinn_get_profile(crvpinn_ctx *ctx, double *ms_sum /* [4] */, int64_t *n_iters, int reset);
+
+/* Number of kernel launches one Adam iteration issues (for the bench's gpu_launches). */
+int crvpinn_launches_per_iter(const crvpinn_ctx *ctx);
+
+/* Context stream (cudaStream_t) for callers that synchronise with it. */
+void *crvpinn_stream(const crvpinn_ctx *ctx);
+
+const char *crvpinn_last_error(const crvpinn_ctx *ctx);   /* ctx may be NULL (global error) */
+
+void crvpinn_destroy(crvpinn_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRVPINN_H */

@@ -1,0 +1,216 @@
+"""Python binding of the CRVPINN sm_100a library (include/crvpinn.h).
+
+Argument marshalling only: every step of the CRVPINN update runs in the CUDA kernels of
+libcrvpinn.so. There is no CPU fallback: if the library is missing this module raises, and
+without an sm_100 device every call fails with CRVPINN_ECUDA.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcrvpinn.so")
+
+CRVPINN_OK, CRVPINN_EINVAL, CRVPINN_ENOMEM, CRVPINN_ECUDA, CRVPINN_ENONFINITE, CRVPINN_EDOMAIN = 0, -1, -2, -3, -4, -5
+PREC_TENSOR, PREC_FP32 = 0, 1
+
+# every symbol include/crvpinn.h declares
+EXPORTS = [
+    "crvpinn_default_opts", "crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device",
+    "crvpinn_pretrain", "crvpinn_step", "crvpinn_eval", "crvpinn_loss_grad", "crvpinn_get_intermediates",
+    "crvpinn_num_params", "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
+    "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter", "crvpinn_stream",
+    "crvpinn_last_error", "crvpinn_destroy",
+]
+
+
+class CrvpinnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"crvpinn error {code}: {msg}")
+        self.code = code
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("mobility_ratio", ctypes.c_double), ("precision", ctypes.c_int),
+                ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p), ("device", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libcrvpinn.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2604_20731_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(path)
+    P, F, D, I = ctypes.c_void_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double), ctypes.c_int
+    I64P = ctypes.POINTER(ctypes.c_int64)
+    L.crvpinn_default_opts.argtypes = [ctypes.POINTER(Opts)]
+    L.crvpinn_create.argtypes = [ctypes.POINTER(P), I, I, ctypes.POINTER(I), F, F, F, F, ctypes.POINTER(Opts)]
+    L.crvpinn_set_saturation.argtypes = [P, F]
+    L.crvpinn_set_saturation_device.argtypes = [P, P]
+    L.crvpinn_pretrain.argtypes = [P, I, D]
+    L.crvpinn_step.argtypes = [P, I, D]
+    L.crvpinn_eval.argtypes = [P, F]
+    L.crvpinn_loss_grad.argtypes = [P, D, F]
+    L.crvpinn_get_intermediates.argtypes = [P, F, F, F, F]
+    L.crvpinn_num_params.restype = ctypes.c_size_t
+    L.crvpinn_num_params.argtypes = [P]
+    L.crvpinn_get_params.argtypes = [P, F]
+    L.crvpinn_set_params.argtypes = [P, F]
+    L.crvpinn_get_adam.argtypes = [P, F, F, I64P]
+    L.crvpinn_set_adam.argtypes = [P, F, F, ctypes.c_int64]
+    L.crvpinn_set_profiling.argtypes = [P, I]
+    L.crvpinn_get_profile.argtypes = [P, D, I64P, I]
+    L.crvpinn_launches_per_iter.argtypes = [P]
+    L.crvpinn_stream.restype = P
+    L.crvpinn_stream.argtypes = [P]
+    L.crvpinn_last_error.restype = ctypes.c_char_p
+    L.crvpinn_last_error.argtypes = [P]
+    L.crvpinn_destroy.argtypes = [P]
+    for name in ["crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device", "crvpinn_pretrain",
+                 "crvpinn_step", "crvpinn_eval", "crvpinn_loss_grad", "crvpinn_get_intermediates",
+                 "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
+                 "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter"]:
+        getattr(L, name).restype = I
+    _lib = L
+    return L
+
+
+def _f32(a, n=None):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if n is not None and a.size != n:
+        raise ValueError(f"expected {n} values, got {a.size}")
+    return a
+
+
+def _fp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def default_opts() -> Opts:
+    o = Opts()
+    load().crvpinn_default_opts(ctypes.byref(o))
+    return o
+
+
+class Crvpinn:
+    """One CRVPINN problem on one GPU (wraps crvpinn_ctx)."""
+
+    def __init__(self, N: int, widths: Sequence[int], K, S, f, theta0=None, *, precision: int = PREC_TENSOR,
+                 lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 mobility_ratio: Optional[float] = None, seed: int = 0, stream: Optional[int] = None,
+                 device: int = 0):
+        L = load()
+        self.N = int(N)
+        self.widths = tuple(int(w) for w in widths)
+        nn = (self.N + 1) ** 2
+        o = default_opts()
+        o.lr, o.beta1, o.beta2, o.eps = lr, beta1, beta2, eps
+        if mobility_ratio is not None:
+            o.mobility_ratio = mobility_ratio
+        o.precision, o.seed, o.device = precision, seed, device
+        o.stream = stream
+        w = (ctypes.c_int * len(self.widths))(*self.widths)
+        K, S, f = _f32(K, nn), _f32(S, nn), _f32(f, nn)
+        th = None if theta0 is None else _f32(theta0)
+        h = ctypes.c_void_p()
+        rc = L.crvpinn_create(ctypes.byref(h), self.N, len(self.widths), w, _fp(K), _fp(S), _fp(f),
+                              None if th is None else _fp(th), ctypes.byref(o))
+        if rc != 0:
+            raise CrvpinnError(rc, L.crvpinn_last_error(None).decode())
+        self._h = h
+        self.precision = precision
+        self.np = int(L.crvpinn_num_params(h))
+
+    def _check(self, rc):
+        if rc != 0:
+            raise CrvpinnError(rc, load().crvpinn_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().crvpinn_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # ---- the boundary calls (same names as include/crvpinn.h)
+    def set_saturation(self, S):
+        self._check(load().crvpinn_set_saturation(self._h, _fp(_f32(S, (self.N + 1) ** 2))))
+
+    def set_saturation_device(self, ptr: int):
+        self._check(load().crvpinn_set_saturation_device(self._h, ctypes.c_void_p(ptr)))
+
+    def pretrain(self, n_iters: int, history: bool = True):
+        hist = np.empty(n_iters) if history else None
+        self._check(load().crvpinn_pretrain(self._h, int(n_iters),
+                                            None if hist is None else hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return hist
+
+    def step(self, n_adam: int = 100, history: bool = True):
+        hist = np.empty(n_adam) if history else None
+        self._check(load().crvpinn_step(self._h, int(n_adam),
+                                        None if hist is None else hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return hist
+
+    def eval(self) -> np.ndarray:
+        out = np.empty((self.N + 1) ** 2, np.float32)
+        self._check(load().crvpinn_eval(self._h, _fp(out)))
+        return out
+
+    def loss_grad(self, grad: bool = True):
+        loss = ctypes.c_double()
+        g = np.empty(self.np, np.float32) if grad else None
+        self._check(load().crvpinn_loss_grad(self._h, ctypes.byref(loss), None if g is None else _fp(g)))
+        return (loss.value, g) if grad else loss.value
+
+    def intermediates(self):
+        nn, n2 = (self.N + 1) ** 2, (self.N - 1) ** 2
+        u, r, q, gu = (np.empty(nn, np.float32), np.empty(n2, np.float32), np.empty(n2, np.float32),
+                       np.empty(nn, np.float32))
+        self._check(load().crvpinn_get_intermediates(self._h, _fp(u), _fp(r), _fp(q), _fp(gu)))
+        return dict(u=u, res=r, q=q, gu=gu)
+
+    @property
+    def theta(self) -> np.ndarray:
+        out = np.empty(self.np, np.float32)
+        self._check(load().crvpinn_get_params(self._h, _fp(out)))
+        return out
+
+    @theta.setter
+    def theta(self, th):
+        self._check(load().crvpinn_set_params(self._h, _fp(_f32(th, self.np))))
+
+    def adam_state(self):
+        m, v, t = np.empty(self.np, np.float32), np.empty(self.np, np.float32), ctypes.c_int64()
+        self._check(load().crvpinn_get_adam(self._h, _fp(m), _fp(v), ctypes.byref(t)))
+        return m, v, int(t.value)
+
+    def set_adam_state(self, m, v, t: int):
+        self._check(load().crvpinn_set_adam(self._h, _fp(_f32(m, self.np)), _fp(_f32(v, self.np)), int(t)))
+
+    def set_profiling(self, on: bool):
+        self._check(load().crvpinn_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self, reset: bool = False):
+        ms = (ctypes.c_double * 4)()
+        n = ctypes.c_int64()
+        self._check(load().crvpinn_get_profile(self._h, ms, ctypes.byref(n), 1 if reset else 0))
+        return list(ms), int(n.value)
+
+    @property
+    def launches_per_iter(self) -> int:
+        return int(load().crvpinn_launches_per_iter(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(load().crvpinn_stream(self._h) or 0)

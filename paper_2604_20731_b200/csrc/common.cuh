@@ -1,0 +1,108 @@
+// common.cuh -- shared device/host definitions of the CRVPINN sm_100a library.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md §1).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#define CRV_MAX_LAYERS 16
+
+namespace crv {
+
+// Device-resident per-context scalars. One instance lives in device memory.
+struct DevState {
+    double loss;          // LOSS of the last evaluated iteration (Eq. 27)
+    double bc1, bc2;      // Adam bias corrections 1-beta^t for the pending update
+    int64_t t;            // Adam step counter (persists across calls, reading R8)
+    int it;               // index into the loss history for the current call
+    int nonfinite;        // set when a non-finite loss / gradient is seen
+    float gscale;         // power-of-two scale applied to dLOSS/dnet in the tensor backward
+    float inv_gscale;
+    unsigned gmax_bits;   // max |dLOSS/dnet| of the current iteration (float bits, atomicMax)
+    int pad;
+};
+
+// Geometry and network description passed by value to kernels.
+struct Net {
+    int N;                // grid intervals; MLP points are (i,j) in [1..N]^2 -> P = N*N
+    int n;                // N-1 interior nodes per axis
+    int P;                // N*N MLP points
+    int nl;               // weight layers (hidden + output)
+    int widths[CRV_MAX_LAYERS + 1];
+    long woff[CRV_MAX_LAYERS];
+    long boff[CRV_MAX_LAYERS];
+};
+
+// Job of the deterministic partial-sum reducer: dst[o] = scale * sum_{z<nsplit} src[z*stride + off(o)],
+// o < count, off(o) = o, or (transposed) (o % cols) * ld + o / cols.
+struct RedJob {
+    long src;      // offset in the partial buffer
+    long dst;      // offset in the gradient vector
+    long stride;   // floats between consecutive splits
+    int count;
+    int nsplit;
+    int cols, ld;  // transposed layout parameters
+    int transposed;
+    int scaled;    // multiply by DevState::inv_gscale (tensor backward partials)
+};
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// MLP point p -> lattice node (i, j) in [1..N]^2
+__device__ __forceinline__ void point_ij(int p, int N, int &i, int &j) {
+    i = (p & (N - 1)) + 1;   // N is a power of two
+    j = (p / N) + 1;
+}
+
+__device__ __forceinline__ float cutoff(float x, float y) {
+    return 16.0f * x * (1.0f - x) * y * (1.0f - y);
+}
+
+}  // namespace crv
+
+// ------------------------------------------------------------------ launch wrappers
+// (defined in the .cu files; all take the context stream)
+namespace crv {
+// fields.cu
+void launch_alpha(const float *K, const float *S, float *alpha, int N, float mobility, cudaStream_t s);
+void launch_scale_b(const float *f, float *b, int N, cudaStream_t s);
+void launch_residual(const float *u, const float *alpha, const float *b, float *res, int N, cudaStream_t s);
+void launch_loss_partials(const float *res, const float *q, double *part, int n2, int nblk, cudaStream_t s);
+void launch_loss_final(const double *part, int nblk, DevState *st, double *hist, int n_hist,
+                       double beta1, double beta2, cudaStream_t s);
+void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_lattice, int N,
+                    DevState *st, int track_max, cudaStream_t s);
+void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
+                 DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
+void launch_begin_call(DevState *st, cudaStream_t s);
+void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int max_count,
+                   const DevState *st, cudaStream_t s);
+int loss_partial_blocks(int n2);
+// gram.cu
+void gram_init_constants(float *S, float *lam, int N, cudaStream_t s);
+void launch_gram_apply(const float *res, float *q, const float *S, const float *lam, float *w1,
+                       float *w2, int N, cudaStream_t s);
+// mlp_simt.cu -- fp32 FFMA MLP path (CRVPINN_PREC_FP32)
+struct MlpPlan {
+    long offW[CRV_MAX_LAYERS], offB[CRV_MAX_LAYERS];   // partial-buffer offsets per layer
+    int splitW[CRV_MAX_LAYERS];                       // K-splits of the weight-gradient GEMM
+    int cs_split;                                     // row chunks of the column reductions
+    int rows_per;
+    long partial_floats;
+    int njobs, max_count;
+    RedJob jobs[2 * CRV_MAX_LAYERS];
+};
+struct SimtBufs {
+    float *act;        // [hidden a=1..L][P][w_a] fp32, slot stride P*wmax
+    float *delta0, *delta1;
+    float *gbar;       // [P]
+    float *partial;    // reduction partials (MlpPlan)
+    const RedJob *jobs;// device copy of plan.jobs
+};
+void simt_make_plan(const Net &net, MlpPlan &plan);
+void simt_forward(const Net &net, const float *theta, const SimtBufs &b, float *u, cudaStream_t s);
+void simt_backward(const Net &net, const MlpPlan &plan, const float *theta, const SimtBufs &b,
+                   float *grad, cudaStream_t s);
+int simt_launches_fwd(const Net &net);
+int simt_launches_bwd(const Net &net);
+}  // namespace crv

@@ -1,0 +1,540 @@
+// crvpinn.cu -- host side of the C ABI (include/crvpinn.h): context, device buffers, the
+// per-iteration launch sequence (A1..A8) and its CUDA-graph capture.
+#include "../../include/crvpinn.h"
+#include "common.cuh"
+#include "mlp_tc.cuh"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+using namespace crv;
+
+namespace {
+
+std::string g_err;   // errors raised before a context exists
+
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    double *hist = nullptr;               // device loss history of this graph's n iterations
+    std::vector<cudaEvent_t> ev;          // 5 per iteration when captured with profiling
+};
+
+}  // namespace
+
+struct crvpinn_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    crvpinn_opts opts{};
+    Net net{};
+    long np = 0;
+    // fields
+    float *K = nullptr, *S = nullptr, *f = nullptr, *alpha = nullptr, *b = nullptr;
+    float *u = nullptr, *res = nullptr, *q = nullptr, *gu_lat = nullptr;
+    float *gS = nullptr, *glam = nullptr, *gw1 = nullptr, *gw2 = nullptr;
+    double *loss_part = nullptr;
+    int loss_nblk = 0;
+    DevState *st = nullptr, *snap_st = nullptr;
+    float *theta = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
+    float *snap_theta = nullptr, *snap_m = nullptr, *snap_v = nullptr;
+    // MLP buffers
+    SimtBufs simt{};
+    MlpPlan plan{};
+    RedJob *d_jobs = nullptr;
+    TcBufs tc{};
+    // host staging (pinned)
+    float *h_field = nullptr;
+    double *h_hist = nullptr;
+    int h_hist_cap = 0;
+    DevState *h_state = nullptr;
+    // graphs and profiling
+    std::map<int, GraphEntry> graphs;
+    bool profiling = false;
+    double prof_ms[4] = {0, 0, 0, 0};
+    int64_t prof_iters = 0;
+    std::string err;
+    std::vector<void *> allocs;
+};
+
+#define CK(call)                                                                 \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);      \
+            return CRVPINN_ECUDA;                                                \
+        }                                                                        \
+    } while (0)
+
+static int fail(crvpinn_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->err = msg; else g_err = msg;
+    return code;
+}
+
+template <class T>
+static int dalloc(crvpinn_ctx *ctx, T **p, size_t count) {
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    if (e != cudaSuccess) {
+        ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+        return e == cudaErrorMemoryAllocation ? CRVPINN_ENOMEM : CRVPINN_ECUDA;
+    }
+    cudaMemset(q, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    ctx->allocs.push_back(q);
+    *p = (T *)q;
+    return CRVPINN_OK;
+}
+
+#define DALLOC(ptr, count)                                   \
+    do {                                                     \
+        int rc_ = dalloc(ctx, &(ptr), (size_t)(count));      \
+        if (rc_ != CRVPINN_OK) return rc_;                   \
+    } while (0)
+
+// ---------------------------------------------------------------- one iteration
+// Launches A1..A8 on the context stream. train = 0: evaluation only (no Adam, t unchanged).
+// Event-record nodes inside a captured graph need cudaEventRecordExternal (a plain record during
+// capture only expresses a dependency and is never executed as a timestamp).
+static void record(cudaEvent_t e, cudaStream_t s) { cudaEventRecordWithFlags(e, s, cudaEventRecordExternal); }
+
+static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool train, cudaEvent_t *ev) {
+    cudaStream_t s = ctx->stream;
+    const Net &net = ctx->net;
+    const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
+    if (ev) record(ev[0], s);
+    // A1: network at every MLP point -> u on the lattice
+    if (tc) tc_forward(net, ctx->tc, ctx->u, s);
+    else simt_forward(net, ctx->theta, ctx->simt, ctx->u, s);
+    if (ev) record(ev[1], s);
+    // A2-A5: residual, Gram solve, loss, adjoint
+    int n = net.n;
+    launch_residual(ctx->u, ctx->alpha, ctx->b, ctx->res, net.N, s);
+    launch_gram_apply(ctx->res, ctx->q, ctx->gS, ctx->glam, ctx->gw1, ctx->gw2, net.N, s);
+    launch_loss_partials(ctx->res, ctx->q, ctx->loss_part, n * n, ctx->loss_nblk, s);
+    launch_loss_final(ctx->loss_part, ctx->loss_nblk, ctx->st, hist, n_hist,
+                      train ? ctx->opts.beta1 : -1.0, ctx->opts.beta2, s);
+    float *gbar = tc ? ctx->tc.gbar : ctx->simt.gbar;
+    launch_adjoint(ctx->q, ctx->alpha, gbar, ctx->gu_lat, net.N, ctx->st, tc ? 1 : 0, s);
+    if (ev) record(ev[2], s);
+    // A6-A7: backward and deterministic weight-gradient reduction
+    if (tc) tc_backward(net, ctx->tc, ctx->st, ctx->grad, s);
+    else simt_backward(net, ctx->plan, ctx->theta, ctx->simt, ctx->grad, s);
+    if (ev) record(ev[3], s);
+    // A8: Adam (+ refresh of the tensor-core weight copies)
+    if (train) {
+        launch_adam(ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, ctx->st,
+                    (float)ctx->opts.lr, (float)ctx->opts.beta1, (float)ctx->opts.beta2,
+                    (float)ctx->opts.eps, s);
+        if (tc) tc_refresh_weights(net, ctx->tc, ctx->theta, s);
+    }
+    if (ev) record(ev[4], s);
+}
+
+static int launches_per_iter(const crvpinn_ctx *ctx) {
+    const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
+    int mlp = tc ? tc_launches(ctx->net) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
+    return mlp + 1 /*residual*/ + 4 /*gram*/ + 2 /*loss*/ + 1 /*adjoint*/ + 1 /*adam*/;
+}
+
+static void drop_graphs(crvpinn_ctx *ctx) {
+    for (auto &kv : ctx->graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.hist) cudaFree(kv.second.hist);
+        for (auto e : kv.second.ev) cudaEventDestroy(e);
+    }
+    ctx->graphs.clear();
+}
+
+static int snapshot_copies(crvpinn_ctx *ctx, bool to_snap) {
+    cudaStream_t s = ctx->stream;
+    size_t bytes = sizeof(float) * ctx->np;
+    float *a[3] = {ctx->theta, ctx->m, ctx->v}, *b[3] = {ctx->snap_theta, ctx->snap_m, ctx->snap_v};
+    for (int k = 0; k < 3; ++k)
+        CK(cudaMemcpyAsync(to_snap ? b[k] : a[k], to_snap ? a[k] : b[k], bytes, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(to_snap ? ctx->snap_st : ctx->st, to_snap ? ctx->st : ctx->snap_st, sizeof(DevState),
+                       cudaMemcpyDeviceToDevice, s));
+    return CRVPINN_OK;
+}
+
+static int get_graph(crvpinn_ctx *ctx, int n, GraphEntry **out) {
+    auto it = ctx->graphs.find(n);
+    if (it != ctx->graphs.end()) { *out = &it->second; return CRVPINN_OK; }
+    GraphEntry ge;
+    CK(cudaMalloc(&ge.hist, sizeof(double) * (size_t)n));
+    if (ctx->profiling) {
+        ge.ev.resize((size_t)5 * n);
+        for (auto &e : ge.ev) CK(cudaEventCreate(&e));
+    }
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    launch_begin_call(ctx->st, ctx->stream);
+    int rc = snapshot_copies(ctx, true);
+    for (int k = 0; k < n && rc == CRVPINN_OK; ++k)
+        launch_iteration(ctx, ge.hist, n, true, ctx->profiling ? &ge.ev[(size_t)5 * k] : nullptr);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc != CRVPINN_OK) return rc;
+    if (e != cudaSuccess) return fail(ctx, CRVPINN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&ge.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, CRVPINN_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    ctx->graphs[n] = ge;
+    *out = &ctx->graphs[n];
+    return CRVPINN_OK;
+}
+
+static bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+static uint64_t splitmix(uint64_t &s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+static int check_field(crvpinn_ctx *ctx, const float *F, int N, bool positive, const char *name) {
+    long nn = (long)(N + 1) * (N + 1);
+    for (long i = 0; i < nn; ++i) {
+        float x = F[i];
+        if (!std::isfinite(x) || (positive && !(x > 0.0f)))
+            return fail(ctx, CRVPINN_EDOMAIN, std::string(name) + (positive ? " must be finite and > 0" : " must be finite"));
+    }
+    return CRVPINN_OK;
+}
+
+static int upload_field(crvpinn_ctx *ctx, float *dst, const float *src) {
+    size_t bytes = sizeof(float) * (size_t)(ctx->net.N + 1) * (ctx->net.N + 1);
+    CK(cudaStreamSynchronize(ctx->stream));   // staging buffer reuse
+    memcpy(ctx->h_field, src, bytes);
+    CK(cudaMemcpyAsync(dst, ctx->h_field, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return CRVPINN_OK;
+}
+
+extern "C" {
+
+void crvpinn_default_opts(crvpinn_opts *o) {
+    if (!o) return;
+    o->lr = 1e-3;
+    o->beta1 = 0.9;
+    o->beta2 = 0.999;
+    o->eps = 1e-8;
+    o->mobility_ratio = 25.35 / 3.95;
+    o->precision = CRVPINN_PREC_TENSOR;
+    o->seed = 0;
+    o->stream = nullptr;
+    o->device = 0;
+}
+
+const char *crvpinn_last_error(const crvpinn_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+size_t crvpinn_num_params(const crvpinn_ctx *ctx) { return ctx ? (size_t)ctx->np : 0; }
+
+void *crvpinn_stream(const crvpinn_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int crvpinn_launches_per_iter(const crvpinn_ctx *ctx) { return ctx ? launches_per_iter(ctx) : 0; }
+
+void crvpinn_destroy(crvpinn_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    drop_graphs(ctx);
+    for (void *p : ctx->allocs) cudaFree(p);
+    if (ctx->h_field) cudaFreeHost(ctx->h_field);
+    if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths, const float *K,
+                       const float *S, const float *f, const float *theta0) {
+    // ---- geometry
+    Net &net = ctx->net;
+    net.N = N; net.n = N - 1; net.P = N * N; net.nl = n_widths - 1;
+    long np = 0;
+    for (int l = 0; l < n_widths; ++l) net.widths[l] = widths[l];
+    for (int l = 0; l < net.nl; ++l) {
+        net.woff[l] = np; np += (long)widths[l + 1] * widths[l];
+        net.boff[l] = np; np += widths[l + 1];
+    }
+    ctx->np = np;
+    // ---- device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= ctx->opts.device)
+        return fail(ctx, CRVPINN_ECUDA, "no CUDA device available (this library has no CPU fallback)");
+    CK(cudaSetDevice(ctx->opts.device));
+    ctx->device = ctx->opts.device;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, ctx->device));
+    if (prop.major != 10)
+        return fail(ctx, CRVPINN_ECUDA, "device is not sm_100 (B200); this build targets sm_100a only");
+    if (ctx->opts.stream) {
+        ctx->stream = (cudaStream_t)ctx->opts.stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    long nn = (long)(N + 1) * (N + 1);
+    int n = N - 1;
+    DALLOC(ctx->K, nn); DALLOC(ctx->S, nn); DALLOC(ctx->f, nn);
+    DALLOC(ctx->alpha, nn); DALLOC(ctx->b, nn); DALLOC(ctx->u, nn); DALLOC(ctx->gu_lat, nn);
+    DALLOC(ctx->res, (long)n * n); DALLOC(ctx->q, (long)n * n);
+    DALLOC(ctx->gS, (long)n * n); DALLOC(ctx->glam, n);
+    DALLOC(ctx->gw1, (long)n * n); DALLOC(ctx->gw2, (long)n * n);
+    ctx->loss_nblk = loss_partial_blocks(n * n);
+    DALLOC(ctx->loss_part, ctx->loss_nblk);
+    DALLOC(ctx->st, 1); DALLOC(ctx->snap_st, 1);
+    DALLOC(ctx->theta, np); DALLOC(ctx->m, np); DALLOC(ctx->v, np); DALLOC(ctx->grad, np);
+    DALLOC(ctx->snap_theta, np); DALLOC(ctx->snap_m, np); DALLOC(ctx->snap_v, np);
+    CK(cudaMallocHost(&ctx->h_field, sizeof(float) * nn));
+    CK(cudaMallocHost(&ctx->h_state, sizeof(DevState)));
+    // ---- MLP buffers
+    int wmax = 0;
+    for (int l = 1; l < net.nl; ++l) wmax = widths[l] > wmax ? widths[l] : wmax;
+    if (ctx->opts.precision == CRVPINN_PREC_FP32) {
+        simt_make_plan(net, ctx->plan);
+        DALLOC(ctx->simt.act, (long)(net.nl - 1) * net.P * wmax);
+        DALLOC(ctx->simt.delta0, (long)net.P * wmax);
+        DALLOC(ctx->simt.delta1, (long)net.P * wmax);
+        DALLOC(ctx->simt.gbar, net.P);
+        DALLOC(ctx->simt.partial, ctx->plan.partial_floats);
+        DALLOC(ctx->d_jobs, ctx->plan.njobs);
+        CK(cudaMemcpy(ctx->d_jobs, ctx->plan.jobs, sizeof(RedJob) * ctx->plan.njobs, cudaMemcpyHostToDevice));
+        ctx->simt.jobs = ctx->d_jobs;
+    } else {
+        int rc = tc_create(net, ctx->tc, ctx->err);
+        if (rc != 0) return rc;
+    }
+    // ---- inputs, A0, Gram constants
+    std::vector<float> th((size_t)np);
+    if (theta0) {
+        memcpy(th.data(), theta0, sizeof(float) * np);
+    } else {
+        uint64_t sd = ctx->opts.seed;
+        for (int l = 0; l < net.nl; ++l) {
+            int fin = widths[l], fout = widths[l + 1];
+            double a = std::sqrt(6.0 / (fin + fout));
+            for (long k = 0; k < (long)fin * fout; ++k) {
+                double r = (double)(splitmix(sd) >> 11) * (1.0 / 9007199254740992.0);
+                th[net.woff[l] + k] = (float)((2.0 * r - 1.0) * a);
+            }
+            for (int k = 0; k < fout; ++k) th[net.boff[l] + k] = 0.0f;
+        }
+    }
+    CK(cudaMemcpy(ctx->theta, th.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->K, K, sizeof(float) * nn, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->S, S, sizeof(float) * nn, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->f, f, sizeof(float) * nn, cudaMemcpyHostToDevice));
+    launch_alpha(ctx->K, ctx->S, ctx->alpha, N, (float)ctx->opts.mobility_ratio, ctx->stream);
+    launch_scale_b(ctx->f, ctx->b, N, ctx->stream);
+    gram_init_constants(ctx->gS, ctx->glam, N, ctx->stream);
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    return CRVPINN_OK;
+}
+
+int crvpinn_create(crvpinn_ctx **out, int N, int n_widths, const int *widths, const float *K,
+                   const float *S, const float *f, const float *theta0, const crvpinn_opts *opts) {
+    if (!out) return fail(nullptr, CRVPINN_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!widths || !K || !S || !f) return fail(nullptr, CRVPINN_EINVAL, "widths, K, S, f are required");
+    if (!is_pow2(N) || N < 16 || N > 2048) return fail(nullptr, CRVPINN_EINVAL, "N must be a power of two in [16, 2048]");
+    if (n_widths < 3 || n_widths > CRV_MAX_LAYERS + 1) return fail(nullptr, CRVPINN_EINVAL, "need 3..17 widths");
+    if (widths[0] != 2 || widths[n_widths - 1] != 1) return fail(nullptr, CRVPINN_EINVAL, "widths must be {2, ..., 1}");
+    for (int l = 1; l < n_widths - 1; ++l)
+        if (widths[l] < 32 || widths[l] > 256 || widths[l] % 32 != 0)
+            return fail(nullptr, CRVPINN_EINVAL, "hidden widths must be multiples of 32 in [32, 256]");
+    crvpinn_ctx *ctx = new crvpinn_ctx();
+    if (opts) ctx->opts = *opts; else crvpinn_default_opts(&ctx->opts);
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) {
+        for (int l = 2; l < n_widths - 1; ++l)
+            if (widths[l] != widths[1]) {
+                delete ctx;
+                return fail(nullptr, CRVPINN_EINVAL, "tensor path needs equal hidden widths");
+            }
+    } else if (ctx->opts.precision != CRVPINN_PREC_FP32) {
+        delete ctx;
+        return fail(nullptr, CRVPINN_EINVAL, "unknown precision");
+    }
+    int rc = check_field(ctx, K, N, true, "K");
+    if (rc == CRVPINN_OK) rc = check_field(ctx, S, N, false, "S");
+    if (rc == CRVPINN_OK) rc = check_field(ctx, f, N, false, "f");
+    if (rc == CRVPINN_OK) rc = create_impl(ctx, N, n_widths, widths, K, S, f, theta0);
+    if (rc != CRVPINN_OK) {
+        g_err = ctx->err;
+        crvpinn_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return CRVPINN_OK;
+}
+
+int crvpinn_set_saturation(crvpinn_ctx *ctx, const float *S) {
+    if (!ctx || !S) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    int rc = check_field(ctx, S, ctx->net.N, false, "S");
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    rc = upload_field(ctx, ctx->S, S);
+    if (rc) return rc;
+    launch_alpha(ctx->K, ctx->S, ctx->alpha, ctx->net.N, (float)ctx->opts.mobility_ratio, ctx->stream);
+    CK(cudaGetLastError());
+    return CRVPINN_OK;
+}
+
+int crvpinn_set_saturation_device(crvpinn_ctx *ctx, const void *S_dev) {
+    if (!ctx || !S_dev) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    size_t bytes = sizeof(float) * (size_t)(ctx->net.N + 1) * (ctx->net.N + 1);
+    CK(cudaMemcpyAsync(ctx->S, S_dev, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    launch_alpha(ctx->K, ctx->S, ctx->alpha, ctx->net.N, (float)ctx->opts.mobility_ratio, ctx->stream);
+    CK(cudaGetLastError());
+    return CRVPINN_OK;
+}
+
+int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist) {
+    if (!ctx || n_adam < 1) return fail(ctx, CRVPINN_EINVAL, "n_adam must be >= 1");
+    CK(cudaSetDevice(ctx->device));
+    GraphEntry *ge = nullptr;
+    int rc = get_graph(ctx, n_adam, &ge);
+    if (rc) return rc;
+    CK(cudaGraphLaunch(ge->exec, ctx->stream));
+    if (loss_hist) {
+        if (ctx->h_hist_cap < n_adam) {
+            if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+            CK(cudaMallocHost(&ctx->h_hist, sizeof(double) * n_adam));
+            ctx->h_hist_cap = n_adam;
+        }
+        CK(cudaMemcpyAsync(ctx->h_hist, ge->hist, sizeof(double) * n_adam, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    if (loss_hist) memcpy(loss_hist, ctx->h_hist, sizeof(double) * n_adam);
+    if (ctx->profiling) {
+        for (int k = 0; k < n_adam; ++k)
+            for (int s = 0; s < 4; ++s) {
+                float ms = 0.0f;
+                CK(cudaEventElapsedTime(&ms, ge->ev[(size_t)5 * k + s], ge->ev[(size_t)5 * k + s + 1]));
+                ctx->prof_ms[s] += ms;
+            }
+        ctx->prof_iters += n_adam;
+    }
+    if (ctx->h_state->nonfinite) {
+        rc = snapshot_copies(ctx, false);
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(ctx->stream));
+        return fail(ctx, CRVPINN_ENONFINITE, "non-finite loss or gradient; theta and Adam state restored");
+    }
+    return CRVPINN_OK;
+}
+
+int crvpinn_pretrain(crvpinn_ctx *ctx, int n_iters, double *loss_hist) {
+    return crvpinn_step(ctx, n_iters, loss_hist);
+}
+
+int crvpinn_eval(crvpinn_ctx *ctx, float *p_out) {
+    if (!ctx || !p_out) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_forward(ctx->net, ctx->tc, ctx->u, ctx->stream);
+    else simt_forward(ctx->net, ctx->theta, ctx->simt, ctx->u, ctx->stream);
+    size_t nn = (size_t)(ctx->net.N + 1) * (ctx->net.N + 1);
+    CK(cudaMemcpyAsync(ctx->h_field, ctx->u, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    memcpy(p_out, ctx->h_field, sizeof(float) * nn);
+    return CRVPINN_OK;
+}
+
+int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad) {
+    if (!ctx || !loss) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    launch_begin_call(ctx->st, ctx->stream);
+    launch_iteration(ctx, nullptr, 0, false, nullptr);
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    if (grad) CK(cudaMemcpyAsync(grad, ctx->grad, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    *loss = ctx->h_state->loss;
+    if (!std::isfinite(*loss)) return fail(ctx, CRVPINN_ENONFINITE, "non-finite loss");
+    return CRVPINN_OK;
+}
+
+int crvpinn_get_intermediates(crvpinn_ctx *ctx, float *u, float *res, float *q, float *gu) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    CK(cudaSetDevice(ctx->device));
+    size_t nn = (size_t)(ctx->net.N + 1) * (ctx->net.N + 1), n2 = (size_t)ctx->net.n * ctx->net.n;
+    if (u) CK(cudaMemcpyAsync(u, ctx->u, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+    if (res) CK(cudaMemcpyAsync(res, ctx->res, sizeof(float) * n2, cudaMemcpyDeviceToHost, ctx->stream));
+    if (q) CK(cudaMemcpyAsync(q, ctx->q, sizeof(float) * n2, cudaMemcpyDeviceToHost, ctx->stream));
+    if (gu) CK(cudaMemcpyAsync(gu, ctx->gu_lat, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CRVPINN_OK;
+}
+
+int crvpinn_get_params(crvpinn_ctx *ctx, float *theta) {
+    if (!ctx || !theta) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(theta, ctx->theta, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CRVPINN_OK;
+}
+
+int crvpinn_set_params(crvpinn_ctx *ctx, const float *theta) {
+    if (!ctx || !theta) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(ctx->theta, theta, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CRVPINN_OK;
+}
+
+int crvpinn_get_adam(crvpinn_ctx *ctx, float *m, float *v, int64_t *t) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    CK(cudaSetDevice(ctx->device));
+    if (m) CK(cudaMemcpyAsync(m, ctx->m, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
+    if (v) CK(cudaMemcpyAsync(v, ctx->v, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (t) *t = ctx->h_state->t;
+    return CRVPINN_OK;
+}
+
+int crvpinn_set_adam(crvpinn_ctx *ctx, const float *m, const float *v, int64_t t) {
+    if (!ctx || !m || !v || t < 0) return fail(ctx, CRVPINN_EINVAL, "bad argument");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(ctx->m, m, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->v, v, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    ctx->h_state->t = t;
+    CK(cudaMemcpy(ctx->st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice));
+    return CRVPINN_OK;
+}
+
+int crvpinn_set_profiling(crvpinn_ctx *ctx, int on) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((bool)on != ctx->profiling) {
+        drop_graphs(ctx);
+        ctx->profiling = on != 0;
+    }
+    return CRVPINN_OK;
+}
+
+int crvpinn_get_profile(crvpinn_ctx *ctx, double *ms_sum, int64_t *n_iters, int reset) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    if (ms_sum) for (int s = 0; s < 4; ++s) ms_sum[s] = ctx->prof_ms[s];
+    if (n_iters) *n_iters = ctx->prof_iters;
+    if (reset) {
+        for (int s = 0; s < 4; ++s) ctx->prof_ms[s] = 0.0;
+        ctx->prof_iters = 0;
+    }
+    return CRVPINN_OK;
+}
+
+}  // extern "C"

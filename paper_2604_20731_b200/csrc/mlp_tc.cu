@@ -1,0 +1,799 @@
+// mlp_tc.cu -- A1 and A6/A7 on the 5th-generation tensor cores (tcgen05 + TMEM), sm_100a.
+//
+// The network PINN(x,y) = 16x(1-x)y(1-y) net_theta(x,y) (readings R5/R6) is
+// evaluated over all P = N^2 MLP points in tiles of 128 points. Every hidden-to-hidden layer
+// is a 128 x WP x WP GEMM on tcgen05.mma kind::f16 with fp32 accumulators in TMEM:
+//  * forward (k_tc_forward, all layers fused per tile): activations t are split t = hi + lo
+//    with hi = fp16(t), lo = fp16(t - hi), and Z = T_hi W^T + T_lo W^T (2 MMAs) -- the
+//    activation rounding of a single 10-bit-mantissa pass is what breaks loss parity at 512^2
+//    (SURVEY.md key finding 4); weights are rounded once to fp16 (10-bit mantissa, as TF32).
+//    Epilogue warps read TMEM, add bias, apply tanh, split, write the next A operand into
+//    shared memory (SWIZZLE_128B K-major) and stream t_hi to HBM with bulk copies.
+//  * backward: Delta_{a} = (Delta_{a+1} W) (.) (1 - t_a^2) on tcgen05 (k_tc_dx, one layer per
+//    launch, W^T streamed as the B operand), and dW = sum_p Delta^T t as a split-K tcgen05
+//    GEMM over points with MN-major operands read straight from the stored tiles (k_tc_dw).
+//    Delta is stored in fp16 after a power-of-two scaling of dLOSS/dnet (DevState::gscale)
+//    so that it stays in fp16's normal range; partial sums are unscaled in the reduction.
+// Weights are streamed into shared memory by cp.async.bulk (the TMA engine) from fp16 copies
+// that k_tc_refresh re-lays out after every Adam step (zero-padded to WP = 64*ceil(w/64)).
+#include "mlp_tc.cuh"
+#include "tc_ptx.cuh"
+#include "../../include/crvpinn.h"
+#include <math.h>
+
+namespace crv {
+
+using namespace ptx;
+
+constexpr uint32_t CHUNK_BYTES = 128 * 128;   // one tile-chunk block: 128 rows x 128 B
+constexpr int CHUNK_HALVES = 128 * 64;
+constexpr int NST_W = 2;                      // weight ring stages
+constexpr int EPI_THREADS = 256;              // 8 epilogue warps
+constexpr int TC_THREADS = 64 + EPI_THREADS;  // producer warp + MMA warp + epilogue
+
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+    return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+// byte offset of element (r, f%64) inside a tile-chunk block
+__device__ __forceinline__ uint32_t blk_off(int r, int f) {
+    return (uint32_t)(r * 128 + ((((f & 63) >> 3) ^ (r & 7)) << 4) + ((f & 7) << 1));
+}
+
+// Butterfly reduce-scatter: on entry v[k] is this lane's value for column k (0..31); on exit
+// v[0] holds the sum over the warp's 32 lanes of column `lane`.
+__device__ __forceinline__ void warp_reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            float send = upper ? v[i] : v[i + s];
+            float keep = upper ? v[i + s] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+}
+
+// ================================================================ forward
+struct FwdArgs {
+    int N, ntiles, L, G;
+    const __half *Wf;      // [G][KC] blocks
+    const float *W1p, *bp, *Wop;
+    __half *act;           // [L][ntiles][KC] blocks
+    float *u;              // lattice (N+1)^2
+};
+
+template <int WP>
+__host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 256) * 4 +
+           16 * 8 + 16;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
+    constexpr int KC = WP / 64;
+    constexpr uint32_t WBLK = WP * 128;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *A_hi = smem;
+    uint8_t *A_lo = A_hi + KC * CHUNK_BYTES;
+    uint8_t *Wr = A_lo + KC * CHUNK_BYTES;
+    float *sW1 = (float *)(Wr + NST_W * WBLK);
+    float *sB = sW1 + 2 * WP;
+    float *sWo = sB + a.L * WP;          // WP + 1 (bias last)
+    float *sRed = sWo + WP + 1;          // 256
+    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 256) + 7) & ~(uintptr_t)7);
+    uint64_t *w_full = bars, *w_empty = bars + NST_W, *a_full = bars + 2 * NST_W, *acc_full = a_full + 1;
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
+    for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
+    for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST_W; ++s) {
+            mbar_init(&w_full[s], 1);
+            mbar_init(&w_empty[s], 1);
+        }
+        mbar_init(a_full, 1);
+        mbar_init(acc_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, WP);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer: weight K-chunks through the ring (bulk copies)
+        if (lane == 0 && a.G > 0) {
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
+                for (int g = 0; g < a.G; ++g)
+                    for (int c = 0; c < KC; ++c) {
+                        mbar_wait(&w_empty[stage], ph ^ 1);
+                        mbar_arrive_expect_tx(&w_full[stage], WBLK);
+                        bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.Wf + (size_t)(g * KC + c) * WBLK, WBLK,
+                                 &w_full[stage]);
+                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                    }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread)
+        if (lane == 0 && a.G > 0) {
+            constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
+            int stage = 0;
+            uint32_t ph = 0, aph = 0;
+            const uint32_t ahi = smem_u32(A_hi), alo = smem_u32(A_lo), wr = smem_u32(Wr);
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
+                for (int g = 0; g < a.G; ++g) {
+                    mbar_wait(a_full, aph);
+                    aph ^= 1;
+                    tc_fence_after();
+                    for (int c = 0; c < KC; ++c) {
+                        mbar_wait(&w_full[stage], ph);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
+                            uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                            uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                            mma_f16(tmem, dh, bd, idesc, (c | kk) != 0);
+                            mma_f16(tmem, dl, bd, idesc, 1u);
+                        }
+                        mma_commit(&w_empty[stage]);
+                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                    }
+                    mma_commit(acc_full);
+                }
+        }
+    } else {
+        // ---------------- epilogue: 8 warps; warp%4 selects the TMEM lane quarter (= rows)
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int hf = (warp - 2) >> 2;         // column half
+        constexpr int HALF = WP / 2;
+        const int col0 = hf * HALF;
+        const int ep_tid = threadIdx.x - 64;
+        const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+        uint32_t acc_ph = 0;
+        const int N = a.N;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+            const int p = tile * 128 + row;
+            int pi, pj;
+            point_ij(p, N, pi, pj);
+            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            float dot = 0.0f;
+            for (int layer = 1; layer <= a.L; ++layer) {
+                const bool last = layer == a.L;
+                if (layer > 1) {
+                    mbar_wait(acc_full, acc_ph);
+                    acc_ph ^= 1;
+                    tc_fence_after();
+                }
+                // previous bulk store must have finished reading A_hi before it is rewritten
+                if (ep_tid == 0) bulk_wait_read0();
+                named_bar(1, EPI_THREADS);
+                const float *bias = sB + (layer - 1) * WP;
+#pragma unroll 1
+                for (int cc = col0; cc < col0 + HALF; cc += 32) {
+                    float v[32];
+                    if (layer == 1) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            v[k] = fmaf(sW1[2 * (cc + k)], x, fmaf(sW1[2 * (cc + k) + 1], y, bias[cc + k]));
+                    } else {
+                        tmem_ld32(t_lane + cc, v);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) v[k] += bias[cc + k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = tanh_fast(v[k]);
+                    if (last) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) dot = fmaf(sWo[cc + k], v[k], dot);
+                    }
+                    const int c = cc >> 6;
+                    const uint32_t base_hi = smem_u32(A_hi) + c * CHUNK_BYTES + row * 128;
+                    const uint32_t base_lo = smem_u32(A_lo) + c * CHUNK_BYTES + row * 128;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int lg = ((cc & 63) >> 3) + j;
+                        const uint32_t off = (uint32_t)((lg ^ (row & 7)) << 4);
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            float t0 = v[8 * j + 2 * m], t1 = v[8 * j + 2 * m + 1];
+                            __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
+                            __half2 hh = __halves2half2(h0, h1);
+                            hw[m] = *reinterpret_cast<uint32_t *>(&hh);
+                            lw[m] = pack_half2(t0 - __half2float(h0), t1 - __half2float(h1));
+                        }
+                        st_shared_v4(base_hi + off, hw[0], hw[1], hw[2], hw[3]);
+                        if (!last) st_shared_v4(base_lo + off, lw[0], lw[1], lw[2], lw[3]);
+                    }
+                }
+                tc_fence_before();
+                fence_proxy_async_smem();
+                named_bar(1, EPI_THREADS);
+                if (ep_tid == 0) {
+                    __half *dst = a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES);
+                    bulk_s2g(dst, A_hi, KC * CHUNK_BYTES);
+                    bulk_commit();
+                    if (!last) mbar_arrive(a_full);
+                }
+            }
+            // output layer: net = W_out t_L + b_out; u = cutoff * net
+            sRed[hf * 128 + row] = dot;
+            named_bar(1, EPI_THREADS);
+            if (hf == 0) {
+                float net = dot + sRed[128 + row] + sWo[WP];
+                a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
+            }
+        }
+        if (ep_tid == 0) bulk_wait0();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, WP);
+}
+
+// ================================================================ backward: output layer
+// Delta_L = s * gbar * W_out (.) (1 - t_L^2) (fp16, tile-chunk format), with
+// s = 2^(7 - ceil(log2 max|gbar|)) so max|s gbar| is in (64, 128].
+// Partials per block: [WP] sum s*gbar*t_L (dW_out) | [WP] sum Delta_L (db) | [1] sum s*gbar (db_out).
+__device__ __forceinline__ float grad_scale(const DevState *st) {
+    float gm = __uint_as_float(st->gmax_bits);
+    if (!(gm > 0.0f) || !isfinite(gm)) return 1.0f;
+    int e = (int)ceilf(log2f(gm));
+    return exp2f((float)(7 - e));
+}
+
+__global__ void k_tc_out_bwd(int WP, int KC, int ntiles, const __half *__restrict__ actL,
+                             const float *__restrict__ gbar, const float *__restrict__ Wop,
+                             __half *__restrict__ deltaL, float *__restrict__ partial, DevState *st) {
+    __shared__ float sg[128];
+    const int f = threadIdx.x;          // feature (blockDim.x == WP)
+    const float s = grad_scale(st);
+    if (blockIdx.x == 0 && f == 0) {
+        st->gscale = s;
+        st->inv_gscale = 1.0f / s;
+    }
+    const float wo = Wop[f];
+    float acc_w = 0.0f, acc_b = 0.0f, acc_g = 0.0f;
+    const int c = f >> 6;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        for (int r = f; r < 128; r += blockDim.x) sg[r] = gbar[tile * 128 + r] * s;
+        __syncthreads();
+        const size_t base = ((size_t)tile * KC + c) * CHUNK_HALVES;
+        const uint8_t *src = (const uint8_t *)(actL + base);
+        uint8_t *dst = (uint8_t *)(deltaL + base);
+#pragma unroll 4
+        for (int r = 0; r < 128; ++r) {
+            const uint32_t off = blk_off(r, f);
+            const float t = __half2float(*(const __half *)(src + off));
+            const float g = sg[r];
+            const float d = g * wo * (1.0f - t * t);
+            *(__half *)(dst + off) = __float2half_rn(d);
+            acc_w = fmaf(g, t, acc_w);
+            acc_b += d;
+            if (f == 0) acc_g += g;
+        }
+    }
+    float *pb = partial + (size_t)blockIdx.x * (2 * WP + 1);
+    pb[f] = acc_w;
+    pb[WP + f] = acc_b;
+    if (f == 0) pb[2 * WP] = acc_g;
+}
+
+// ================================================================ backward: dX GEMM
+// Delta_in = (Delta_out W) (.) (1 - t_in^2): A = Delta_out tile (K = out features), B = W^T
+// blocks (rows = in features), epilogue in place on the t_in tile, bulk-stored to delta_in.
+// Column sums of Delta_in (bias gradient; for the first layer also weighted by x and y) are
+// reduced per CTA. Partial layout per CTA: [2*WP] (x,y)-weighted sums interleaved | [WP] sums.
+struct DxArgs {
+    int N, ntiles, first;
+    const __half *dout;   // Delta_{a+1}  [ntiles][KC] blocks
+    const __half *tin;    // t_a          [ntiles][KC]
+    __half *din;          // Delta_a      [ntiles][KC]
+    const __half *WTf;    // [KC] blocks of W^T
+    float *partial;       // [grid][3*WP]
+};
+
+template <int WP>
+__host__ __device__ constexpr uint32_t dx_smem_bytes() {
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + 4 * 3 * WP * 4 + 16 * 8 + 16;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
+    constexpr int KC = WP / 64;
+    constexpr uint32_t WBLK = WP * 128;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *A = smem;
+    uint8_t *T = A + KC * CHUNK_BYTES;
+    uint8_t *Wr = T + KC * CHUNK_BYTES;
+    float *sRed = (float *)(Wr + NST_W * WBLK);    // [4][3*WP]
+    uint64_t *bars = (uint64_t *)(sRed + 4 * 3 * WP);
+    uint64_t *w_full = bars, *w_empty = bars + NST_W;
+    uint64_t *ab_full = bars + 2 * NST_W, *ab_empty = ab_full + 1, *acc_full = ab_full + 2,
+             *acc_empty = ab_full + 3;
+    uint32_t *tmem_slot = (uint32_t *)(acc_empty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST_W; ++s) {
+            mbar_init(&w_full[s], 1);
+            mbar_init(&w_empty[s], 1);
+        }
+        mbar_init(ab_full, 1);
+        mbar_init(ab_empty, 1);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, WP);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t TILE_BYTES = KC * CHUNK_BYTES;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t ph = 0, abph = 0;
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+                mbar_wait(ab_empty, abph ^ 1);
+                abph ^= 1;
+                mbar_arrive_expect_tx(ab_full, 2 * TILE_BYTES);
+                bulk_g2s(A, (const uint8_t *)a.dout + (size_t)tile * TILE_BYTES, TILE_BYTES, ab_full);
+                bulk_g2s(T, (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES, TILE_BYTES, ab_full);
+                for (int c = 0; c < KC; ++c) {
+                    mbar_wait(&w_empty[stage], ph ^ 1);
+                    mbar_arrive_expect_tx(&w_full[stage], WBLK);
+                    bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.WTf + (size_t)c * WBLK, WBLK, &w_full[stage]);
+                    if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
+            int stage = 0;
+            uint32_t ph = 0, abph = 0, eph = 0;
+            const uint32_t as = smem_u32(A), wr = smem_u32(Wr);
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+                mbar_wait(ab_full, abph);
+                abph ^= 1;
+                mbar_wait(acc_empty, eph ^ 1);
+                eph ^= 1;
+                tc_fence_after();
+                for (int c = 0; c < KC; ++c) {
+                    mbar_wait(&w_full[stage], ph);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint64_t ad = sdesc_sw128(as + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                        uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
+                        mma_f16(tmem, ad, bd, idesc, (c | kk) != 0);
+                    }
+                    mma_commit(&w_empty[stage]);
+                    if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                }
+                mma_commit(acc_full);
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int hf = (warp - 2) >> 2;
+        constexpr int HALF = WP / 2;
+        constexpr int NCH = HALF / 32;
+        const int col0 = hf * HALF;
+        const int ep_tid = threadIdx.x - 64;
+        const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+        float cs[NCH], csx[NCH], csy[NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) cs[k] = csx[k] = csy[k] = 0.0f;
+        uint32_t acc_ph = 0;
+        const int N = a.N;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+            int pi, pj;
+            point_ij(tile * 128 + row, N, pi, pj);
+            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            mbar_wait(acc_full, acc_ph);
+            acc_ph ^= 1;
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const int cc = col0 + 32 * k;
+                float v[32];
+                tmem_ld32(t_lane + cc, v);
+                const uint32_t base = smem_u32(T) + (cc >> 6) * CHUNK_BYTES + row * 128;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int lg = ((cc & 63) >> 3) + j;
+                    const uint32_t addr = base + (uint32_t)((lg ^ (row & 7)) << 4);
+                    uint32_t w[4];
+                    ld_shared_v4(addr, w[0], w[1], w[2], w[3]);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        __half2 th = *reinterpret_cast<__half2 *>(&w[m]);
+                        float2 tf = __half22float2(th);
+                        v[8 * j + 2 * m] *= (1.0f - tf.x * tf.x);
+                        v[8 * j + 2 * m + 1] *= (1.0f - tf.y * tf.y);
+                        w[m] = pack_half2(v[8 * j + 2 * m], v[8 * j + 2 * m + 1]);
+                    }
+                    st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+                }
+                if (a.first) {
+                    float vx[32], vy[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
+                    warp_reduce_scatter32(vx, lane);
+                    warp_reduce_scatter32(vy, lane);
+                    csx[k] += vx[0];
+                    csy[k] += vy[0];
+                }
+                warp_reduce_scatter32(v, lane);
+                cs[k] += v[0];
+            }
+            tc_fence_before();
+            fence_proxy_async_smem();
+            named_bar(1, EPI_THREADS);
+            if (ep_tid == 0) {
+                mbar_arrive(acc_empty);
+                bulk_s2g((uint8_t *)a.din + (size_t)tile * TILE_BYTES, T, TILE_BYTES);
+                bulk_commit();
+                bulk_wait_read0();
+                mbar_arrive(ab_empty);
+            }
+        }
+        // combine the 4 row quarters (fixed order) and write this CTA's partial
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int col = col0 + 32 * k + lane;
+            sRed[(q * 3 + 0) * WP + col] = csx[k];
+            sRed[(q * 3 + 1) * WP + col] = csy[k];
+            sRed[(q * 3 + 2) * WP + col] = cs[k];
+        }
+        named_bar(1, EPI_THREADS);
+        float *pb = a.partial + (size_t)blockIdx.x * 3 * WP;
+        for (int col = ep_tid; col < WP; col += EPI_THREADS) {
+            float sx = 0.f, sy = 0.f, sb = 0.f;
+            for (int qq = 0; qq < 4; ++qq) {
+                sx += sRed[(qq * 3 + 0) * WP + col];
+                sy += sRed[(qq * 3 + 1) * WP + col];
+                sb += sRed[(qq * 3 + 2) * WP + col];
+            }
+            pb[2 * col] = sx;
+            pb[2 * col + 1] = sy;
+            pb[2 * WP + col] = sb;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, WP);
+}
+
+// ================================================================ backward: dW GEMM (split-K)
+// dW_g[o][i] = sum_p Delta_{g+2}[p][o] t_{g+1}[p][i]: M = out features (MN-major A), N = in
+// features (MN-major B), K = points, in stages of 64 points (half tiles). CTA b handles layer
+// b / cpl and a contiguous range of half tiles; its fp32 partial is written transposed
+// ([i][o], coalesced TMEM read-out) to partial[b][WP*WP].
+struct DwArgs {
+    int ntiles, G, cpl;
+    const __half *delta;   // [L][ntiles][KC]
+    const __half *act;     // [L][ntiles][KC]
+    float *partial;        // [G*cpl][WP*WP]
+};
+
+constexpr int NST_DW = 3;
+constexpr int DW_THREADS = 192;
+
+template <int WP>
+__host__ __device__ constexpr int dw_kca() { return WP / 64 < 2 ? 2 : WP / 64; }
+
+template <int WP>
+__host__ __device__ constexpr uint32_t dw_smem_bytes() {
+    return 1024 + NST_DW * (dw_kca<WP>() + WP / 64) * 8192 + 16 * 8 + 16;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(DW_THREADS, 1) k_tc_dw(DwArgs a) {
+    constexpr int KC = WP / 64;
+    constexpr int KCA = dw_kca<WP>();           // A chunks per stage (>= 2 for M = 128)
+    constexpr int MH = WP > 128 ? 2 : 1;        // M halves of 128 out features
+    constexpr int TMCOLS = MH * WP;
+    constexpr uint32_t HBLK = 8192;             // 64 rows x 128 B
+    constexpr uint32_t STAGE = (KCA + KC) * HBLK;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint64_t *bars = (uint64_t *)(smem + NST_DW * STAGE);
+    uint64_t *full = bars, *empty = bars + NST_DW, *acc_full = bars + 2 * NST_DW;
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int layer = blockIdx.x / a.cpl, part = blockIdx.x % a.cpl;
+    const int nh = 2 * a.ntiles;
+    const int h0 = (int)((long)nh * part / a.cpl), h1 = (int)((long)nh * (part + 1) / a.cpl);
+    const size_t lay = (size_t)a.ntiles * KC * CHUNK_HALVES;
+    const uint8_t *dsrc = (const uint8_t *)(a.delta + (size_t)(layer + 1) * lay);   // Delta_{g+2}
+    const uint8_t *tsrc = (const uint8_t *)(a.act + (size_t)layer * lay);           // t_{g+1}
+    if (KCA > KC) {   // WP = 64: the upper 64 rows of M read zeros
+        for (int s = 0; s < NST_DW; ++s)
+            for (int i = threadIdx.x; i < (int)(HBLK / 16); i += blockDim.x)
+                ((uint4 *)(smem + s * STAGE + KC * HBLK))[i] = make_uint4(0, 0, 0, 0);
+        fence_proxy_async_smem();
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST_DW; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, TMCOLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int h = h0; h < h1; ++h) {
+                const int tile = h >> 1, half = h & 1;
+                mbar_wait(&empty[stage], ph ^ 1);
+                mbar_arrive_expect_tx(&full[stage], 2 * KC * HBLK);
+                uint8_t *st = smem + stage * STAGE;
+                for (int c = 0; c < KC; ++c) {
+                    const size_t blk = ((size_t)tile * KC + c) * CHUNK_BYTES + half * HBLK;
+                    bulk_g2s(st + c * HBLK, dsrc + blk, HBLK, &full[stage]);
+                    bulk_g2s(st + (KCA + c) * HBLK, tsrc + blk, HBLK, &full[stage]);
+                }
+                if (++stage == NST_DW) { stage = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, WP, 1, 1);
+            int stage = 0;
+            uint32_t ph = 0;
+            bool first = true;
+            for (int h = h0; h < h1; ++h) {
+                mbar_wait(&full[stage], ph);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + stage * STAGE);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t bd = sdesc_sw128(st + KCA * HBLK + kk * 2048, HBLK, 1024);
+#pragma unroll
+                    for (int mh = 0; mh < MH; ++mh) {
+                        const uint64_t ad = sdesc_sw128(st + (2 * mh) * HBLK + kk * 2048, HBLK, 1024);
+                        mma_f16(tmem + mh * WP, ad, bd, idesc, first ? 0u : 1u);
+                    }
+                    first = false;
+                }
+                mma_commit(&empty[stage]);
+                if (++stage == NST_DW) { stage = 0; ph ^= 1; }
+            }
+            mma_commit(acc_full);
+        }
+    } else {
+        // epilogue: 4 warps, warp%4 = TMEM lane quarter = out-feature quarter of each M half
+        const int q = warp & 3;
+        float *pb = a.partial + (size_t)blockIdx.x * WP * WP;
+        if (h1 > h0) {
+            mbar_wait(acc_full, 0);
+            tc_fence_after();
+        }
+#pragma unroll 1
+        for (int mh = 0; mh < MH; ++mh) {
+            const int o = mh * 128 + q * 32 + lane;
+#pragma unroll 1
+            for (int cc = 0; cc < WP; cc += 32) {
+                float v[32];
+                if (h1 > h0) {
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mh * WP + cc, v);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+                }
+                if (o < WP) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) pb[(size_t)(cc + k) * WP + o] = v[k];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, TMCOLS);
+}
+
+// ================================================================ weight re-layout
+// After each Adam step: fp16 copies of the hidden weights in the B-operand block layout
+// (forward: rows = out features; backward-dX: rows = in features), zero padded to WP.
+__global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float *__restrict__ theta,
+                             __half *__restrict__ Wf, __half *__restrict__ WTf, float *__restrict__ W1p,
+                             float *__restrict__ bp, float *__restrict__ Wop) {
+    const long nW = (long)G * WP * WP;
+    const long nsmall = 2L * WP + (long)L * WP + WP + 1;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nW + nsmall; e += (long)gridDim.x * blockDim.x) {
+        if (e < nW) {
+            const int g = (int)(e / ((long)WP * WP));
+            const int rem = (int)(e % ((long)WP * WP));
+            const int n = rem / WP, k = rem % WP;     // element (row n, K index k) of the block set
+            const int l = g + 1;                      // theta layer
+            const int wout = net.widths[l + 1], win = net.widths[l];
+            const float *W = theta + net.woff[l];
+            const float vf = (n < wout && k < win) ? W[(long)n * win + k] : 0.0f;   // W[n][k]
+            const float vt = (k < wout && n < win) ? W[(long)k * win + n] : 0.0f;   // W^T[n][k]
+            const size_t blk = ((size_t)g * KC + (k >> 6)) * (size_t)WP * 64;
+            const uint32_t off = (uint32_t)(n * 64 + ((((k & 63) >> 3) ^ (n & 7)) << 3) + (k & 7));
+            Wf[blk + off] = __float2half_rn(vf);
+            WTf[blk + off] = __float2half_rn(vt);
+        } else {
+            long s = e - nW;
+            if (s < 2L * WP) {
+                const int r = (int)(s >> 1), d = (int)(s & 1);
+                W1p[s] = r < net.widths[1] ? theta[net.woff[0] + 2 * r + d] : 0.0f;
+            } else if ((s -= 2L * WP) < (long)L * WP) {
+                const int l = (int)(s / WP), r = (int)(s % WP);
+                bp[s] = r < net.widths[l + 1] ? theta[net.boff[l] + r] : 0.0f;
+            } else {
+                s -= (long)L * WP;
+                if (s < WP) Wop[s] = s < net.widths[L] ? theta[net.woff[L] + s] : 0.0f;
+                else Wop[WP] = theta[net.boff[L]];
+            }
+        }
+    }
+}
+
+// ================================================================ host side
+template <int WP>
+static void set_attrs(int L) {
+    cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
+    cudaFuncSetAttribute(k_tc_dx<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dx_smem_bytes<WP>());
+    cudaFuncSetAttribute(k_tc_dw<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes<WP>());
+}
+
+int tc_create(const Net &net, TcBufs &b, std::string &err) {
+    const int L = net.nl - 1;
+    int w = net.widths[1];
+    b.WP = ((w + 63) / 64) * 64;
+    b.KC = b.WP / 64;
+    b.L = L;
+    b.G = L - 1;
+    b.ntiles = net.P / 128;
+    const int WP = b.WP, KC = b.KC, G = b.G;
+    if (fwd_smem_bytes<256>(L) > 232448 && WP == 256) {
+        err = "too many layers for the shared-memory budget of the fused forward";
+        return CRVPINN_EINVAL;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
+    b.grid_dx = b.grid_fwd;
+    b.grid_ob = b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm;
+    b.dw_cpl = G > 0 ? (nsm / G > 0 ? nsm / G : 1) : 0;
+    if (b.dw_cpl > 2 * b.ntiles) b.dw_cpl = 2 * b.ntiles;
+    auto al = [&](void **p, size_t bytes) -> bool {
+        if (cudaMalloc(p, bytes > 0 ? bytes : 16) != cudaSuccess) return false;
+        cudaMemset(*p, 0, bytes > 0 ? bytes : 16);
+        return true;
+    };
+    const size_t wblocks = (size_t)(G > 0 ? G : 1) * KC * WP * 64;
+    const size_t actn = (size_t)L * b.ntiles * KC * CHUNK_HALVES;
+    b.off_ob = 0;
+    b.off_dx = b.off_ob + (long)b.grid_ob * (2 * WP + 1);
+    b.off_dw = b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP;
+    const long ptotal = b.off_dw + (long)(G > 0 ? G * b.dw_cpl : 1) * WP * WP;
+    if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
+        !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
+        !al((void **)&b.Wop, (WP + 1) * 4) || !al((void **)&b.act, actn * 2) || !al((void **)&b.delta, actn * 2) ||
+        !al((void **)&b.gbar, (size_t)net.P * 4) || !al((void **)&b.partial, ptotal * 4)) {
+        err = "cudaMalloc failed for the tensor-core buffers";
+        return CRVPINN_ENOMEM;
+    }
+    // reduction jobs (all partials are in gscale units -> scaled = 1)
+    RedJob jobs[2 * CRV_MAX_LAYERS];
+    int nj = 0;
+    b.max_count = 0;
+    auto job = [&](long src, long dst, int count, int nsplit, long stride, int transposed, int cols, int ld) {
+        RedJob &j = jobs[nj++];
+        j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
+        j.transposed = transposed; j.cols = cols; j.ld = ld; j.scaled = 1;
+        if (count > b.max_count) b.max_count = count;
+    };
+    const int nl = net.nl;
+    for (int l = 0; l < nl; ++l) {
+        const int win = net.widths[l], wout = net.widths[l + 1];
+        if (l == nl - 1) {   // output layer: from k_tc_out_bwd
+            job(b.off_ob, net.woff[l], win, b.grid_ob, 2 * WP + 1, 0, 1, 1);
+            job(b.off_ob + 2 * WP, net.boff[l], 1, b.grid_ob, 2 * WP + 1, 0, 1, 1);
+            continue;
+        }
+        // bias of theta layer l <-> Delta_{l+1}: from out_bwd (l = L-1) or dx(g = l)
+        if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1);
+        else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1);
+        if (l == 0) {
+            if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
+        } else {
+            job(b.off_dw + (long)(l - 1) * b.dw_cpl * WP * WP, net.woff[l], wout * win, b.dw_cpl, (long)WP * WP, 1,
+                win, WP);
+        }
+    }
+    if (G == 0) {
+        err = "the tensor-core path needs at least two hidden layers";
+        return CRVPINN_EINVAL;
+    }
+    b.njobs = nj;
+    if (!al((void **)&b.jobs, sizeof(RedJob) * nj)) {
+        err = "cudaMalloc failed";
+        return CRVPINN_ENOMEM;
+    }
+    cudaMemcpy(b.jobs, jobs, sizeof(RedJob) * nj, cudaMemcpyHostToDevice);
+    if (WP == 64) set_attrs<64>(L);
+    else if (WP == 128) set_attrs<128>(L);
+    else if (WP == 192) { err = "hidden width 160/192 not supported by the tensor path"; return CRVPINN_EINVAL; }
+    else set_attrs<256>(L);
+    b.ready = 1;
+    return CRVPINN_OK;
+}
+
+void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s) {
+    const long total = (long)b.G * b.WP * b.WP + 2L * b.WP + (long)b.L * b.WP + b.WP + 1;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    k_tc_refresh<<<blocks, 256, 0, s>>>(net, b.WP, b.KC, b.G, b.L, theta, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
+}
+
+template <int WP>
+static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
+    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u};
+    k_tc_forward<WP><<<b.grid_fwd, TC_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+}
+
+void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
+    if (b.WP == 64) fwd_launch<64>(net, b, u, s);
+    else if (b.WP == 128) fwd_launch<128>(net, b, u, s);
+    else fwd_launch<256>(net, b, u, s);
+}
+
+template <int WP>
+static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
+    const size_t lay = (size_t)b.ntiles * b.KC * CHUNK_HALVES;
+    const int L = b.L;
+    k_tc_out_bwd<<<b.grid_ob, WP, 0, s>>>(WP, b.KC, b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+                                          b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
+    for (int g = b.G - 1; g >= 0; --g) {
+        DxArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.delta + (size_t)(g + 1) * lay, b.act + (size_t)g * lay,
+                 b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
+                 b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP};
+        k_tc_dx<WP><<<b.grid_dx, TC_THREADS, dx_smem_bytes<WP>(), s>>>(a);
+    }
+    DwArgs d{b.ntiles, b.G, b.dw_cpl, b.delta, b.act, b.partial + b.off_dw};
+    k_tc_dw<WP><<<b.G * b.dw_cpl, DW_THREADS, dw_smem_bytes<WP>(), s>>>(d);
+    launch_reduce(b.partial, grad, b.jobs, b.njobs, b.max_count, st, s);
+}
+
+void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
+    if (b.WP == 64) bwd_launch<64>(net, b, st, grad, s);
+    else if (b.WP == 128) bwd_launch<128>(net, b, st, grad, s);
+    else bwd_launch<256>(net, b, st, grad, s);
+}
+
+int tc_launches(const Net &net) {
+    const int G = net.nl - 2;
+    return 1 /*fwd*/ + 1 /*out_bwd*/ + G /*dx*/ + 1 /*dw*/ + 1 /*reduce*/ + 1 /*refresh*/;
+}
+
+}  // namespace crv

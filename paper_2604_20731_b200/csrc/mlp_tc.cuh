@@ -1,0 +1,39 @@
+// mlp_tc.cuh -- tensor-core (tcgen05/TMEM) MLP path, CRVPINN_PREC_TENSOR.
+#pragma once
+#include "common.cuh"
+#include <cuda_fp16.h>
+#include <string>
+
+namespace crv {
+
+// Activation / delta storage ("tile-chunk" format): for hidden layer a, tile t
+// (128 MLP points) and feature chunk c (64 features), one 16 KiB block holding 128 rows x 64
+// fp16 in the UMMA SWIZZLE_128B K-major layout: element (r, f) at byte
+// r*128 + (((f%64)/8) ^ (r%8))*16 + (f%8)*2. The same bytes are a valid MN-major operand
+// (features contiguous), which the weight-gradient GEMM uses.
+struct TcBufs {
+    int ready = 0;
+    int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0;
+    __half *Wf = nullptr;    // [G][KC] blocks of WP rows x 128 B: B operand of the forward GEMMs
+    __half *WTf = nullptr;   // [G][KC] blocks: B operand of the backward-dX GEMMs (W^T)
+    float *W1p = nullptr;    // [WP][2]   first layer (zero padded)
+    float *bp = nullptr;     // [L][WP]   hidden biases (zero padded)
+    float *Wop = nullptr;    // [WP + 1]  output weights, output bias at [WP]
+    __half *act = nullptr;   // [L][ntiles][KC][128*64]
+    __half *delta = nullptr; // [L][ntiles][KC][128*64]  (scaled by DevState::gscale)
+    float *gbar = nullptr;   // [P] dLOSS/dnet (unscaled)
+    float *partial = nullptr;
+    long off_ob = 0, off_dx = 0, off_dw = 0;
+    int grid_ob = 0, grid_dx = 0, grid_fwd = 0, dw_cpl = 0;
+    RedJob *jobs = nullptr;  // device copy
+    int njobs = 0, max_count = 0;
+    const float *theta = nullptr;
+};
+
+int tc_create(const Net &net, TcBufs &b, std::string &err);
+void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
+void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
+void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
+int tc_launches(const Net &net);
+
+}  // namespace crv
