@@ -34,7 +34,7 @@ struct Net {
 };
 
 // Job of the deterministic partial-sum reducer: dst[o] = scale * sum_{z<nsplit} src[z*stride + off(o)],
-// o < count, off(o) = o, or (transposed) (o % cols) * ld + o / cols.
+// o < count, off(o) = o (transposed = 0), (o % cols) * ld + o / cols (1), (o / cols) * ld + o % cols (2).
 struct RedJob {
     long src;      // offset in the partial buffer
     long dst;      // offset in the gradient vector
@@ -79,9 +79,15 @@ void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int nj
                    const DevState *st, cudaStream_t s);
 int loss_partial_blocks(int n2);
 // gram.cu
-void gram_init_constants(float *S, float *lam, int N, cudaStream_t s);
-void launch_gram_apply(const float *res, float *q, const float *S, const float *lam, float *w1,
-                       float *w2, int N, cudaStream_t s);
+struct GramConsts {
+    float2 *tw = nullptr;   // FFT twiddles exp(-2 pi i k / 2N), k < N
+    float *etab = nullptr;  // per-mode Thomas pivots 1/w_j, [n][n]
+    float *work = nullptr;  // 2 n^2 scratch
+    int logM = 0, seg = 0;
+};
+GramConsts gram_make_constants(int N);
+void gram_free_constants(GramConsts &c);
+void launch_gram_apply(const float *res, float *q, const GramConsts &c, int N, cudaStream_t s);
 // mlp_simt.cu -- fp32 FFMA MLP path (CRVPINN_PREC_FP32)
 struct MlpPlan {
     long offW[CRV_MAX_LAYERS], offB[CRV_MAX_LAYERS];   // partial-buffer offsets per layer

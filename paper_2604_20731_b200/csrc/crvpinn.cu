@@ -35,7 +35,7 @@ struct crvpinn_ctx {
     // fields
     float *K = nullptr, *S = nullptr, *f = nullptr, *alpha = nullptr, *b = nullptr;
     float *u = nullptr, *res = nullptr, *q = nullptr, *gu_lat = nullptr;
-    float *gS = nullptr, *glam = nullptr, *gw1 = nullptr, *gw2 = nullptr;
+    GramConsts gram{};
     double *loss_part = nullptr;
     int loss_nblk = 0;
     DevState *st = nullptr, *snap_st = nullptr;
@@ -112,7 +112,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
     // A2-A5: residual, Gram solve, loss, adjoint
     int n = net.n;
     launch_residual(ctx->u, ctx->alpha, ctx->b, ctx->res, net.N, s);
-    launch_gram_apply(ctx->res, ctx->q, ctx->gS, ctx->glam, ctx->gw1, ctx->gw2, net.N, s);
+    launch_gram_apply(ctx->res, ctx->q, ctx->gram, net.N, s);
     launch_loss_partials(ctx->res, ctx->q, ctx->loss_part, n * n, ctx->loss_nblk, s);
     launch_loss_final(ctx->loss_part, ctx->loss_nblk, ctx->st, hist, n_hist,
                       train ? ctx->opts.beta1 : -1.0, ctx->opts.beta2, s);
@@ -136,7 +136,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
 static int launches_per_iter(const crvpinn_ctx *ctx) {
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
     int mlp = tc ? tc_launches(ctx->net) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
-    return mlp + 1 /*residual*/ + 4 /*gram*/ + 2 /*loss*/ + 1 /*adjoint*/ + 1 /*adam*/;
+    return mlp + 1 /*residual*/ + 3 /*gram*/ + 2 /*loss*/ + 1 /*adjoint*/ + 1 /*adam*/;
 }
 
 static void drop_graphs(crvpinn_ctx *ctx) {
@@ -240,6 +240,7 @@ void crvpinn_destroy(crvpinn_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
+    gram_free_constants(ctx->gram);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_field) cudaFreeHost(ctx->h_field);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
@@ -281,8 +282,8 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     DALLOC(ctx->K, nn); DALLOC(ctx->S, nn); DALLOC(ctx->f, nn);
     DALLOC(ctx->alpha, nn); DALLOC(ctx->b, nn); DALLOC(ctx->u, nn); DALLOC(ctx->gu_lat, nn);
     DALLOC(ctx->res, (long)n * n); DALLOC(ctx->q, (long)n * n);
-    DALLOC(ctx->gS, (long)n * n); DALLOC(ctx->glam, n);
-    DALLOC(ctx->gw1, (long)n * n); DALLOC(ctx->gw2, (long)n * n);
+    ctx->gram = gram_make_constants(N);
+    if (!ctx->gram.etab || !ctx->gram.work) return fail(ctx, CRVPINN_ENOMEM, "Gram constants allocation failed");
     ctx->loss_nblk = loss_partial_blocks(n * n);
     DALLOC(ctx->loss_part, ctx->loss_nblk);
     DALLOC(ctx->st, 1); DALLOC(ctx->snap_st, 1);
@@ -329,7 +330,6 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     CK(cudaMemcpy(ctx->f, f, sizeof(float) * nn, cudaMemcpyHostToDevice));
     launch_alpha(ctx->K, ctx->S, ctx->alpha, N, (float)ctx->opts.mobility_ratio, ctx->stream);
     launch_scale_b(ctx->f, ctx->b, N, ctx->stream);
-    gram_init_constants(ctx->gS, ctx->glam, N, ctx->stream);
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());

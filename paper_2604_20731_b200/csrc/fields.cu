@@ -181,10 +181,19 @@ __global__ void k_reduce(const float *__restrict__ partial, float *__restrict__ 
     RedJob jb = jobs[blockIdx.y];
     int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= jb.count) return;
-    long off = jb.transposed ? (long)(o % jb.cols) * jb.ld + (o / jb.cols) : (long)o;
+    long off = jb.transposed == 1 ? (long)(o % jb.cols) * jb.ld + (o / jb.cols)
+             : jb.transposed == 2 ? (long)(o / jb.cols) * jb.ld + (o % jb.cols) : (long)o;
     const float *src = partial + jb.src + off;
     float s = 0.0f;
-    for (int z = 0; z < jb.nsplit; ++z) s += src[(long)z * jb.stride];
+    int z = 0;
+    for (; z + 8 <= jb.nsplit; z += 8) {   // 8 independent loads in flight, summed in z order
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (long)(z + k) * jb.stride);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    for (; z < jb.nsplit; ++z) s += src[(long)z * jb.stride];
     grad[jb.dst + o] = jb.scaled ? s * st->inv_gscale : s;
 }
 

@@ -67,9 +67,13 @@ struct FwdArgs {
 template <int WP>
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
     return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 256) * 4 +
-           16 * 8 + 16;
+           32 * 8 + 16;
 }
 
+// Pipelining: two TMEM accumulators (GEMMs alternate), and per-64-feature-chunk
+// barriers a_full[c]: the epilogue producing activation t_a chunk c releases it to the MMA of the
+// next GEMM immediately, so that GEMM runs under the rest of the epilogue. All 8 epilogue warps
+// work on the same chunk at a time (warp pair sharing a TMEM lane quarter splits its 64 columns).
 template <int WP>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
     constexpr int KC = WP / 64;
@@ -84,8 +88,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
     float *sWo = sB + a.L * WP;          // WP + 1 (bias last)
     float *sRed = sWo + WP + 1;          // 256
     uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 256) + 7) & ~(uintptr_t)7);
-    uint64_t *w_full = bars, *w_empty = bars + NST_W, *a_full = bars + 2 * NST_W, *acc_full = a_full + 1;
-    uint32_t *tmem_slot = (uint32_t *)(acc_full + 1);
+    uint64_t *w_full = bars, *w_empty = bars + NST_W;
+    uint64_t *a_full = bars + 2 * NST_W;          // [KC]
+    uint64_t *acc_full = a_full + KC;             // [2]
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
@@ -96,11 +102,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
-        mbar_init(a_full, 1);
-        mbar_init(acc_full, 1);
+        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], EPI_THREADS / 32);
+        mbar_init(&acc_full[0], 1);
+        mbar_init(&acc_full[1], 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, WP);
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -127,13 +134,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
             int stage = 0;
             uint32_t ph = 0, aph = 0;
+            int gi = 0;   // running GEMM counter -> accumulator gi & 1
             const uint32_t ahi = smem_u32(A_hi), alo = smem_u32(A_lo), wr = smem_u32(Wr);
             for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
-                for (int g = 0; g < a.G; ++g) {
-                    mbar_wait(a_full, aph);
-                    aph ^= 1;
-                    tc_fence_after();
+                for (int g = 0; g < a.G; ++g, ++gi) {
+                    const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
                     for (int c = 0; c < KC; ++c) {
+                        mbar_wait(&a_full[c], aph);
                         mbar_wait(&w_full[stage], ph);
                         tc_fence_after();
 #pragma unroll
@@ -141,25 +148,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                             uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
                             uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
                             uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                            mma_f16(tmem, dh, bd, idesc, (c | kk) != 0);
-                            mma_f16(tmem, dl, bd, idesc, 1u);
+                            mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
+                            mma_f16(acc, dl, bd, idesc, 1u);
                         }
                         mma_commit(&w_empty[stage]);
                         if (++stage == NST_W) { stage = 0; ph ^= 1; }
                     }
-                    mma_commit(acc_full);
+                    aph ^= 1;
+                    mma_commit(&acc_full[gi & 1]);
                 }
         }
     } else {
-        // ---------------- epilogue: 8 warps; warp%4 selects the TMEM lane quarter (= rows)
+        // ---------------- epilogue: 8 warps; warp%4 selects the TMEM lane quarter (= rows),
+        // the two warps of a quarter split every 64-column chunk into halves of 32.
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int hf = (warp - 2) >> 2;         // column half
-        constexpr int HALF = WP / 2;
-        const int col0 = hf * HALF;
+        const int hf = (warp - 2) >> 2;
         const int ep_tid = threadIdx.x - 64;
         const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-        uint32_t acc_ph = 0;
+        uint32_t acc_ph[2] = {0u, 0u};
+        int gi = 0;
         const int N = a.N;
         for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
             const int p = tile * 128 + row;
@@ -169,24 +177,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             float dot = 0.0f;
             for (int layer = 1; layer <= a.L; ++layer) {
                 const bool last = layer == a.L;
+                uint32_t acc = 0;
                 if (layer > 1) {
-                    mbar_wait(acc_full, acc_ph);
-                    acc_ph ^= 1;
+                    const int ai = gi & 1;
+                    mbar_wait(&acc_full[ai], acc_ph[ai]);
+                    acc_ph[ai] ^= 1;
+                    acc = tmem + (uint32_t)(ai * WP);
+                    ++gi;
                     tc_fence_after();
                 }
-                // previous bulk store must have finished reading A_hi before it is rewritten
+                // the previous bulk store of A_hi must have finished reading it
                 if (ep_tid == 0) bulk_wait_read0();
                 named_bar(1, EPI_THREADS);
                 const float *bias = sB + (layer - 1) * WP;
 #pragma unroll 1
-                for (int cc = col0; cc < col0 + HALF; cc += 32) {
+                for (int c = 0; c < KC; ++c) {
+                    const int cc = c * 64 + hf * 32;
                     float v[32];
                     if (layer == 1) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k)
                             v[k] = fmaf(sW1[2 * (cc + k)], x, fmaf(sW1[2 * (cc + k) + 1], y, bias[cc + k]));
                     } else {
-                        tmem_ld32(t_lane + cc, v);
+                        tmem_ld32(t_lane + acc + cc, v);
 #pragma unroll
                         for (int k = 0; k < 32; ++k) v[k] += bias[cc + k];
                     }
@@ -196,12 +209,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k) dot = fmaf(sWo[cc + k], v[k], dot);
                     }
-                    const int c = cc >> 6;
                     const uint32_t base_hi = smem_u32(A_hi) + c * CHUNK_BYTES + row * 128;
                     const uint32_t base_lo = smem_u32(A_lo) + c * CHUNK_BYTES + row * 128;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int lg = ((cc & 63) >> 3) + j;
+                        const int lg = hf * 4 + j;
                         const uint32_t off = (uint32_t)((lg ^ (row & 7)) << 4);
                         uint32_t hw[4], lw[4];
 #pragma unroll
@@ -215,15 +227,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                         st_shared_v4(base_hi + off, hw[0], hw[1], hw[2], hw[3]);
                         if (!last) st_shared_v4(base_lo + off, lw[0], lw[1], lw[2], lw[3]);
                     }
+                    if (!last) {
+                        // release chunk c to the next GEMM
+                        tc_fence_before();
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&a_full[c]);
+                    }
                 }
-                tc_fence_before();
+                // stream t_hi of this layer to HBM (backward operand)
                 fence_proxy_async_smem();
                 named_bar(1, EPI_THREADS);
                 if (ep_tid == 0) {
                     __half *dst = a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES);
                     bulk_s2g(dst, A_hi, KC * CHUNK_BYTES);
                     bulk_commit();
-                    if (!last) mbar_arrive(a_full);
                 }
             }
             // output layer: net = W_out t_L + b_out; u = cutoff * net
@@ -238,7 +256,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, WP);
+    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
 }
 
 // ================================================================ backward: output layer
@@ -252,42 +270,83 @@ __device__ __forceinline__ float grad_scale(const DevState *st) {
     return exp2f((float)(7 - e));
 }
 
-__global__ void k_tc_out_bwd(int WP, int KC, int ntiles, const __half *__restrict__ actL,
-                             const float *__restrict__ gbar, const float *__restrict__ Wop,
-                             __half *__restrict__ deltaL, float *__restrict__ partial, DevState *st) {
+constexpr int OB_THREADS = 256;
+
+// Vectorised: thread T owns logical granule lg = T%8 (8 features) of chunk c = (T/8)%KC for the
+// rows r = rg, rg+NRG, ... (rg = T/(8 KC)); a warp covers whole 128-byte rows (coalesced).
+template <int WP>
+__global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __half *__restrict__ actL,
+                                                           const float *__restrict__ gbar,
+                                                           const float *__restrict__ Wop,
+                                                           __half *__restrict__ deltaL,
+                                                           float *__restrict__ partial, DevState *st) {
+    constexpr int KC = WP / 64;
+    constexpr int NRG = OB_THREADS / (8 * KC);   // row groups
+    constexpr int RPT = 128 / NRG;               // rows per thread per tile
     __shared__ float sg[128];
-    const int f = threadIdx.x;          // feature (blockDim.x == WP)
+    __shared__ float sred[2][NRG][WP];
+    __shared__ float sgsum[NRG];
+    const int T = threadIdx.x;
+    const int lg = T & 7, c = (T >> 3) % KC, rg = T / (8 * KC);
+    const int f0 = c * 64 + lg * 8;
     const float s = grad_scale(st);
-    if (blockIdx.x == 0 && f == 0) {
+    if (blockIdx.x == 0 && T == 0) {
         st->gscale = s;
         st->inv_gscale = 1.0f / s;
     }
-    const float wo = Wop[f];
-    float acc_w = 0.0f, acc_b = 0.0f, acc_g = 0.0f;
-    const int c = f >> 6;
+    float wo[8], aw[8], ab[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { wo[e] = Wop[f0 + e]; aw[e] = 0.0f; ab[e] = 0.0f; }
+    float ag = 0.0f;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
-        for (int r = f; r < 128; r += blockDim.x) sg[r] = gbar[tile * 128 + r] * s;
+        if (T < 128) sg[T] = gbar[tile * 128 + T] * s;
         __syncthreads();
-        const size_t base = ((size_t)tile * KC + c) * CHUNK_HALVES;
-        const uint8_t *src = (const uint8_t *)(actL + base);
-        uint8_t *dst = (uint8_t *)(deltaL + base);
+        const size_t base = ((size_t)tile * KC + c) * CHUNK_BYTES;
+        const uint8_t *src = (const uint8_t *)actL + base;
+        uint8_t *dst = (uint8_t *)deltaL + base;
 #pragma unroll 4
-        for (int r = 0; r < 128; ++r) {
-            const uint32_t off = blk_off(r, f);
-            const float t = __half2float(*(const __half *)(src + off));
+        for (int k = 0; k < RPT; ++k) {
+            const int r = rg + k * NRG;
+            const uint32_t off = (uint32_t)(r * 128 + ((lg ^ (r & 7)) << 4));
+            uint4 raw = *(const uint4 *)(src + off);
             const float g = sg[r];
-            const float d = g * wo * (1.0f - t * t);
-            *(__half *)(dst + off) = __float2half_rn(d);
-            acc_w = fmaf(g, t, acc_w);
-            acc_b += d;
-            if (f == 0) acc_g += g;
+            ag += g;
+            uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                float2 t = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
+                const float d0 = g * wo[2 * m] * (1.0f - t.x * t.x);
+                const float d1 = g * wo[2 * m + 1] * (1.0f - t.y * t.y);
+                aw[2 * m] = fmaf(g, t.x, aw[2 * m]);
+                aw[2 * m + 1] = fmaf(g, t.y, aw[2 * m + 1]);
+                ab[2 * m] += d0;
+                ab[2 * m + 1] += d1;
+                w[m] = pack_half2(d0, d1);
+            }
+            *(uint4 *)(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
+    // fixed-order combination over row groups
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        sred[0][rg][f0 + e] = aw[e];
+        sred[1][rg][f0 + e] = ab[e];
+    }
+    if (c == 0 && lg == 0) sgsum[rg] = ag;
+    __syncthreads();
     float *pb = partial + (size_t)blockIdx.x * (2 * WP + 1);
-    pb[f] = acc_w;
-    pb[WP + f] = acc_b;
-    if (f == 0) pb[2 * WP] = acc_g;
+    for (int f = T; f < WP; f += OB_THREADS) {
+        float sw = 0.0f, sb = 0.0f;
+        for (int q = 0; q < NRG; ++q) { sw += sred[0][q][f]; sb += sred[1][q][f]; }
+        pb[f] = sw;
+        pb[WP + f] = sb;
+    }
+    if (T == 0) {
+        float sgt = 0.0f;
+        for (int q = 0; q < NRG; ++q) sgt += sgsum[q];
+        pb[2 * WP] = sgt;
+    }
 }
 
 // ================================================================ backward: dX GEMM
@@ -607,8 +666,9 @@ __global__ void __launch_bounds__(DW_THREADS, 1) k_tc_dw(DwArgs a) {
                     for (int k = 0; k < 32; ++k) v[k] = 0.0f;
                 }
                 if (o < WP) {
+                    float4 *dst = (float4 *)(pb + (size_t)o * WP + cc);
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) pb[(size_t)(cc + k) * WP + o] = v[k];
+                    for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                 }
             }
         }
@@ -682,7 +742,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
     b.grid_dx = b.grid_fwd;
-    b.grid_ob = b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm;
+    b.grid_ob = b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm;
     b.dw_cpl = G > 0 ? (nsm / G > 0 ? nsm / G : 1) : 0;
     if (b.dw_cpl > 2 * b.ntiles) b.dw_cpl = 2 * b.ntiles;
     auto al = [&](void **p, size_t bytes) -> bool {
@@ -692,9 +752,10 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     };
     const size_t wblocks = (size_t)(G > 0 ? G : 1) * KC * WP * 64;
     const size_t actn = (size_t)L * b.ntiles * KC * CHUNK_HALVES;
+    auto up64 = [](long v) { return (v + 63) / 64 * 64; };   // 256-byte aligned regions (float4 stores)
     b.off_ob = 0;
-    b.off_dx = b.off_ob + (long)b.grid_ob * (2 * WP + 1);
-    b.off_dw = b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP;
+    b.off_dx = up64(b.off_ob + (long)b.grid_ob * (2 * WP + 1));
+    b.off_dw = up64(b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP);
     const long ptotal = b.off_dw + (long)(G > 0 ? G * b.dw_cpl : 1) * WP * WP;
     if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
         !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
@@ -727,7 +788,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         if (l == 0) {
             if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
         } else {
-            job(b.off_dw + (long)(l - 1) * b.dw_cpl * WP * WP, net.woff[l], wout * win, b.dw_cpl, (long)WP * WP, 1,
+            job(b.off_dw + (long)(l - 1) * b.dw_cpl * WP * WP, net.woff[l], wout * win, b.dw_cpl, (long)WP * WP, 2,
                 win, WP);
         }
     }
@@ -772,8 +833,8 @@ template <int WP>
 static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
     const size_t lay = (size_t)b.ntiles * b.KC * CHUNK_HALVES;
     const int L = b.L;
-    k_tc_out_bwd<<<b.grid_ob, WP, 0, s>>>(WP, b.KC, b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
-                                          b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
+    k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+                                                      b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
     for (int g = b.G - 1; g >= 0; --g) {
         DxArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.delta + (size_t)(g + 1) * lay, b.act + (size_t)g * lay,
                  b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
