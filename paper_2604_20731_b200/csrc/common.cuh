@@ -75,7 +75,8 @@ void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_l
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 void launch_begin_call(DevState *st, cudaStream_t s);
-void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int max_count,
+// total_groups = sum over jobs of ceil(count/32)
+void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s);
 int loss_partial_blocks(int n2);
 // gram.cu
@@ -95,7 +96,7 @@ struct MlpPlan {
     int cs_split;                                     // row chunks of the column reductions
     int rows_per;
     long partial_floats;
-    int njobs, max_count;
+    int njobs, max_count, groups;
     RedJob jobs[2 * CRV_MAX_LAYERS];
 };
 struct SimtBufs {

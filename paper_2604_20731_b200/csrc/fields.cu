@@ -176,31 +176,48 @@ void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_l
 }
 
 // ---------------------------------------------------------------- A7: deterministic reduction
-__global__ void k_reduce(const float *__restrict__ partial, float *__restrict__ grad,
-                         const RedJob *__restrict__ jobs, const DevState *st) {
-    RedJob jb = jobs[blockIdx.y];
-    int o = blockIdx.x * blockDim.x + threadIdx.x;
-    if (o >= jb.count) return;
-    long off = jb.transposed == 1 ? (long)(o % jb.cols) * jb.ld + (o / jb.cols)
-             : jb.transposed == 2 ? (long)(o / jb.cols) * jb.ld + (o % jb.cols) : (long)o;
-    const float *src = partial + jb.src + off;
+// One block per (job, group of 32 outputs). Warp w sums splits z = w, w+32, ... for the 32
+// outputs (lane = output, coalesced), with 4 independent loads in flight; the 32 warp sums are
+// then added in warp order. The summation order is fixed by (nsplit, output) only: deterministic.
+constexpr int RED_WARPS = 32;
+
+__global__ void __launch_bounds__(RED_WARPS * 32) k_reduce(const float *__restrict__ partial, float *__restrict__ grad,
+                                                           const RedJob *__restrict__ jobs, int njobs,
+                                                           const DevState *st) {
+    __shared__ float sh[RED_WARPS][33];
+    int j = 0, g = blockIdx.x;
+    while (j < njobs && g >= (jobs[j].count + 31) / 32) { g -= (jobs[j].count + 31) / 32; ++j; }
+    if (j >= njobs) return;
+    const RedJob jb = jobs[j];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int o = g * 32 + lane;
     float s = 0.0f;
-    int z = 0;
-    for (; z + 8 <= jb.nsplit; z += 8) {   // 8 independent loads in flight, summed in z order
-        float v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (long)(z + k) * jb.stride);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s += v[k];
+    if (o < jb.count) {
+        const long off = jb.transposed == 1 ? (long)(o % jb.cols) * jb.ld + (o / jb.cols)
+                       : jb.transposed == 2 ? (long)(o / jb.cols) * jb.ld + (o % jb.cols) : (long)o;
+        const float *src = partial + jb.src + off;
+        int z = warp;
+        for (; z + 3 * RED_WARPS < jb.nsplit; z += 4 * RED_WARPS) {
+            const float v0 = __ldg(src + (long)z * jb.stride);
+            const float v1 = __ldg(src + (long)(z + RED_WARPS) * jb.stride);
+            const float v2 = __ldg(src + (long)(z + 2 * RED_WARPS) * jb.stride);
+            const float v3 = __ldg(src + (long)(z + 3 * RED_WARPS) * jb.stride);
+            s += v0; s += v1; s += v2; s += v3;
+        }
+        for (; z < jb.nsplit; z += RED_WARPS) s += __ldg(src + (long)z * jb.stride);
     }
-    for (; z < jb.nsplit; ++z) s += src[(long)z * jb.stride];
-    grad[jb.dst + o] = jb.scaled ? s * st->inv_gscale : s;
+    sh[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && o < jb.count) {
+        float t = 0.0f;
+        for (int w = 0; w < RED_WARPS; ++w) t += sh[w][lane];
+        grad[jb.dst + o] = jb.scaled ? t * st->inv_gscale : t;
+    }
 }
 
-void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int max_count,
+void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s) {
-    dim3 grid(ceil_div(max_count, 256), njobs);
-    k_reduce<<<grid, 256, 0, s>>>(partial, grad, jobs, st);
+    k_reduce<<<total_groups, RED_WARPS * 32, 0, s>>>(partial, grad, jobs, njobs, st);
 }
 
 // ---------------------------------------------------------------- A8: Adam

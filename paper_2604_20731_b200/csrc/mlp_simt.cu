@@ -157,11 +157,13 @@ void simt_make_plan(const Net &net, MlpPlan &plan) {
     long off = 0;
     plan.njobs = 0;
     plan.max_count = 0;
+    plan.groups = 0;
     auto job = [&](long src, long dst, int count, int nsplit, long stride) {
         RedJob &j = plan.jobs[plan.njobs++];
         j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
         j.cols = 1; j.ld = 1; j.transposed = 0; j.scaled = 0;
         if (count > plan.max_count) plan.max_count = count;
+        plan.groups += (count + 31) / 32;
     };
     for (int l = 0; l < nl; ++l) {
         int win = net.widths[l], wout = net.widths[l + 1];
@@ -218,7 +220,7 @@ void simt_backward(const Net &net, const MlpPlan &plan, const float *theta, cons
     int w1 = net.widths[1];
     k_colsum<CS_FIRST><<<plan.cs_split, w1, 0, s>>>(dcur, w1, P, plan.rows_per, nullptr,
                                                     b.partial + plan.offW[0], b.partial + plan.offB[0], N);
-    launch_reduce(b.partial, grad, b.jobs, plan.njobs, plan.max_count, nullptr, s);
+    launch_reduce(b.partial, grad, b.jobs, plan.njobs, plan.groups, nullptr, s);
 }
 
 int simt_launches_bwd(const Net &net) { return 2 + 3 * (net.nl - 2) + 1 + 1; }

@@ -218,11 +218,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                         uint32_t hw[4], lw[4];
 #pragma unroll
                         for (int m = 0; m < 4; ++m) {
-                            float t0 = v[8 * j + 2 * m], t1 = v[8 * j + 2 * m + 1];
-                            __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
-                            __half2 hh = __halves2half2(h0, h1);
-                            hw[m] = *reinterpret_cast<uint32_t *>(&hh);
-                            lw[m] = pack_half2(t0 - __half2float(h0), t1 - __half2float(h1));
+                            // split t = hi + lo: hi = t with the low 13 mantissa bits cleared (exact in
+                            // fp16's 10-bit mantissa), lo = t - hi exactly in fp32, then rounded to fp16
+                            const float t0 = v[8 * j + 2 * m], t1 = v[8 * j + 2 * m + 1];
+                            const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
+                            const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
+                            hw[m] = pack_half2(h0, h1);
+                            lw[m] = pack_half2(t0 - h0, t1 - h1);
                         }
                         st_shared_v4(base_hi + off, hw[0], hw[1], hw[2], hw[3]);
                         if (!last) st_shared_v4(base_lo + off, lw[0], lw[1], lw[2], lw[3]);
@@ -350,10 +352,13 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
 }
 
 // ================================================================ backward: dX GEMM
-// Delta_in = (Delta_out W) (.) (1 - t_in^2): A = Delta_out tile (K = out features), B = W^T
-// blocks (rows = in features), epilogue in place on the t_in tile, bulk-stored to delta_in.
-// Column sums of Delta_in (bias gradient; for the first layer also weighted by x and y) are
-// reduced per CTA. Partial layout per CTA: [2*WP] (x,y)-weighted sums interleaved | [WP] sums.
+// Delta_in = (Delta_out W) (.) (1 - t_in^2): A = Delta_out tile (K = out features, bulk-loaded
+// into a 2-slot ring so the next tile streams in under the current MMA/epilogue), B = W^T blocks
+// (rows = in features, streamed), two TMEM accumulators (the next tile's MMA runs under the
+// current epilogue). The epilogue reads t_in and writes Delta_in (fp16) straight from registers
+// to HBM at the tile-chunk positions. Column sums of Delta_in (bias gradient; for the first layer
+// also weighted by x and y) are reduced per CTA with warp reduce-scatter butterflies.
+// Partial layout per CTA: [2*WP] (x,y)-weighted sums interleaved | [WP] sums.
 struct DxArgs {
     int N, ntiles, first;
     const __half *dout;   // Delta_{a+1}  [ntiles][KC] blocks
@@ -372,46 +377,47 @@ template <int WP>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
     constexpr int KC = WP / 64;
     constexpr uint32_t WBLK = WP * 128;
+    constexpr uint32_t TILE_BYTES = KC * CHUNK_BYTES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *A = smem;
-    uint8_t *T = A + KC * CHUNK_BYTES;
-    uint8_t *Wr = T + KC * CHUNK_BYTES;
-    float *sRed = (float *)(Wr + NST_W * WBLK);    // [4][3*WP]
+    uint8_t *Aring = smem;                          // 2 slots
+    uint8_t *Wr = Aring + 2 * TILE_BYTES;
+    float *sRed = (float *)(Wr + NST_W * WBLK);     // [4][3*WP]
     uint64_t *bars = (uint64_t *)(sRed + 4 * 3 * WP);
     uint64_t *w_full = bars, *w_empty = bars + NST_W;
-    uint64_t *ab_full = bars + 2 * NST_W, *ab_empty = ab_full + 1, *acc_full = ab_full + 2,
-             *acc_empty = ab_full + 3;
-    uint32_t *tmem_slot = (uint32_t *)(acc_empty + 1);
+    uint64_t *a_full = bars + 2 * NST_W, *a_empty = a_full + 2, *acc_full = a_full + 4, *acc_empty = a_full + 6;
+    uint32_t *tmem_slot = (uint32_t *)(acc_empty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST_W; ++s) {
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
-        mbar_init(ab_full, 1);
-        mbar_init(ab_empty, 1);
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 1);
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], EPI_THREADS / 32);
+        }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, WP);
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t TILE_BYTES = KC * CHUNK_BYTES;
 
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
-            uint32_t ph = 0, abph = 0;
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-                mbar_wait(ab_empty, abph ^ 1);
-                abph ^= 1;
-                mbar_arrive_expect_tx(ab_full, 2 * TILE_BYTES);
-                bulk_g2s(A, (const uint8_t *)a.dout + (size_t)tile * TILE_BYTES, TILE_BYTES, ab_full);
-                bulk_g2s(T, (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES, TILE_BYTES, ab_full);
+            uint32_t ph = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+                const int slot = it & 1;
+                mbar_wait(&a_empty[slot], ((it >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&a_full[slot], TILE_BYTES);
+                bulk_g2s(Aring + slot * TILE_BYTES, (const uint8_t *)a.dout + (size_t)tile * TILE_BYTES, TILE_BYTES,
+                         &a_full[slot]);
                 for (int c = 0; c < KC; ++c) {
                     mbar_wait(&w_empty[stage], ph ^ 1);
                     mbar_arrive_expect_tx(&w_full[stage], WBLK);
@@ -424,27 +430,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
             int stage = 0;
-            uint32_t ph = 0, abph = 0, eph = 0;
-            const uint32_t as = smem_u32(A), wr = smem_u32(Wr);
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-                mbar_wait(ab_full, abph);
-                abph ^= 1;
-                mbar_wait(acc_empty, eph ^ 1);
-                eph ^= 1;
+            uint32_t ph = 0;
+            int it = 0;
+            const uint32_t as = smem_u32(Aring), wr = smem_u32(Wr);
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+                const int slot = it & 1;
+                const uint32_t par = (it >> 1) & 1;
+                mbar_wait(&a_full[slot], par);
+                mbar_wait(&acc_empty[slot], par ^ 1);
                 tc_fence_after();
+                const uint32_t acc = tmem + (uint32_t)(slot * WP);
                 for (int c = 0; c < KC; ++c) {
                     mbar_wait(&w_full[stage], ph);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        uint64_t ad = sdesc_sw128(as + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                        uint64_t ad = sdesc_sw128(as + slot * TILE_BYTES + c * CHUNK_BYTES + kk * 32, 16, 1024);
                         uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
-                        mma_f16(tmem, ad, bd, idesc, (c | kk) != 0);
+                        mma_f16(acc, ad, bd, idesc, (c | kk) != 0);
                     }
                     mma_commit(&w_empty[stage]);
                     if (++stage == NST_W) { stage = 0; ph ^= 1; }
                 }
-                mma_commit(acc_full);
+                mma_commit(&a_empty[slot]);
+                mma_commit(&acc_full[slot]);
             }
         }
     } else {
@@ -459,36 +468,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
         float cs[NCH], csx[NCH], csy[NCH];
 #pragma unroll
         for (int k = 0; k < NCH; ++k) cs[k] = csx[k] = csy[k] = 0.0f;
-        uint32_t acc_ph = 0;
         const int N = a.N;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        int it = 0;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+            const int slot = it & 1;
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
-            mbar_wait(acc_full, acc_ph);
-            acc_ph ^= 1;
+            const uint8_t *trow = (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES + row * 128;
+            uint8_t *drow = (uint8_t *)a.din + (size_t)tile * TILE_BYTES + row * 128;
+            mbar_wait(&acc_full[slot], (it >> 1) & 1);
             tc_fence_after();
+            const uint32_t acc = t_lane + (uint32_t)(slot * WP);
 #pragma unroll
             for (int k = 0; k < NCH; ++k) {
                 const int cc = col0 + 32 * k;
-                float v[32];
-                tmem_ld32(t_lane + cc, v);
-                const uint32_t base = smem_u32(T) + (cc >> 6) * CHUNK_BYTES + row * 128;
+                const uint32_t cbase = (cc >> 6) * CHUNK_BYTES;
+                uint4 tg[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int lg = ((cc & 63) >> 3) + j;
-                    const uint32_t addr = base + (uint32_t)((lg ^ (row & 7)) << 4);
-                    uint32_t w[4];
-                    ld_shared_v4(addr, w[0], w[1], w[2], w[3]);
+                    tg[j] = __ldg((const uint4 *)(trow + cbase + ((lg ^ (row & 7)) << 4)));
+                }
+                float v[32];
+                tmem_ld32(acc + cc, v);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t w[4] = {tg[j].x, tg[j].y, tg[j].z, tg[j].w};
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
-                        __half2 th = *reinterpret_cast<__half2 *>(&w[m]);
-                        float2 tf = __half22float2(th);
+                        float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
                         v[8 * j + 2 * m] *= (1.0f - tf.x * tf.x);
                         v[8 * j + 2 * m + 1] *= (1.0f - tf.y * tf.y);
                         w[m] = pack_half2(v[8 * j + 2 * m], v[8 * j + 2 * m + 1]);
                     }
-                    st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+                    const int lg = ((cc & 63) >> 3) + j;
+                    *(uint4 *)(drow + cbase + ((lg ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
                 }
                 if (a.first) {
                     float vx[32], vy[32];
@@ -503,15 +518,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
                 cs[k] += v[0];
             }
             tc_fence_before();
-            fence_proxy_async_smem();
-            named_bar(1, EPI_THREADS);
-            if (ep_tid == 0) {
-                mbar_arrive(acc_empty);
-                bulk_s2g((uint8_t *)a.din + (size_t)tile * TILE_BYTES, T, TILE_BYTES);
-                bulk_commit();
-                bulk_wait_read0();
-                mbar_arrive(ab_empty);
-            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[slot]);
         }
         // combine the 4 row quarters (fixed order) and write this CTA's partial
 #pragma unroll
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, WP);
+    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
 }
 
 // ================================================================ backward: dW GEMM (split-K)
@@ -768,11 +776,13 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     RedJob jobs[2 * CRV_MAX_LAYERS];
     int nj = 0;
     b.max_count = 0;
+    b.groups = 0;
     auto job = [&](long src, long dst, int count, int nsplit, long stride, int transposed, int cols, int ld) {
         RedJob &j = jobs[nj++];
         j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
         j.transposed = transposed; j.cols = cols; j.ld = ld; j.scaled = 1;
         if (count > b.max_count) b.max_count = count;
+        b.groups += (count + 31) / 32;
     };
     const int nl = net.nl;
     for (int l = 0; l < nl; ++l) {
@@ -843,7 +853,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
     }
     DwArgs d{b.ntiles, b.G, b.dw_cpl, b.delta, b.act, b.partial + b.off_dw};
     k_tc_dw<WP><<<b.G * b.dw_cpl, DW_THREADS, dw_smem_bytes<WP>(), s>>>(d);
-    launch_reduce(b.partial, grad, b.jobs, b.njobs, b.max_count, st, s);
+    launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
 }
 
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {

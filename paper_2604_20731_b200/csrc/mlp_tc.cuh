@@ -26,7 +26,7 @@ struct TcBufs {
     long off_ob = 0, off_dx = 0, off_dw = 0;
     int grid_ob = 0, grid_dx = 0, grid_fwd = 0, dw_cpl = 0;
     RedJob *jobs = nullptr;  // device copy
-    int njobs = 0, max_count = 0;
+    int njobs = 0, max_count = 0, groups = 0;
     const float *theta = nullptr;
 };
 
