@@ -75,7 +75,8 @@ void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_l
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 void launch_begin_call(DevState *st, cudaStream_t s);
-// total_groups = sum over jobs of ceil(count/32)
+// total_groups = reduce_groups(host copy of jobs)
+int reduce_groups(const RedJob *jobs, int njobs);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s);
 int loss_partial_blocks(int n2);

@@ -176,26 +176,54 @@ void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_l
 }
 
 // ---------------------------------------------------------------- A7: deterministic reduction
-// One block per (job, group of 32 outputs). Warp w sums splits z = w, w+32, ... for the 32
-// outputs (lane = output, coalesced), with 4 independent loads in flight; the 32 warp sums are
-// then added in warp order. The summation order is fixed by (nsplit, output) only: deterministic.
-constexpr int RED_WARPS = 32;
+// Blocks of 1024 threads. A job with few splits (nsplit <= 64: the weight-gradient GEMM partials)
+// is "wide": one thread per output, 8 independent loads in flight, summed in split order. A job
+// with many splits and few outputs (column-sum partials of the per-CTA kernels) is "deep": one
+// block per 32 outputs, warp w sums splits w, w+32, ..., then the 32 warp sums are added in warp
+// order. Either way the order depends only on (nsplit, output): deterministic.
+constexpr int RED_THREADS = 1024;
+constexpr int RED_WARPS = RED_THREADS / 32;
 
-__global__ void __launch_bounds__(RED_WARPS * 32) k_reduce(const float *__restrict__ partial, float *__restrict__ grad,
-                                                           const RedJob *__restrict__ jobs, int njobs,
-                                                           const DevState *st) {
+__host__ __device__ inline int red_groups(const RedJob &j) {
+    return j.nsplit <= 64 ? (j.count + RED_THREADS - 1) / RED_THREADS : (j.count + 31) / 32;
+}
+
+__device__ __forceinline__ long red_off(const RedJob &jb, int o) {
+    return jb.transposed == 1 ? (long)(o % jb.cols) * jb.ld + (o / jb.cols)
+         : jb.transposed == 2 ? (long)(o / jb.cols) * jb.ld + (o % jb.cols) : (long)o;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict__ partial, float *__restrict__ grad,
+                                                        const RedJob *__restrict__ jobs, int njobs,
+                                                        const DevState *st) {
     __shared__ float sh[RED_WARPS][33];
     int j = 0, g = blockIdx.x;
-    while (j < njobs && g >= (jobs[j].count + 31) / 32) { g -= (jobs[j].count + 31) / 32; ++j; }
+    while (j < njobs && g >= red_groups(jobs[j])) { g -= red_groups(jobs[j]); ++j; }
     if (j >= njobs) return;
     const RedJob jb = jobs[j];
+    const float sc = jb.scaled ? st->inv_gscale : 1.0f;
+    if (jb.nsplit <= 64) {
+        const int o = g * RED_THREADS + threadIdx.x;
+        if (o >= jb.count) return;
+        const float *src = partial + jb.src + red_off(jb, o);
+        float s = 0.0f;
+        int z = 0;
+        for (; z + 8 <= jb.nsplit; z += 8) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (long)(z + k) * jb.stride);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += v[k];
+        }
+        for (; z < jb.nsplit; ++z) s += __ldg(src + (long)z * jb.stride);
+        grad[jb.dst + o] = s * sc;
+        return;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int o = g * 32 + lane;
     float s = 0.0f;
     if (o < jb.count) {
-        const long off = jb.transposed == 1 ? (long)(o % jb.cols) * jb.ld + (o / jb.cols)
-                       : jb.transposed == 2 ? (long)(o / jb.cols) * jb.ld + (o % jb.cols) : (long)o;
-        const float *src = partial + jb.src + off;
+        const float *src = partial + jb.src + red_off(jb, o);
         int z = warp;
         for (; z + 3 * RED_WARPS < jb.nsplit; z += 4 * RED_WARPS) {
             const float v0 = __ldg(src + (long)z * jb.stride);
@@ -211,13 +239,19 @@ __global__ void __launch_bounds__(RED_WARPS * 32) k_reduce(const float *__restri
     if (warp == 0 && o < jb.count) {
         float t = 0.0f;
         for (int w = 0; w < RED_WARPS; ++w) t += sh[w][lane];
-        grad[jb.dst + o] = jb.scaled ? t * st->inv_gscale : t;
+        grad[jb.dst + o] = t * sc;
     }
+}
+
+int reduce_groups(const RedJob *jobs, int njobs) {
+    int gsum = 0;
+    for (int j = 0; j < njobs; ++j) gsum += red_groups(jobs[j]);
+    return gsum;
 }
 
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s) {
-    k_reduce<<<total_groups, RED_WARPS * 32, 0, s>>>(partial, grad, jobs, njobs, st);
+    k_reduce<<<total_groups, RED_THREADS, 0, s>>>(partial, grad, jobs, njobs, st);
 }
 
 // ---------------------------------------------------------------- A8: Adam

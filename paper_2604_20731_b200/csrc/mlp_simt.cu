@@ -163,7 +163,6 @@ void simt_make_plan(const Net &net, MlpPlan &plan) {
         j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
         j.cols = 1; j.ld = 1; j.transposed = 0; j.scaled = 0;
         if (count > plan.max_count) plan.max_count = count;
-        plan.groups += (count + 31) / 32;
     };
     for (int l = 0; l < nl; ++l) {
         int win = net.widths[l], wout = net.widths[l + 1];
@@ -192,6 +191,7 @@ void simt_make_plan(const Net &net, MlpPlan &plan) {
         }
     }
     plan.partial_floats = off;
+    plan.groups = reduce_groups(plan.jobs, plan.njobs);
 }
 
 void simt_backward(const Net &net, const MlpPlan &plan, const float *theta, const SimtBufs &b,

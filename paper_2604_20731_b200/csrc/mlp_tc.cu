@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
-        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], EPI_THREADS / 32);
+        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], EPI_THREADS);
         mbar_init(&acc_full[0], 1);
         mbar_init(&acc_full[1], 1);
         fence_mbar_init();
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
                 for (int g = 0; g < a.G; ++g)
                     for (int c = 0; c < KC; ++c) {
-                        mbar_wait(&w_empty[stage], ph ^ 1);
+                        mbar_wait_sleep(&w_empty[stage], ph ^ 1);
                         mbar_arrive_expect_tx(&w_full[stage], WBLK);
                         bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.Wf + (size_t)(g * KC + c) * WBLK, WBLK,
                                  &w_full[stage]);
@@ -196,18 +196,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                     float v[32];
                     if (layer == 1) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            v[k] = fmaf(sW1[2 * (cc + k)], x, fmaf(sW1[2 * (cc + k) + 1], y, bias[cc + k]));
+                        for (int k = 0; k < 32; k += 2) {
+                            const float4 w4 = *(const float4 *)(sW1 + 2 * (cc + k));
+                            const float2 b2 = *(const float2 *)(bias + cc + k);
+                            v[k] = fmaf(w4.x, x, fmaf(w4.y, y, b2.x));
+                            v[k + 1] = fmaf(w4.z, x, fmaf(w4.w, y, b2.y));
+                        }
                     } else {
                         tmem_ld32(t_lane + acc + cc, v);
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) v[k] += bias[cc + k];
+                        for (int k = 0; k < 32; k += 4) {
+                            const float4 b4 = *(const float4 *)(bias + cc + k);
+                            v[k] += b4.x; v[k + 1] += b4.y; v[k + 2] += b4.z; v[k + 3] += b4.w;
+                        }
                     }
 #pragma unroll
                     for (int k = 0; k < 32; ++k) v[k] = tanh_fast(v[k]);
                     if (last) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) dot = fmaf(sWo[cc + k], v[k], dot);
+                        for (int k = 0; k < 32; k += 4) {
+                            const float4 w4 = *(const float4 *)(sWo + cc + k);
+                            dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
+                        }
                     }
                     const uint32_t base_hi = smem_u32(A_hi) + c * CHUNK_BYTES + row * 128;
                     const uint32_t base_lo = smem_u32(A_lo) + c * CHUNK_BYTES + row * 128;
@@ -230,11 +240,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                         if (!last) st_shared_v4(base_lo + off, lw[0], lw[1], lw[2], lw[3]);
                     }
                     if (!last) {
-                        // release chunk c to the next GEMM
+                        // release chunk c to the next GEMM (every epilogue thread arrives)
                         tc_fence_before();
                         fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&a_full[c]);
+                        mbar_arrive(&a_full[c]);
                     }
                 }
                 // stream t_hi of this layer to HBM (backward operand)
@@ -686,6 +695,254 @@ __global__ void __launch_bounds__(DW_THREADS, 1) k_tc_dw(DwArgs a) {
     if (warp == 1) tmem_dealloc(tmem, TMCOLS);
 }
 
+// ================================================================ backward: fused layer (dX + dW)
+// One launch per hidden GEMM g: reads Delta_out (= Delta_{g+2}) and t_in (= t_{g+1}) ONCE and
+// produces both Delta_in = (Delta_out W) (.) (1 - t_in^2) and this CTA's share of
+// dW = sum_p Delta_out^T t_in. TMEM: dX accumulator (WP columns) + dW accumulator (WP columns,
+// M = 128 out features). For WP = 256 the 256 out features do not fit one CTA's TMEM next to
+// the dX accumulator, so CTAs work in PAIRS on the same tile sequence: CTA k of a pair owns dW
+// rows [128k, 128k+128) for every tile of the pair and computes dX for every other tile; the
+// second read of each tile is an L2 hit. For WP <= 128 (PF = 1) each CTA does everything.
+struct BwdArgs {
+    int N, ntiles, first, npairs;
+    const __half *dout;   // Delta_{g+2}  [ntiles][KC] blocks
+    const __half *tin;    // t_{g+1}      [ntiles][KC]
+    __half *din;          // Delta_{g+1}  [ntiles][KC]
+    const __half *WTf;    // [KC] blocks of W^T
+    float *part_dx;       // [grid][3*WP]   column sums (xy-weighted | plain)
+    float *part_dw;       // [npairs][WP*WP] rows = out features
+};
+
+template <int WP>
+__host__ __device__ constexpr int bwd_pf() { return WP > 128 ? 2 : 1; }
+
+template <int WP>
+__host__ __device__ constexpr uint32_t bwd_smem_bytes() {
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + (WP == 64 ? CHUNK_BYTES : 0) + NST_W * WP * 128 +
+           4 * 3 * WP * 4 + 16 * 8 + 16;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
+    constexpr int KC = WP / 64;
+    constexpr int PF = bwd_pf<WP>();
+    constexpr uint32_t WBLK = WP * 128;
+    constexpr uint32_t TILE_BYTES = KC * CHUNK_BYTES;
+    // Delta_out buffer is followed by a zero block when WP = 64 (dW M = 128 reads 2 chunks)
+    constexpr uint32_t ABUF = TILE_BYTES + (WP == 64 ? CHUNK_BYTES : 0);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *Ab = smem;
+    uint8_t *Tb = Ab + ABUF;
+    uint8_t *Wr = Tb + TILE_BYTES;
+    float *sRed = (float *)(Wr + NST_W * WBLK);
+    uint64_t *bars = (uint64_t *)(sRed + 4 * 3 * WP);
+    uint64_t *w_full = bars, *w_empty = bars + NST_W;
+    uint64_t *ld_full = bars + 2 * NST_W, *ld_empty = ld_full + 1, *acc_full = ld_full + 2,
+             *acc_empty = ld_full + 3, *dw_full = ld_full + 4;
+    uint32_t *tmem_slot = (uint32_t *)(dw_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = blockIdx.x / PF, kk_pf = blockIdx.x % PF;
+    if (WP == 64) {
+        for (int i = threadIdx.x; i < (int)(CHUNK_BYTES / 16); i += blockDim.x)
+            ((uint4 *)(Ab + TILE_BYTES))[i] = make_uint4(0, 0, 0, 0);
+        fence_proxy_async_smem();
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST_W; ++s) {
+            mbar_init(&w_full[s], 1);
+            mbar_init(&w_empty[s], 1);
+        }
+        mbar_init(ld_full, 1);
+        mbar_init(ld_empty, 1);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, EPI_THREADS / 32);
+        mbar_init(dw_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tm_dx = tmem, tm_dw = tmem + WP;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t ph = 0;
+            int i = 0;
+            for (int tile = pair; tile < a.ntiles; tile += a.npairs, ++i) {
+                mbar_wait_sleep(ld_empty, (i & 1) ^ 1);
+                mbar_arrive_expect_tx(ld_full, 2 * TILE_BYTES);
+                bulk_g2s(Ab, (const uint8_t *)a.dout + (size_t)tile * TILE_BYTES, TILE_BYTES, ld_full);
+                bulk_g2s(Tb, (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES, TILE_BYTES, ld_full);
+                if (i % PF == kk_pf) {
+                    for (int c = 0; c < KC; ++c) {
+                        mbar_wait(&w_empty[stage], ph ^ 1);
+                        mbar_arrive_expect_tx(&w_full[stage], WBLK);
+                        bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.WTf + (size_t)c * WBLK, WBLK, &w_full[stage]);
+                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc_dx = idesc_f16(128, WP, 0, 0);
+            constexpr uint32_t idesc_dw = idesc_f16(128, WP, 1, 1);
+            int stage = 0;
+            uint32_t ph = 0;
+            int i = 0, ndx = 0;
+            const uint32_t ab = smem_u32(Ab), tb = smem_u32(Tb), wr = smem_u32(Wr);
+            const uint32_t a_dw = ab + (uint32_t)(2 * kk_pf) * CHUNK_BYTES;   // out-feature chunks 2k, 2k+1
+            for (int tile = pair; tile < a.ntiles; tile += a.npairs, ++i) {
+                mbar_wait(ld_full, i & 1);
+                tc_fence_after();
+                // dW share: D[o][i] += sum_p Delta_out[p][o] t_in[p][i], K = 128 points (8 x 16)
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(a_dw + ks * 2048, CHUNK_BYTES, 1024);
+                    const uint64_t bd = sdesc_sw128(tb + ks * 2048, CHUNK_BYTES, 1024);
+                    mma_f16(tm_dw, ad, bd, idesc_dw, (i | ks) != 0);
+                }
+                if (i % PF == kk_pf) {
+                    mbar_wait(acc_empty, (ndx & 1) ^ 1);
+                    tc_fence_after();
+                    for (int c = 0; c < KC; ++c) {
+                        mbar_wait(&w_full[stage], ph);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kq = 0; kq < 4; ++kq) {
+                            const uint64_t ad = sdesc_sw128(ab + c * CHUNK_BYTES + kq * 32, 16, 1024);
+                            const uint64_t bd = sdesc_sw128(wr + stage * WBLK + kq * 32, 16, 1024);
+                            mma_f16(tm_dx, ad, bd, idesc_dx, (c | kq) != 0);
+                        }
+                        mma_commit(&w_empty[stage]);
+                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                    }
+                    mma_commit(acc_full);
+                    ++ndx;
+                }
+                mma_commit(ld_empty);
+            }
+            mma_commit(dw_full);
+        }
+    } else {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int hf = (warp - 2) >> 2;
+        constexpr int HALF = WP / 2;
+        constexpr int NCH = HALF / 32;
+        const int col0 = hf * HALF;
+        const int ep_tid = threadIdx.x - 64;
+        const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+        float cs[NCH], csx[NCH], csy[NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) cs[k] = csx[k] = csy[k] = 0.0f;
+        const int N = a.N;
+        int i = 0, ndx = 0;
+        for (int tile = pair; tile < a.ntiles; tile += a.npairs, ++i) {
+            if (i % PF != kk_pf) continue;
+            int pi, pj;
+            point_ij(tile * 128 + row, N, pi, pj);
+            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            const uint8_t *trow = (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES + row * 128;
+            uint8_t *drow = (uint8_t *)a.din + (size_t)tile * TILE_BYTES + row * 128;
+            mbar_wait(acc_full, ndx & 1);
+            ++ndx;
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < NCH; ++k) {
+                const int cc = col0 + 32 * k;
+                const uint32_t cbase = (cc >> 6) * CHUNK_BYTES;
+                uint4 tg[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int lg = ((cc & 63) >> 3) + j;
+                    tg[j] = __ldg((const uint4 *)(trow + cbase + ((lg ^ (row & 7)) << 4)));
+                }
+                float v[32];
+                tmem_ld32(tm_dx + t_lane + cc, v);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t w[4] = {tg[j].x, tg[j].y, tg[j].z, tg[j].w};
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
+                        v[8 * j + 2 * m] *= (1.0f - tf.x * tf.x);
+                        v[8 * j + 2 * m + 1] *= (1.0f - tf.y * tf.y);
+                        w[m] = pack_half2(v[8 * j + 2 * m], v[8 * j + 2 * m + 1]);
+                    }
+                    const int lg = ((cc & 63) >> 3) + j;
+                    *(uint4 *)(drow + cbase + ((lg ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                if (a.first) {
+                    float vx[32], vy[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
+                    warp_reduce_scatter32(vx, lane);
+                    warp_reduce_scatter32(vy, lane);
+                    csx[k] += vx[0];
+                    csy[k] += vy[0];
+                }
+                warp_reduce_scatter32(v, lane);
+                cs[k] += v[0];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+        }
+        // column-sum partials (fixed order over the 4 row quarters)
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int col = col0 + 32 * k + lane;
+            sRed[(q * 3 + 0) * WP + col] = csx[k];
+            sRed[(q * 3 + 1) * WP + col] = csy[k];
+            sRed[(q * 3 + 2) * WP + col] = cs[k];
+        }
+        named_bar(1, EPI_THREADS);
+        float *pb = a.part_dx + (size_t)blockIdx.x * 3 * WP;
+        for (int col = ep_tid; col < WP; col += EPI_THREADS) {
+            float sx = 0.f, sy = 0.f, sb = 0.f;
+            for (int qq = 0; qq < 4; ++qq) {
+                sx += sRed[(qq * 3 + 0) * WP + col];
+                sy += sRed[(qq * 3 + 1) * WP + col];
+                sb += sRed[(qq * 3 + 2) * WP + col];
+            }
+            pb[2 * col] = sx;
+            pb[2 * col + 1] = sy;
+            pb[2 * WP + col] = sb;
+        }
+        // dW share -> part_dw[pair][o][i] (rows o = 128k + lane quarter)
+        const bool any = pair < a.ntiles;
+        if (any) {
+            mbar_wait(dw_full, 0);
+            tc_fence_after();
+        }
+        const int o = kk_pf * 128 + row;
+        float *pw = a.part_dw + (size_t)pair * WP * WP;
+#pragma unroll 1
+        for (int cc = hf * HALF; cc < hf * HALF + HALF; cc += 32) {
+            float v[32];
+            if (any) {
+                tmem_ld32(tm_dw + t_lane + cc, v);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+            }
+            if (o < WP) {
+                float4 *dst = (float4 *)(pw + (size_t)o * WP + cc);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
+}
+
 // ================================================================ weight re-layout
 // After each Adam step: fp16 copies of the hidden weights in the B-operand block layout
 // (forward: rows = out features; backward-dX: rows = in features), zero padded to WP.
@@ -731,6 +988,7 @@ static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     cudaFuncSetAttribute(k_tc_dx<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dx_smem_bytes<WP>());
     cudaFuncSetAttribute(k_tc_dw<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes<WP>());
+    cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
 }
 
 int tc_create(const Net &net, TcBufs &b, std::string &err) {
@@ -749,7 +1007,13 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
-    b.grid_dx = b.grid_fwd;
+    {
+        const int PF = WP > 128 ? 2 : 1;
+        int np_ = nsm / PF;
+        if (np_ > b.ntiles) np_ = b.ntiles;
+        b.npairs = np_;
+        b.grid_dx = np_ * PF;
+    }
     b.grid_ob = b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm;
     b.dw_cpl = G > 0 ? (nsm / G > 0 ? nsm / G : 1) : 0;
     if (b.dw_cpl > 2 * b.ntiles) b.dw_cpl = 2 * b.ntiles;
@@ -764,7 +1028,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     b.off_ob = 0;
     b.off_dx = up64(b.off_ob + (long)b.grid_ob * (2 * WP + 1));
     b.off_dw = up64(b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP);
-    const long ptotal = b.off_dw + (long)(G > 0 ? G * b.dw_cpl : 1) * WP * WP;
+    const long ptotal = b.off_dw + (long)(G > 0 ? G * b.npairs : 1) * WP * WP;
     if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
         !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
         !al((void **)&b.Wop, (WP + 1) * 4) || !al((void **)&b.act, actn * 2) || !al((void **)&b.delta, actn * 2) ||
@@ -782,7 +1046,6 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
         j.transposed = transposed; j.cols = cols; j.ld = ld; j.scaled = 1;
         if (count > b.max_count) b.max_count = count;
-        b.groups += (count + 31) / 32;
     };
     const int nl = net.nl;
     for (int l = 0; l < nl; ++l) {
@@ -798,7 +1061,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         if (l == 0) {
             if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
         } else {
-            job(b.off_dw + (long)(l - 1) * b.dw_cpl * WP * WP, net.woff[l], wout * win, b.dw_cpl, (long)WP * WP, 2,
+            job(b.off_dw + (long)(l - 1) * b.npairs * WP * WP, net.woff[l], wout * win, b.npairs, (long)WP * WP, 2,
                 win, WP);
         }
     }
@@ -807,6 +1070,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         return CRVPINN_EINVAL;
     }
     b.njobs = nj;
+    b.groups = reduce_groups(jobs, nj);
     if (!al((void **)&b.jobs, sizeof(RedJob) * nj)) {
         err = "cudaMalloc failed";
         return CRVPINN_ENOMEM;
@@ -846,13 +1110,11 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
     k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
                                                       b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
     for (int g = b.G - 1; g >= 0; --g) {
-        DxArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.delta + (size_t)(g + 1) * lay, b.act + (size_t)g * lay,
-                 b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
-                 b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP};
-        k_tc_dx<WP><<<b.grid_dx, TC_THREADS, dx_smem_bytes<WP>(), s>>>(a);
+        BwdArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.npairs, b.delta + (size_t)(g + 1) * lay, b.act + (size_t)g * lay,
+                  b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
+                  b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP, b.partial + b.off_dw + (long)g * b.npairs * WP * WP};
+        k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
     }
-    DwArgs d{b.ntiles, b.G, b.dw_cpl, b.delta, b.act, b.partial + b.off_dw};
-    k_tc_dw<WP><<<b.G * b.dw_cpl, DW_THREADS, dw_smem_bytes<WP>(), s>>>(d);
     launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
 }
 
@@ -864,7 +1126,7 @@ void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cud
 
 int tc_launches(const Net &net) {
     const int G = net.nl - 2;
-    return 1 /*fwd*/ + 1 /*out_bwd*/ + G /*dx*/ + 1 /*dw*/ + 1 /*reduce*/ + 1 /*refresh*/;
+    return 1 /*fwd*/ + 1 /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
 }
 
 }  // namespace crv

@@ -144,10 +144,32 @@ __device__ __forceinline__ void ld_shared_v4(uint32_t saddr, uint32_t &a, uint32
     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(saddr));
 }
 
-// Accurate-enough tanh for the split forward: 1 - 2/(1+e^{2x}); |abs err| ~ 5e-7.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// tanh for the split forward: 1 - 2/(1+e^{2x}) with one MUFU.EX2 and one MUFU.RCP
+// (no range fix-ups: e^{2x} -> inf gives rcp 0 -> 1, e^{2x} -> 0 gives -1); |abs err| ~ 5e-7.
 __device__ __forceinline__ float tanh_fast(float x) {
-    float e = exp2f(x * 2.8853900817779268f);   // e^{2x}; ex2.approx
-    return 1.0f - __fdividef(2.0f, 1.0f + e);
+    const float e = ex2_approx(x * 2.8853900817779268f);
+    return fmaf(-2.0f, rcp_approx(1.0f + e), 1.0f);
+}
+// mbarrier wait with a suspend-time hint: the waiting thread sleeps in hardware instead of
+// spinning (used by the single-thread producer / MMA roles so they do not steal issue slots).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
 }
 
 }  // namespace ptx
