@@ -176,16 +176,19 @@ void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_l
 }
 
 // ---------------------------------------------------------------- A7: deterministic reduction
-// Blocks of 1024 threads. A job with few splits (nsplit <= 64: the weight-gradient GEMM partials)
-// is "wide": one thread per output, 8 independent loads in flight, summed in split order. A job
+// Blocks of 1024 threads. A job with few splits (nsplit <= 64) or many outputs (the weight-gradient
+// GEMM partials) is "wide": one thread per output, 8 independent loads in flight, summed in split order. A job
 // with many splits and few outputs (column-sum partials of the per-CTA kernels) is "deep": one
 // block per 32 outputs, warp w sums splits w, w+32, ..., then the 32 warp sums are added in warp
 // order. Either way the order depends only on (nsplit, output): deterministic.
 constexpr int RED_THREADS = 1024;
 constexpr int RED_WARPS = RED_THREADS / 32;
 
+// wide: few splits, or enough outputs to fill the GPU with one thread per output
+__host__ __device__ inline bool red_wide(const RedJob &j) { return j.nsplit <= 64 || j.count >= 8192; }
+
 __host__ __device__ inline int red_groups(const RedJob &j) {
-    return j.nsplit <= 64 ? (j.count + RED_THREADS - 1) / RED_THREADS : (j.count + 31) / 32;
+    return red_wide(j) ? (j.count + RED_THREADS - 1) / RED_THREADS : (j.count + 31) / 32;
 }
 
 __device__ __forceinline__ long red_off(const RedJob &jb, int o) {
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
     if (j >= njobs) return;
     const RedJob jb = jobs[j];
     const float sc = jb.scaled ? st->inv_gscale : 1.0f;
-    if (jb.nsplit <= 64) {
+    if (red_wide(jb)) {
         const int o = g * RED_THREADS + threadIdx.x;
         if (o >= jb.count) return;
         const float *src = partial + jb.src + red_off(jb, o);

@@ -360,341 +360,6 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
     }
 }
 
-// ================================================================ backward: dX GEMM
-// Delta_in = (Delta_out W) (.) (1 - t_in^2): A = Delta_out tile (K = out features, bulk-loaded
-// into a 2-slot ring so the next tile streams in under the current MMA/epilogue), B = W^T blocks
-// (rows = in features, streamed), two TMEM accumulators (the next tile's MMA runs under the
-// current epilogue). The epilogue reads t_in and writes Delta_in (fp16) straight from registers
-// to HBM at the tile-chunk positions. Column sums of Delta_in (bias gradient; for the first layer
-// also weighted by x and y) are reduced per CTA with warp reduce-scatter butterflies.
-// Partial layout per CTA: [2*WP] (x,y)-weighted sums interleaved | [WP] sums.
-struct DxArgs {
-    int N, ntiles, first;
-    const __half *dout;   // Delta_{a+1}  [ntiles][KC] blocks
-    const __half *tin;    // t_a          [ntiles][KC]
-    __half *din;          // Delta_a      [ntiles][KC]
-    const __half *WTf;    // [KC] blocks of W^T
-    float *partial;       // [grid][3*WP]
-};
-
-template <int WP>
-__host__ __device__ constexpr uint32_t dx_smem_bytes() {
-    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + 4 * 3 * WP * 4 + 16 * 8 + 16;
-}
-
-template <int WP>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_dx(DxArgs a) {
-    constexpr int KC = WP / 64;
-    constexpr uint32_t WBLK = WP * 128;
-    constexpr uint32_t TILE_BYTES = KC * CHUNK_BYTES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = align1024(smem_raw);
-    uint8_t *Aring = smem;                          // 2 slots
-    uint8_t *Wr = Aring + 2 * TILE_BYTES;
-    float *sRed = (float *)(Wr + NST_W * WBLK);     // [4][3*WP]
-    uint64_t *bars = (uint64_t *)(sRed + 4 * 3 * WP);
-    uint64_t *w_full = bars, *w_empty = bars + NST_W;
-    uint64_t *a_full = bars + 2 * NST_W, *a_empty = a_full + 2, *acc_full = a_full + 4, *acc_empty = a_full + 6;
-    uint32_t *tmem_slot = (uint32_t *)(acc_empty + 2);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NST_W; ++s) {
-            mbar_init(&w_full[s], 1);
-            mbar_init(&w_empty[s], 1);
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&a_full[s], 1);
-            mbar_init(&a_empty[s], 1);
-            mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], EPI_THREADS / 32);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t ph = 0;
-            int it = 0;
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-                const int slot = it & 1;
-                mbar_wait(&a_empty[slot], ((it >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&a_full[slot], TILE_BYTES);
-                bulk_g2s(Aring + slot * TILE_BYTES, (const uint8_t *)a.dout + (size_t)tile * TILE_BYTES, TILE_BYTES,
-                         &a_full[slot]);
-                for (int c = 0; c < KC; ++c) {
-                    mbar_wait(&w_empty[stage], ph ^ 1);
-                    mbar_arrive_expect_tx(&w_full[stage], WBLK);
-                    bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.WTf + (size_t)c * WBLK, WBLK, &w_full[stage]);
-                    if (++stage == NST_W) { stage = 0; ph ^= 1; }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
-            int stage = 0;
-            uint32_t ph = 0;
-            int it = 0;
-            const uint32_t as = smem_u32(Aring), wr = smem_u32(Wr);
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-                const int slot = it & 1;
-                const uint32_t par = (it >> 1) & 1;
-                mbar_wait(&a_full[slot], par);
-                mbar_wait(&acc_empty[slot], par ^ 1);
-                tc_fence_after();
-                const uint32_t acc = tmem + (uint32_t)(slot * WP);
-                for (int c = 0; c < KC; ++c) {
-                    mbar_wait(&w_full[stage], ph);
-                    tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        uint64_t ad = sdesc_sw128(as + slot * TILE_BYTES + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                        uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
-                        mma_f16(acc, ad, bd, idesc, (c | kk) != 0);
-                    }
-                    mma_commit(&w_empty[stage]);
-                    if (++stage == NST_W) { stage = 0; ph ^= 1; }
-                }
-                mma_commit(&a_empty[slot]);
-                mma_commit(&acc_full[slot]);
-            }
-        }
-    } else {
-        const int q = warp & 3;
-        const int row = q * 32 + lane;
-        const int hf = (warp - 2) >> 2;
-        constexpr int HALF = WP / 2;
-        constexpr int NCH = HALF / 32;
-        const int col0 = hf * HALF;
-        const int ep_tid = threadIdx.x - 64;
-        const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-        float cs[NCH], csx[NCH], csy[NCH];
-#pragma unroll
-        for (int k = 0; k < NCH; ++k) cs[k] = csx[k] = csy[k] = 0.0f;
-        const int N = a.N;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
-            const int slot = it & 1;
-            int pi, pj;
-            point_ij(tile * 128 + row, N, pi, pj);
-            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
-            const uint8_t *trow = (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES + row * 128;
-            uint8_t *drow = (uint8_t *)a.din + (size_t)tile * TILE_BYTES + row * 128;
-            mbar_wait(&acc_full[slot], (it >> 1) & 1);
-            tc_fence_after();
-            const uint32_t acc = t_lane + (uint32_t)(slot * WP);
-#pragma unroll
-            for (int k = 0; k < NCH; ++k) {
-                const int cc = col0 + 32 * k;
-                const uint32_t cbase = (cc >> 6) * CHUNK_BYTES;
-                uint4 tg[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int lg = ((cc & 63) >> 3) + j;
-                    tg[j] = __ldg((const uint4 *)(trow + cbase + ((lg ^ (row & 7)) << 4)));
-                }
-                float v[32];
-                tmem_ld32(acc + cc, v);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t w[4] = {tg[j].x, tg[j].y, tg[j].z, tg[j].w};
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
-                        v[8 * j + 2 * m] *= (1.0f - tf.x * tf.x);
-                        v[8 * j + 2 * m + 1] *= (1.0f - tf.y * tf.y);
-                        w[m] = pack_half2(v[8 * j + 2 * m], v[8 * j + 2 * m + 1]);
-                    }
-                    const int lg = ((cc & 63) >> 3) + j;
-                    *(uint4 *)(drow + cbase + ((lg ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-                }
-                if (a.first) {
-                    float vx[32], vy[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
-                    warp_reduce_scatter32(vx, lane);
-                    warp_reduce_scatter32(vy, lane);
-                    csx[k] += vx[0];
-                    csy[k] += vy[0];
-                }
-                warp_reduce_scatter32(v, lane);
-                cs[k] += v[0];
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[slot]);
-        }
-        // combine the 4 row quarters (fixed order) and write this CTA's partial
-#pragma unroll
-        for (int k = 0; k < NCH; ++k) {
-            const int col = col0 + 32 * k + lane;
-            sRed[(q * 3 + 0) * WP + col] = csx[k];
-            sRed[(q * 3 + 1) * WP + col] = csy[k];
-            sRed[(q * 3 + 2) * WP + col] = cs[k];
-        }
-        named_bar(1, EPI_THREADS);
-        float *pb = a.partial + (size_t)blockIdx.x * 3 * WP;
-        for (int col = ep_tid; col < WP; col += EPI_THREADS) {
-            float sx = 0.f, sy = 0.f, sb = 0.f;
-            for (int qq = 0; qq < 4; ++qq) {
-                sx += sRed[(qq * 3 + 0) * WP + col];
-                sy += sRed[(qq * 3 + 1) * WP + col];
-                sb += sRed[(qq * 3 + 2) * WP + col];
-            }
-            pb[2 * col] = sx;
-            pb[2 * col + 1] = sy;
-            pb[2 * WP + col] = sb;
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
-}
-
-// ================================================================ backward: dW GEMM (split-K)
-// dW_g[o][i] = sum_p Delta_{g+2}[p][o] t_{g+1}[p][i]: M = out features (MN-major A), N = in
-// features (MN-major B), K = points, in stages of 64 points (half tiles). CTA b handles layer
-// b / cpl and a contiguous range of half tiles; its fp32 partial is written transposed
-// ([i][o], coalesced TMEM read-out) to partial[b][WP*WP].
-struct DwArgs {
-    int ntiles, G, cpl;
-    const __half *delta;   // [L][ntiles][KC]
-    const __half *act;     // [L][ntiles][KC]
-    float *partial;        // [G*cpl][WP*WP]
-};
-
-constexpr int NST_DW = 3;
-constexpr int DW_THREADS = 192;
-
-template <int WP>
-__host__ __device__ constexpr int dw_kca() { return WP / 64 < 2 ? 2 : WP / 64; }
-
-template <int WP>
-__host__ __device__ constexpr uint32_t dw_smem_bytes() {
-    return 1024 + NST_DW * (dw_kca<WP>() + WP / 64) * 8192 + 16 * 8 + 16;
-}
-
-template <int WP>
-__global__ void __launch_bounds__(DW_THREADS, 1) k_tc_dw(DwArgs a) {
-    constexpr int KC = WP / 64;
-    constexpr int KCA = dw_kca<WP>();           // A chunks per stage (>= 2 for M = 128)
-    constexpr int MH = WP > 128 ? 2 : 1;        // M halves of 128 out features
-    constexpr int TMCOLS = MH * WP;
-    constexpr uint32_t HBLK = 8192;             // 64 rows x 128 B
-    constexpr uint32_t STAGE = (KCA + KC) * HBLK;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = align1024(smem_raw);
-    uint64_t *bars = (uint64_t *)(smem + NST_DW * STAGE);
-    uint64_t *full = bars, *empty = bars + NST_DW, *acc_full = bars + 2 * NST_DW;
-    uint32_t *tmem_slot = (uint32_t *)(acc_full + 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int layer = blockIdx.x / a.cpl, part = blockIdx.x % a.cpl;
-    const int nh = 2 * a.ntiles;
-    const int h0 = (int)((long)nh * part / a.cpl), h1 = (int)((long)nh * (part + 1) / a.cpl);
-    const size_t lay = (size_t)a.ntiles * KC * CHUNK_HALVES;
-    const uint8_t *dsrc = (const uint8_t *)(a.delta + (size_t)(layer + 1) * lay);   // Delta_{g+2}
-    const uint8_t *tsrc = (const uint8_t *)(a.act + (size_t)layer * lay);           // t_{g+1}
-    if (KCA > KC) {   // WP = 64: the upper 64 rows of M read zeros
-        for (int s = 0; s < NST_DW; ++s)
-            for (int i = threadIdx.x; i < (int)(HBLK / 16); i += blockDim.x)
-                ((uint4 *)(smem + s * STAGE + KC * HBLK))[i] = make_uint4(0, 0, 0, 0);
-        fence_proxy_async_smem();
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NST_DW; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(acc_full, 1);
-        fence_mbar_init();
-    }
-    if (warp == 1) tmem_alloc(tmem_slot, TMCOLS);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t ph = 0;
-            for (int h = h0; h < h1; ++h) {
-                const int tile = h >> 1, half = h & 1;
-                mbar_wait(&empty[stage], ph ^ 1);
-                mbar_arrive_expect_tx(&full[stage], 2 * KC * HBLK);
-                uint8_t *st = smem + stage * STAGE;
-                for (int c = 0; c < KC; ++c) {
-                    const size_t blk = ((size_t)tile * KC + c) * CHUNK_BYTES + half * HBLK;
-                    bulk_g2s(st + c * HBLK, dsrc + blk, HBLK, &full[stage]);
-                    bulk_g2s(st + (KCA + c) * HBLK, tsrc + blk, HBLK, &full[stage]);
-                }
-                if (++stage == NST_DW) { stage = 0; ph ^= 1; }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(128, WP, 1, 1);
-            int stage = 0;
-            uint32_t ph = 0;
-            bool first = true;
-            for (int h = h0; h < h1; ++h) {
-                mbar_wait(&full[stage], ph);
-                tc_fence_after();
-                const uint32_t st = smem_u32(smem + stage * STAGE);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t bd = sdesc_sw128(st + KCA * HBLK + kk * 2048, HBLK, 1024);
-#pragma unroll
-                    for (int mh = 0; mh < MH; ++mh) {
-                        const uint64_t ad = sdesc_sw128(st + (2 * mh) * HBLK + kk * 2048, HBLK, 1024);
-                        mma_f16(tmem + mh * WP, ad, bd, idesc, first ? 0u : 1u);
-                    }
-                    first = false;
-                }
-                mma_commit(&empty[stage]);
-                if (++stage == NST_DW) { stage = 0; ph ^= 1; }
-            }
-            mma_commit(acc_full);
-        }
-    } else {
-        // epilogue: 4 warps, warp%4 = TMEM lane quarter = out-feature quarter of each M half
-        const int q = warp & 3;
-        float *pb = a.partial + (size_t)blockIdx.x * WP * WP;
-        if (h1 > h0) {
-            mbar_wait(acc_full, 0);
-            tc_fence_after();
-        }
-#pragma unroll 1
-        for (int mh = 0; mh < MH; ++mh) {
-            const int o = mh * 128 + q * 32 + lane;
-#pragma unroll 1
-            for (int cc = 0; cc < WP; cc += 32) {
-                float v[32];
-                if (h1 > h0) {
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + mh * WP + cc, v);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) v[k] = 0.0f;
-                }
-                if (o < WP) {
-                    float4 *dst = (float4 *)(pb + (size_t)o * WP + cc);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, TMCOLS);
-}
-
 // ================================================================ backward: fused layer (dX + dW)
 // One launch per hidden GEMM g: reads Delta_out (= Delta_{g+2}) and t_in (= t_{g+1}) ONCE and
 // produces both Delta_in = (Delta_out W) (.) (1 - t_in^2) and this CTA's share of
@@ -943,6 +608,351 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
     if (warp == 1) tmem_dealloc(tmem, 2 * WP);
 }
 
+// ================================================================ backward v2 (WP >= 128): cluster pairs
+// One launch per hidden GEMM g. A cluster of NS = WP/128 CTAs walks a tile sequence; CTA c of
+// the cluster owns the input features i in [128c, 128c+128):
+//   dX : Delta_in[p, i] = sum_o Delta_out[p, o] W[o, i]      M = 128 points, N = 128 (own i), K = WP
+//   dW : dW^T[i, o]    += sum_p t_in[p, i] Delta_out[p, o]   M = 128 (own i), N = WP, K = 128 points
+// so every CTA needs the FULL Delta_out tile (bulk-loaded once per cluster with multicast: CTA r
+// issues chunks j = r mod NS for both CTAs), only its own half of t_in (unicast), and only its
+// own half of W^T, which stays resident in shared memory for the whole launch. Shared memory:
+// W^T half (KC x 16 KiB) + Delta ring (KC+2 chunk slots) + t ring (2 tiles x 2 chunks) = 224 KiB
+// at WP = 256. L2 traffic per tile is the algorithmic 3 x 64 KiB (Delta_out, t_in, Delta_in).
+// TMEM: dX accumulators (2 x 128 columns, double buffered) + dW accumulator (WP columns).
+// For the first backward GEMM (outl = 1) the Delta ring receives t_L instead, and the epilogue
+// warps turn it into Delta_L = s*gbar*W_out (.) (1 - t_L^2) in place (the output-layer backward,
+// fused), reducing the output-layer gradients on the way. The last GEMM (g = 0) does not store
+// Delta_1 (only its column sums are needed: bias and first-layer weights).
+struct Bwd2Args {
+    int N, ntiles, npairs, first, outl;
+    const __half *dsrc;   // Delta_{g+2} (or t_L when outl)   [ntiles][KC] blocks
+    const __half *tin;    // t_{g+1}                           [ntiles][KC]
+    __half *din;          // Delta_{g+1}                       [ntiles][KC] (unused when first)
+    const __half *WTf;    // [KC] blocks of W^T (WP rows each)
+    const float *gbar;    // dLOSS/dnet per MLP point (outl)
+    const float *Wop;     // output weights (outl)
+    float *part_ob;       // [npairs][2*WP+1]  (outl)
+    float *part_dx;       // [npairs][3*WP]
+    float *part_dw;       // [npairs][WP*WP]   rows = out features
+    DevState *st;
+};
+
+template <int WP>
+struct B2 {
+    static constexpr int NS = WP / 128;
+    static constexpr int KC = WP / 64;
+    static constexpr int DS = KC + 2;   // Delta ring slots
+    static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 4) * CHUNK_BYTES + 64 * 8;
+};
+
+template <int WP>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
+    constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS;
+    constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *Wt = smem;                          // [KC] x 16 KiB: W^T rows i in [128c, 128c+128)
+    uint8_t *Dr = Wt + KC * CHUNK_BYTES;         // [DS] x 16 KiB
+    uint8_t *Tr = Dr + DS * CHUNK_BYTES;         // [2 tiles][2 chunks] x 16 KiB
+    uint64_t *bars = (uint64_t *)(Tr + 4 * CHUNK_BYTES);
+    uint64_t *wfull = bars;
+    uint64_t *dfull = bars + 1, *dempty = dfull + DS, *dready = dempty + DS;
+    uint64_t *tfull = dready + DS, *tempty = tfull + 2, *xfull = tempty + 2, *xempty = xfull + 2;
+    uint64_t *wdone = xempty + 2;
+    uint32_t *tmem_slot = (uint32_t *)(wdone + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = NS > 1 ? cluster_rank() : 0u;
+    const int pair = blockIdx.x / NS;
+    const int nk = pair < a.ntiles ? (a.ntiles - pair + a.npairs - 1) / a.npairs : 0;
+    if (threadIdx.x == 0) {
+        mbar_init(wfull, 1);
+        for (int s = 0; s < DS; ++s) {
+            mbar_init(&dfull[s], 1);
+            mbar_init(&dempty[s], NS);
+            mbar_init(&dready[s], EPI_THREADS);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 1 + EPI_THREADS / 32);
+            mbar_init(&xfull[s], 1);
+            mbar_init(&xempty[s], EPI_THREADS / 32);
+        }
+        mbar_init(wdone, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    if (NS > 1) cluster_sync_all();   // every CTA's barriers exist before any multicast lands
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tm_w = tmem + 256;   // dW^T accumulator; dX accumulators at columns 0 / 128
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (lane == 0) {
+            mbar_arrive_expect_tx(wfull, KC * CHUNK_BYTES);
+            for (int kc = 0; kc < KC; ++kc)
+                bulk_g2s(Wt + kc * CHUNK_BYTES, (const uint8_t *)a.WTf + ((size_t)kc * WP + 128 * rank) * 128,
+                         CHUNK_BYTES, wfull);
+            int dn = 0;   // running Delta chunk counter
+            for (int k = 0; k < nk; ++k) {
+                const int tile = pair + k * a.npairs;
+                for (int j = 0; j < KC; ++j, ++dn) {
+                    const int slot = dn % DS;
+                    mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&dfull[slot], CHUNK_BYTES);
+                    const uint8_t *src = (const uint8_t *)a.dsrc + ((size_t)tile * KC + j) * CHUNK_BYTES;
+                    if (NS == 1) bulk_g2s(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot]);
+                    else if ((uint32_t)(j % NS) == rank)
+                        bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], MASK);
+                }
+                const int b = k & 1;
+                mbar_wait_sleep(&tempty[b], ((k >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&tfull[b], 2 * CHUNK_BYTES);
+                bulk_g2s(Tr + b * 2 * CHUNK_BYTES,
+                         (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
+                         &tfull[b]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_x = idesc_f16(128, 128, 0, 0);
+            constexpr uint32_t idesc_w = idesc_f16(128, 128, 1, 1);
+            const uint32_t wt = smem_u32(Wt), dr = smem_u32(Dr), tr = smem_u32(Tr);
+            mbar_wait(wfull, 0);
+            int dn = 0;
+            for (int k = 0; k < nk; ++k) {
+                const int b = k & 1;
+                const int slot0 = dn % DS;
+                mbar_wait(&tfull[b], (k >> 1) & 1);
+                mbar_wait(&xempty[b], ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t accx = tmem + (uint32_t)(b * 128);
+                for (int j = 0; j < KC; ++j) {
+                    const int slot = (dn + j) % DS;
+                    mbar_wait(a.outl ? &dready[slot] : &dfull[slot], ((dn + j) / DS) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kq = 0; kq < 4; ++kq) {
+                        const uint64_t ad = sdesc_sw128(dr + slot * CHUNK_BYTES + kq * 32, 16, 1024);
+                        const uint64_t bd = sdesc_sw128(wt + j * CHUNK_BYTES + kq * 32, 16, 1024);
+                        mma_f16(accx, ad, bd, idesc_x, (j | kq) != 0);
+                    }
+                }
+                mma_commit(&xfull[b]);
+                // dW^T over this tile's 128 points, in N halves of 128 out features (chunk pairs
+                // sit in consecutive ring slots: slot0 + 2h is even and <= DS - 2)
+                for (int h = 0; h < KC / 2; ++h) {
+                    const int sl = (slot0 + 2 * h) % DS;
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint64_t ad = sdesc_sw128(tr + b * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                        const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                        mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
+                    }
+                }
+                for (int j = 0; j < KC; ++j) {
+                    if (NS == 1) mma_commit(&dempty[(dn + j) % DS]);
+                    else mma_commit_mc(&dempty[(dn + j) % DS], MASK);
+                }
+                mma_commit(&tempty[b]);
+                dn += KC;
+            }
+            mma_commit(wdone);
+        }
+    } else {
+        // ---------------- epilogue warps
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int hf = (warp - 2) >> 2;          // local t chunk 0/1 -> 64 columns
+        const int ep_tid = threadIdx.x - 64;
+        const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+        const int N = a.N;
+        float cs[2] = {0.f, 0.f}, csx[2] = {0.f, 0.f}, csy[2] = {0.f, 0.f};
+        // output-layer transform state (outl)
+        constexpr int CPT = 8 * KC;              // threads per row
+        constexpr int RG = EPI_THREADS / CPT;    // row groups
+        const int olg = ep_tid & 7, och = (ep_tid >> 3) % KC, org = ep_tid / CPT;
+        const int of0 = och * 64 + olg * 8;
+        float wo[8], aw[8], ab[8], ag = 0.f;
+        float s = 1.0f;
+        if (a.outl) {
+            s = grad_scale(a.st);
+            if (blockIdx.x == 0 && ep_tid == 0) {
+                a.st->gscale = s;
+                a.st->inv_gscale = 1.0f / s;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { wo[e] = a.Wop[of0 + e]; aw[e] = 0.f; ab[e] = 0.f; }
+        }
+        int dn = 0;
+        for (int k = 0; k <= nk; ++k) {
+            if (a.outl && k < nk) {
+                // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
+                const int tile = pair + k * a.npairs;
+                const int slot = (dn + och) % DS;
+                mbar_wait(&dfull[slot], ((dn + och) / DS) & 1);
+                uint8_t *blk = Dr + slot * CHUNK_BYTES;
+#pragma unroll 4
+                for (int m = 0; m < 128 / RG; ++m) {
+                    const int r = org + m * RG;
+                    const float g = s * __ldg(a.gbar + (size_t)tile * 128 + r);
+                    ag += (och == 0 && olg == 0) ? g : 0.f;
+                    const uint32_t off = (uint32_t)(r * 128 + ((olg ^ (r & 7)) << 4));
+                    uint32_t w[4];
+                    ld_shared_v4(smem_u32(blk) + off, w[0], w[1], w[2], w[3]);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float2 t = __half22float2(*reinterpret_cast<__half2 *>(&w[mm]));
+                        const float d0 = g * wo[2 * mm] * (1.0f - t.x * t.x);
+                        const float d1 = g * wo[2 * mm + 1] * (1.0f - t.y * t.y);
+                        aw[2 * mm] = fmaf(g, t.x, aw[2 * mm]);
+                        aw[2 * mm + 1] = fmaf(g, t.y, aw[2 * mm + 1]);
+                        ab[2 * mm] += d0;
+                        ab[2 * mm + 1] += d1;
+                        w[mm] = pack_half2(d0, d1);
+                    }
+                    st_shared_v4(smem_u32(blk) + off, w[0], w[1], w[2], w[3]);
+                }
+                fence_proxy_async_smem();
+                // every epilogue thread arrives on all KC slots of this tile (count = EPI_THREADS)
+                for (int j = 0; j < KC; ++j) mbar_arrive(&dready[(dn + j) % DS]);
+                dn += KC;
+            }
+            if (k == 0) continue;
+            // ---- dX epilogue of tile k-1
+            const int kk = k - 1, b = kk & 1;
+            const int tile = pair + kk * a.npairs;
+            int pi, pj;
+            point_ij(tile * 128 + row, N, pi, pj);
+            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            mbar_wait(&xfull[b], (kk >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tb = smem_u32(Tr) + (uint32_t)((b * 2 + hf) * CHUNK_BYTES + row * 128);
+            uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
+#pragma unroll
+            for (int g2 = 0; g2 < 2; ++g2) {
+                float v[32];
+                tmem_ld32(tmem + t_lane + (uint32_t)(b * 128 + hf * 64 + g2 * 32), v);
+                uint32_t w[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int lg = g2 * 4 + j;
+                    uint32_t tw[4];
+                    ld_shared_v4(tb + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&tw[mm]));
+                        v[8 * j + 2 * mm] *= (1.0f - tf.x * tf.x);
+                        v[8 * j + 2 * mm + 1] *= (1.0f - tf.y * tf.y);
+                        w[4 * j + mm] = pack_half2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
+                    }
+                }
+                if (!a.first) {
+                    // logical granules (2m, 2m+1) occupy one 32-byte sector, swapped when row is odd
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const int lg = g2 * 4 + 2 * m;
+                        const int pos = (lg ^ (row & 7)) & ~1;
+                        const uint32_t *g0 = &w[8 * m], *g1 = &w[8 * m + 4];
+                        if (row & 1)
+                            st_global_v8(drow + pos * 16, g1[0], g1[1], g1[2], g1[3], g0[0], g0[1], g0[2], g0[3]);
+                        else
+                            st_global_v8(drow + pos * 16, g0[0], g0[1], g0[2], g0[3], g1[0], g1[1], g1[2], g1[3]);
+                    }
+                }
+                if (a.first) {
+                    float vx[32], vy[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
+                    warp_reduce_scatter32(vx, lane);
+                    warp_reduce_scatter32(vy, lane);
+                    csx[g2] += vx[0];
+                    csy[g2] += vy[0];
+                }
+                warp_reduce_scatter32(v, lane);
+                cs[g2] += v[0];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&xempty[b]);
+                mbar_arrive(&tempty[b]);
+            }
+        }
+        // ---- end: all MMAs done -> the rings are free for the reductions
+        if (nk > 0) mbar_wait(wdone, 0);
+        tc_fence_after();
+        named_bar(1, EPI_THREADS);
+        float *sred = (float *)Dr;   // [4 quarters][3][128]
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) {
+            const int col = hf * 64 + g2 * 32 + lane;
+            sred[(q * 3 + 0) * 128 + col] = csx[g2];
+            sred[(q * 3 + 1) * 128 + col] = csy[g2];
+            sred[(q * 3 + 2) * 128 + col] = cs[g2];
+        }
+        float *sob = sred + 12 * 128;   // [RG][WP] + [RG] (outl)
+        if (a.outl) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                sob[org * WP + of0 + e] = aw[e];
+                sob[RG * WP + org * WP + of0 + e] = ab[e];
+            }
+            if (och == 0 && olg == 0) sob[2 * RG * WP + org] = ag;
+        }
+        named_bar(1, EPI_THREADS);
+        if (ep_tid < 128) {
+            const int col = ep_tid, ig = (int)rank * 128 + col;
+            float sx = 0.f, sy = 0.f, sb = 0.f;
+            for (int qq = 0; qq < 4; ++qq) {
+                sx += sred[(qq * 3 + 0) * 128 + col];
+                sy += sred[(qq * 3 + 1) * 128 + col];
+                sb += sred[(qq * 3 + 2) * 128 + col];
+            }
+            float *pb = a.part_dx + (size_t)pair * 3 * WP;
+            pb[2 * ig] = sx;
+            pb[2 * ig + 1] = sy;
+            pb[2 * WP + ig] = sb;
+            if (a.outl) {
+                float sw = 0.f, sbb = 0.f;
+                for (int r = 0; r < RG; ++r) {
+                    sw += sob[r * WP + ig];
+                    sbb += sob[RG * WP + r * WP + ig];
+                }
+                float *po = a.part_ob + (size_t)pair * (2 * WP + 1);
+                po[ig] = sw;
+                po[WP + ig] = sbb;
+                if (rank == 0 && col == 0) {
+                    float sg = 0.f;
+                    for (int r = 0; r < RG; ++r) sg += sob[2 * RG * WP + r];
+                    po[2 * WP] = sg;
+                }
+            }
+        }
+        // dW^T (rows i local = TMEM lanes, columns o) -> part_dw[pair][o][i], coalesced over i
+        float *pw = a.part_dw + (size_t)pair * WP * WP + rank * 128 + row;
+#pragma unroll 1
+        for (int oc = hf * (WP / 2); oc < (hf + 1) * (WP / 2); oc += 32) {
+            float v[32];
+            if (nk > 0) {
+                tmem_ld32(tm_w + t_lane + (uint32_t)oc, v);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) pw[(size_t)(oc + e) * WP] = v[e];
+        }
+    }
+    tc_fence_before();
+    if (NS > 1) cluster_sync_all();   // no CTA leaves while a peer may still multicast into it
+    else __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // ================================================================ weight re-layout
 // After each Adam step: fp16 copies of the hidden weights in the B-operand block layout
 // (forward: rows = out features; backward-dX: rows = in features), zero padded to WP.
@@ -986,9 +996,11 @@ __global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float 
 template <int WP>
 static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
-    cudaFuncSetAttribute(k_tc_dx<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dx_smem_bytes<WP>());
-    cudaFuncSetAttribute(k_tc_dw<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes<WP>());
-    cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
+    if constexpr (WP >= 128) {
+        cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+    } else {
+        cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
+    }
 }
 
 int tc_create(const Net &net, TcBufs &b, std::string &err) {
@@ -1008,15 +1020,15 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
     {
-        const int PF = WP > 128 ? 2 : 1;
-        int np_ = nsm / PF;
+        // WP >= 128: clusters of NS = WP/128 CTAs (k_tc_bwd2); WP = 64: one CTA per "pair"
+        const int NS = WP >= 128 ? WP / 128 : 1;
+        int np_ = nsm / NS;
         if (np_ > b.ntiles) np_ = b.ntiles;
         b.npairs = np_;
-        b.grid_dx = np_ * PF;
+        b.grid_dx = np_;              // rows of the column-sum partials
+        b.grid_bwd = np_ * NS;        // CTAs per backward launch
     }
-    b.grid_ob = b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm;
-    b.dw_cpl = G > 0 ? (nsm / G > 0 ? nsm / G : 1) : 0;
-    if (b.dw_cpl > 2 * b.ntiles) b.dw_cpl = 2 * b.ntiles;
+    b.grid_ob = WP >= 128 ? b.npairs : (b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm);
     auto al = [&](void **p, size_t bytes) -> bool {
         if (cudaMalloc(p, bytes > 0 ? bytes : 16) != cudaSuccess) return false;
         cudaMemset(*p, 0, bytes > 0 ? bytes : 16);
@@ -1050,7 +1062,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     const int nl = net.nl;
     for (int l = 0; l < nl; ++l) {
         const int win = net.widths[l], wout = net.widths[l + 1];
-        if (l == nl - 1) {   // output layer: from k_tc_out_bwd
+        if (l == nl - 1) {   // output layer: from k_tc_out_bwd (WP = 64) / the outl launch of k_tc_bwd2
             job(b.off_ob, net.woff[l], win, b.grid_ob, 2 * WP + 1, 0, 1, 1);
             job(b.off_ob + 2 * WP, net.boff[l], 1, b.grid_ob, 2 * WP + 1, 0, 1, 1);
             continue;
@@ -1107,13 +1119,39 @@ template <int WP>
 static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
     const size_t lay = (size_t)b.ntiles * b.KC * CHUNK_HALVES;
     const int L = b.L;
-    k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
-                                                      b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
-    for (int g = b.G - 1; g >= 0; --g) {
-        BwdArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.npairs, b.delta + (size_t)(g + 1) * lay, b.act + (size_t)g * lay,
-                  b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
-                  b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP, b.partial + b.off_dw + (long)g * b.npairs * WP * WP};
-        k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
+    if constexpr (WP >= 128) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = B2<WP>::NS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(b.grid_bwd);
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = B2<WP>::SMEM;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        for (int g = b.G - 1; g >= 0; --g) {
+            const bool outl = g == b.G - 1;
+            Bwd2Args a{net.N, b.ntiles, b.npairs, g == 0 ? 1 : 0, outl ? 1 : 0,
+                       outl ? b.act + (size_t)(L - 1) * lay : b.delta + (size_t)(g + 1) * lay,
+                       b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
+                       b.gbar, b.Wop, b.partial + b.off_ob,
+                       b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
+                       b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st};
+            cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP>, a);
+        }
+    } else {
+        k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+                                                          b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
+        for (int g = b.G - 1; g >= 0; --g) {
+            BwdArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.npairs, b.delta + (size_t)(g + 1) * lay,
+                      b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
+                      b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
+                      b.partial + b.off_dw + (long)g * b.npairs * WP * WP};
+            k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
+        }
     }
     launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
 }
@@ -1126,7 +1164,8 @@ void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cud
 
 int tc_launches(const Net &net) {
     const int G = net.nl - 2;
-    return 1 /*fwd*/ + 1 /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
+    const int wp = ((net.widths[1] + 63) / 64) * 64;
+    return 1 /*fwd*/ + (wp == 64 ? 1 : 0) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
 }
 
 }  // namespace crv

@@ -24,7 +24,7 @@ struct TcBufs {
     float *gbar = nullptr;   // [P] dLOSS/dnet (unscaled)
     float *partial = nullptr;
     long off_ob = 0, off_dx = 0, off_dw = 0;
-    int grid_ob = 0, grid_dx = 0, grid_fwd = 0, dw_cpl = 0, npairs = 0;
+    int grid_ob = 0, grid_dx = 0, grid_fwd = 0, grid_bwd = 0, npairs = 0;
     RedJob *jobs = nullptr;  // device copy
     int njobs = 0, max_count = 0, groups = 0;
     const float *theta = nullptr;
