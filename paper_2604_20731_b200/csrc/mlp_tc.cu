@@ -20,6 +20,7 @@
 #include "tc_ptx.cuh"
 #include "../../include/crvpinn.h"
 #include <math.h>
+#include <cstdlib>
 
 namespace crv {
 
@@ -695,9 +696,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             for (int kc = 0; kc < KC; ++kc)
                 bulk_g2s(Wt + kc * CHUNK_BYTES, (const uint8_t *)a.WTf + ((size_t)kc * WP + 128 * rank) * 128,
                          CHUNK_BYTES, wfull);
+            // L2 prefetch PD tiles ahead: the shared-memory rings hold < 2 tiles, so the loads
+            // that refill them must hit L2, not wait a full HBM round trip
+            constexpr int PD = 3;
+            auto prefetch = [&](int kp) {
+                if (kp >= nk) return;
+                const int tp = pair + kp * a.npairs;
+                for (int j = (int)rank; j < KC; j += NS)
+                    bulk_prefetch_l2((const uint8_t *)a.dsrc + ((size_t)tp * KC + j) * CHUNK_BYTES, CHUNK_BYTES);
+                bulk_prefetch_l2((const uint8_t *)a.tin + ((size_t)tp * KC + 2 * rank) * CHUNK_BYTES,
+                                 2 * CHUNK_BYTES);
+            };
+            for (int kp = 1; kp < PD; ++kp) prefetch(kp);
             int dn = 0;   // running Delta chunk counter
             for (int k = 0; k < nk; ++k) {
                 const int tile = pair + k * a.npairs;
+                prefetch(k + PD);
                 for (int j = 0; j < KC; ++j, ++dn) {
                     const int slot = dn % DS;
                     mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
@@ -730,33 +744,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 mbar_wait(&xempty[b], ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t accx = tmem + (uint32_t)(b * 128);
-                for (int j = 0; j < KC; ++j) {
-                    const int slot = (dn + j) % DS;
-                    mbar_wait(a.outl ? &dready[slot] : &dfull[slot], ((dn + j) / DS) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int kq = 0; kq < 4; ++kq) {
-                        const uint64_t ad = sdesc_sw128(dr + slot * CHUNK_BYTES + kq * 32, 16, 1024);
-                        const uint64_t bd = sdesc_sw128(wt + j * CHUNK_BYTES + kq * 32, 16, 1024);
-                        mma_f16(accx, ad, bd, idesc_x, (j | kq) != 0);
-                    }
-                }
-                mma_commit(&xfull[b]);
-                // dW^T over this tile's 128 points, in N halves of 128 out features (chunk pairs
-                // sit in consecutive ring slots: slot0 + 2h is even and <= DS - 2)
+                // chunk pairs (2h, 2h+1): dX over those K chunks, then the dW^T N-half h, then release
+                // the two ring slots -- the next tile's loads refill them mid-tile. Pairs sit in
+                // consecutive slots (slot0 + 2h is even and <= DS - 2).
                 for (int h = 0; h < KC / 2; ++h) {
                     const int sl = (slot0 + 2 * h) % DS;
+                    for (int j = 2 * h; j < 2 * h + 2; ++j) {
+                        mbar_wait(a.outl ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kq = 0; kq < 4; ++kq) {
+                            const uint64_t ad = sdesc_sw128(dr + (sl + j - 2 * h) * CHUNK_BYTES + kq * 32, 16, 1024);
+                            const uint64_t bd = sdesc_sw128(wt + j * CHUNK_BYTES + kq * 32, 16, 1024);
+                            mma_f16(accx, ad, bd, idesc_x, (j | kq) != 0);
+                        }
+                    }
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
                         const uint64_t ad = sdesc_sw128(tr + b * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
                     }
+                    for (int j = 0; j < 2; ++j) {
+                        if (NS == 1) mma_commit(&dempty[sl + j]);
+                        else mma_commit_mc(&dempty[sl + j], MASK);
+                    }
                 }
-                for (int j = 0; j < KC; ++j) {
-                    if (NS == 1) mma_commit(&dempty[(dn + j) % DS]);
-                    else mma_commit_mc(&dempty[(dn + j) % DS], MASK);
-                }
+                mma_commit(&xfull[b]);
                 mma_commit(&tempty[b]);
                 dn += KC;
             }
@@ -771,12 +785,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         const uint32_t t_lane = (uint32_t)(q * 32) << 16;
         const int N = a.N;
         float cs[2] = {0.f, 0.f}, csx[2] = {0.f, 0.f}, csy[2] = {0.f, 0.f};
-        // output-layer transform state (outl)
-        constexpr int CPT = 8 * KC;              // threads per row
-        constexpr int RG = EPI_THREADS / CPT;    // row groups
-        const int olg = ep_tid & 7, och = (ep_tid >> 3) % KC, org = ep_tid / CPT;
-        const int of0 = och * 64 + olg * 8;
-        float wo[8], aw[8], ab[8], ag = 0.f;
+        // output-layer transform state (outl). Thread -> granule lg (8 features) of every chunk,
+        // rows rr + 32m (m < 4); chunks are transformed in order so the MMA can start on chunk 0
+        // while later chunks are still being transformed. Delta_L is formed in half2 arithmetic
+        // (it is stored in fp16 anyway); the output-layer column sums (dW_out = sum g t_L,
+        // db_L = sum Delta_L) are fp32 and cover this CTA's own half of the features only.
+        const int olg = ep_tid & 7, orr = ep_tid >> 3;
+        __half2 wo2[KC][4];
+        float aw[2][8], ab[2][8], ag = 0.f;
         float s = 1.0f;
         if (a.outl) {
             s = grad_scale(a.st);
@@ -785,40 +801,60 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 a.st->inv_gscale = 1.0f / s;
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) { wo[e] = a.Wop[of0 + e]; aw[e] = 0.f; ab[e] = 0.f; }
+            for (int j = 0; j < KC; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    wo2[j][e] = __floats2half2_rn(a.Wop[j * 64 + olg * 8 + 2 * e], a.Wop[j * 64 + olg * 8 + 2 * e + 1]);
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) aw[jj][e] = ab[jj][e] = 0.f;
         }
         int dn = 0;
         for (int k = 0; k <= nk; ++k) {
             if (a.outl && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
                 const int tile = pair + k * a.npairs;
-                const int slot = (dn + och) % DS;
-                mbar_wait(&dfull[slot], ((dn + och) / DS) & 1);
-                uint8_t *blk = Dr + slot * CHUNK_BYTES;
-#pragma unroll 4
-                for (int m = 0; m < 128 / RG; ++m) {
-                    const int r = org + m * RG;
-                    const float g = s * __ldg(a.gbar + (size_t)tile * 128 + r);
-                    ag += (och == 0 && olg == 0) ? g : 0.f;
-                    const uint32_t off = (uint32_t)(r * 128 + ((olg ^ (r & 7)) << 4));
-                    uint32_t w[4];
-                    ld_shared_v4(smem_u32(blk) + off, w[0], w[1], w[2], w[3]);
+                float g[4];
+                __half2 g2[4];
 #pragma unroll
-                    for (int mm = 0; mm < 4; ++mm) {
-                        const float2 t = __half22float2(*reinterpret_cast<__half2 *>(&w[mm]));
-                        const float d0 = g * wo[2 * mm] * (1.0f - t.x * t.x);
-                        const float d1 = g * wo[2 * mm + 1] * (1.0f - t.y * t.y);
-                        aw[2 * mm] = fmaf(g, t.x, aw[2 * mm]);
-                        aw[2 * mm + 1] = fmaf(g, t.y, aw[2 * mm + 1]);
-                        ab[2 * mm] += d0;
-                        ab[2 * mm + 1] += d1;
-                        w[mm] = pack_half2(d0, d1);
-                    }
-                    st_shared_v4(smem_u32(blk) + off, w[0], w[1], w[2], w[3]);
+                for (int m = 0; m < 4; ++m) {
+                    g[m] = s * __ldg(a.gbar + (size_t)tile * 128 + orr + 32 * m);
+                    g2[m] = __floats2half2_rn(g[m], g[m]);
+                    if (olg == 0) ag += g[m];
                 }
-                fence_proxy_async_smem();
-                // every epilogue thread arrives on all KC slots of this tile (count = EPI_THREADS)
-                for (int j = 0; j < KC; ++j) mbar_arrive(&dready[(dn + j) % DS]);
+                const __half2 one2 = __floats2half2_rn(1.0f, 1.0f);
+#pragma unroll
+                for (int j = 0; j < KC; ++j) {
+                    const int slot = (dn + j) % DS;
+                    mbar_wait(&dfull[slot], ((dn + j) / DS) & 1);
+                    const uint32_t blk = smem_u32(Dr + slot * CHUNK_BYTES);
+                    const bool own = NS == 1 || (j >> 1) == (int)rank;
+                    const int jj = NS == 1 ? j : (j & 1);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int r = orr + 32 * m;
+                        const uint32_t off = (uint32_t)(r * 128 + ((olg ^ (r & 7)) << 4));
+                        uint32_t w[4];
+                        ld_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const __half2 t = *reinterpret_cast<__half2 *>(&w[e]);
+                            const __half2 d = __hmul2(__hmul2(__hfma2(__hneg2(t), t, one2), wo2[j][e]), g2[m]);
+                            if (own && jj < 2) {
+                                const float2 tf = __half22float2(t), df = __half22float2(d);
+                                aw[jj][2 * e] = fmaf(g[m], tf.x, aw[jj][2 * e]);
+                                aw[jj][2 * e + 1] = fmaf(g[m], tf.y, aw[jj][2 * e + 1]);
+                                ab[jj][2 * e] += df.x;
+                                ab[jj][2 * e + 1] += df.y;
+                            }
+                            w[e] = *reinterpret_cast<const uint32_t *>(&d);
+                        }
+                        st_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive(&dready[slot]);   // count = EPI_THREADS
+                }
                 dn += KC;
             }
             if (k == 0) continue;
@@ -894,14 +930,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             sred[(q * 3 + 1) * 128 + col] = csy[g2];
             sred[(q * 3 + 2) * 128 + col] = cs[g2];
         }
-        float *sob = sred + 12 * 128;   // [RG][WP] + [RG] (outl)
+        float *sob = sred + 12 * 128;   // [32 row groups][2 kinds][128 own features] + [32] (outl)
         if (a.outl) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                sob[org * WP + of0 + e] = aw[e];
-                sob[RG * WP + org * WP + of0 + e] = ab[e];
-            }
-            if (och == 0 && olg == 0) sob[2 * RG * WP + org] = ag;
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    sob[(orr * 2 + 0) * 128 + jj * 64 + olg * 8 + e] = aw[jj][e];
+                    sob[(orr * 2 + 1) * 128 + jj * 64 + olg * 8 + e] = ab[jj][e];
+                }
+            if (olg == 0) sob[64 * 128 + orr] = ag;
         }
         named_bar(1, EPI_THREADS);
         if (ep_tid < 128) {
@@ -918,16 +956,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             pb[2 * WP + ig] = sb;
             if (a.outl) {
                 float sw = 0.f, sbb = 0.f;
-                for (int r = 0; r < RG; ++r) {
-                    sw += sob[r * WP + ig];
-                    sbb += sob[RG * WP + r * WP + ig];
+                for (int r = 0; r < 32; ++r) {
+                    sw += sob[(r * 2 + 0) * 128 + col];
+                    sbb += sob[(r * 2 + 1) * 128 + col];
                 }
                 float *po = a.part_ob + (size_t)pair * (2 * WP + 1);
                 po[ig] = sw;
                 po[WP + ig] = sbb;
                 if (rank == 0 && col == 0) {
                     float sg = 0.f;
-                    for (int r = 0; r < RG; ++r) sg += sob[2 * RG * WP + r];
+                    for (int r = 0; r < 32; ++r) sg += sob[64 * 128 + r];
                     po[2 * WP] = sg;
                 }
             }
@@ -1029,6 +1067,10 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         b.grid_bwd = np_ * NS;        // CTAs per backward launch
     }
     b.grid_ob = WP >= 128 ? b.npairs : (b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm);
+    {
+        const char *e = getenv("CRVPINN_FUSE_OUTL");   // tuning knob: fused output-layer backward
+        b.fuse_outl = WP >= 128 && !(e && e[0] == '0');
+    }
     auto al = [&](void **p, size_t bytes) -> bool {
         if (cudaMalloc(p, bytes > 0 ? bytes : 16) != cudaSuccess) return false;
         cudaMemset(*p, 0, bytes > 0 ? bytes : 16);
@@ -1132,8 +1174,12 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         cfg.stream = s;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (!b.fuse_outl)
+            k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+                                                              b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob,
+                                                              st);
         for (int g = b.G - 1; g >= 0; --g) {
-            const bool outl = g == b.G - 1;
+            const bool outl = g == b.G - 1 && b.fuse_outl;
             Bwd2Args a{net.N, b.ntiles, b.npairs, g == 0 ? 1 : 0, outl ? 1 : 0,
                        outl ? b.act + (size_t)(L - 1) * lay : b.delta + (size_t)(g + 1) * lay,
                        b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
@@ -1165,7 +1211,9 @@ void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cud
 int tc_launches(const Net &net) {
     const int G = net.nl - 2;
     const int wp = ((net.widths[1] + 63) / 64) * 64;
-    return 1 /*fwd*/ + (wp == 64 ? 1 : 0) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
+    const char *e = getenv("CRVPINN_FUSE_OUTL");
+    const bool fused = wp >= 128 && !(e && e[0] == '0');
+    return 1 /*fwd*/ + (fused ? 0 : 1) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
 }
 
 }  // namespace crv
