@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrvpinn.so")
+LIB_PATH = os.environ.get("CRVPINN_LIB", os.path.join(_HERE, "libcrvpinn.so"))   # override: A/B builds
 
 CRVPINN_OK, CRVPINN_EINVAL, CRVPINN_ENOMEM, CRVPINN_ECUDA, CRVPINN_ENONFINITE, CRVPINN_EDOMAIN = 0, -1, -2, -3, -4, -5
 PREC_TENSOR, PREC_FP32 = 0, 1

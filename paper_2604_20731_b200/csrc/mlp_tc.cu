@@ -63,20 +63,30 @@ struct FwdArgs {
     const float *W1p, *bp, *Wop;
     __half *act;           // [L][ntiles][KC] blocks
     float *u;              // lattice (N+1)^2
+    long long *trace;      // debug timeline (CTA 0), nullptr normally
 };
+#define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
+
+
+
+constexpr int FWD_EPI_WARPS = 16;                       // 4 per TMEM lane quarter
+constexpr int FWD_THREADS = 64 + 32 * FWD_EPI_WARPS;     // producer warp + MMA warp + epilogue
 
 template <int WP>
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
-    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 256) * 4 +
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128) * 4 +
            32 * 8 + 16;
 }
 
-// Pipelining: two TMEM accumulators (GEMMs alternate), and per-64-feature-chunk
+// Pipelining: two TMEM accumulators (GEMMs alternate) and per-64-feature-chunk
 // barriers a_full[c]: the epilogue producing activation t_a chunk c releases it to the MMA of the
-// next GEMM immediately, so that GEMM runs under the rest of the epilogue. All 8 epilogue warps
-// work on the same chunk at a time (warp pair sharing a TMEM lane quarter splits its 64 columns).
+// next GEMM immediately, so that GEMM runs under the rest of the epilogue. 16 epilogue warps work
+// on the same chunk at a time (the 4 warps sharing a TMEM lane quarter take 16 columns each);
+// there is no block-wide barrier inside a tile. t_hi goes to HBM straight from registers
+// (one 32-byte sector per thread and chunk). (Pre-scaling the fp16 weights by 2 log2 e to save
+// the multiply in tanh was measured 3-4x less accurate in u on B200 and is not used.)
 template <int WP>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   // 18 warps -> <= 96 regs (5 warps on SMSP 0/1)
     constexpr int KC = WP / 64;
     constexpr uint32_t WBLK = WP * 128;
     extern __shared__ uint8_t smem_raw[];
@@ -87,8 +97,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
     float *sW1 = (float *)(Wr + NST_W * WBLK);
     float *sB = sW1 + 2 * WP;
     float *sWo = sB + a.L * WP;          // WP + 1 (bias last)
-    float *sRed = sWo + WP + 1;          // 256
-    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 256) + 7) & ~(uintptr_t)7);
+    float *sRed = sWo + WP + 1;          // [2 parity][4][128]
+    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
     uint64_t *w_full = bars, *w_empty = bars + NST_W;
     uint64_t *a_full = bars + 2 * NST_W;          // [KC]
     uint64_t *acc_full = a_full + KC;             // [2]
@@ -103,7 +113,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
-        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], EPI_THREADS);
+        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], FWD_EPI_WARPS);
         mbar_init(&acc_full[0], 1);
         mbar_init(&acc_full[1], 1);
         fence_mbar_init();
@@ -142,7 +152,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                     const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
                     for (int c = 0; c < KC; ++c) {
                         mbar_wait(&a_full[c], aph);
+                        FTRACE(2048 + (gi * KC + c) * 4 + 0);
+                        // t_hi chunk c of layer g+1 -> HBM (the backward's operand)
+                        bulk_s2g(a.act + ((size_t)g * a.ntiles + tile) * (KC * CHUNK_HALVES) + c * CHUNK_HALVES,
+                                 A_hi + c * CHUNK_BYTES, CHUNK_BYTES);
+                        bulk_commit();
                         mbar_wait(&w_full[stage], ph);
+                        FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
@@ -152,25 +168,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                             mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
                             mma_f16(acc, dl, bd, idesc, 1u);
                         }
+                        FTRACE(2048 + (gi * KC + c) * 4 + 2);
                         mma_commit(&w_empty[stage]);
                         if (++stage == NST_W) { stage = 0; ph ^= 1; }
                     }
                     aph ^= 1;
+                    // the epilogue overwrites A_hi only after acc_full: the HBM copies of this GEMM's
+                    // A chunks must have been read out by then
+                    bulk_wait_read0();
                     mma_commit(&acc_full[gi & 1]);
                 }
+            bulk_wait0();
         }
     } else {
-        // ---------------- epilogue: 8 warps; warp%4 selects the TMEM lane quarter (= rows),
-        // the two warps of a quarter split every 64-column chunk into halves of 32.
+        // ---------------- epilogue: 16 warps; warp % 4 = TMEM lane quarter (rows), wq = which
+        // 16 of the 64 columns of the current chunk
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int hf = (warp - 2) >> 2;
-        const int ep_tid = threadIdx.x - 64;
+        const int wq = (warp - 2) >> 2;
         const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-        uint32_t acc_ph[2] = {0u, 0u};
-        int gi = 0;
+        const int lg0 = 2 * wq;                                   // logical granules lg0, lg0+1
+        const int pos = (lg0 ^ (row & 7)) & ~1;                   // their 32-byte sector in the row
+        const bool swap = (row & 1) != 0;
+        const uint32_t off0 = (uint32_t)(row * 128 + ((lg0 ^ (row & 7)) << 4));
+        const uint32_t off1 = (uint32_t)(row * 128 + (((lg0 + 1) ^ (row & 7)) << 4));
+        uint32_t acc_ph = 0u;   // bit i: parity of acc_full[i]
+        int gi = 0, par = 0;
         const int N = a.N;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, par ^= 1) {
             const int p = tile * 128 + row;
             int pi, pj;
             point_ij(p, N, pi, pj);
@@ -181,94 +206,336 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_forward(FwdArgs a) {
                 uint32_t acc = 0;
                 if (layer > 1) {
                     const int ai = gi & 1;
-                    mbar_wait(&acc_full[ai], acc_ph[ai]);
-                    acc_ph[ai] ^= 1;
-                    acc = tmem + (uint32_t)(ai * WP);
+                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
+                    mbar_wait(&acc_full[ai], (acc_ph >> ai) & 1u);
+                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
+                    acc_ph ^= 1u << ai;
+                    acc = (uint32_t)(ai * WP);
                     ++gi;
                     tc_fence_after();
                 }
-                // the previous bulk store of A_hi must have finished reading it
-                if (ep_tid == 0) bulk_wait_read0();
-                named_bar(1, EPI_THREADS);
                 const float *bias = sB + (layer - 1) * WP;
-#pragma unroll 1
+                uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
+                                row * 128 + pos * 16;
+                // TMEM loads run one chunk ahead of the math. t_hi of layers 1..L-1 reaches HBM by a
+                // bulk copy of the released A_hi chunk (issued by the MMA thread), so the epilogue
+                // issues no global stores there and its fence.proxy.async (a MEMBAR.ALL.CTA) does
+                // not wait on any; the last layer stores t_hi from registers.
+                uint32_t rbuf[16];
+                if (layer > 1) tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
+#pragma unroll
                 for (int c = 0; c < KC; ++c) {
-                    const int cc = c * 64 + hf * 32;
-                    float v[32];
+                    const int cc = c * 64 + wq * 16;
+                    float v[16];
                     if (layer == 1) {
 #pragma unroll
-                        for (int k = 0; k < 32; k += 2) {
+                        for (int k = 0; k < 16; k += 4) {
+                            const float4 w4a = lds_f4(sW1 + 2 * (cc + k)), w4b = lds_f4(sW1 + 2 * (cc + k) + 4);
+                            const float4 b4 = lds_f4(bias + cc + k);
+                            v[k] = fmaf(w4a.x, x, fmaf(w4a.y, y, b4.x));
+                            v[k + 1] = fmaf(w4a.z, x, fmaf(w4a.w, y, b4.y));
+                            v[k + 2] = fmaf(w4b.x, x, fmaf(w4b.y, y, b4.z));
+                            v[k + 3] = fmaf(w4b.z, x, fmaf(w4b.w, y, b4.w));
+                        }
+                    } else {
+                        tmem_wait_ld16(rbuf);
+#pragma unroll
+                        for (int k = 0; k < 16; k += 4) {
+                            const float4 b4 = lds_f4(bias + cc + k);
+                            v[k] = __uint_as_float(rbuf[k]) + b4.x;
+                            v[k + 1] = __uint_as_float(rbuf[k + 1]) + b4.y;
+                            v[k + 2] = __uint_as_float(rbuf[k + 2]) + b4.z;
+                            v[k + 3] = __uint_as_float(rbuf[k + 3]) + b4.w;
+                        }
+                        if (c + 1 < KC) tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
+                    }
+                    // tanh(z) = 1 - 2 / (1 + 2^(2 z log2 e)) for 16 elements as a skewed pipeline:
+                    // ex2 of element i, rcp of element i-2 and the finish (t, hi/lo split, fp16 pack)
+                    // of pair (i-5, i-4) are issued together, so MUFU and ALU work interleave
+                    float e[16], r[16];
+                    uint32_t hw[8], lw[8];
+#pragma unroll
+                    for (int i = 0; i < 16 + 5; ++i) {
+                        if (i < 16) e[i] = ex2_v(v[i] * 2.8853900817779268f);
+                        if (i >= 2 && i < 18) r[i - 2] = rcp_v(1.0f + e[i - 2]);
+                        if (i >= 5 && ((i - 5) & 1) == 0) {
+                            const int m = (i - 5) >> 1;
+                            if (m < 8) finish_pair(r[2 * m], r[2 * m + 1], hw[m], lw[m]);
+                        }
+                    }
+                    if (last) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) v[k] = fmaf(-2.0f, r[k], 1.0f);
+                    }
+                    if (!last) {
+                        const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
+                        st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);
+                        st_shared_v4(bh + off1, hw[4], hw[5], hw[6], hw[7]);
+                        st_shared_v4(bl + off0, lw[0], lw[1], lw[2], lw[3]);
+                        st_shared_v4(bl + off1, lw[4], lw[5], lw[6], lw[7]);
+                        // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
+                        if (lane == 0) mbar_arrive(&a_full[c]);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 16; k += 4) {
+                            const float4 w4 = lds_f4(sWo + cc + k);
+                            dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
+                        }
+                        if (swap)
+                            st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
+                        else
+                            st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+                    }
+                }
+            }
+            // output layer: net = W_out t_L + b_out; u = cutoff * net (4 partial dots per row)
+            sRed[(par * 4 + wq) * 128 + row] = dot;
+            named_bar(1, 32 * FWD_EPI_WARPS);
+            if (wq == 0) {
+                const float *r = sRed + par * 4 * 128 + row;
+                const float net = ((r[0] + r[128]) + (r[256] + r[384])) + sWo[WP];
+                a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
+}
+
+// ================================================================ forward v2: CTA pairs (cta_group::2)
+// Same epilogue as k_tc_forward, but two CTAs (one cluster, one TPC) run each hidden GEMM as ONE
+// M = 256 tcgen05.mma.cta_group::2 issued by the leader CTA: each CTA supplies its own tile's
+// activations (A, 128 rows) and HALF of every weight K-chunk (B, WP/2 rows), and receives its
+// 128 x WP accumulator in its own TMEM. Per SM this halves the weight stream (L2 traffic and
+// ring bytes), so the ring holds NST2 = 4 K-chunks in flight instead of 2 -- the 2-deep ring of
+// the 1-CTA kernel left the tensor pipe waiting on L2 latency (ncu: tensor 36 %, XU 45 %).
+// Readiness of the follower's data reaches the leader's MMA thread through remote mbarrier
+// arrivals (epilogue chunk releases: a_full counts 2 x 16 warps; weight halves: the follower's
+// MMA warp forwards its w_full completions to the leader's w_peer); MMA completion is committed
+// to both CTAs at once (multicast commit). A pair walks tile pairs (2j, 2j+1); when ntiles is odd
+// the follower's last tile is a dummy whose results are not stored.
+constexpr int NST2 = 4;
+
+template <int WP>
+__host__ __device__ constexpr uint32_t fwd2_smem_bytes(int L) {
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST2 * (WP / 2) * 128 +
+           (2 * WP + L * WP + WP + 1 + 2 * 4 * 128) * 4 + 32 * 8 + 16;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
+    constexpr int KC = WP / 64;
+    constexpr uint32_t WBLK = WP * 128;          // one K-chunk of the full weight block
+    constexpr uint32_t HB = (WP / 2) * 128;      // this CTA's half (rows [rank*WP/2, +WP/2))
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *A_hi = smem;
+    uint8_t *A_lo = A_hi + KC * CHUNK_BYTES;
+    uint8_t *Wr = A_lo + KC * CHUNK_BYTES;
+    float *sW1 = (float *)(Wr + NST2 * HB);
+    float *sB = sW1 + 2 * WP;
+    float *sWo = sB + a.L * WP;
+    float *sRed = sWo + WP + 1;
+    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
+    uint64_t *w_full = bars, *w_peer = bars + NST2, *w_empty = bars + 2 * NST2;
+    uint64_t *a_full = bars + 3 * NST2;           // [KC] (used in the leader)
+    uint64_t *acc_full = a_full + KC;             // [2]
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int ntp = (a.ntiles + 1) >> 1;          // tile pairs
+    for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
+    for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
+    for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST2; ++s) {
+            mbar_init(&w_full[s], 1);
+            mbar_init(&w_peer[s], 1);
+            mbar_init(&w_empty[s], 1);
+        }
+        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], 2 * FWD_EPI_WARPS);
+        mbar_init(&acc_full[0], 1);
+        mbar_init(&acc_full[1], 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc2(tmem_slot, 2 * WP);
+    tc_fence_before();
+    cluster_sync_all();   // barriers of both CTAs initialised before any remote arrival
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer (both CTAs): this CTA's half of every weight K-chunk
+        if (lane == 0 && a.G > 0) {
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int tp = pair; tp < ntp; tp += npairs)
+                for (int g = 0; g < a.G; ++g)
+                    for (int c = 0; c < KC; ++c) {
+                        mbar_wait_sleep(&w_empty[stage], ph ^ 1);
+                        mbar_arrive_expect_tx(&w_full[stage], HB);
+                        bulk_g2s(Wr + stage * HB, (const uint8_t *)a.Wf + (size_t)(g * KC + c) * WBLK + rank * HB, HB,
+                                 &w_full[stage]);
+                        if (++stage == NST2) { stage = 0; ph ^= 1; }
+                    }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && a.G > 0) {
+            if (leader) {
+                // ---------------- MMA issuer (leader only): M = 256 over the pair
+                constexpr uint32_t idesc = idesc_f16(256, WP, 0, 0);
+                int stage = 0;
+                uint32_t ph = 0, aph = 0;
+                int gi = 0;
+                const uint32_t ahi = smem_u32(A_hi), alo = smem_u32(A_lo), wr = smem_u32(Wr);
+                for (int tp = pair; tp < ntp; tp += npairs)
+                    for (int g = 0; g < a.G; ++g, ++gi) {
+                        const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
+                        for (int c = 0; c < KC; ++c) {
+                            mbar_wait_cluster(&a_full[c], aph);
+                            mbar_wait(&w_full[stage], ph);
+                            mbar_wait_cluster(&w_peer[stage], ph);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t bd = sdesc_sw128(wr + stage * HB + kk * 32, 16, 1024);
+                                const uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                const uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                mma2_f16(acc, dh, bd, idesc, (c | kk) != 0);
+                                mma2_f16(acc, dl, bd, idesc, 1u);
+                            }
+                            mma2_commit_mc(&w_empty[stage], 3);
+                            if (++stage == NST2) { stage = 0; ph ^= 1; }
+                        }
+                        aph ^= 1;
+                        mma2_commit_mc(&acc_full[gi & 1], 3);
+                    }
+            } else {
+                // ---------------- forwarder (follower): my weight half landed -> tell the leader
+                const uint32_t peer0 = mapa_shared(w_peer, 0);
+                int stage = 0;
+                uint32_t ph = 0;
+                for (int tp = pair; tp < ntp; tp += npairs)
+                    for (int g = 0; g < a.G; ++g)
+                        for (int c = 0; c < KC; ++c) {
+                            mbar_wait(&w_full[stage], ph);
+                            mbar_arrive_cluster(peer0 + stage * 8);
+                            if (++stage == NST2) { stage = 0; ph ^= 1; }
+                        }
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int wq = (warp - 2) >> 2;
+        const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
+        const int lg0 = 2 * wq;
+        const int pos = (lg0 ^ (row & 7)) & ~1;
+        const bool swap = (row & 1) != 0;
+        const uint32_t off0 = (uint32_t)(row * 128 + ((lg0 ^ (row & 7)) << 4));
+        const uint32_t off1 = (uint32_t)(row * 128 + (((lg0 + 1) ^ (row & 7)) << 4));
+        const uint32_t afull0 = mapa_shared(a_full, 0);   // the leader's chunk barriers
+        uint32_t acc_ph = 0u;
+        int gi = 0, par = 0;
+        const int N = a.N;
+        for (int tp = pair; tp < ntp; tp += npairs, par ^= 1) {
+            const int tile = 2 * tp + (int)rank;
+            const bool valid = tile < a.ntiles;
+            const int p = tile * 128 + row;
+            int pi, pj;
+            point_ij(p, N, pi, pj);
+            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            float dot = 0.0f;
+            for (int layer = 1; layer <= a.L; ++layer) {
+                const bool last = layer == a.L;
+                uint32_t acc = 0;
+                if (layer > 1) {
+                    const int ai = gi & 1;
+                    mbar_wait(&acc_full[ai], (acc_ph >> ai) & 1u);
+                    acc_ph ^= 1u << ai;
+                    acc = (uint32_t)(ai * WP);
+                    ++gi;
+                    tc_fence_after();
+                }
+                const float *bias = sB + (layer - 1) * WP;
+                uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
+                                row * 128 + pos * 16;
+#pragma unroll 1
+                for (int c = 0; c < KC; ++c) {
+                    const int cc = c * 64 + wq * 16;
+                    float v[16];
+                    if (layer == 1) {
+#pragma unroll
+                        for (int k = 0; k < 16; k += 2) {
                             const float4 w4 = *(const float4 *)(sW1 + 2 * (cc + k));
                             const float2 b2 = *(const float2 *)(bias + cc + k);
                             v[k] = fmaf(w4.x, x, fmaf(w4.y, y, b2.x));
                             v[k + 1] = fmaf(w4.z, x, fmaf(w4.w, y, b2.y));
                         }
                     } else {
-                        tmem_ld32(t_lane + acc + cc, v);
+                        tmem_ld16(t_lane + acc + cc, v);
 #pragma unroll
-                        for (int k = 0; k < 32; k += 4) {
+                        for (int k = 0; k < 16; k += 4) {
                             const float4 b4 = *(const float4 *)(bias + cc + k);
                             v[k] += b4.x; v[k + 1] += b4.y; v[k + 2] += b4.z; v[k + 3] += b4.w;
                         }
                     }
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) v[k] = tanh_fast(v[k]);
+                    for (int k = 0; k < 16; ++k) v[k] = tanh_fast(v[k]);
                     if (last) {
 #pragma unroll
-                        for (int k = 0; k < 32; k += 4) {
+                        for (int k = 0; k < 16; k += 4) {
                             const float4 w4 = *(const float4 *)(sWo + cc + k);
                             dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
                         }
                     }
-                    const uint32_t base_hi = smem_u32(A_hi) + c * CHUNK_BYTES + row * 128;
-                    const uint32_t base_lo = smem_u32(A_lo) + c * CHUNK_BYTES + row * 128;
+                    uint32_t hw[8], lw[8];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int lg = hf * 4 + j;
-                        const uint32_t off = (uint32_t)((lg ^ (row & 7)) << 4);
-                        uint32_t hw[4], lw[4];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            // split t = hi + lo: hi = t with the low 13 mantissa bits cleared (exact in
-                            // fp16's 10-bit mantissa), lo = t - hi exactly in fp32, then rounded to fp16
-                            const float t0 = v[8 * j + 2 * m], t1 = v[8 * j + 2 * m + 1];
-                            const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
-                            const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
-                            hw[m] = pack_half2(h0, h1);
-                            lw[m] = pack_half2(t0 - h0, t1 - h1);
-                        }
-                        st_shared_v4(base_hi + off, hw[0], hw[1], hw[2], hw[3]);
-                        if (!last) st_shared_v4(base_lo + off, lw[0], lw[1], lw[2], lw[3]);
+                    for (int m = 0; m < 8; ++m) {
+                        const float t0 = v[2 * m], t1 = v[2 * m + 1];
+                        const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
+                        const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
+                        hw[m] = pack_half2(h0, h1);
+                        lw[m] = pack_half2(t0 - h0, t1 - h1);
+                    }
+                    if (valid) {
+                        if (swap)
+                            st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
+                        else
+                            st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
                     }
                     if (!last) {
-                        // release chunk c to the next GEMM (every epilogue thread arrives)
+                        const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
+                        st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);
+                        st_shared_v4(bh + off1, hw[4], hw[5], hw[6], hw[7]);
+                        st_shared_v4(bl + off0, lw[0], lw[1], lw[2], lw[3]);
+                        st_shared_v4(bl + off1, lw[4], lw[5], lw[6], lw[7]);
                         tc_fence_before();
                         fence_proxy_async_smem();
-                        mbar_arrive(&a_full[c]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(afull0 + c * 8);
                     }
                 }
-                // stream t_hi of this layer to HBM (backward operand)
-                fence_proxy_async_smem();
-                named_bar(1, EPI_THREADS);
-                if (ep_tid == 0) {
-                    __half *dst = a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES);
-                    bulk_s2g(dst, A_hi, KC * CHUNK_BYTES);
-                    bulk_commit();
-                }
             }
-            // output layer: net = W_out t_L + b_out; u = cutoff * net
-            sRed[hf * 128 + row] = dot;
-            named_bar(1, EPI_THREADS);
-            if (hf == 0) {
-                float net = dot + sRed[128 + row] + sWo[WP];
+            sRed[(par * 4 + wq) * 128 + row] = dot;
+            named_bar(1, 32 * FWD_EPI_WARPS);
+            if (wq == 0 && valid) {
+                const float *r = sRed + par * 4 * 128 + row;
+                const float net = ((r[0] + r[128]) + (r[256] + r[384])) + sWo[WP];
                 a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
             }
         }
-        if (ep_tid == 0) bulk_wait0();
     }
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 2 * WP);
+    cluster_sync_all();
+    if (warp == 1) tmem_dealloc2(tmem, 2 * WP);
 }
 
 // ================================================================ backward: output layer
@@ -992,6 +1259,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 }
 
 // ================================================================ weight re-layout
+
+
 // After each Adam step: fp16 copies of the hidden weights in the B-operand block layout
 // (forward: rows = out features; backward-dX: rows = in features), zero padded to WP.
 __global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float *__restrict__ theta,
@@ -1034,6 +1303,7 @@ __global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float 
 template <int WP>
 static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
+    cudaFuncSetAttribute(k_tc_forward2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd2_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
         cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
     } else {
@@ -1056,7 +1326,12 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     }
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
+    {
+        const char *e = getenv("CRVPINN_FWD_PAIRS");   // tuning knob: CTA-pair (cta_group::2) forward
+        b.fwd_pairs = e && e[0] == '1';
+        const int ntp = (b.ntiles + 1) / 2;
+        b.grid_fwd = b.fwd_pairs ? 2 * (ntp < nsm / 2 ? ntp : nsm / 2) : (b.ntiles < nsm ? b.ntiles : nsm);
+    }
     {
         // WP >= 128: clusters of NS = WP/128 CTAs (k_tc_bwd2); WP = 64: one CTA per "pair"
         const int NS = WP >= 128 ? WP / 128 : 1;
@@ -1147,8 +1422,36 @@ void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cud
 
 template <int WP>
 static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
-    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u};
-    k_tc_forward<WP><<<b.grid_fwd, TC_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+    static long long *trace = nullptr;
+    const char *te = getenv("CRVPINN_FWD_TRACE");
+    if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
+    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr};
+    if (te) {
+        k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+        cudaStreamSynchronize(s);
+        static long long h[4096];
+        cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+        FILE *f = fopen(te, "wb");
+        if (f) { fwrite(h, 8, 4096, f); fclose(f); }
+        return;
+    }
+    if (b.fwd_pairs) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(b.grid_fwd);
+        cfg.blockDim = dim3(FWD_THREADS);
+        cfg.dynamicSmemBytes = fwd2_smem_bytes<WP>(b.L);
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_tc_forward2<WP>, a);
+    } else {
+        k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+    }
 }
 
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {

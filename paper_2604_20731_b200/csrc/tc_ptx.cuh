@@ -144,6 +144,11 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 __device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
+__device__ __forceinline__ float4 lds_f4(const float *p) {   // explicit shared-space 16-byte load
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
+    return v;
+}
 __device__ __forceinline__ void ld_shared_v4(uint32_t saddr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
     asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(saddr));
 }
@@ -164,6 +169,36 @@ __device__ __forceinline__ float tanh_fast(float x) {
     const float e = ex2_approx(x * 2.8853900817779268f);
     return fmaf(-2.0f, rcp_approx(1.0f + e), 1.0f);
 }
+// Volatile MUFU wrappers: their relative order is kept by the compiler, which lets a hand-skewed
+// loop interleave MUFU issue with the ALU work of other elements (4 warps per SMSP otherwise run
+// their MUFU phases in lockstep and leave the XU pipe idle during the ALU phases).
+__device__ __forceinline__ float ex2_v(float x) {
+    float y;
+    asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_v(float x) {
+    float y;
+    asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// t = 1 - 2 r for two elements, split t = hi + lo (hi: low 13 mantissa bits cleared, exact in
+// fp16; lo = t - hi exact in fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
+__device__ __forceinline__ void finish_pair(float r0, float r1, uint32_t &hw, uint32_t &lw) {
+    asm volatile(
+        "{\n\t.reg .f32 t0, t1, h0, h1, l0, l1;\n\t.reg .b32 b0, b1;\n\t"
+        "fma.rn.f32 t0, %2, 0fC0000000, 0f3F800000;\n\t"
+        "fma.rn.f32 t1, %3, 0fC0000000, 0f3F800000;\n\t"
+        "mov.b32 b0, t0;\n\tmov.b32 b1, t1;\n\t"
+        "and.b32 b0, b0, 0xFFFFE000;\n\tand.b32 b1, b1, 0xFFFFE000;\n\t"
+        "mov.b32 h0, b0;\n\tmov.b32 h1, b1;\n\t"
+        "sub.f32 l0, t0, h0;\n\tsub.f32 l1, t1, h1;\n\t"
+        "cvt.rn.f16x2.f32 %0, h1, h0;\n\t"
+        "cvt.rn.f16x2.f32 %1, l1, l0;\n\t}"
+        : "=r"(hw), "=r"(lw)
+        : "f"(r0), "f"(r1));
+}
+
 // mbarrier wait with a suspend-time hint: the waiting thread sleeps in hardware instead of
 // spinning (used by the single-thread producer / MMA roles so they do not steal issue slots).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
@@ -174,6 +209,25 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(1000000)
         : "memory");
+}
+
+// asynchronous 32x32b.x16 TMEM load: the registers are valid only after tmem_wait_ld16 on them
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+// wait for all outstanding TMEM loads; the fake in/out operands keep every use of r after it
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15])
+                 :
+                 : "memory");
 }
 
 // ---------------------------------------------------------------- clusters
@@ -222,6 +276,56 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// wait with cluster-scope acquire (pairs with mbar_arrive_cluster from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// D[tmem of both CTAs] (+)= A[smem of both CTAs] * B[smem of both CTAs]^T, M = 256 (128 rows per CTA);
+// issued by the leader CTA only
+__device__ __forceinline__ void mma2_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of ctaMask when the pair's MMAs complete
+__device__ __forceinline__ void mma2_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 
 }  // namespace ptx
