@@ -66,12 +66,6 @@ namespace crv {
 // fields.cu
 void launch_alpha(const float *K, const float *S, float *alpha, int N, float mobility, cudaStream_t s);
 void launch_scale_b(const float *f, float *b, int N, cudaStream_t s);
-void launch_residual(const float *u, const float *alpha, const float *b, float *res, int N, cudaStream_t s);
-void launch_loss_partials(const float *res, const float *q, double *part, int n2, int nblk, cudaStream_t s);
-void launch_loss_final(const double *part, int nblk, DevState *st, double *hist, int n_hist,
-                       double beta1, double beta2, cudaStream_t s);
-void launch_adjoint(const float *q, const float *alpha, float *gbar, float *gu_lattice, int N,
-                    DevState *st, int track_max, cudaStream_t s);
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 void launch_begin_call(DevState *st, cudaStream_t s);
@@ -79,17 +73,20 @@ void launch_begin_call(DevState *st, cudaStream_t s);
 int reduce_groups(const RedJob *jobs, int njobs);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s);
-int loss_partial_blocks(int n2);
 // gram.cu
 struct GramConsts {
     float2 *tw = nullptr;   // FFT twiddles exp(-2 pi i k / 2N), k < N
-    float *etab = nullptr;  // per-mode Thomas pivots 1/w_j, [n][n]
-    float *work = nullptr;  // 2 n^2 scratch
+    float *etab = nullptr;  // per-mode Thomas pivots 1/w_j, mode-major [a][j]
+    float *work = nullptr;  // 2 n^2 scratch (R^, Z^)
     int logM = 0, seg = 0;
 };
 GramConsts gram_make_constants(int N);
 void gram_free_constants(GramConsts &c);
-void launch_gram_apply(const float *res, float *q, const GramConsts &c, int N, cudaStream_t s);
+// A2-A5 fused: residual + DST, tridiagonal solves, inverse DST + loss partials, adjoint + loss
+int field_chain_loss_blocks(int N);
+void launch_field_chain(const float *u, const float *alpha, const float *b, float *res, float *q, float *gbar,
+                        float *gu_lat, double *loss_part, const GramConsts &c, int N, DevState *st, int track_max,
+                        double *hist, int n_hist, double beta1, double beta2, int advance, cudaStream_t s);
 // mlp_simt.cu -- fp32 FFMA MLP path (CRVPINN_PREC_FP32)
 struct MlpPlan {
     long offW[CRV_MAX_LAYERS], offB[CRV_MAX_LAYERS];   // partial-buffer offsets per layer

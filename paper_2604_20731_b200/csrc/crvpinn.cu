@@ -110,14 +110,9 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
     else simt_forward(net, ctx->theta, ctx->simt, ctx->u, s);
     if (ev) record(ev[1], s);
     // A2-A5: residual, Gram solve, loss, adjoint
-    int n = net.n;
-    launch_residual(ctx->u, ctx->alpha, ctx->b, ctx->res, net.N, s);
-    launch_gram_apply(ctx->res, ctx->q, ctx->gram, net.N, s);
-    launch_loss_partials(ctx->res, ctx->q, ctx->loss_part, n * n, ctx->loss_nblk, s);
-    launch_loss_final(ctx->loss_part, ctx->loss_nblk, ctx->st, hist, n_hist,
-                      train ? ctx->opts.beta1 : -1.0, ctx->opts.beta2, s);
     float *gbar = tc ? ctx->tc.gbar : ctx->simt.gbar;
-    launch_adjoint(ctx->q, ctx->alpha, gbar, ctx->gu_lat, net.N, ctx->st, tc ? 1 : 0, s);
+    launch_field_chain(ctx->u, ctx->alpha, ctx->b, ctx->res, ctx->q, gbar, ctx->gu_lat, ctx->loss_part, ctx->gram,
+                       net.N, ctx->st, tc ? 1 : 0, hist, n_hist, ctx->opts.beta1, ctx->opts.beta2, train ? 1 : 0, s);
     if (ev) record(ev[2], s);
     // A6-A7: backward and deterministic weight-gradient reduction
     if (tc) tc_backward(net, ctx->tc, ctx->st, ctx->grad, s);
@@ -136,7 +131,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
 static int launches_per_iter(const crvpinn_ctx *ctx) {
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
     int mlp = tc ? tc_launches(ctx->net) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
-    return mlp + 1 /*residual*/ + 3 /*gram*/ + 2 /*loss*/ + 1 /*adjoint*/ + 1 /*adam*/;
+    return mlp + 4 /*residual+DST, tridiagonal, inverse DST+loss, adjoint+loss final*/ + 1 /*adam*/;
 }
 
 static void drop_graphs(crvpinn_ctx *ctx) {
@@ -284,7 +279,7 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     DALLOC(ctx->res, (long)n * n); DALLOC(ctx->q, (long)n * n);
     ctx->gram = gram_make_constants(N);
     if (!ctx->gram.etab || !ctx->gram.work) return fail(ctx, CRVPINN_ENOMEM, "Gram constants allocation failed");
-    ctx->loss_nblk = loss_partial_blocks(n * n);
+    ctx->loss_nblk = field_chain_loss_blocks(N);
     DALLOC(ctx->loss_part, ctx->loss_nblk);
     DALLOC(ctx->st, 1); DALLOC(ctx->snap_st, 1);
     DALLOC(ctx->theta, np); DALLOC(ctx->m, np); DALLOC(ctx->v, np); DALLOC(ctx->grad, np);

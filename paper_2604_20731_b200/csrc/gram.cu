@@ -1,4 +1,6 @@
-// gram.cu -- A3: q = G^-1 RES for the Gram matrix of Eq. 26.
+// gram.cu -- A2-A5 as one fused chain of four kernels: the residual stencil
+// (Eq. 25), q = G^-1 RES for the Gram matrix of Eq. 26, LOSS = RES^T q
+// (Eq. 27) and the adjoint dLOSS/du = 2 A(alpha) q.
 //
 // G = h^-2 (T_x (x) I + I (x) T_y), T = tridiag(-1, 2, -1) of size n = N-1, is a Kronecker SUM.
 // The paper's per-axis Thomas shortcut is for the Kronecker-PRODUCT mass
@@ -6,11 +8,19 @@
 // transform along x:
 //   1. R^[j][a] = sum_k RES[j][k] S[k][a]        (DST-I along x, S_ka = sqrt(2/N) sin(pi k a/N))
 //   2. for every mode a: (lam_a I + T_y) Z^[:,a] = h^2 R^[:,a],  lam_a = 4 sin^2(pi a/(2N))
-//      -- n independent shifted tridiagonal systems along y (batched, one warp each)
 //   3. q[j][k] = sum_a Z^[j][a] S[a][k]          (the inverse DST-I along x: S = S^T = S^-1)
-// The "factorise once" of Eq. 28 is the per-mode Thomas factor table e[a][j] (built once at
-// create, fp64 on the host); every iteration only substitutes. The DSTs are length-2N complex
-// FFTs in shared memory (two real rows packed as real/imaginary parts of one complex sequence).
+// The "factorise once" of Eq. 28 is the per-mode Thomas pivot table e[j][a] (built once at
+// create, fp64 on the host); every iteration only substitutes.
+//
+// RES and q are row-major [j][k]; R^, Z^ and the pivots are mode-major [a][j]:
+//   k_res_dst   : one block per 2 rows: RES of rows j0, j0+1 from the stencil (u, alpha, b),
+//                 stored, and their DST-I via one length-2N complex FFT in shared memory
+//                 (the two real rows packed as real/imaginary parts).
+//   k_tridiag   : one warp per mode, Thomas sweeps as warp-level affine scans.
+//   k_idst_loss : inverse DST of 2 rows -> q, plus this block's sum of RES . q (fp64).
+//   k_adj_final : adjoint stencil on q -> dLOSS/dnet at every MLP point (+ max |.| for the
+//                 tensor path's gradient scaling); block 0 also finishes LOSS (fixed-order
+//                 fp64 sum of the k_idst_loss partials) and the per-iteration bookkeeping.
 #include "common.cuh"
 #include <cmath>
 #include <vector>
@@ -20,34 +30,10 @@ namespace crv {
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ long latx(int i, int j, int N) { return (long)j * (N + 1) + i; }
 
-// DST-I of two rows per block via a length-M = 2N FFT of the odd extensions packed as
-// y = y1 + i y2:  Y = -2i X1 + 2 X2  =>  X1_k = -Im(Y_k)/2, X2_k = Re(Y_k)/2.
-// in/out are n x n, addressed (row j, index k) either row-major (j*n+k) or mode-major (k*n+j).
-__global__ void k_dst_rows(const float *__restrict__ in, float *__restrict__ out, const float2 *__restrict__ tw,
-                           int N, int logM, int in_mode_major, int out_mode_major, float scale) {
-    extern __shared__ float2 sa[];
-    const int n = N - 1, M = 2 * N;
-    const int j0 = 2 * blockIdx.x, j1 = j0 + 1;
-    const bool has1 = j1 < n;
-    for (int m = threadIdx.x; m < M; m += blockDim.x) {
-        int src = -1;
-        float sgn = 1.0f;
-        if (m >= 1 && m <= n) src = m - 1;
-        else if (m > N) { src = M - m - 1; sgn = -1.0f; }
-        float v1 = 0.0f, v2 = 0.0f;
-        if (src >= 0) {
-            if (in_mode_major) {
-                v1 = in[(long)src * n + j0];
-                if (has1) v2 = in[(long)src * n + j1];
-            } else {
-                v1 = in[(long)j0 * n + src];
-                if (has1) v2 = in[(long)j1 * n + src];
-            }
-        }
-        sa[__brev((unsigned)m) >> (32 - logM)] = make_float2(sgn * v1, sgn * v2);
-    }
-    __syncthreads();
+// In-place radix-2 FFT of sa[0..M) (input already in bit-reversed order).
+__device__ __forceinline__ void fft_inplace(float2 *sa, const float2 *tw, int M, int logM) {
     for (int lh = 0; lh < logM; ++lh) {
         const int hs = 1 << lh;
         const int tstride = M >> (lh + 1);
@@ -61,16 +47,52 @@ __global__ void k_dst_rows(const float *__restrict__ in, float *__restrict__ out
         }
         __syncthreads();
     }
+}
+
+// DST-I of two rows via a length-M = 2N FFT of their odd extensions packed as y = y1 + i y2:
+// Y = -2i X1 + 2 X2  =>  X1_k = -Im(Y_k)/2, X2_k = Re(Y_k)/2.
+// Stage 1: RES_kl = a_{k-1,l}(u_kl-u_{k-1,l}) + a_{k,l-1}(u_kl-u_{k,l-1}) + a_kl(2u_kl-u_{k+1,l}-u_{k,l+1}) - b_kl
+// (the closed form of (alpha grad+ u, grad+ delta_kl)_h - (RHS, delta_kl)_h, reading R16).
+__global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__ alpha, const float *__restrict__ bvec,
+                          float *__restrict__ res, float *__restrict__ rhat, const float2 *__restrict__ tw, int N,
+                          int logM, float scale, DevState *st) {
+    extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
+    const int n = N - 1, M = 2 * N;
+    float2 *stw = sa + M;
+    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    const int j0 = 2 * blockIdx.x;
+    const bool has1 = j0 + 1 < n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->gmax_bits = 0u;   // k_adj_final folds this iteration's max
+    // odd extension y_m: y_0 = y_N = 0, y_{k+1} = RES_k, y_{M-1-k} = -RES_k (bit-reversed slots)
+    const int shift = 32 - logM;
+    if (threadIdx.x == 0) {
+        sa[0] = make_float2(0.0f, 0.0f);
+        sa[__brev((unsigned)N) >> shift] = make_float2(0.0f, 0.0f);
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        float v[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int j = j0 + r;
+            if (r == 1 && !has1) break;
+            const int i = k + 1, l = j + 1;   // lattice node of RES[j][k]
+            const float uc = u[latx(i, l, N)];
+            const float rr = alpha[latx(i - 1, l, N)] * (uc - u[latx(i - 1, l, N)]) +
+                             alpha[latx(i, l - 1, N)] * (uc - u[latx(i, l - 1, N)]) +
+                             alpha[latx(i, l, N)] * ((uc - u[latx(i + 1, l, N)]) + (uc - u[latx(i, l + 1, N)])) -
+                             bvec[latx(i, l, N)];
+            res[(long)j * n + k] = rr;
+            v[r] = rr;
+        }
+        sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v[0], v[1]);
+        sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v[0], -v[1]);
+    }
+    __syncthreads();
+    fft_inplace(sa, stw, M, logM);
     for (int k = threadIdx.x + 1; k <= n; k += blockDim.x) {
         const float2 Y = sa[k];
-        const float x1 = -0.5f * Y.y * scale, x2 = 0.5f * Y.x * scale;
-        if (out_mode_major) {
-            out[(long)(k - 1) * n + j0] = x1;
-            if (has1) out[(long)(k - 1) * n + j1] = x2;
-        } else {
-            out[(long)j0 * n + (k - 1)] = x1;
-            if (has1) out[(long)j1 * n + (k - 1)] = x2;
-        }
+        rhat[(long)(k - 1) * n + j0] = -0.5f * Y.y * scale;   // mode-major [a][j]
+        if (has1) rhat[(long)(k - 1) * n + j0 + 1] = 0.5f * Y.x * scale;
     }
 }
 
@@ -79,7 +101,7 @@ __global__ void k_dst_rows(const float *__restrict__ in, float *__restrict__ out
 // e_j = 1/w_j the precomputed pivots) and evaluated as warp-level affine scans: each lane owns a
 // contiguous segment, segment maps are combined with __shfl_up/__shfl_down (Kogge-Stone), then
 // every lane replays its segment. Rows are staged in shared memory (odd segment stride: no bank
-// conflicts).
+// conflicts). R^, Z^ and the pivot table are mode-major ([a][j]) so each warp's row is contiguous.
 constexpr int TRI_WARPS = 4;
 
 __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restrict__ etab, float *__restrict__ z,
@@ -144,6 +166,120 @@ __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restric
     for (int j = lane; j < n; j += 32) zo[j] = sr[j];
 }
 
+
+// Inverse DST of two rows of z (mode-major input) -> q (row-major), and this block's part of
+// LOSS = sum RES q.
+__global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict__ res, float *__restrict__ q,
+                            double *__restrict__ part, const float2 *__restrict__ tw, int N, int logM, float scale) {
+    extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
+    __shared__ double sred[32];
+    const int n = N - 1, M = 2 * N;
+    float2 *stw = sa + M;
+    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    const int j0 = 2 * blockIdx.x;
+    const bool has1 = j0 + 1 < n;
+    const int shift = 32 - logM;
+    if (threadIdx.x == 0) {
+        sa[0] = make_float2(0.0f, 0.0f);
+        sa[__brev((unsigned)N) >> shift] = make_float2(0.0f, 0.0f);
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const float v1 = z[(long)k * n + j0], v2 = has1 ? z[(long)k * n + j0 + 1] : 0.0f;   // mode-major
+        sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v1, v2);
+        sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v1, -v2);
+    }
+    __syncthreads();
+    fft_inplace(sa, stw, M, logM);
+    double acc = 0.0;
+    for (int k = threadIdx.x + 1; k <= n; k += blockDim.x) {
+        const float2 Y = sa[k];
+        const float q1 = -0.5f * Y.y * scale, q2 = 0.5f * Y.x * scale;
+        q[(long)j0 * n + (k - 1)] = q1;
+        acc += (double)(res[(long)j0 * n + (k - 1)] * q1);
+        if (has1) {
+            q[(long)(j0 + 1) * n + (k - 1)] = q2;
+            acc += (double)(res[(long)(j0 + 1) * n + (k - 1)] * q2);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+// g_u = dLOSS/du = 2 A(alpha) q (A symmetric: the same stencil on q, q = 0 off the interior),
+// gbar_p = g_u * cutoff(x_p, y_p) at every MLP point p = (i,j) in [1..N]^2 (zero on the rows
+// i = N or j = N). With track_max the block maxima of |gbar| are folded into DevState::gmax_bits
+// (order-independent, deterministic). Block 0 finishes LOSS (fixed-order fp64 sum) and the
+// bookkeeping: history slot, non-finite flag, Adam bias corrections for step t+1 (advance).
+__global__ void k_adj_final(const float *__restrict__ q, const float *__restrict__ alpha, float *__restrict__ gbar,
+                            float *__restrict__ gu_lat, int N, DevState *st, int track_max,
+                            const double *__restrict__ part, int nblk, double *hist, int n_hist, double beta1,
+                            double beta2, int advance) {
+    __shared__ float smax[8];
+    __shared__ double sh[256];
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    float g = 0.0f, gb = 0.0f;
+    const int n = N - 1;
+    if (p < N * N) {
+        int i, j;
+        point_ij(p, N, i, j);
+        if (i <= n && j <= n) {
+            auto Q = [&](int a, int c) -> float {
+                return (a >= 1 && a <= n && c >= 1 && c <= n) ? q[(long)(c - 1) * n + (a - 1)] : 0.0f;
+            };
+            const float qc = Q(i, j);
+            const float aq = alpha[latx(i - 1, j, N)] * (qc - Q(i - 1, j)) + alpha[latx(i, j - 1, N)] * (qc - Q(i, j - 1)) +
+                             alpha[latx(i, j, N)] * ((qc - Q(i + 1, j)) + (qc - Q(i, j + 1)));
+            g = 2.0f * aq;
+            const float x = (float)i / (float)N, y = (float)j / (float)N;
+            gb = g * cutoff(x, y);
+        }
+        gbar[p] = gb;
+        if (gu_lat) gu_lat[latx(i, j, N)] = g;
+    }
+    if (track_max) {
+        float m = fabsf(gb);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < 8; ++w) m = fmaxf(m, smax[w]);
+            if (m > 0.0f) atomicMax(&st->gmax_bits, __float_as_uint(m));
+        }
+    }
+    if (blockIdx.x == 0) {
+        double acc = 0.0;
+        for (int b = threadIdx.x; b < nblk; b += blockDim.x) acc += part[b];
+        sh[threadIdx.x] = acc;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const double loss = sh[0];
+            st->loss = loss;
+            if (hist != nullptr && st->it < n_hist) hist[st->it] = loss;
+            st->it += 1;
+            if (!isfinite(loss)) st->nonfinite = 1;
+            if (advance && !st->nonfinite) {
+                const int64_t t = st->t + 1;
+                st->bc1 = 1.0 - pow(beta1, (double)t);
+                st->bc2 = 1.0 - pow(beta2, (double)t);
+            }
+        }
+    }
+}
+
+static int fft_threads(int N) { return N < 32 ? 32 : (N < 512 ? N : 512); }   // M/2 butterflies per stage, >= 1 warp
+
 GramConsts gram_make_constants(int N) {
     GramConsts c{};
     const int n = N - 1, M = 2 * N;
@@ -157,6 +293,7 @@ GramConsts gram_make_constants(int N) {
         const double ang = -2.0 * M_PI * (double)k / (double)M;
         tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
     }
+    // Thomas pivots e[a][j] = 1/w_j of the (lam_a + 2, -1) tridiagonal, mode-major
     std::vector<float> e((size_t)n * n);
     for (int a = 0; a < n; ++a) {
         const double s = std::sin(M_PI * (double)(a + 1) / (2.0 * N));
@@ -172,10 +309,11 @@ GramConsts gram_make_constants(int N) {
     cudaMalloc(&c.work, sizeof(float) * 2 * (size_t)n * n);
     cudaMemcpy(c.tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(c.etab, e.data(), sizeof(float) * e.size(), cudaMemcpyHostToDevice);
-    const int smem_fft = (int)(sizeof(float2) * M);
-    const int smem_tri = (int)(sizeof(float) * TRI_WARPS * 2 * 32 * c.seg);
-    cudaFuncSetAttribute(k_dst_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);
-    cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tri);
+    const int smem_fft = (int)(sizeof(float2) * (M + M / 2));
+    cudaFuncSetAttribute(k_res_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);
+    cudaFuncSetAttribute(k_idst_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);
+    cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(float) * TRI_WARPS * 2 * 32 * c.seg));
     return c;
 }
 
@@ -186,17 +324,23 @@ void gram_free_constants(GramConsts &c) {
     c = GramConsts{};
 }
 
-void launch_gram_apply(const float *res, float *q, const GramConsts &c, int N, cudaStream_t s) {
+int field_chain_loss_blocks(int N) { return N / 2; }   // ceil((N-1)/2) rows pairs
+
+void launch_field_chain(const float *u, const float *alpha, const float *b, float *res, float *q, float *gbar,
+                        float *gu_lat, double *loss_part, const GramConsts &c, int N, DevState *st, int track_max,
+                        double *hist, int n_hist, double beta1, double beta2, int advance, cudaStream_t s) {
     const int n = N - 1, M = 2 * N;
     const float h = 1.0f / (float)N;
     const float nrm = sqrtf(2.0f / (float)N);
-    float *rhat = c.work, *zhat = c.work + (size_t)n * n;
-    const int fft_threads = M / 2 < 512 ? M / 2 : 512;
+    float *rhat = c.work, *z = c.work + (size_t)n * n;
     const int rows = (n + 1) / 2;
-    k_dst_rows<<<rows, fft_threads, sizeof(float2) * M, s>>>(res, rhat, c.tw, N, c.logM, 0, 1, nrm);
+    k_res_dst<<<rows, fft_threads(N), sizeof(float2) * (M + M / 2), s>>>(u, alpha, b, res, rhat, c.tw, N, c.logM, nrm, st);
     k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(
-        rhat, c.etab, zhat, n, c.seg, h * h);
-    k_dst_rows<<<rows, fft_threads, sizeof(float2) * M, s>>>(zhat, q, c.tw, N, c.logM, 1, 0, nrm);
+        rhat, c.etab, z, n, c.seg, h * h);
+    k_idst_loss<<<rows, fft_threads(N), sizeof(float2) * (M + M / 2), s>>>(z, res, q, loss_part, c.tw, N, c.logM, nrm);
+    const int P = N * N;
+    k_adj_final<<<ceil_div(P, 256), 256, 0, s>>>(q, alpha, gbar, gu_lat, N, st, track_max, loss_part, rows, hist,
+                                                 n_hist, beta1, beta2, advance);
 }
 
 }  // namespace crv

@@ -903,7 +903,9 @@ struct Bwd2Args {
     float *part_dx;       // [npairs][3*WP]
     float *part_dw;       // [npairs][WP*WP]   rows = out features
     DevState *st;
+    long long *trace;     // debug timeline (CTA 0), nullptr normally
 };
+#define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
 template <int WP>
 struct B2 {
@@ -989,7 +991,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], MASK);
                 }
                 const int b = k & 1;
+                BTRACE(k * 8 + 0);
                 mbar_wait_sleep(&tempty[b], ((k >> 1) & 1) ^ 1);
+                BTRACE(k * 8 + 1);
                 mbar_arrive_expect_tx(&tfull[b], 2 * CHUNK_BYTES);
                 bulk_g2s(Tr + b * 2 * CHUNK_BYTES,
                          (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
@@ -1008,7 +1012,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 const int b = k & 1;
                 const int slot0 = dn % DS;
                 mbar_wait(&tfull[b], (k >> 1) & 1);
+                BTRACE(k * 8 + 2);
                 mbar_wait(&xempty[b], ((k >> 1) & 1) ^ 1);
+                BTRACE(k * 8 + 7);
                 tc_fence_after();
                 const uint32_t accx = tmem + (uint32_t)(b * 128);
                 // chunk pairs (2h, 2h+1): dX over those K chunks, then the dW^T N-half h, then release
@@ -1038,6 +1044,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
                 }
                 mma_commit(&xfull[b]);
+                BTRACE(k * 8 + 3);
                 mma_commit(&tempty[b]);
                 dn += KC;
             }
@@ -1131,7 +1138,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            if (warp == 2 && lane == 0) BTRACE(kk * 8 + 4);
             mbar_wait(&xfull[b], (kk >> 1) & 1);
+            if (warp == 2 && lane == 0) BTRACE(kk * 8 + 5);
             tc_fence_after();
             const uint32_t tb = smem_u32(Tr) + (uint32_t)((b * 2 + hf) * CHUNK_BYTES + row * 128);
             uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
@@ -1181,6 +1190,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
+                if (warp == 2) BTRACE(kk * 8 + 6);
                 mbar_arrive(&xempty[b]);
                 mbar_arrive(&tempty[b]);
             }
@@ -1488,8 +1498,22 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
                        b.gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
-                       b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st};
+                       b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr};
+            static long long *trace = nullptr;
+            const char *te = getenv("CRVPINN_BWD_TRACE");
+            if (te && g == 1) {
+                if (!trace) cudaMalloc(&trace, 4096 * 8);
+                cudaMemset(trace, 0, 4096 * 8);
+                a.trace = trace;
+            }
             cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP>, a);
+            if (te && g == 1) {
+                cudaStreamSynchronize(s);
+                static long long h[4096];
+                cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+                FILE *f = fopen(te, "wb");
+                if (f) { fwrite(h, 8, 4096, f); fclose(f); }
+            }
         }
     } else {
         k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
