@@ -21,6 +21,9 @@
 #include "../../include/crvpinn.h"
 #include <math.h>
 #include <cstdlib>
+#ifndef CRV_TANH_MIX
+#define CRV_TANH_MIX 1
+#endif
 
 namespace crv {
 
@@ -69,6 +72,7 @@ struct FwdArgs {
 
 
 
+constexpr float TANH_C = 2.8853900817779268f;   // 2 log2(e): tanh(z) = 1 - 2 / (1 + 2^(TANH_C z))
 constexpr int FWD_EPI_WARPS = 16;                       // 4 per TMEM lane quarter
 constexpr int FWD_THREADS = 64 + 32 * FWD_EPI_WARPS;     // producer warp + MMA warp + epilogue
 
@@ -241,23 +245,31 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         tmem_wait_ld16(rbuf);
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
-                            const float4 b4 = lds_f4(bias + cc + k);
-                            v[k] = __uint_as_float(rbuf[k]) + b4.x;
-                            v[k + 1] = __uint_as_float(rbuf[k + 1]) + b4.y;
-                            v[k + 2] = __uint_as_float(rbuf[k + 2]) + b4.z;
-                            v[k + 3] = __uint_as_float(rbuf[k + 3]) + b4.w;
+                            const float4 b4 = lds_f4(bias + cc + k);   // 2 log2(e) b
+                            v[k] = fmaf(__uint_as_float(rbuf[k]), TANH_C, b4.x);
+                            v[k + 1] = fmaf(__uint_as_float(rbuf[k + 1]), TANH_C, b4.y);
+                            v[k + 2] = fmaf(__uint_as_float(rbuf[k + 2]), TANH_C, b4.z);
+                            v[k + 3] = fmaf(__uint_as_float(rbuf[k + 3]), TANH_C, b4.w);
                         }
                         if (c + 1 < KC) tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
                     }
-                    // tanh(z) = 1 - 2 / (1 + 2^(2 z log2 e)) for 16 elements as a skewed pipeline:
+                    // v = 2 log2(e) z (the fp32 first layer and biases arrive pre-scaled by
+                    // k_tc_refresh; the fp16 GEMM weights do not -- that was measured less accurate)
+                    // tanh(z) = 1 - 2 / (1 + 2^v) for 16 elements as a skewed pipeline:
                     // ex2 of element i, rcp of element i-2 and the finish (t, hi/lo split, fp16 pack)
                     // of pair (i-5, i-4) are issued together, so MUFU and ALU work interleave
                     float e[16], r[16];
                     uint32_t hw[8], lw[8];
 #pragma unroll
                     for (int i = 0; i < 16 + 5; ++i) {
-                        if (i < 16) e[i] = ex2_v(v[i] * 2.8853900817779268f);
+                        if (i < 16) e[i] = ex2_v(fminf(v[i], 60.0f));
+#if CRV_TANH_MIX
+                        // odd elements take the reciprocal on the FMA pipe (MUFU : ALU balance)
+                        if (i >= 2 && i < 18)
+                            r[i - 2] = ((i - 2) & 1) ? rcp_newton(1.0f + e[i - 2]) : rcp_v(1.0f + e[i - 2]);
+#else
                         if (i >= 2 && i < 18) r[i - 2] = rcp_v(1.0f + e[i - 2]);
+#endif
                         if (i >= 5 && ((i - 5) & 1) == 0) {
                             const int m = (i - 5) >> 1;
                             if (m < 8) finish_pair(r[2 * m], r[2 * m + 1], hw[m], lw[m]);
@@ -400,8 +412,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
                         const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
                         for (int c = 0; c < KC; ++c) {
                             mbar_wait_cluster(&a_full[c], aph);
+                            FTRACE(2048 + (gi * KC + c) * 4 + 0);
                             mbar_wait(&w_full[stage], ph);
                             mbar_wait_cluster(&w_peer[stage], ph);
+                            FTRACE(2048 + (gi * KC + c) * 4 + 1);
                             tc_fence_after();
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
@@ -411,6 +425,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
                                 mma2_f16(acc, dh, bd, idesc, (c | kk) != 0);
                                 mma2_f16(acc, dl, bd, idesc, 1u);
                             }
+                            FTRACE(2048 + (gi * KC + c) * 4 + 2);
                             mma2_commit_mc(&w_empty[stage], 3);
                             if (++stage == NST2) { stage = 0; ph ^= 1; }
                         }
@@ -458,7 +473,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
                 uint32_t acc = 0;
                 if (layer > 1) {
                     const int ai = gi & 1;
+                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
                     mbar_wait(&acc_full[ai], (acc_ph >> ai) & 1u);
+                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
                     acc_ph ^= 1u << ai;
                     acc = (uint32_t)(ai * WP);
                     ++gi;
@@ -484,11 +501,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
                             const float4 b4 = *(const float4 *)(bias + cc + k);
-                            v[k] += b4.x; v[k + 1] += b4.y; v[k + 2] += b4.z; v[k + 3] += b4.w;
+                            v[k] = fmaf(v[k], TANH_C, b4.x); v[k + 1] = fmaf(v[k + 1], TANH_C, b4.y);
+                            v[k + 2] = fmaf(v[k + 2], TANH_C, b4.z); v[k + 3] = fmaf(v[k + 3], TANH_C, b4.w);
                         }
                     }
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) v[k] = tanh_fast(v[k]);
+                    for (int k = 0; k < 16; ++k) v[k] = fmaf(-2.0f, rcp_approx(1.0f + ex2_approx(v[k])), 1.0f);
                     if (last) {
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
@@ -520,6 +538,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
                         tc_fence_before();
                         fence_proxy_async_smem();
                         __syncwarp();
+                        if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
                         if (lane == 0) mbar_arrive_cluster(afull0 + c * 8);
                     }
                 }
@@ -1296,10 +1315,10 @@ __global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float 
             long s = e - nW;
             if (s < 2L * WP) {
                 const int r = (int)(s >> 1), d = (int)(s & 1);
-                W1p[s] = r < net.widths[1] ? theta[net.woff[0] + 2 * r + d] : 0.0f;
+                W1p[s] = r < net.widths[1] ? TANH_C * theta[net.woff[0] + 2 * r + d] : 0.0f;   // fp32, pre-scaled
             } else if ((s -= 2L * WP) < (long)L * WP) {
                 const int l = (int)(s / WP), r = (int)(s % WP);
-                bp[s] = r < net.widths[l + 1] ? theta[net.boff[l] + r] : 0.0f;
+                bp[s] = r < net.widths[l + 1] ? TANH_C * theta[net.boff[l] + r] : 0.0f;        // fp32, pre-scaled
             } else {
                 s -= (long)L * WP;
                 if (s < WP) Wop[s] = s < net.widths[L] ? theta[net.woff[L] + s] : 0.0f;
@@ -1437,7 +1456,23 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
     FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr};
     if (te) {
-        k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+        if (b.fwd_pairs) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(b.grid_fwd);
+            cfg.blockDim = dim3(FWD_THREADS);
+            cfg.dynamicSmemBytes = fwd2_smem_bytes<WP>(b.L);
+            cfg.stream = s;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, k_tc_forward2<WP>, a);
+        } else {
+            k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+        }
         cudaStreamSynchronize(s);
         static long long h[4096];
         cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);

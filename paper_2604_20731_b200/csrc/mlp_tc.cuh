@@ -18,8 +18,8 @@ struct TcBufs {
     int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0;
     __half *Wf = nullptr;    // [G][KC] blocks of WP rows x 128 B: B operand of the forward GEMMs
     __half *WTf = nullptr;   // [G][KC] blocks: B operand of the backward-dX GEMMs (W^T)
-    float *W1p = nullptr;    // [WP][2]   first layer (zero padded)
-    float *bp = nullptr;     // [L][WP]   hidden biases (zero padded)
+    float *W1p = nullptr;    // [WP][2]   first layer x 2 log2(e) (zero padded)
+    float *bp = nullptr;     // [L][WP]   hidden biases x 2 log2(e) (zero padded)
     float *Wop = nullptr;    // [WP + 1]  output weights, output bias at [WP]
     __half *act = nullptr;   // [L][ntiles][KC][128*64]
     __half *delta = nullptr; // [L][ntiles][KC][128*64]  (scaled by DevState::gscale)

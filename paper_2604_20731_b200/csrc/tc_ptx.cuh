@@ -65,6 +65,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {   // non-blocking arrival
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
@@ -181,6 +184,17 @@ __device__ __forceinline__ float rcp_v(float x) {
     float y;
     asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 1/d on the FMA pipe (d in [1, 2^60]): bit-trick seed (rel. error < 0.125) and three Newton
+// steps (error 0.125 -> 1.6e-2 -> 2.4e-4 -> 6e-8), to take load off the MUFU pipe
+__device__ __forceinline__ float rcp_newton(float d) {
+    float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        const float e = fmaf(-d, r, 1.0f);
+        r = fmaf(r, e, r);
+    }
+    return r;
 }
 // t = 1 - 2 r for two elements, split t = hi + lo (hi: low 13 mantissa bits cleared, exact in
 // fp16; lo = t - hi exact in fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
