@@ -2,6 +2,7 @@
 // engine, cp.async.bulk), tcgen05 (alloc / mma / commit / ld) and UMMA descriptors.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 
 namespace crv {
@@ -25,6 +26,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+#ifdef CRV_DEBUG_HANG
+// debug build: give up after ~2^24 polls and report the barrier (the kernel then runs to the end
+// with garbage, printf flushes at the next synchronisation)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    for (long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1L << 22)) {
+            if ((threadIdx.x & 31) == 0 && blockIdx.x < 4)
+                printf("HANG block %d thread %d bar_smem 0x%x parity %u\n", blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+            return;
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -34,6 +57,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- bulk copies (TMA engine)
 // global -> shared, completion counted on an mbarrier (bytes multiple of 16, 16B aligned)
@@ -215,6 +239,9 @@ __device__ __forceinline__ void finish_pair(float r0, float r1, uint32_t &hw, ui
 
 // mbarrier wait with a suspend-time hint: the waiting thread sleeps in hardware instead of
 // spinning (used by the single-thread producer / MMA roles so they do not steal issue slots).
+#ifdef CRV_DEBUG_HANG
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+#else
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -224,6 +251,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         "r"(parity), "r"(1000000)
         : "memory");
 }
+#endif
 
 // asynchronous 32x32b.x16 TMEM load: the registers are valid only after tmem_wait_ld16 on them
 __device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
@@ -261,6 +289,16 @@ __device__ __forceinline__ void bulk_g2s_mc(void *dst_smem, const void *src_gmem
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
         "%4;" ::"r"(smem_u32(dst_smem)),
         "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+// bulk copy of local shared memory into a peer CTA's shared memory (DSMEM); dst_cluster and
+// bar_cluster are shared::cluster addresses in the peer (mapa), completion counted there
+__device__ __forceinline__ void bulk_s2s_peer(uint32_t dst_cluster, const void *src_smem, uint32_t bytes,
+                                              uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(smem_u32(src_smem)), "r"(bytes), "r"(bar_cluster)
         : "memory");
 }
 // arrive (once) on the mbarrier at this offset in every CTA of ctaMask when this thread's

@@ -1,3 +1,4 @@
-timeout -s KILL 120 python scripts/fwd_time.py C5 50 > gpurun_out/fwd_time25.log 2>&1
-CRVPINN_LIB=$PWD/paper_2604_20731_b200/libexp_nolo.so timeout -s KILL 120 python scripts/fwd_time.py C5 50 >> gpurun_out/fwd_time25.log 2>&1
-CRVPINN_LIB=$PWD/paper_2604_20731_b200/libexp_nolo.so CRVPINN_FWD_TRACE=gpurun_out/fwd_trace_nolo.bin timeout -s KILL 120 python scripts/fwd_time.py C5 3 > gpurun_out/trace.log 2>&1
+timeout -s KILL 60 python scripts/outl_case.py 128 256 3 > gpurun_out/outl_dbg4.log 2>&1
+timeout -s KILL 60 python scripts/outl_case.py 256 256 4 >> gpurun_out/outl_dbg4.log 2>&1
+timeout -s KILL 300 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/r01v28_pytest.log 2>&1 && \
+timeout -s KILL 200 bash scripts/gpu_times.sh r01v28
