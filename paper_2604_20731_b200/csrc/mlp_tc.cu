@@ -21,6 +21,12 @@
 #include "../../include/crvpinn.h"
 #include <math.h>
 #include <cstdlib>
+#ifndef CRV_B2_DSX
+#define CRV_B2_DSX 2
+#endif
+#ifndef CRV_B2_NT
+#define CRV_B2_NT 2
+#endif
 #ifndef CRV_TANH_MIX
 #define CRV_TANH_MIX 1
 #endif
@@ -79,7 +85,7 @@ constexpr int FWD_THREADS = 64 + 32 * FWD_EPI_WARPS;     // producer warp + MMA 
 template <int WP>
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
     return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128) * 4 +
-           32 * 8 + 16;
+           40 * 8 + 16;
 }
 
 // Pipelining: two TMEM accumulators (GEMMs alternate) and per-64-feature-chunk
@@ -105,8 +111,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
     uint64_t *w_full = bars, *w_empty = bars + NST_W;
     uint64_t *a_full = bars + 2 * NST_W;          // [KC]
-    uint64_t *acc_full = a_full + KC;             // [2]
-    uint32_t *tmem_slot = (uint32_t *)(acc_full + 2);
+    uint64_t *acc_full = a_full + KC;             // [2 accumulators][2 N-halves]
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
@@ -118,8 +124,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             mbar_init(&w_empty[s], 1);
         }
         for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], FWD_EPI_WARPS);
-        mbar_init(&acc_full[0], 1);
-        mbar_init(&acc_full[1], 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&acc_full[i], 1);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
         // ---------------- MMA issuer (one thread)
         if (lane == 0 && a.G > 0) {
             constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
+            constexpr uint32_t idesc_h = idesc_f16(128, WP / 2, 0, 0);
             int stage = 0;
             uint32_t ph = 0, aph = 0;
             int gi = 0;   // running GEMM counter -> accumulator gi & 1
@@ -164,23 +170,40 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         mbar_wait(&w_full[stage], ph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
+                        if (c + 1 < KC) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
-                            uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                            uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                            mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
-                            mma_f16(acc, dl, bd, idesc, 1u);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
+                                uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
+                                mma_f16(acc, dl, bd, idesc, 1u);
+                            }
+                        } else {
+                            // last K chunk in two N halves, each committed on its own barrier: the
+                            // next epilogue starts on output features [0, WP/2) while the MMAs for
+                            // [WP/2, WP) still run (shortens the per-layer MMA tail by half a chunk)
+                            // -- the HBM copies of this GEMM's A chunks must have been read out
+                            // before the epilogue overwrites A_hi
+                            bulk_wait_read0();
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk) {
+                                    uint64_t bd = sdesc_sw128(wr + stage * WBLK + hh * (WP / 2) * 128 + kk * 32, 16, 1024);
+                                    uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                    uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                    mma_f16(acc + hh * (WP / 2), dh, bd, idesc_h, (c | kk) != 0);
+                                    mma_f16(acc + hh * (WP / 2), dl, bd, idesc_h, 1u);
+                                }
+                                mma_commit(&acc_full[(gi & 1) * 2 + hh]);
+                            }
                         }
                         FTRACE(2048 + (gi * KC + c) * 4 + 2);
                         mma_commit(&w_empty[stage]);
                         if (++stage == NST_W) { stage = 0; ph ^= 1; }
                     }
                     aph ^= 1;
-                    // the epilogue overwrites A_hi only after acc_full: the HBM copies of this GEMM's
-                    // A chunks must have been read out by then
-                    bulk_wait_read0();
-                    mma_commit(&acc_full[gi & 1]);
                 }
             bulk_wait0();
         }
@@ -208,13 +231,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             for (int layer = 1; layer <= a.L; ++layer) {
                 const bool last = layer == a.L;
                 uint32_t acc = 0;
+                int ab = 0;          // acc_full barrier pair of this layer's accumulator
+                bool got1 = true;    // output half [WP/2, WP) available
                 if (layer > 1) {
                     const int ai = gi & 1;
+                    ab = ai * 2;
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
-                    mbar_wait(&acc_full[ai], (acc_ph >> ai) & 1u);
+                    mbar_wait(&acc_full[ab], (acc_ph >> ab) & 1u);
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
-                    acc_ph ^= 1u << ai;
+                    acc_ph ^= 1u << ab;
                     acc = (uint32_t)(ai * WP);
+                    got1 = false;
                     ++gi;
                     tc_fence_after();
                 }
@@ -226,7 +253,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 // issues no global stores there and its fence.proxy.async (a MEMBAR.ALL.CTA) does
                 // not wait on any; the last layer stores t_hi from registers.
                 uint32_t rbuf[16];
-                if (layer > 1) tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
+                auto need_half1 = [&](int col) {
+                    if (col >= WP / 2 && !got1) {
+                        mbar_wait(&acc_full[ab + 1], (acc_ph >> (ab + 1)) & 1u);
+                        acc_ph ^= 1u << (ab + 1);
+                        got1 = true;
+                        tc_fence_after();
+                    }
+                };
+                if (layer > 1) {
+                    need_half1(wq * 16);
+                    tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
+                }
 #pragma unroll
                 for (int c = 0; c < KC; ++c) {
                     const int cc = c * 64 + wq * 16;
@@ -251,7 +289,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                             v[k + 2] = fmaf(__uint_as_float(rbuf[k + 2]), TANH_C, b4.z);
                             v[k + 3] = fmaf(__uint_as_float(rbuf[k + 3]), TANH_C, b4.w);
                         }
-                        if (c + 1 < KC) tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
+                        if (c + 1 < KC) {
+                            need_half1(cc + 64);
+                            tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
+                        }
                     }
                     // v = 2 log2(e) z (the fp32 first layer and biases arrive pre-scaled by
                     // k_tc_refresh; the fp16 GEMM weights do not -- that was measured less accurate)
@@ -930,23 +971,24 @@ template <int WP>
 struct B2 {
     static constexpr int NS = WP / 128;
     static constexpr int KC = WP / 64;
-    static constexpr int DS = KC + 2;   // Delta ring slots
-    static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 4) * CHUNK_BYTES + 64 * 8;
+    static constexpr int DS = KC + CRV_B2_DSX;   // Delta ring slots
+    static constexpr int NT = CRV_B2_NT;         // t ring depth (tiles of 2 chunks)
+    static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 64 * 8;
 };
 
 template <int WP>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
-    constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS;
+    constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *Wt = smem;                          // [KC] x 16 KiB: W^T rows i in [128c, 128c+128)
     uint8_t *Dr = Wt + KC * CHUNK_BYTES;         // [DS] x 16 KiB
-    uint8_t *Tr = Dr + DS * CHUNK_BYTES;         // [2 tiles][2 chunks] x 16 KiB
-    uint64_t *bars = (uint64_t *)(Tr + 4 * CHUNK_BYTES);
+    uint8_t *Tr = Dr + DS * CHUNK_BYTES;         // [NT tiles][2 chunks] x 16 KiB
+    uint64_t *bars = (uint64_t *)(Tr + 2 * NT * CHUNK_BYTES);
     uint64_t *wfull = bars;
     uint64_t *dfull = bars + 1, *dempty = dfull + DS, *dready = dempty + DS;
-    uint64_t *tfull = dready + DS, *tempty = tfull + 2, *xfull = tempty + 2, *xempty = xfull + 2;
+    uint64_t *tfull = dready + DS, *tempty = tfull + NT, *xfull = tempty + NT, *xempty = xfull + 2;
     uint64_t *wdone = xempty + 2;
     uint32_t *tmem_slot = (uint32_t *)(wdone + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -960,9 +1002,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_init(&dempty[s], NS);
             mbar_init(&dready[s], EPI_THREADS);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NT; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], 1 + EPI_THREADS / 32);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&xfull[s], 1);
             mbar_init(&xempty[s], EPI_THREADS / 32);
         }
@@ -1009,14 +1053,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     else if ((uint32_t)(j % NS) == rank)
                         bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], MASK);
                 }
-                const int b = k & 1;
+                const int tb = k % NT;
                 BTRACE(k * 8 + 0);
-                mbar_wait_sleep(&tempty[b], ((k >> 1) & 1) ^ 1);
+                mbar_wait_sleep(&tempty[tb], ((k / NT) & 1) ^ 1);
                 BTRACE(k * 8 + 1);
-                mbar_arrive_expect_tx(&tfull[b], 2 * CHUNK_BYTES);
-                bulk_g2s(Tr + b * 2 * CHUNK_BYTES,
+                mbar_arrive_expect_tx(&tfull[tb], 2 * CHUNK_BYTES);
+                bulk_g2s(Tr + tb * 2 * CHUNK_BYTES,
                          (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
-                         &tfull[b]);
+                         &tfull[tb]);
             }
         }
     } else if (warp == 1) {
@@ -1028,9 +1072,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(wfull, 0);
             int dn = 0;
             for (int k = 0; k < nk; ++k) {
-                const int b = k & 1;
+                const int b = k & 1, tb = k % NT;
                 const int slot0 = dn % DS;
-                mbar_wait(&tfull[b], (k >> 1) & 1);
+                mbar_wait(&tfull[tb], (k / NT) & 1);
                 BTRACE(k * 8 + 2);
                 mbar_wait(&xempty[b], ((k >> 1) & 1) ^ 1);
                 BTRACE(k * 8 + 7);
@@ -1053,7 +1097,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
-                        const uint64_t ad = sdesc_sw128(tr + b * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                        const uint64_t ad = sdesc_sw128(tr + tb * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
                     }
@@ -1064,7 +1108,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 }
                 mma_commit(&xfull[b]);
                 BTRACE(k * 8 + 3);
-                mma_commit(&tempty[b]);
+                mma_commit(&tempty[tb]);
                 dn += KC;
             }
             mma_commit(wdone);
@@ -1108,6 +1152,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (a.outl && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
                 const int tile = pair + k * a.npairs;
+                if (warp == 2 && lane == 0) BTRACE(2048 + k * 4 + 0);
                 float g[4];
                 __half2 g2[4];
 #pragma unroll
@@ -1147,12 +1192,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
                     fence_proxy_async_smem();
                     mbar_arrive(&dready[slot]);   // count = EPI_THREADS
+                    if (warp == 2 && lane == 0 && j == 0) BTRACE(2048 + k * 4 + 2);
                 }
+                if (warp == 2 && lane == 0) BTRACE(2048 + k * 4 + 1);
                 dn += KC;
             }
             if (k == 0) continue;
             // ---- dX epilogue of tile k-1
-            const int kk = k - 1, b = kk & 1;
+            const int kk = k - 1, b = kk & 1, tb = kk % NT;
             const int tile = pair + kk * a.npairs;
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
@@ -1161,7 +1208,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(&xfull[b], (kk >> 1) & 1);
             if (warp == 2 && lane == 0) BTRACE(kk * 8 + 5);
             tc_fence_after();
-            const uint32_t tb = smem_u32(Tr) + (uint32_t)((b * 2 + hf) * CHUNK_BYTES + row * 128);
+            const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + hf) * CHUNK_BYTES + row * 128);
             uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
 #pragma unroll
             for (int g2 = 0; g2 < 2; ++g2) {
@@ -1172,7 +1219,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 for (int j = 0; j < 4; ++j) {
                     const int lg = g2 * 4 + j;
                     uint32_t tw[4];
-                    ld_shared_v4(tb + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
+                    ld_shared_v4(tsm + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
                         const float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&tw[mm]));
@@ -1211,7 +1258,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (lane == 0) {
                 if (warp == 2) BTRACE(kk * 8 + 6);
                 mbar_arrive(&xempty[b]);
-                mbar_arrive(&tempty[b]);
+                mbar_arrive(&tempty[tb]);
             }
         }
         // ---- end: all MMAs done -> the rings are free for the reductions
@@ -1536,13 +1583,13 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
-            if (te && g == 1) {
+            if (te && g == b.G - 1) {
                 if (!trace) cudaMalloc(&trace, 4096 * 8);
                 cudaMemset(trace, 0, 4096 * 8);
                 a.trace = trace;
             }
             cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP>, a);
-            if (te && g == 1) {
+            if (te && g == b.G - 1) {
                 cudaStreamSynchronize(s);
                 static long long h[4096];
                 cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
