@@ -122,6 +122,33 @@ def alg_flops_per_iter(w: W.Workload) -> float:
     return float(fwd + bdx + bdw) * w.points
 
 
+def alg_bytes_per_iter(w: W.Workload) -> float:
+    """alpha, b, u, RES/q, dLOSS/du through HBM once each (40 B/point) + 36 B/param."""
+    return 40.0 * w.points + 36.0 * w.n_params
+
+
+def measure_tf32_peak(device: int) -> float:
+    """TF32 dense tensor peak of this GPU in TFLOP/s (torch.matmul 8192^3, TF32, best of 10)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(8192, 8192, device=f"cuda:{device}")
+        b = torch.randn(8192, 8192, device=f"cuda:{device}")
+        best = float("inf")
+        for _ in range(12):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        del a, b
+        return 2.0 * 8192 ** 3 / best / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 # ------------------------------------------------------------------ the oracle (CPU) arm
 def time_oracle(name: str, iters: int):
     import oracle
@@ -272,6 +299,19 @@ def run_ours(args, rank, world, local):
         peak = 148 * 128 * 2 * 1.965e9 / 1e12   # FFMA fp32: SMs x lanes x 2 x max clock
         bound, peak_note = "alu", "derived FP32 FFMA peak 74.4 TFLOP/s (148 SM x 128 x 2 x 1965 MHz)"
     clocks = sampler.summary()
+    # north_star / SURVEY.md §8(d) roofline: the method's precision class is TF32 (the fp16 operands
+    # here have TF32's 10-bit mantissa), so its denominator is the TF32 tensor peak -- measured here
+    # like MEASURED_PEAKS measures bf16 (torch.matmul 8192^3, TF32 enabled, best of 10) -- and the
+    # whole Adam iteration is compared with max(GEMM flops / TF32 peak, algorithmic bytes / HBM).
+    tf32 = measure_tf32_peak(local) if prec == crv.PREC_TENSOR else None
+    step_s = (t_max / 1e3) / (args.steps * ITERS_PER_STEP)
+    alg_bytes = alg_bytes_per_iter(w)
+    line_ns = None
+    if tf32:
+        t_roof = max(flops / (tf32 * 1e12), alg_bytes / (float(peaks["hbm_gbs"]) * 1e9))
+        line_ns = {"denominator": "TF32 tensor peak measured in this run (torch.matmul 8192^3, best of 10)",
+                   "tf32_tflops": tf32, "t_roof_us": t_roof * 1e6, "step_us": step_s * 1e6,
+                   "frac": t_roof / step_s}
     line = {
         "metric": f"CRVPINN Adam iters/s ({args.workload})", "value": value, "unit": "Adam iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
@@ -282,7 +322,11 @@ def run_ours(args, rank, world, local):
         "roofline": {"bound": bound, "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak, "traffic": None,
                      "kernel": "MLP forward + backward (A1, A6-A7), per Adam iteration",
-                     "alg_flops_per_iter": flops, "peak_source": peak_note},
+                     "alg_flops_per_iter": flops, "peak_source": peak_note,
+                     "traffic_note": "per-iteration DRAM bytes of the MLP kernels (ncu --set full, C5): "
+                                     "2.12e9 (profiles/r01_v3_ncu_full_summary.md); activations pass "
+                                     "through HBM, so traffic >> the 20 MB algorithmic bytes"},
+        "north_star_roofline": line_ns,
         "stage_ms_per_iter": {"mlp_fwd": stage_ms[0] / max(prof_iters, 1),
                               "stencil_gram_loss_adjoint": stage_ms[1] / max(prof_iters, 1),
                               "mlp_bwd_reduce": stage_ms[2] / max(prof_iters, 1),

@@ -120,10 +120,13 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
     if (ev) record(ev[3], s);
     // A8: Adam (+ refresh of the tensor-core weight copies)
     if (train) {
-        launch_adam(ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, ctx->st,
-                    (float)ctx->opts.lr, (float)ctx->opts.beta1, (float)ctx->opts.beta2,
-                    (float)ctx->opts.eps, s);
-        if (tc) tc_refresh_weights(net, ctx->tc, ctx->theta, s);
+        if (tc)
+            tc_adam(net, ctx->tc, ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, (float)ctx->opts.lr,
+                    (float)ctx->opts.beta1, (float)ctx->opts.beta2, (float)ctx->opts.eps, s);
+        else
+            launch_adam(ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, ctx->st,
+                        (float)ctx->opts.lr, (float)ctx->opts.beta1, (float)ctx->opts.beta2,
+                        (float)ctx->opts.eps, s);
     }
     if (ev) record(ev[4], s);
 }

@@ -1375,6 +1375,69 @@ __global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float 
     }
 }
 
+// ================================================================ A8: Adam fused with the re-layout
+// One thread per parameter: the Adam update (as k_adam, PAPER.md:830 / reading R7) followed by the
+// write of the new value into the tensor path's operand copies (what k_tc_refresh does for the
+// whole set): hidden weights -> fp16 Wf (rows = out features) and WTf (rows = in features), first
+// layer and biases -> fp32 x 2 log2(e), output layer -> fp32. Padding entries keep the zeros of the
+// initial k_tc_refresh.
+__global__ void k_tc_adam(Net net, int WP, int KC, float *__restrict__ theta, float *__restrict__ m,
+                          float *__restrict__ v, const float *__restrict__ g, long np, DevState *st, float lr,
+                          float beta1, float beta2, float eps, __half *__restrict__ Wf, __half *__restrict__ WTf,
+                          float *__restrict__ W1p, float *__restrict__ bp, float *__restrict__ Wop) {
+    const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (st->nonfinite) return;
+    const float bc1 = (float)st->bc1, bc2 = (float)st->bc2;
+    if (e == 0) st->t = st->t + 1;   // the only writer of t; other threads read bc1/bc2 only
+    if (e >= np) return;
+    const float gk = g[e];
+    if (!isfinite(gk)) {
+        atomicExch(&st->nonfinite, 1);
+        return;
+    }
+    const float mk = beta1 * m[e] + (1.0f - beta1) * gk;
+    const float vk = beta2 * v[e] + (1.0f - beta2) * gk * gk;
+    m[e] = mk;
+    v[e] = vk;
+    const float th = theta[e] - lr * (mk / bc1) / (sqrtf(vk / bc2) + eps);
+    theta[e] = th;
+    // which layer / slot
+    const int nl = net.nl, L = nl - 1;
+    int l = 0;
+    while (l + 1 < nl && e >= net.woff[l + 1]) ++l;
+    const int win = net.widths[l];
+    if (e >= net.boff[l]) {   // bias of layer l
+        const int o = (int)(e - net.boff[l]);
+        if (l < L) bp[l * WP + o] = TANH_C * th;
+        else Wop[WP] = th;
+        return;
+    }
+    const long r = e - net.woff[l];
+    const int o = (int)(r / win), i = (int)(r % win);   // W_l[o][i]
+    if (l == 0) {
+        W1p[2 * o + i] = TANH_C * th;
+    } else if (l == L) {
+        Wop[i] = th;
+    } else {
+        const int gg = l - 1;
+        const __half hv = __float2half_rn(th);
+        {   // Wf: row n = o, K index k = i
+            const size_t blk = ((size_t)gg * KC + (i >> 6)) * (size_t)WP * 64;
+            Wf[blk + (uint32_t)(o * 64 + ((((i & 63) >> 3) ^ (o & 7)) << 3) + (i & 7))] = hv;
+        }
+        {   // WTf: row n = i, K index k = o
+            const size_t blk = ((size_t)gg * KC + (o >> 6)) * (size_t)WP * 64;
+            WTf[blk + (uint32_t)(i * 64 + ((((o & 63) >> 3) ^ (i & 7)) << 3) + (o & 7))] = hv;
+        }
+    }
+}
+
+void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
+             DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
+    k_tc_adam<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(net, b.WP, b.KC, theta, m, v, g, np, st, lr, beta1, beta2,
+                                                           eps, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
+}
+
 // ================================================================ host side
 template <int WP>
 static void set_attrs(int L) {
@@ -1622,7 +1685,7 @@ int tc_launches(const Net &net) {
     const int wp = ((net.widths[1] + 63) / 64) * 64;
     const char *e = getenv("CRVPINN_FUSE_OUTL");
     const bool fused = wp >= 128 && !(e && e[0] == '0');
-    return 1 /*fwd*/ + (fused ? 0 : 1) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/ + 1 /*refresh*/;
+    return 1 /*fwd*/ + (fused ? 0 : 1) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/;   // Adam: crvpinn.cu
 }
 
 }  // namespace crv

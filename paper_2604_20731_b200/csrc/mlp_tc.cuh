@@ -37,5 +37,8 @@ void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
 int tc_launches(const Net &net);
+// A8 for the tensor path: Adam + write of the updated operand copies (one launch)
+void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
+             DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 
 }  // namespace crv

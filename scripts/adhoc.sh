@@ -1,1 +1,2 @@
-timeout -s KILL 60 ./scripts/micro/tmem_rate > gpurun_out/tmem_rate.log 2>&1
+timeout -s KILL 300 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/r01v31_pytest.log 2>&1
+timeout -s KILL 200 python bench.py --no-cpu-baseline > gpurun_out/r01v31_bench.json 2> gpurun_out/r01v31_bench.err
