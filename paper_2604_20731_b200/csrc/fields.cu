@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
                                                         const RedJob *__restrict__ jobs, int njobs,
                                                         const DevState *st) {
     __shared__ float sh[RED_WARPS][33];
+    pdl_wait();
+    pdl_trigger();
     int j = 0, g = blockIdx.x;
     while (j < njobs && g >= red_groups(jobs[j])) { g -= red_groups(jobs[j]); ++j; }
     if (j >= njobs) return;
@@ -114,7 +116,7 @@ int reduce_groups(const RedJob *jobs, int njobs) {
 
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s) {
-    k_reduce<<<total_groups, RED_THREADS, 0, s>>>(partial, grad, jobs, njobs, st);
+    launch_pdl(k_reduce, dim3(total_groups), dim3(RED_THREADS), 0, s, 1, partial, grad, jobs, njobs, st);
 }
 
 // ---------------------------------------------------------------- A8: Adam

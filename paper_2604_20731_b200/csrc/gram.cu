@@ -59,7 +59,9 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
     extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
+    pdl_wait();
+    pdl_trigger();
     const int j0 = 2 * blockIdx.x;
     const bool has1 = j0 + 1 < n;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->gmax_bits = 0u;   // k_adj_final folds this iteration's max
@@ -106,6 +108,8 @@ constexpr int TRI_WARPS = 4;
 
 __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restrict__ etab, float *__restrict__ z,
                           int n, int seg, float h2) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int a = blockIdx.x * TRI_WARPS + warp;
@@ -176,6 +180,8 @@ __global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
     for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    pdl_wait();
+    pdl_trigger();
     const int j0 = 2 * blockIdx.x;
     const bool has1 = j0 + 1 < n;
     const int shift = 32 - logM;
@@ -223,6 +229,8 @@ __global__ void k_adj_final(const float *__restrict__ q, const float *__restrict
                             double beta2, int advance) {
     __shared__ float smax[8];
     __shared__ double sh[256];
+    pdl_wait();
+    pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     float g = 0.0f, gb = 0.0f;
     const int n = N - 1;
@@ -334,13 +342,15 @@ void launch_field_chain(const float *u, const float *alpha, const float *b, floa
     const float nrm = sqrtf(2.0f / (float)N);
     float *rhat = c.work, *z = c.work + (size_t)n * n;
     const int rows = (n + 1) / 2;
-    k_res_dst<<<rows, fft_threads(N), sizeof(float2) * (M + M / 2), s>>>(u, alpha, b, res, rhat, c.tw, N, c.logM, nrm, st);
-    k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(
-        rhat, c.etab, z, n, c.seg, h * h);
-    k_idst_loss<<<rows, fft_threads(N), sizeof(float2) * (M + M / 2), s>>>(z, res, q, loss_part, c.tw, N, c.logM, nrm);
+    launch_pdl(k_res_dst, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (M + M / 2), s, 1, u, alpha, b, res, rhat,
+               c.tw, N, c.logM, nrm, st);
+    launch_pdl(k_tridiag, dim3(ceil_div(n, TRI_WARPS)), dim3(32 * TRI_WARPS), sizeof(float) * TRI_WARPS * 2 * 32 * c.seg,
+               s, 1, rhat, c.etab, z, n, c.seg, h * h);
+    launch_pdl(k_idst_loss, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (M + M / 2), s, 1, z, res, q, loss_part,
+               c.tw, N, c.logM, nrm);
     const int P = N * N;
-    k_adj_final<<<ceil_div(P, 256), 256, 0, s>>>(q, alpha, gbar, gu_lat, N, st, track_max, loss_part, rows, hist,
-                                                 n_hist, beta1, beta2, advance);
+    launch_pdl(k_adj_final, dim3(ceil_div(P, 256)), dim3(256), 0, s, 1, q, alpha, gbar, gu_lat, N, st, track_max,
+               loss_part, rows, hist, n_hist, beta1, beta2, advance);
 }
 
 }  // namespace crv

@@ -115,9 +115,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     uint32_t *tmem_slot = (uint32_t *)(acc_full + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
-    for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
-    for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST_W; ++s) {
             mbar_init(&w_full[s], 1);
@@ -128,6 +125,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
+    // everything above is local; the weights (written by the previous iteration's Adam) are read
+    // only after the programmatic dependency resolves
+    pdl_wait();
+    pdl_trigger();
+    for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
+    for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
+    for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1014,6 +1018,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
+    pdl_wait();   // inputs of this GEMM come from the previous launch
+    pdl_trigger();
     tc_fence_before();
     if (NS > 1) cluster_sync_all();   // every CTA's barriers exist before any multicast lands
     else __syncthreads();
@@ -1386,6 +1392,8 @@ __global__ void k_tc_adam(Net net, int WP, int KC, float *__restrict__ theta, fl
                           float beta1, float beta2, float eps, __half *__restrict__ Wf, __half *__restrict__ WTf,
                           float *__restrict__ W1p, float *__restrict__ bp, float *__restrict__ Wop) {
     const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
     if (st->nonfinite) return;
     const float bc1 = (float)st->bc1, bc2 = (float)st->bc2;
     if (e == 0) st->t = st->t + 1;   // the only writer of t; other threads read bc1/bc2 only
@@ -1434,8 +1442,8 @@ __global__ void k_tc_adam(Net net, int WP, int KC, float *__restrict__ theta, fl
 
 void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
              DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
-    k_tc_adam<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(net, b.WP, b.KC, theta, m, v, g, np, st, lr, beta1, beta2,
-                                                           eps, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
+    launch_pdl(k_tc_adam, dim3((unsigned)((np + 255) / 256)), dim3(256), 0, s, 1, net, b.WP, b.KC, theta, m, v, g, np,
+               st, lr, beta1, beta2, eps, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
 }
 
 // ================================================================ host side
@@ -1605,7 +1613,7 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, k_tc_forward2<WP>, a);
     } else {
-        k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+        launch_pdl(k_tc_forward<WP>, dim3(b.grid_fwd), dim3(FWD_THREADS), fwd_smem_bytes<WP>(b.L), s, 1, a);
     }
 }
 
@@ -1621,17 +1629,19 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
     const int L = b.L;
     if constexpr (WP >= 128) {
         cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = B2<WP>::NS;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.gridDim = dim3(b.grid_bwd);
         cfg.blockDim = dim3(TC_THREADS);
         cfg.dynamicSmemBytes = B2<WP>::SMEM;
         cfg.stream = s;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         if (!b.fuse_outl)
             k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
                                                               b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob,
