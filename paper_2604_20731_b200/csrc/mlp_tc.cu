@@ -363,245 +363,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     if (warp == 1) tmem_dealloc(tmem, 2 * WP);
 }
 
-// ================================================================ forward v2: CTA pairs (cta_group::2)
-// Same epilogue as k_tc_forward, but two CTAs (one cluster, one TPC) run each hidden GEMM as ONE
-// M = 256 tcgen05.mma.cta_group::2 issued by the leader CTA: each CTA supplies its own tile's
-// activations (A, 128 rows) and HALF of every weight K-chunk (B, WP/2 rows), and receives its
-// 128 x WP accumulator in its own TMEM. Per SM this halves the weight stream (L2 traffic and
-// ring bytes), so the ring holds NST2 = 4 K-chunks in flight instead of 2 -- the 2-deep ring of
-// the 1-CTA kernel left the tensor pipe waiting on L2 latency (ncu: tensor 36 %, XU 45 %).
-// Readiness of the follower's data reaches the leader's MMA thread through remote mbarrier
-// arrivals (epilogue chunk releases: a_full counts 2 x 16 warps; weight halves: the follower's
-// MMA warp forwards its w_full completions to the leader's w_peer); MMA completion is committed
-// to both CTAs at once (multicast commit). A pair walks tile pairs (2j, 2j+1); when ntiles is odd
-// the follower's last tile is a dummy whose results are not stored.
-constexpr int NST2 = 4;
-
-template <int WP>
-__host__ __device__ constexpr uint32_t fwd2_smem_bytes(int L) {
-    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST2 * (WP / 2) * 128 +
-           (2 * WP + L * WP + WP + 1 + 2 * 4 * 128) * 4 + 32 * 8 + 16;
-}
-
-template <int WP>
-__global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward2(FwdArgs a) {
-    constexpr int KC = WP / 64;
-    constexpr uint32_t WBLK = WP * 128;          // one K-chunk of the full weight block
-    constexpr uint32_t HB = (WP / 2) * 128;      // this CTA's half (rows [rank*WP/2, +WP/2))
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = align1024(smem_raw);
-    uint8_t *A_hi = smem;
-    uint8_t *A_lo = A_hi + KC * CHUNK_BYTES;
-    uint8_t *Wr = A_lo + KC * CHUNK_BYTES;
-    float *sW1 = (float *)(Wr + NST2 * HB);
-    float *sB = sW1 + 2 * WP;
-    float *sWo = sB + a.L * WP;
-    float *sRed = sWo + WP + 1;
-    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
-    uint64_t *w_full = bars, *w_peer = bars + NST2, *w_empty = bars + 2 * NST2;
-    uint64_t *a_full = bars + 3 * NST2;           // [KC] (used in the leader)
-    uint64_t *acc_full = a_full + KC;             // [2]
-    uint32_t *tmem_slot = (uint32_t *)(acc_full + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const bool leader = rank == 0;
-    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const int ntp = (a.ntiles + 1) >> 1;          // tile pairs
-    for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
-    for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
-    for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NST2; ++s) {
-            mbar_init(&w_full[s], 1);
-            mbar_init(&w_peer[s], 1);
-            mbar_init(&w_empty[s], 1);
-        }
-        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], 2 * FWD_EPI_WARPS);
-        mbar_init(&acc_full[0], 1);
-        mbar_init(&acc_full[1], 1);
-        fence_mbar_init();
-    }
-    if (warp == 1) tmem_alloc2(tmem_slot, 2 * WP);
-    tc_fence_before();
-    cluster_sync_all();   // barriers of both CTAs initialised before any remote arrival
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        // ---------------- producer (both CTAs): this CTA's half of every weight K-chunk
-        if (lane == 0 && a.G > 0) {
-            int stage = 0;
-            uint32_t ph = 0;
-            for (int tp = pair; tp < ntp; tp += npairs)
-                for (int g = 0; g < a.G; ++g)
-                    for (int c = 0; c < KC; ++c) {
-                        mbar_wait_sleep(&w_empty[stage], ph ^ 1);
-                        mbar_arrive_expect_tx(&w_full[stage], HB);
-                        bulk_g2s(Wr + stage * HB, (const uint8_t *)a.Wf + (size_t)(g * KC + c) * WBLK + rank * HB, HB,
-                                 &w_full[stage]);
-                        if (++stage == NST2) { stage = 0; ph ^= 1; }
-                    }
-        }
-    } else if (warp == 1) {
-        if (lane == 0 && a.G > 0) {
-            if (leader) {
-                // ---------------- MMA issuer (leader only): M = 256 over the pair
-                constexpr uint32_t idesc = idesc_f16(256, WP, 0, 0);
-                int stage = 0;
-                uint32_t ph = 0, aph = 0;
-                int gi = 0;
-                const uint32_t ahi = smem_u32(A_hi), alo = smem_u32(A_lo), wr = smem_u32(Wr);
-                for (int tp = pair; tp < ntp; tp += npairs)
-                    for (int g = 0; g < a.G; ++g, ++gi) {
-                        const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
-                        for (int c = 0; c < KC; ++c) {
-                            mbar_wait_cluster(&a_full[c], aph);
-                            FTRACE(2048 + (gi * KC + c) * 4 + 0);
-                            mbar_wait(&w_full[stage], ph);
-                            mbar_wait_cluster(&w_peer[stage], ph);
-                            FTRACE(2048 + (gi * KC + c) * 4 + 1);
-                            tc_fence_after();
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t bd = sdesc_sw128(wr + stage * HB + kk * 32, 16, 1024);
-                                const uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                const uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                mma2_f16(acc, dh, bd, idesc, (c | kk) != 0);
-                                mma2_f16(acc, dl, bd, idesc, 1u);
-                            }
-                            FTRACE(2048 + (gi * KC + c) * 4 + 2);
-                            mma2_commit_mc(&w_empty[stage], 3);
-                            if (++stage == NST2) { stage = 0; ph ^= 1; }
-                        }
-                        aph ^= 1;
-                        mma2_commit_mc(&acc_full[gi & 1], 3);
-                    }
-            } else {
-                // ---------------- forwarder (follower): my weight half landed -> tell the leader
-                const uint32_t peer0 = mapa_shared(w_peer, 0);
-                int stage = 0;
-                uint32_t ph = 0;
-                for (int tp = pair; tp < ntp; tp += npairs)
-                    for (int g = 0; g < a.G; ++g)
-                        for (int c = 0; c < KC; ++c) {
-                            mbar_wait(&w_full[stage], ph);
-                            mbar_arrive_cluster(peer0 + stage * 8);
-                            if (++stage == NST2) { stage = 0; ph ^= 1; }
-                        }
-            }
-        }
-    } else {
-        const int q = warp & 3;
-        const int row = q * 32 + lane;
-        const int wq = (warp - 2) >> 2;
-        const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-        const int lg0 = 2 * wq;
-        const int pos = (lg0 ^ (row & 7)) & ~1;
-        const bool swap = (row & 1) != 0;
-        const uint32_t off0 = (uint32_t)(row * 128 + ((lg0 ^ (row & 7)) << 4));
-        const uint32_t off1 = (uint32_t)(row * 128 + (((lg0 + 1) ^ (row & 7)) << 4));
-        const uint32_t afull0 = mapa_shared(a_full, 0);   // the leader's chunk barriers
-        uint32_t acc_ph = 0u;
-        int gi = 0, par = 0;
-        const int N = a.N;
-        for (int tp = pair; tp < ntp; tp += npairs, par ^= 1) {
-            const int tile = 2 * tp + (int)rank;
-            const bool valid = tile < a.ntiles;
-            const int p = tile * 128 + row;
-            int pi, pj;
-            point_ij(p, N, pi, pj);
-            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
-            float dot = 0.0f;
-            for (int layer = 1; layer <= a.L; ++layer) {
-                const bool last = layer == a.L;
-                uint32_t acc = 0;
-                if (layer > 1) {
-                    const int ai = gi & 1;
-                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
-                    mbar_wait(&acc_full[ai], (acc_ph >> ai) & 1u);
-                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
-                    acc_ph ^= 1u << ai;
-                    acc = (uint32_t)(ai * WP);
-                    ++gi;
-                    tc_fence_after();
-                }
-                const float *bias = sB + (layer - 1) * WP;
-                uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
-                                row * 128 + pos * 16;
-#pragma unroll 1
-                for (int c = 0; c < KC; ++c) {
-                    const int cc = c * 64 + wq * 16;
-                    float v[16];
-                    if (layer == 1) {
-#pragma unroll
-                        for (int k = 0; k < 16; k += 2) {
-                            const float4 w4 = *(const float4 *)(sW1 + 2 * (cc + k));
-                            const float2 b2 = *(const float2 *)(bias + cc + k);
-                            v[k] = fmaf(w4.x, x, fmaf(w4.y, y, b2.x));
-                            v[k + 1] = fmaf(w4.z, x, fmaf(w4.w, y, b2.y));
-                        }
-                    } else {
-                        tmem_ld16(t_lane + acc + cc, v);
-#pragma unroll
-                        for (int k = 0; k < 16; k += 4) {
-                            const float4 b4 = *(const float4 *)(bias + cc + k);
-                            v[k] = fmaf(v[k], TANH_C, b4.x); v[k + 1] = fmaf(v[k + 1], TANH_C, b4.y);
-                            v[k + 2] = fmaf(v[k + 2], TANH_C, b4.z); v[k + 3] = fmaf(v[k + 3], TANH_C, b4.w);
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) v[k] = fmaf(-2.0f, rcp_approx(1.0f + ex2_approx(v[k])), 1.0f);
-                    if (last) {
-#pragma unroll
-                        for (int k = 0; k < 16; k += 4) {
-                            const float4 w4 = *(const float4 *)(sWo + cc + k);
-                            dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
-                        }
-                    }
-                    uint32_t hw[8], lw[8];
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        const float t0 = v[2 * m], t1 = v[2 * m + 1];
-                        const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
-                        const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
-                        hw[m] = pack_half2(h0, h1);
-                        lw[m] = pack_half2(t0 - h0, t1 - h1);
-                    }
-                    if (valid) {
-                        if (swap)
-                            st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
-                        else
-                            st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
-                    }
-                    if (!last) {
-                        const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
-                        st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);
-                        st_shared_v4(bh + off1, hw[4], hw[5], hw[6], hw[7]);
-                        st_shared_v4(bl + off0, lw[0], lw[1], lw[2], lw[3]);
-                        st_shared_v4(bl + off1, lw[4], lw[5], lw[6], lw[7]);
-                        tc_fence_before();
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
-                        if (lane == 0) mbar_arrive_cluster(afull0 + c * 8);
-                    }
-                }
-            }
-            sRed[(par * 4 + wq) * 128 + row] = dot;
-            named_bar(1, 32 * FWD_EPI_WARPS);
-            if (wq == 0 && valid) {
-                const float *r = sRed + par * 4 * 128 + row;
-                const float net = ((r[0] + r[128]) + (r[256] + r[384])) + sWo[WP];
-                a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
-            }
-        }
-    }
-    tc_fence_before();
-    cluster_sync_all();
-    if (warp == 1) tmem_dealloc2(tmem, 2 * WP);
-}
-
 // ================================================================ backward: output layer
 // Delta_L = s * gbar * W_out (.) (1 - t_L^2) (fp16, tile-chunk format), with
 // s = 2^(7 - ceil(log2 max|gbar|)) so max|s gbar| is in (64, 128].
@@ -1450,7 +1211,6 @@ void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, 
 template <int WP>
 static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
-    cudaFuncSetAttribute(k_tc_forward2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd2_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
         cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
     } else {
@@ -1473,12 +1233,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     }
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    {
-        const char *e = getenv("CRVPINN_FWD_PAIRS");   // tuning knob: CTA-pair (cta_group::2) forward
-        b.fwd_pairs = e && e[0] == '1';
-        const int ntp = (b.ntiles + 1) / 2;
-        b.grid_fwd = b.fwd_pairs ? 2 * (ntp < nsm / 2 ? ntp : nsm / 2) : (b.ntiles < nsm ? b.ntiles : nsm);
-    }
+    b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
     {
         // WP >= 128: clusters of NS = WP/128 CTAs (k_tc_bwd2); WP = 64: one CTA per "pair"
         const int NS = WP >= 128 ? WP / 128 : 1;
@@ -1570,27 +1325,11 @@ void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cud
 template <int WP>
 static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
     static long long *trace = nullptr;
-    const char *te = getenv("CRVPINN_FWD_TRACE");
+    const char *te = getenv("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
     FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr};
     if (te) {
-        if (b.fwd_pairs) {
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(b.grid_fwd);
-            cfg.blockDim = dim3(FWD_THREADS);
-            cfg.dynamicSmemBytes = fwd2_smem_bytes<WP>(b.L);
-            cfg.stream = s;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            cudaLaunchKernelEx(&cfg, k_tc_forward2<WP>, a);
-        } else {
-            k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
-        }
+        k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
         cudaStreamSynchronize(s);
         static long long h[4096];
         cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1598,23 +1337,7 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
         if (f) { fwrite(h, 8, 4096, f); fclose(f); }
         return;
     }
-    if (b.fwd_pairs) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(b.grid_fwd);
-        cfg.blockDim = dim3(FWD_THREADS);
-        cfg.dynamicSmemBytes = fwd2_smem_bytes<WP>(b.L);
-        cfg.stream = s;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, k_tc_forward2<WP>, a);
-    } else {
-        launch_pdl(k_tc_forward<WP>, dim3(b.grid_fwd), dim3(FWD_THREADS), fwd_smem_bytes<WP>(b.L), s, 1, a);
-    }
+    launch_pdl(k_tc_forward<WP>, dim3(b.grid_fwd), dim3(FWD_THREADS), fwd_smem_bytes<WP>(b.L), s, 1, a);
 }
 
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {

@@ -14,7 +14,7 @@ namespace crv {
 struct TcBufs {
     int ready = 0;
     int fuse_outl = 1;
-    int fwd_pairs = 1;       // forward as CTA pairs (k_tc_forward2, cta_group::2)       // WP >= 128: output-layer backward fused into the first k_tc_bwd2 launch
+       // WP >= 128: output-layer backward fused into the first k_tc_bwd2 launch
     int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0;
     __half *Wf = nullptr;    // [G][KC] blocks of WP rows x 128 B: B operand of the forward GEMMs
     __half *WTf = nullptr;   // [G][KC] blocks: B operand of the backward-dX GEMMs (W^T)
