@@ -732,6 +732,13 @@ struct Bwd2Args {
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
+#ifndef CRV_B2_EPI_WARPS
+#define CRV_B2_EPI_WARPS 8
+#endif
+constexpr int B2_EPI_WARPS = CRV_B2_EPI_WARPS;    // 8 or 16 (4 per TMEM lane quarter)
+constexpr int B2_EPI_THREADS = 32 * B2_EPI_WARPS;
+constexpr int B2_THREADS = 64 + B2_EPI_THREADS;
+
 template <int WP>
 struct B2 {
     static constexpr int NS = WP / 128;
@@ -742,7 +749,7 @@ struct B2 {
 };
 
 template <int WP>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
+__global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
     extern __shared__ uint8_t smem_raw[];
@@ -765,15 +772,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         for (int s = 0; s < DS; ++s) {
             mbar_init(&dfull[s], 1);
             mbar_init(&dempty[s], NS);
-            mbar_init(&dready[s], EPI_THREADS);
+            mbar_init(&dready[s], B2_EPI_THREADS);
         }
         for (int s = 0; s < NT; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 1 + EPI_THREADS / 32);
+            mbar_init(&tempty[s], 1 + B2_EPI_WARPS);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&xfull[s], 1);
-            mbar_init(&xempty[s], EPI_THREADS / 32);
+            mbar_init(&xempty[s], B2_EPI_WARPS);
         }
         mbar_init(wdone, 1);
         fence_mbar_init();
@@ -881,19 +888,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mma_commit(wdone);
         }
     } else {
-        // ---------------- epilogue warps
+        // ---------------- epilogue warps: B2_EPI_WARPS, warp % 4 = TMEM lane quarter (rows); the
+        // warps of a quarter split the CTA's 128 dX columns into CPW-wide slices
+        constexpr int EWQ = B2_EPI_WARPS / 4;    // warps per lane quarter
+        constexpr int CPW = 128 / EWQ;           // dX columns per warp (multiple of 32)
+        constexpr int EPT = B2_EPI_THREADS;
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int hf = (warp - 2) >> 2;          // local t chunk 0/1 -> 64 columns
+        const int wq = (warp - 2) >> 2;
         const int ep_tid = threadIdx.x - 64;
         const uint32_t t_lane = (uint32_t)(q * 32) << 16;
         const int N = a.N;
-        float cs[2] = {0.f, 0.f}, csx[2] = {0.f, 0.f}, csy[2] = {0.f, 0.f};
+        float cs[CPW / 32], csx[CPW / 32], csy[CPW / 32];
+#pragma unroll
+        for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = csx[g2] = csy[g2] = 0.f;
         // output-layer transform state (outl). Thread -> granule lg (8 features) of every chunk,
-        // rows rr + 32m (m < 4); chunks are transformed in order so the MMA can start on chunk 0
+        // rows orr + (EPT/8) m; chunks are transformed in order so the MMA can start on chunk 0
         // while later chunks are still being transformed. Delta_L is formed in half2 arithmetic
         // (it is stored in fp16 anyway); the output-layer column sums (dW_out = sum g t_L,
         // db_L = sum Delta_L) are fp32 and cover this CTA's own half of the features only.
+        constexpr int ORG = EPT / 8;             // row groups of the transform
+        constexpr int ORM = 128 / ORG;           // rows per thread and chunk
         const int olg = ep_tid & 7, orr = ep_tid >> 3;
         __half2 wo2[KC][4];
         float aw[2][8], ab[2][8], ag = 0.f;
@@ -919,12 +934,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (a.outl && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
                 const int tile = pair + k * a.npairs;
-                if (warp == 2 && lane == 0) BTRACE(2048 + k * 4 + 0);
-                float g[4];
-                __half2 g2[4];
+                float g[ORM];
+                __half2 g2[ORM];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    g[m] = s * __ldg(a.gbar + (size_t)tile * 128 + orr + 32 * m);
+                for (int m = 0; m < ORM; ++m) {
+                    g[m] = s * __ldg(a.gbar + (size_t)tile * 128 + orr + ORG * m);
                     g2[m] = __floats2half2_rn(g[m], g[m]);
                     if (olg == 0) ag += g[m];
                 }
@@ -937,8 +951,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     const bool own = NS == 1 || (j >> 1) == (int)rank;
                     const int jj = NS == 1 ? j : (j & 1);
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int r = orr + 32 * m;
+                    for (int m = 0; m < ORM; ++m) {
+                        const int r = orr + ORG * m;
                         const uint32_t off = (uint32_t)(r * 128 + ((olg ^ (r & 7)) << 4));
                         uint32_t w[4];
                         ld_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
@@ -958,10 +972,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         st_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
                     }
                     fence_proxy_async_smem();
-                    mbar_arrive(&dready[slot]);   // count = EPI_THREADS
-                    if (warp == 2 && lane == 0 && j == 0) BTRACE(2048 + k * 4 + 2);
+                    mbar_arrive(&dready[slot]);   // count = B2_EPI_THREADS
                 }
-                if (warp == 2 && lane == 0) BTRACE(2048 + k * 4 + 1);
                 dn += KC;
             }
             if (k == 0) continue;
@@ -975,16 +987,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(&xfull[b], (kk >> 1) & 1);
             if (warp == 2 && lane == 0) BTRACE(kk * 8 + 5);
             tc_fence_after();
-            const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + hf) * CHUNK_BYTES + row * 128);
-            uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
 #pragma unroll
-            for (int g2 = 0; g2 < 2; ++g2) {
+            for (int g2 = 0; g2 < CPW / 32; ++g2) {
+                const int col0 = wq * CPW + g2 * 32;     // local dX column (i - 128 rank)
+                const int hf = col0 >> 6;                // local t chunk
+                const int lgb = (col0 & 63) >> 3;        // first logical granule in the chunk
+                const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + hf) * CHUNK_BYTES + row * 128);
+                uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
                 float v[32];
-                tmem_ld32(tmem + t_lane + (uint32_t)(b * 128 + hf * 64 + g2 * 32), v);
+                tmem_ld32(tmem + t_lane + (uint32_t)(b * 128 + col0), v);
                 uint32_t w[16];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int lg = g2 * 4 + j;
+                    const int lg = lgb + j;
                     uint32_t tw[4];
                     ld_shared_v4(tsm + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
 #pragma unroll
@@ -999,7 +1014,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     // logical granules (2m, 2m+1) occupy one 32-byte sector, swapped when row is odd
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
-                        const int lg = g2 * 4 + 2 * m;
+                        const int lg = lgb + 2 * m;
                         const int pos = (lg ^ (row & 7)) & ~1;
                         const uint32_t *g0 = &w[8 * m], *g1 = &w[8 * m + 4];
                         if (row & 1)
@@ -1031,27 +1046,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         // ---- end: all MMAs done -> the rings are free for the reductions
         if (nk > 0) mbar_wait(wdone, 0);
         tc_fence_after();
-        named_bar(1, EPI_THREADS);
+        named_bar(1, EPT);
         float *sred = (float *)Dr;   // [4 quarters][3][128]
 #pragma unroll
-        for (int g2 = 0; g2 < 2; ++g2) {
-            const int col = hf * 64 + g2 * 32 + lane;
+        for (int g2 = 0; g2 < CPW / 32; ++g2) {
+            const int col = wq * CPW + g2 * 32 + lane;
             sred[(q * 3 + 0) * 128 + col] = csx[g2];
             sred[(q * 3 + 1) * 128 + col] = csy[g2];
             sred[(q * 3 + 2) * 128 + col] = cs[g2];
         }
-        float *sob = sred + 12 * 128;   // [32 row groups][2 kinds][128 own features] + [32] (outl)
+        // outl: pre-reduce the 4 row groups of a warp (lanes l, l^8, l^16, l^24 share olg) -> one
+        // [2 kinds][128 own features] row per epilogue warp, then [EW] rows of g sums
+        float *sob = sred + 12 * 128;
         if (a.outl) {
+            const int ew = warp - 2;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    sob[(orr * 2 + 0) * 128 + jj * 64 + olg * 8 + e] = aw[jj][e];
-                    sob[(orr * 2 + 1) * 128 + jj * 64 + olg * 8 + e] = ab[jj][e];
+                    float x1 = aw[jj][e], x2 = ab[jj][e];
+                    x1 += __shfl_xor_sync(0xffffffffu, x1, 8);
+                    x1 += __shfl_xor_sync(0xffffffffu, x1, 16);
+                    x2 += __shfl_xor_sync(0xffffffffu, x2, 8);
+                    x2 += __shfl_xor_sync(0xffffffffu, x2, 16);
+                    if (lane < 8) {
+                        sob[(ew * 2 + 0) * 128 + jj * 64 + olg * 8 + e] = x1;
+                        sob[(ew * 2 + 1) * 128 + jj * 64 + olg * 8 + e] = x2;
+                    }
                 }
-            if (olg == 0) sob[64 * 128 + orr] = ag;
+            float gs = ag;
+            gs += __shfl_xor_sync(0xffffffffu, gs, 8);
+            gs += __shfl_xor_sync(0xffffffffu, gs, 16);
+            if (lane == 0) sob[B2_EPI_WARPS * 2 * 128 + ew] = gs;
         }
-        named_bar(1, EPI_THREADS);
+        named_bar(1, EPT);
         if (ep_tid < 128) {
             const int col = ep_tid, ig = (int)rank * 128 + col;
             float sx = 0.f, sy = 0.f, sb = 0.f;
@@ -1066,7 +1094,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             pb[2 * WP + ig] = sb;
             if (a.outl) {
                 float sw = 0.f, sbb = 0.f;
-                for (int r = 0; r < 32; ++r) {
+                for (int r = 0; r < B2_EPI_WARPS; ++r) {
                     sw += sob[(r * 2 + 0) * 128 + col];
                     sbb += sob[(r * 2 + 1) * 128 + col];
                 }
@@ -1075,7 +1103,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 po[WP + ig] = sbb;
                 if (rank == 0 && col == 0) {
                     float sg = 0.f;
-                    for (int r = 0; r < 32; ++r) sg += sob[64 * 128 + r];
+                    for (int r = 0; r < B2_EPI_WARPS; ++r) sg += sob[B2_EPI_WARPS * 2 * 128 + r];
                     po[2 * WP] = sg;
                 }
             }
@@ -1083,7 +1111,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         // dW^T (rows i local = TMEM lanes, columns o) -> part_dw[pair][o][i], coalesced over i
         float *pw = a.part_dw + (size_t)pair * WP * WP + rank * 128 + row;
 #pragma unroll 1
-        for (int oc = hf * (WP / 2); oc < (hf + 1) * (WP / 2); oc += 32) {
+        for (int oc = wq * (WP / EWQ); oc < (wq + 1) * (WP / EWQ); oc += 32) {
             float v[32];
             if (nk > 0) {
                 tmem_ld32(tm_w + t_lane + (uint32_t)oc, v);
@@ -1360,7 +1388,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.gridDim = dim3(b.grid_bwd);
-        cfg.blockDim = dim3(TC_THREADS);
+        cfg.blockDim = dim3(B2_THREADS);
         cfg.dynamicSmemBytes = B2<WP>::SMEM;
         cfg.stream = s;
         cfg.attrs = attr;
