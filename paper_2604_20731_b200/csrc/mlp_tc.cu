@@ -718,6 +718,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
 // Delta_1 (only its column sums are needed: bias and first-layer weights).
 struct Bwd2Args {
     int N, ntiles, npairs, first, outl;
+    int rev;              // walk the tile sequence backwards (alternating launches: L2 reuse)
     const __half *dsrc;   // Delta_{g+2} (or t_L when outl)   [ntiles][KC] blocks
     const __half *tin;    // t_{g+1}                           [ntiles][KC]
     __half *din;          // Delta_{g+1}                       [ntiles][KC] (unused when first)
@@ -807,7 +808,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             constexpr int PD = 3;
             auto prefetch = [&](int kp) {
                 if (kp >= nk) return;
-                const int tp = pair + kp * a.npairs;
+                const int tp = pair + (a.rev ? nk - 1 - kp : kp) * a.npairs;
                 for (int j = (int)rank; j < KC; j += NS)
                     bulk_prefetch_l2((const uint8_t *)a.dsrc + ((size_t)tp * KC + j) * CHUNK_BYTES, CHUNK_BYTES);
                 bulk_prefetch_l2((const uint8_t *)a.tin + ((size_t)tp * KC + 2 * rank) * CHUNK_BYTES,
@@ -816,7 +817,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             for (int kp = 1; kp < PD; ++kp) prefetch(kp);
             int dn = 0;   // running Delta chunk counter
             for (int k = 0; k < nk; ++k) {
-                const int tile = pair + k * a.npairs;
+                const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
                 prefetch(k + PD);
                 for (int j = 0; j < KC; ++j, ++dn) {
                     const int slot = dn % DS;
@@ -933,7 +934,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         for (int k = 0; k <= nk; ++k) {
             if (a.outl && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
-                const int tile = pair + k * a.npairs;
+                const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
                 float g[ORM];
                 __half2 g2[ORM];
 #pragma unroll
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (k == 0) continue;
             // ---- dX epilogue of tile k-1
             const int kk = k - 1, b = kk & 1, tb = kk % NT;
-            const int tile = pair + kk * a.npairs;
+            const int tile = pair + (a.rev ? nk - 1 - kk : kk) * a.npairs;
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
@@ -1275,6 +1276,8 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     {
         const char *e = getenv("CRVPINN_FUSE_OUTL");   // tuning knob: fused output-layer backward
         b.fuse_outl = WP >= 128 && !(e && e[0] == '0');
+        const char *r = getenv("CRVPINN_BWD_REV");     // tuning knob: alternating tile-walk direction
+        b.bwd_rev = !(r && r[0] == '0');
     }
     auto al = [&](void **p, size_t bytes) -> bool {
         if (cudaMalloc(p, bytes > 0 ? bytes : 16) != cudaSuccess) return false;
@@ -1399,7 +1402,11 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                                                               st);
         for (int g = b.G - 1; g >= 0; --g) {
             const bool outl = g == b.G - 1 && b.fuse_outl;
-            Bwd2Args a{net.N, b.ntiles, b.npairs, g == 0 ? 1 : 0, outl ? 1 : 0,
+            // Launches alternate the direction of their tile walk, starting backwards: the forward
+            // and every launch leave the most recently written tiles (t_L, Delta_in) in L2, and the
+            // next launch reads exactly those first.
+            const int rev = ((b.G - 1 - g) & 1) == 0 ? b.bwd_rev : 0;
+            Bwd2Args a{net.N, b.ntiles, b.npairs, g == 0 ? 1 : 0, outl ? 1 : 0, rev,
                        outl ? b.act + (size_t)(L - 1) * lay : b.delta + (size_t)(g + 1) * lay,
                        b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
                        b.gbar, b.Wop, b.partial + b.off_ob,

@@ -14,6 +14,7 @@ namespace crv {
 struct TcBufs {
     int ready = 0;
     int fuse_outl = 1;
+    int bwd_rev = 1;         // alternate the backward launches' tile-walk direction (L2 reuse)
        // WP >= 128: output-layer backward fused into the first k_tc_bwd2 launch
     int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0;
     __half *Wf = nullptr;    // [G][KC] blocks of WP rows x 128 B: B operand of the forward GEMMs
