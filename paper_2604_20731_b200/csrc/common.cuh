@@ -103,6 +103,8 @@ void launch_adam(float *theta, float *m, float *v, const float *g, long np, cons
 void launch_begin_call(DevState *st, cudaStream_t s);
 // total_groups = reduce_groups(host copy of jobs)
 int reduce_groups(const RedJob *jobs, int njobs);
+void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int nsm,
+                        cudaStream_t s);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s);
 // gram.cu

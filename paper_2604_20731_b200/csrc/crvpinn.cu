@@ -239,6 +239,7 @@ void crvpinn_destroy(crvpinn_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
     gram_free_constants(ctx->gram);
+    tc_destroy(ctx->tc);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_field) cudaFreeHost(ctx->h_field);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);

@@ -108,6 +108,43 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
     }
 }
 
+// One hidden-layer weight job (transposed == 2 layout with cols == ld, count % 4 == 0) with small
+// blocks and no shared memory: a 64-thread CTA fits next to a k_tc_bwd2 CTA (which leaves ~11K
+// registers and ~1.5 KB of shared memory per SM), so the reduction of GEMM g's dW partials runs on
+// a side stream underneath the backward of GEMM g-1 instead of after the last one. Each thread owns
+// four consecutive outputs (float4 loads, eight splits in flight); same summation order as k_reduce.
+constexpr int RW_THREADS = 64;
+__global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restrict__ partial,
+                                                            float *__restrict__ grad, RedJob jb,
+                                                            const DevState *st) {
+    const float sc = jb.scaled ? st->inv_gscale : 1.0f;
+    const int n4 = jb.count >> 2;
+    for (int q = blockIdx.x * RW_THREADS + threadIdx.x; q < n4; q += gridDim.x * RW_THREADS) {
+        const float4 *src = reinterpret_cast<const float4 *>(partial + jb.src + red_off(jb, 4 * q));
+        const long st4 = jb.stride >> 2;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        int z = 0;
+        for (; z + 8 <= jb.nsplit; z += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (long)(z + k) * st4);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { s.x += v[k].x; s.y += v[k].y; s.z += v[k].z; s.w += v[k].w; }
+        }
+        for (; z < jb.nsplit; ++z) {
+            const float4 v = __ldg(src + (long)z * st4);
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+        }
+        float *d = grad + jb.dst + 4 * q;   // dst offsets are not 16-byte aligned in theta
+        d[0] = s.x * sc; d[1] = s.y * sc; d[2] = s.z * sc; d[3] = s.w * sc;
+    }
+}
+
+void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int nsm,
+                        cudaStream_t s) {
+    k_reduce_wide<<<nsm, RW_THREADS, 0, s>>>(partial, grad, job, st);
+}
+
 int reduce_groups(const RedJob *jobs, int njobs) {
     int gsum = 0;
     for (int j = 0; j < njobs; ++j) gsum += red_groups(jobs[j]);

@@ -1322,9 +1322,24 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1);
         if (l == 0) {
             if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
-        } else {
+        }
+    }
+    // hidden-layer weight jobs: with WP >= 128 and a width that is a multiple of 4 they go to the
+    // side-stream reduction (k_reduce_wide, float4 rows) launched right after GEMM g; the rest stay
+    // in the table k_reduce walks after the last GEMM. Side jobs are appended after the deep ones.
+    b.nsm = nsm;
+    const char *sre = getenv("CRVPINN_SIDE_REDUCE");
+    const bool side_ok = !(sre && sre[0] == '0');
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) b.njobs_deep = nj;
+        for (int l = 1; l < nl - 1; ++l) {
+            const int win = net.widths[l], wout = net.widths[l + 1];
+            const bool side = side_ok && WP >= 128 && win % 4 == 0;
+            if (side != (pass == 1)) continue;
             job(b.off_dw + (long)(l - 1) * b.npairs * WP * WP, net.woff[l], wout * win, b.npairs, (long)WP * WP, 2,
                 win, WP);
+            b.wside[l - 1] = side;
+            b.wjobs[l - 1] = jobs[nj - 1];
         }
     }
     if (G == 0) {
@@ -1333,6 +1348,17 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     }
     b.njobs = nj;
     b.groups = reduce_groups(jobs, nj);
+    b.groups_deep = reduce_groups(jobs, b.njobs_deep);
+    if (cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        err = "stream/event creation failed";
+        return CRVPINN_ECUDA;
+    }
+    for (int g = 0; g < G; ++g)
+        if (cudaEventCreateWithFlags(&b.ev_fork[g], cudaEventDisableTiming) != cudaSuccess) {
+            err = "event creation failed";
+            return CRVPINN_ECUDA;
+        }
     if (!al((void **)&b.jobs, sizeof(RedJob) * nj)) {
         err = "cudaMalloc failed";
         return CRVPINN_ENOMEM;
@@ -1344,6 +1370,13 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     else set_attrs<256>(L);
     b.ready = 1;
     return CRVPINN_OK;
+}
+
+void tc_destroy(TcBufs &b) {
+    for (auto &e : b.ev_fork)
+        if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (b.ev_join) { cudaEventDestroy(b.ev_join); b.ev_join = nullptr; }
+    if (b.side) { cudaStreamDestroy(b.side); b.side = nullptr; }
 }
 
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s) {
@@ -1420,6 +1453,10 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 a.trace = trace;
             }
             cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP>, a);
+            // dW of GEMM g is final: reduce it on the side stream while GEMM g-1 runs
+            cudaEventRecord(b.ev_fork[g], s);
+            cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
+            if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, b.nsm, b.side);
             if (te && g == b.G - 1) {
                 cudaStreamSynchronize(s);
                 static long long h[4096];
@@ -1439,7 +1476,13 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
         }
     }
-    launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
+    if constexpr (WP >= 128) {
+        launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s);   // column sums, W1, W_out
+        cudaEventRecord(b.ev_join, b.side);
+        cudaStreamWaitEvent(s, b.ev_join, 0);
+    } else {
+        launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
+    }
 }
 
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {

@@ -30,10 +30,17 @@ struct TcBufs {
     int grid_ob = 0, grid_dx = 0, grid_fwd = 0, grid_bwd = 0, npairs = 0;
     RedJob *jobs = nullptr;  // device copy
     int njobs = 0, max_count = 0, groups = 0;
+    int njobs_deep = 0, groups_deep = 0;   // jobs [0, njobs_deep): column sums, W1, W_out (k_reduce)
+    RedJob wjobs[CRV_MAX_LAYERS];          // hidden-layer weight job of GEMM g
+    bool wside[CRV_MAX_LAYERS] = {};       // ... reduced on the side stream (else inside jobs[0, njobs_deep))
+    int nsm = 148;
+    cudaStream_t side = nullptr;           // side stream of the per-layer weight reductions
+    cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr;
     const float *theta = nullptr;
 };
 
 int tc_create(const Net &net, TcBufs &b, std::string &err);
+void tc_destroy(TcBufs &b);   // side stream + events (device memory is owned by the context)
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
