@@ -138,6 +138,8 @@ class Crvpinn:
 
     def close(self):
         if getattr(self, "_h", None):
+            if load is None:          # interpreter shutdown: module globals already cleared
+                return
             load().crvpinn_destroy(self._h)
             self._h = None
 

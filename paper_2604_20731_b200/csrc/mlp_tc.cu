@@ -27,6 +27,12 @@
 #ifndef CRV_B2_NT
 #define CRV_B2_NT 2
 #endif
+#ifndef CRV_NEWTON_MASK
+#define CRV_NEWTON_MASK 0xAAAA   // which of a thread's 16 elements per chunk take the FMA-pipe reciprocal
+#endif
+#ifndef CRV_CLAMP_NEWTON_ONLY
+#define CRV_CLAMP_NEWTON_ONLY 1
+#endif
 #ifndef CRV_TANH_MIX
 #define CRV_TANH_MIX 1
 #endif
@@ -77,6 +83,26 @@ struct FwdArgs {
 #define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
 
+
+#ifndef CRV_FWD_NSPLIT
+#define CRV_FWD_NSPLIT 1     // last K chunk of each GEMM issued and committed in two N halves
+#endif
+#ifndef CRV_FWD_MMA_SLEEP
+#define CRV_FWD_MMA_SLEEP 1  // MMA-issuer waits suspend (try_wait with a time hint) instead of polling
+#endif
+#ifndef CRV_FWD_EPI_SLEEP
+#define CRV_FWD_EPI_SLEEP 0  // same for the epilogue's accumulator waits
+#endif
+#if CRV_FWD_MMA_SLEEP
+#define FWD_MMA_WAIT mbar_wait_sleep
+#else
+#define FWD_MMA_WAIT mbar_wait
+#endif
+#if CRV_FWD_EPI_SLEEP
+#define FWD_EPI_WAIT mbar_wait_sleep
+#else
+#define FWD_EPI_WAIT mbar_wait
+#endif
 
 constexpr float TANH_C = 2.8853900817779268f;   // 2 log2(e): tanh(z) = 1 - 2 / (1 + 2^(TANH_C z))
 constexpr int FWD_EPI_WARPS = 16;                       // 4 per TMEM lane quarter
@@ -165,13 +191,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 for (int g = 0; g < a.G; ++g, ++gi) {
                     const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
                     for (int c = 0; c < KC; ++c) {
-                        mbar_wait(&a_full[c], aph);
+                        FWD_MMA_WAIT(&a_full[c], aph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 0);
                         // t_hi chunk c of layer g+1 -> HBM (the backward's operand)
                         bulk_s2g(a.act + ((size_t)g * a.ntiles + tile) * (KC * CHUNK_HALVES) + c * CHUNK_HALVES,
                                  A_hi + c * CHUNK_BYTES, CHUNK_BYTES);
                         bulk_commit();
-                        mbar_wait(&w_full[stage], ph);
+                        FWD_MMA_WAIT(&w_full[stage], ph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
                         if (c + 1 < KC) {
@@ -183,6 +209,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                                 mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
                                 mma_f16(acc, dl, bd, idesc, 1u);
                             }
+                        } else if (!CRV_FWD_NSPLIT) {
+                            bulk_wait_read0();
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
+                                uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
+                                mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
+                                mma_f16(acc, dl, bd, idesc, 1u);
+                            }
+                            mma_commit(&acc_full[(gi & 1) * 2]);
+                            mma_commit(&acc_full[(gi & 1) * 2 + 1]);
                         } else {
                             // last K chunk in two N halves, each committed on its own barrier: the
                             // next epilogue starts on output features [0, WP/2) while the MMAs for
@@ -241,8 +279,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     const int ai = gi & 1;
                     ab = ai * 2;
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
-                    mbar_wait(&acc_full[ab], (acc_ph >> ab) & 1u);
+                    FWD_EPI_WAIT(&acc_full[ab], (acc_ph >> ab) & 1u);
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
+                    if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1)) * 16 + (warp - 2));
                     acc_ph ^= 1u << ab;
                     acc = (uint32_t)(ai * WP);
                     got1 = false;
@@ -259,7 +298,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 uint32_t rbuf[16];
                 auto need_half1 = [&](int col) {
                     if (col >= WP / 2 && !got1) {
-                        mbar_wait(&acc_full[ab + 1], (acc_ph >> (ab + 1)) & 1u);
+                        FWD_EPI_WAIT(&acc_full[ab + 1], (acc_ph >> (ab + 1)) & 1u);
                         acc_ph ^= 1u << (ab + 1);
                         got1 = true;
                         tc_fence_after();
@@ -307,11 +346,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     uint32_t hw[8], lw[8];
 #pragma unroll
                     for (int i = 0; i < 16 + 5; ++i) {
+#if CRV_TANH_MIX && CRV_CLAMP_NEWTON_ONLY
+                        // only the Newton reciprocal needs a finite 1 + 2^v (rcp.approx(inf) = 0)
+                        if (i < 16) e[i] = ex2_v(((CRV_NEWTON_MASK >> i) & 1) ? fminf(v[i], 60.0f) : v[i]);
+#else
                         if (i < 16) e[i] = ex2_v(fminf(v[i], 60.0f));
+#endif
 #if CRV_TANH_MIX
                         // odd elements take the reciprocal on the FMA pipe (MUFU : ALU balance)
                         if (i >= 2 && i < 18)
-                            r[i - 2] = ((i - 2) & 1) ? rcp_newton(1.0f + e[i - 2]) : rcp_v(1.0f + e[i - 2]);
+                            r[i - 2] = ((CRV_NEWTON_MASK >> (i - 2)) & 1) ? rcp_newton(1.0f + e[i - 2]) : rcp_v(1.0f + e[i - 2]);
 #else
                         if (i >= 2 && i < 18) r[i - 2] = rcp_v(1.0f + e[i - 2]);
 #endif
@@ -334,6 +378,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
+                        if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
                         if (lane == 0) mbar_arrive(&a_full[c]);
                     } else {
 #pragma unroll

@@ -1,8 +1,8 @@
 #!/bin/bash
-# A/B: side-stream weight reduction on/off, alternating
-for r in 1 2 3; do
-  for v in 1 0; do
-    CRVPINN_SIDE_REDUCE=$v timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/ab_${v}_${r}.log 2>&1
-    echo "side=$v run=$r $(python -c "import json,sys; d=json.loads(open('gpurun_out/ab_${v}_${r}.log').read().strip().splitlines()[-1]); print(round(d['value'],1), d['clocks']['sm_mhz'])")"
+# A/B: default build vs variants under build/ab/ (stage times from the profiled step graph)
+for r in 1 2; do
+  for v in default clampn clampn_m6 clampn_m10 esleep; do
+    if [ $v = default ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
+    CRVPINN_LIB=$L timeout 120 python scripts/stage_time.py C5 5 2>&1 | tail -1 | sed "s|^|$v: |"
   done
 done

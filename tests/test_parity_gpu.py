@@ -140,6 +140,24 @@ def test_workload_100_steps(crv, prec, name):
     assert np.all(np.abs(hist - rhist) <= 0.02 * np.abs(rhist) + 1e-3 * np.abs(rhist).max())
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_c3_pretraining_2000(crv, prec):
+    """C3's pretraining phase (SURVEY.md §8(d) schedule: 2000 Adam iterations before the 10x100
+    updates; parity "after pretraining for C3"): final loss within 2 % of the oracle's, the loss
+    history within 2 % (+ a floor of 1e-3 of its maximum) at every iteration."""
+    z = _golden("C3", "traj2000")
+    F = W.make_fields("C3")
+    w = F.workload
+    g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=prec, lr=w.lr)
+    hist = g.pretrain(2000)
+    final = g.loss_grad(grad=False)
+    rhist, rfinal = z["hist"], float(z["final_loss"])
+    assert abs(final - rfinal) <= 0.02 * abs(rfinal), (final, rfinal)
+    assert abs(hist[0] - rhist[0]) <= TOL[prec][0] * abs(rhist[0])
+    dev = np.abs(hist - rhist) / (np.abs(rhist) + 1e-3 * np.abs(rhist).max())
+    assert dev.max() <= 0.02, (int(dev.argmax()), float(dev.max()))
+
+
 # ------------------------------------------------------------------ semantics and edge cases
 def test_step_composition_and_determinism(crv):
     """step(30)+step(70) == step(100) bitwise (Adam state persists, R8); runs are deterministic."""
