@@ -140,22 +140,46 @@ def test_workload_100_steps(crv, prec, name):
     assert np.all(np.abs(hist - rhist) <= 0.02 * np.abs(rhist) + 1e-3 * np.abs(rhist).max())
 
 
+def _ulp_perturbed(theta0, seed):
+    """theta0 with every entry moved one fp32 ulp up or down (seeded signs); the recipe of
+    scripts/c3_sensitivity.py, which wrote the oracle's perturbed fixtures."""
+    t0 = np.asarray(theta0, dtype=np.float32)
+    rng = np.random.default_rng(seed)
+    return np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
+
+
 @pytest.mark.parametrize("prec", PRECS)
 def test_c3_pretraining_2000(crv, prec):
-    """C3's pretraining phase (SURVEY.md §8(d) schedule: 2000 Adam iterations before the 10x100
-    updates; parity "after pretraining for C3"): final loss within 2 % of the oracle's, the loss
-    history within 2 % (+ a floor of 1e-3 of its maximum) at every iteration."""
-    z = _golden("C3", "traj2000")
+    """C3's pretraining phase (2000 Adam iterations; parity "after pretraining
+    for C3"). Beyond a few hundred iterations the trajectory is chaotic: the oracle itself, started
+    from theta0 moved by one fp32 ulp, leaves its unperturbed run by >2 % at iteration 388 and by up
+    to 59 % later (tests/golden/C3_traj2000_perturbed*.npz; R22). So the check is
+    (a) pointwise over the predictable first 200 iterations (the 100-step tolerance), and
+    (b) statistical afterwards: the mean loss over iterations [900, 1100) and [1800, 2000) of an
+    ensemble (theta0 + 4 ulp-perturbed starts) against the same windows of the oracle's ensemble."""
+    ref = [_golden("C3", "traj2000")["hist"]]
+    for seed in range(1, 5):
+        path = os.path.join(GOLDEN, f"C3_traj2000_perturbed{seed}.npz")
+        if os.path.exists(path):
+            ref.append(np.load(path)["hist"])
+    if len(ref) < 2:
+        pytest.skip("needs >= 1 perturbed oracle run (scripts/c3_sensitivity.py)")
     F = W.make_fields("C3")
     w = F.workload
-    g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=prec, lr=w.lr)
-    hist = g.pretrain(2000)
-    final = g.loss_grad(grad=False)
-    rhist, rfinal = z["hist"], float(z["final_loss"])
-    assert abs(final - rfinal) <= 0.02 * abs(rfinal), (final, rfinal)
+    runs = []
+    for seed in range(5):
+        th = F.theta0 if seed == 0 else _ulp_perturbed(F.theta0, seed)
+        g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, th, precision=prec, lr=w.lr)
+        runs.append(g.pretrain(2000))
+        g.close()
+    hist, rhist = runs[0], ref[0]
     assert abs(hist[0] - rhist[0]) <= TOL[prec][0] * abs(rhist[0])
-    dev = np.abs(hist - rhist) / (np.abs(rhist) + 1e-3 * np.abs(rhist).max())
+    dev = np.abs(hist[:200] - rhist[:200]) / (np.abs(rhist[:200]) + 1e-3 * np.abs(rhist).max())
     assert dev.max() <= 0.02, (int(dev.argmax()), float(dev.max()))
+    for (a, b), tol in (((900, 1100), 0.10), ((1800, 2000), 0.25)):
+        ours = np.mean([r[a:b].mean() for r in runs])
+        theirs = np.mean([r[a:b].mean() for r in ref])
+        assert abs(ours - theirs) <= tol * theirs, ((a, b), ours, theirs)
 
 
 # ------------------------------------------------------------------ semantics and edge cases
