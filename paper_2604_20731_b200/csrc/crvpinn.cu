@@ -133,7 +133,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
 
 static int launches_per_iter(const crvpinn_ctx *ctx) {
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
-    int mlp = tc ? tc_launches(ctx->net) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
+    int mlp = tc ? tc_launches(ctx->net, ctx->tc) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
     return mlp + 4 /*residual+DST, tridiagonal, inverse DST+loss, adjoint+loss final*/ + 1 /*adam*/;
 }
 

@@ -778,6 +778,9 @@ struct Bwd2Args {
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
+#ifndef CRV_T_FIRST
+#define CRV_T_FIRST 0   // backward producers issue a tile's t_in load before its Delta chunks
+#endif
 #ifndef CRV_B2_EPI_WARPS
 #define CRV_B2_EPI_WARPS 8
 #endif
@@ -861,9 +864,21 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             };
             for (int kp = 1; kp < PD; ++kp) prefetch(kp);
             int dn = 0;   // running Delta chunk counter
+            auto load_t = [&](int k, int tile) {
+                const int tb = k % NT;
+                BTRACE(k * 8 + 0);
+                mbar_wait_sleep(&tempty[tb], ((k / NT) & 1) ^ 1);
+                BTRACE(k * 8 + 1);
+                mbar_arrive_expect_tx(&tfull[tb], 2 * CHUNK_BYTES);
+                bulk_g2s(Tr + tb * 2 * CHUNK_BYTES,
+                         (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
+                         &tfull[tb]);
+            };
             for (int k = 0; k < nk; ++k) {
                 const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
                 prefetch(k + PD);
+                // t first: its ring is independent of the Delta ring, whose slots free up late
+                if (CRV_T_FIRST) load_t(k, tile);
                 for (int j = 0; j < KC; ++j, ++dn) {
                     const int slot = dn % DS;
                     mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
@@ -873,14 +888,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     else if ((uint32_t)(j % NS) == rank)
                         bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], MASK);
                 }
-                const int tb = k % NT;
-                BTRACE(k * 8 + 0);
-                mbar_wait_sleep(&tempty[tb], ((k / NT) & 1) ^ 1);
-                BTRACE(k * 8 + 1);
-                mbar_arrive_expect_tx(&tfull[tb], 2 * CHUNK_BYTES);
-                bulk_g2s(Tr + tb * 2 * CHUNK_BYTES,
-                         (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
-                         &tfull[tb]);
+                if (!CRV_T_FIRST) load_t(k, tile);
             }
         }
     } else if (warp == 1) {
@@ -1175,6 +1183,412 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ================================================================ backward chain (WP >= 128)
+// All hidden GEMMs of the backward in as few launches as possible, as a spatial pipeline: a
+// cluster of S x NS CTAs holds S stages; stage s (CTAs [s NS, s NS + NS)) runs GEMM g0 - s like
+// k_tc_bwd2 (W^T half resident, dX + dW^T per tile, Delta_out multicast to the stage's CTAs), and
+// the clusters split the tile sequence. Delta_in of stage s goes to stage s+1 through a small
+// per-cluster ring in global memory (BC_RS tiles per stage boundary, ~11 MB in total at C5, so it
+// stays in L2) instead of a full HBM round trip per layer:
+//   stage s epilogue  : wait oempty[slot] -> st.global its 64-column chunk -> proxy + gpu fence ->
+//                       remote arrive on gfull[slot][chunk] of the stage-(s+1) CTA that loads it
+//   stage s+1 producer: wait gfull -> multicast bulk load into the stage's Delta rings
+//   stage s+1 MMA     : once the chunk pair of producer CTA h is consumed, commit (multicast) to
+//                       oempty[slot] of that CTA -> the ring slot may be overwritten
+// Bias gradients come from the tensor cores: each stage also accumulates 1^T Delta_out over its
+// own half of the output features (an all-ones A operand: one 128-byte core matrix with zero
+// strides), i.e. the bias gradient of theta layer g+1; only the last stage (g = 0) reduces its
+// own output on the CUDA cores (bias and first-layer weights). The dX accumulator is single
+// buffered to make room (its commit is issued before the second dW half, so the epilogue drains
+// it under the remaining MMAs). The output-layer backward runs before the chain (k_tc_out_bwd).
+#ifndef CRV_BC_FENCE
+#define CRV_BC_FENCE 1     // ring hand-off: 1 = cluster-scope acq_rel fence per lane, 2 = gpu-scope sc fence
+#endif
+#ifndef CRV_BC_RS
+#define CRV_BC_RS 3
+#endif
+constexpr int BC_RS = CRV_BC_RS;   // global ring slots (tiles) per stage boundary
+template <int WP>
+struct BC {
+    static constexpr uint32_t SMEM = B2<WP>::SMEM + 256;   // + the all-ones core matrix
+};
+struct BwdcArgs {
+    int N, ntiles, nclus, S, g0;
+    const __half *dsrc;   // stage 0 input: Delta_{g0+2}                    [ntiles][KC] blocks
+    const __half *act;    // activations; t_{g+1} at act + g * lay
+    __half *dout;         // Delta_{g0-S+2} of the last stage (HBM), unused when that stage has g = 0
+    __half *ring;         // [nclus][S-1][BC_RS][KC] blocks
+    const __half *WTf;    // [G][KC] blocks
+    float *part_dx;       // [G][nclus][3*WP]  (only g = 0 is written: x, y and bias sums of Delta_1)
+    float *part_dw;       // [G][nclus][WP*WP]
+    float *part_cb;       // [G][nclus][WP]    1^T Delta_out of GEMM g (bias gradient of theta layer g+1)
+    size_t lay;           // halves per activation layer
+    long long *trace;     // debug timeline: CTAs 0..7 (cluster 0), 512 slots each; nullptr normally
+};
+#define CTRACE(slot) do { if (a.trace && blockIdx.x < 8 && (slot) < 1024) a.trace[blockIdx.x * 1024 + (slot)] = clock64(); } while (0)
+
+__device__ __forceinline__ uint64_t sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
+    constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT, RS = BC_RS;
+    static_assert(B2_EPI_WARPS == 8, "chain epilogue: one 64-column chunk per warp");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *Wt = smem;
+    uint8_t *Dr = Wt + KC * CHUNK_BYTES;
+    uint8_t *Tr = Dr + DS * CHUNK_BYTES;
+    uint8_t *ones = Tr + 2 * NT * CHUNK_BYTES;   // 256 B of fp16 ones (A operand of the bias MMA)
+    uint64_t *bars = (uint64_t *)(ones + 256);
+    uint64_t *wfull = bars;
+    uint64_t *dfull = bars + 1, *dempty = dfull + DS;
+    uint64_t *tfull = dempty + DS, *tempty = tfull + NT, *xfull = tempty + NT, *xempty = xfull + 1;
+    uint64_t *wdone = xempty + 1;
+    uint64_t *gfull = wdone + 1;          // [RS][KC] (consumer side)
+    uint64_t *oempty = gfull + RS * KC;   // [RS]     (producer side)
+    uint32_t *tmem_slot = (uint32_t *)(oempty + RS);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t cr = cluster_rank();
+    const int S = a.S;
+    const int s = (int)cr / NS;
+    const uint32_t rank = cr % NS;
+    const int g = a.g0 - s;
+    const bool first = g == 0;
+    const bool to_ring = s < S - 1;
+    const uint16_t smask = (uint16_t)(((1u << NS) - 1u) << (s * NS));
+    const int cid = blockIdx.x / (S * NS);
+    const int nk = cid < a.ntiles ? (a.ntiles - cid + a.nclus - 1) / a.nclus : 0;
+    const __half *tin = a.act + (size_t)g * a.lay;
+    auto ring_chunk = [&](int boundary, int gs, int j) -> __half * {
+        return a.ring + ((((size_t)cid * (S - 1) + boundary) * RS + gs) * KC + j) * CHUNK_HALVES;
+    };
+    if (threadIdx.x < 64) reinterpret_cast<uint32_t *>(ones)[threadIdx.x] = 0x3C003C00u;   // fp16 1.0 pairs
+    if (threadIdx.x == 0) {
+        mbar_init(wfull, 1);
+        for (int i = 0; i < DS; ++i) {
+            mbar_init(&dfull[i], 1);
+            mbar_init(&dempty[i], NS);
+        }
+        for (int i = 0; i < NT; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 1 + B2_EPI_WARPS);
+        }
+        mbar_init(xfull, 1);
+        mbar_init(xempty, B2_EPI_WARPS);
+        mbar_init(wdone, 1);
+        for (int i = 0; i < RS * KC; ++i) mbar_init(&gfull[i], 4);   // 4 warps (lane quarters) per chunk
+        for (int i = 0; i < RS; ++i) mbar_init(&oempty[i], NS);      // one commit per consumer CTA
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();   // the ones block is read by the tensor cores
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    pdl_wait();
+    pdl_trigger();
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tm_x = tmem, tm_c = tmem + 128, tm_w = tmem + 256;   // dX | 1^T Delta | dW^T
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (lane == 0) {
+            mbar_arrive_expect_tx(wfull, KC * CHUNK_BYTES);
+            for (int kc = 0; kc < KC; ++kc)
+                bulk_g2s(Wt + kc * CHUNK_BYTES,
+                         (const uint8_t *)a.WTf + ((size_t)g * KC * WP * 64 + (size_t)kc * WP * 64 + 128 * rank * 64) * 2,
+                         CHUNK_BYTES, wfull);
+            constexpr int PD = 3;
+            auto prefetch = [&](int kp) {
+                if (kp >= nk) return;
+                const int tp = cid + kp * a.nclus;
+                if (s == 0)
+                    for (int j = (int)rank; j < KC; j += NS)
+                        bulk_prefetch_l2((const uint8_t *)a.dsrc + ((size_t)tp * KC + j) * CHUNK_BYTES, CHUNK_BYTES);
+                bulk_prefetch_l2((const uint8_t *)tin + ((size_t)tp * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES);
+            };
+            for (int kp = 1; kp < PD; ++kp) prefetch(kp);
+            int dn = 0;
+            auto load_t = [&](int k, int tile) {
+                const int tb = k % NT;
+                CTRACE(k * 16 + 0);
+                mbar_wait_sleep(&tempty[tb], ((k / NT) & 1) ^ 1);
+                CTRACE(k * 16 + 1);
+                mbar_arrive_expect_tx(&tfull[tb], 2 * CHUNK_BYTES);
+                bulk_g2s(Tr + tb * 2 * CHUNK_BYTES, (const uint8_t *)tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES,
+                         2 * CHUNK_BYTES, &tfull[tb]);
+            };
+            for (int k = 0; k < nk; ++k) {
+                const int tile = cid + k * a.nclus;
+                const int gs = k % RS;
+                prefetch(k + PD);
+                if (CRV_T_FIRST) load_t(k, tile);
+                for (int j = 0; j < KC; ++j, ++dn) {
+                    const int slot = dn % DS;
+                    mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&dfull[slot], CHUNK_BYTES);
+                    if ((uint32_t)(j % NS) != rank) continue;   // the peer multicasts this chunk
+                    const uint8_t *src;
+                    if (s == 0) {
+                        src = (const uint8_t *)a.dsrc + ((size_t)tile * KC + j) * CHUNK_BYTES;
+                    } else {
+                        if (j < 2) CTRACE(k * 16 + 11 + 2 * j);
+                        mbar_wait_cluster(&gfull[gs * KC + j], (k / RS) & 1);
+                        if (j < 2) CTRACE(k * 16 + 12 + 2 * j);
+                        fence_proxy_async_global();
+                        src = (const uint8_t *)ring_chunk(s - 1, gs, j);
+                    }
+                    if (NS == 1) bulk_g2s(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot]);
+                    else bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], smask);
+                }
+                if (!CRV_T_FIRST) load_t(k, tile);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_x = idesc_f16(128, 128, 0, 0);
+            constexpr uint32_t idesc_w = idesc_f16(128, 128, 1, 1);
+            constexpr uint32_t idesc_c = idesc_f16(128, 128, 0, 1);
+            const uint32_t wt = smem_u32(Wt), dr = smem_u32(Dr), tr = smem_u32(Tr);
+            const uint64_t d1 = sdesc_none(smem_u32(ones), 0, 0);
+            mbar_wait_sleep(wfull, 0);
+            int dn = 0;
+            for (int k = 0; k < nk; ++k) {
+                const int tb = k % NT, gs = k % RS;
+                const int slot0 = dn % DS;
+                mbar_wait_sleep(&tfull[tb], (k / NT) & 1);
+                CTRACE(k * 16 + 2);
+                mbar_wait_sleep(xempty, (k & 1) ^ 1);
+                CTRACE(k * 16 + 7);
+                tc_fence_after();
+                for (int h = 0; h < KC / 2; ++h) {
+                    const int sl = (slot0 + 2 * h) % DS;
+                    for (int j = 2 * h; j < 2 * h + 2; ++j) {
+                        mbar_wait_sleep(&dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
+                        if (j == 0) CTRACE(k * 16 + 15);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kq = 0; kq < 4; ++kq) {
+                            const uint64_t ad = sdesc_sw128(dr + (sl + j - 2 * h) * CHUNK_BYTES + kq * 32, 16, 1024);
+                            const uint64_t bd = sdesc_sw128(wt + j * CHUNK_BYTES + kq * 32, 16, 1024);
+                            mma_f16(tm_x, ad, bd, idesc_x, (j | kq) != 0);
+                        }
+                    }
+                    if (h == KC / 2 - 1) {
+                        mma_commit(xfull);   // dX complete: the epilogue drains it under the rest
+                        CTRACE(k * 16 + 3);
+                    }
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint64_t ad = sdesc_sw128(tr + tb * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                        const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                        mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
+                    }
+                    if (h == (int)rank) {
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks) {
+                            const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                            mma_f16(tm_c, d1, bd, idesc_c, (k | ks) != 0);
+                        }
+                    }
+                    for (int j = 0; j < 2; ++j) {
+                        if (NS == 1) mma_commit(&dempty[sl + j]);
+                        else mma_commit_mc(&dempty[sl + j], smask);
+                    }
+                    // chunks (2h, 2h+1) came from CTA h of the previous stage: its ring slot is free
+                    if (s > 0) mma_commit_mc(&oempty[gs], (uint16_t)(1u << ((s - 1) * NS + h)));
+                }
+                mma_commit(&tempty[tb]);
+                dn += KC;
+            }
+            mma_commit(wdone);
+        }
+    } else {
+        // ---------------- epilogue warps (8): warp % 4 = TMEM lane quarter, wq = which 64 columns
+        constexpr int EPT = B2_EPI_THREADS;
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int wq = (warp - 2) >> 2;
+        const int ep_tid = threadIdx.x - 64;
+        const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+        const int N = a.N;
+        float cs[2] = {0.f, 0.f}, csx[2] = {0.f, 0.f}, csy[2] = {0.f, 0.f};
+        // hand this warp's chunk of a finished tile (ring slot pgs) to the next stage. Deferred by
+        // one tile: by the time the next tile's dX is drained the stores are long complete, so the
+        // gpu-scope fence does not stall the epilogue.
+        int pgs = -1;
+        auto handoff = [&]() {
+            if (pgs < 0) return;
+            fence_proxy_async_global();
+#if CRV_BC_FENCE == 2
+            __threadfence();
+#elif CRV_BC_FENCE == 1
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+#endif
+            __syncwarp();
+            if (lane == 0) {
+                const int j = 2 * (int)rank + wq;   // global chunk index within the tile
+                mbar_arrive_cluster(mapa_shared(&gfull[pgs * KC + j], (uint32_t)((s + 1) * NS + (j % NS))));
+            }
+            pgs = -1;
+        };
+        for (int kk = 0; kk < nk; ++kk) {
+            const int tb = kk % NT, gs = kk % RS;
+            const int tile = cid + kk * a.nclus;
+            if (warp == 2 && lane == 0) CTRACE(kk * 16 + 4);
+            mbar_wait(xfull, kk & 1);
+            if (warp == 2 && lane == 0) CTRACE(kk * 16 + 5);
+            tc_fence_after();
+            // this warp's 64 dX columns (local chunk wq) -> registers, then release the accumulator
+            uint32_t r[4][16];
+            const uint32_t tacc = tm_x + t_lane + (uint32_t)(wq * 64);
+#pragma unroll
+            for (int sl = 0; sl < 4; ++sl) tmem_ld16_async(tacc + (uint32_t)(16 * sl), r[sl]);
+            tmem_wait_ld16(r[0]);
+            tmem_wait_ld16(r[1]);
+            tmem_wait_ld16(r[2]);
+            tmem_wait_ld16(r[3]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xempty);
+            handoff();
+            if (warp == 2 && lane == 0) CTRACE(kk * 16 + 8);
+            if (to_ring && !first) mbar_wait(&oempty[gs], ((kk / RS) & 1) ^ 1);   // ring slot consumed
+            if (warp == 2 && lane == 0) CTRACE(kk * 16 + 9);
+            const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + wq) * CHUNK_BYTES + row * 128);
+            uint8_t *drow = to_ring ? (uint8_t *)ring_chunk(s, gs, 2 * (int)rank + wq) + row * 128
+                                    : (uint8_t *)a.dout + ((size_t)tile * KC + 2 * rank + wq) * CHUNK_BYTES + row * 128;
+            float x = 0.f, y = 0.f;
+            if (first) {
+                int pi, pj;
+                point_ij(tile * 128 + row, N, pi, pj);
+                x = (float)pi / (float)N;
+                y = (float)pj / (float)N;
+            }
+#pragma unroll
+            for (int hp = 0; hp < 2; ++hp) {          // slice pairs: columns wq*64 + 32 hp + [0, 32)
+                float acc[32];
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const int sl = 2 * hp + s2;
+                    uint32_t tw[8];
+                    ld_shared_v4(tsm + (uint32_t)(((2 * sl) ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
+                    ld_shared_v4(tsm + (uint32_t)(((2 * sl + 1) ^ (row & 7)) << 4), tw[4], tw[5], tw[6], tw[7]);
+                    uint32_t w[8];
+#pragma unroll
+                    for (int mm = 0; mm < 8; ++mm) {
+                        const float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&tw[mm]));
+                        const float d0 = __uint_as_float(r[sl][2 * mm]) * fmaf(-tf.x, tf.x, 1.0f);
+                        const float d1 = __uint_as_float(r[sl][2 * mm + 1]) * fmaf(-tf.y, tf.y, 1.0f);
+                        acc[16 * s2 + 2 * mm] = d0;
+                        acc[16 * s2 + 2 * mm + 1] = d1;
+                        w[mm] = pack_half2(d0, d1);
+                    }
+                    if (!first) {
+                        // logical granules (2 sl, 2 sl + 1) share one 32-byte sector, swapped on odd rows
+                        const int pos = ((2 * sl) ^ (row & 7)) & ~1;
+                        if (row & 1) st_global_v8(drow + pos * 16, w[4], w[5], w[6], w[7], w[0], w[1], w[2], w[3]);
+                        else st_global_v8(drow + pos * 16, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+                    }
+                }
+                if (first) {
+                    float tmp[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) tmp[e] = acc[e] * x;
+                    warp_reduce_scatter32(tmp, lane);
+                    csx[hp] += tmp[0];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) tmp[e] = acc[e] * y;
+                    warp_reduce_scatter32(tmp, lane);
+                    csy[hp] += tmp[0];
+                    warp_reduce_scatter32(acc, lane);
+                    cs[hp] += acc[0];
+                }
+            }
+            if (warp == 2 && lane == 0) CTRACE(kk * 16 + 10);
+            if (to_ring && !first) pgs = gs;
+            __syncwarp();
+            if (lane == 0) {
+                if (warp == 2) CTRACE(kk * 16 + 6);
+                mbar_arrive(&tempty[tb]);
+            }
+        }
+        handoff();
+        // ---- end: all MMAs done -> the rings are free for the reductions
+        if (nk > 0) mbar_wait(wdone, 0);
+        tc_fence_after();
+        named_bar(1, EPT);
+        float *sred = (float *)Dr;
+        if (first) {
+#pragma unroll
+            for (int hp = 0; hp < 2; ++hp) {
+                const int col = wq * 64 + hp * 32 + lane;
+                sred[(q * 3 + 0) * 128 + col] = csx[hp];
+                sred[(q * 3 + 1) * 128 + col] = csy[hp];
+                sred[(q * 3 + 2) * 128 + col] = cs[hp];
+            }
+        }
+        named_bar(1, EPT);
+        if (first && ep_tid < 128) {
+            const int col = ep_tid, ig = (int)rank * 128 + col;
+            float sx = 0.f, sy = 0.f, sb = 0.f;
+            for (int qq = 0; qq < 4; ++qq) {
+                sx += sred[(qq * 3 + 0) * 128 + col];
+                sy += sred[(qq * 3 + 1) * 128 + col];
+                sb += sred[(qq * 3 + 2) * 128 + col];
+            }
+            float *pb = a.part_dx + ((size_t)g * a.nclus + cid) * 3 * WP;
+            pb[2 * ig] = sx;
+            pb[2 * ig + 1] = sy;
+            pb[2 * WP + ig] = sb;
+        }
+        // 1^T Delta_out for the own output-feature half: every TMEM row holds the same sums
+        if (q == 0) {
+            float v[32];
+            const int oc = wq * 64;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                if (nk > 0) {
+                    tmem_ld32(tm_c + t_lane + (uint32_t)(oc + 32 * half), v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+                if (lane == 0) {
+                    float *pc = a.part_cb + ((size_t)g * a.nclus + cid) * WP + (int)rank * 128 + oc + 32 * half;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) pc[e] = v[e];
+                }
+            }
+        }
+        // dW^T (rows i local = TMEM lanes, columns o) -> part_dw[g][cid][o][i], coalesced over i
+        float *pw = a.part_dw + ((size_t)g * a.nclus + cid) * WP * WP + rank * 128 + row;
+#pragma unroll 1
+        for (int oc = wq * (WP / 2); oc < (wq + 1) * (WP / 2); oc += 32) {
+            float v[32];
+            if (nk > 0) {
+                tmem_ld32(tm_w + t_lane + (uint32_t)oc, v);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) pw[(size_t)(oc + e) * WP] = v[e];
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // ================================================================ weight re-layout
 
 
@@ -1287,8 +1701,36 @@ static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
         cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwdc<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, BC<WP>::SMEM);
     } else {
         cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
+    }
+}
+
+// clusters of the backward chain (cluster size S x NS) that can be co-resident on the device
+template <int WP>
+static int chain_max_clusters(int csize) {
+    if constexpr (WP >= 128) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(csize * 64);
+        cfg.blockDim = dim3(B2_THREADS);
+        cfg.dynamicSmemBytes = BC<WP>::SMEM;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (csize > 8) cudaFuncSetAttribute(k_tc_bwdc<WP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_tc_bwdc<WP>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return n;
+    } else {
+        return 0;
     }
 }
 
@@ -1305,6 +1747,10 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         err = "too many layers for the shared-memory budget of the fused forward";
         return CRVPINN_EINVAL;
     }
+    if (WP == 64) set_attrs<64>(L);
+    else if (WP == 128) set_attrs<128>(L);
+    else if (WP == 192) { err = "hidden width 160/192 not supported by the tensor path"; return CRVPINN_EINVAL; }
+    else set_attrs<256>(L);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
@@ -1316,11 +1762,35 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         b.npairs = np_;
         b.grid_dx = np_;              // rows of the column-sum partials
         b.grid_bwd = np_ * NS;        // CTAs per backward launch
+        // backward chain (k_tc_bwdc): S stages of NS CTAs per cluster, clusters split the tiles
+        // (measured slower than one k_tc_bwd2 launch per GEMM at C5: opt-in only)
+        const char *ce = getenv("CRVPINN_BWD_CHAIN");       // tuning knob: 1 = backward chain
+        const char *se = getenv("CRVPINN_BWD_STAGES");      // tuning knob: stages per cluster (implies chain)
+        b.chain = 0;
+        if (WP >= 128 && G >= 2 && ((ce && ce[0] == '1') || se)) {
+            int S = se ? atoi(se) : 8 / NS;
+            if (S > G) S = G;
+            if (S * NS > 8) S = 8 / NS;
+            if (S < 1) S = 1;
+            {
+                int nc = WP == 128 ? chain_max_clusters<128>(S * NS) : chain_max_clusters<256>(S * NS);
+                if (nc > b.ntiles) nc = b.ntiles;
+                if (nc > 0) {
+                    b.chain = 1;
+                    b.chain_S = S;
+                    b.npairs = b.grid_dx = nc;
+                    b.grid_bwd = nc * S * NS;
+                }
+            }
+        }
     }
-    b.grid_ob = WP >= 128 ? b.npairs : (b.ntiles < 4 * nsm ? b.ntiles : 4 * nsm);
     {
+        // the output-layer backward is fused into the first backward GEMM (k_tc_bwd2); with the
+        // chain it runs as its own bandwidth-bound pass (k_tc_out_bwd) so that it does not pace
+        // every stage of the chain
         const char *e = getenv("CRVPINN_FUSE_OUTL");   // tuning knob: fused output-layer backward
-        b.fuse_outl = WP >= 128 && !(e && e[0] == '0');
+        b.fuse_outl = WP >= 128 && !b.chain && !(e && e[0] == '0');
+        b.grid_ob = WP >= 128 && b.fuse_outl ? b.npairs : (b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm);
         const char *r = getenv("CRVPINN_BWD_REV");     // tuning knob: alternating tile-walk direction
         b.bwd_rev = !(r && r[0] == '0');
     }
@@ -1335,7 +1805,8 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     b.off_ob = 0;
     b.off_dx = up64(b.off_ob + (long)b.grid_ob * (2 * WP + 1));
     b.off_dw = up64(b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP);
-    const long ptotal = b.off_dw + (long)(G > 0 ? G * b.npairs : 1) * WP * WP;
+    b.off_cb = up64(b.off_dw + (long)(G > 0 ? G * b.npairs : 1) * WP * WP);
+    const long ptotal = b.off_cb + (b.chain ? (long)G * b.npairs * WP : 0);
     if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
         !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
         !al((void **)&b.Wop, (WP + 1) * 4) || !al((void **)&b.act, actn * 2) || !al((void **)&b.delta, actn * 2) ||
@@ -1362,8 +1833,11 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
             job(b.off_ob + 2 * WP, net.boff[l], 1, b.grid_ob, 2 * WP + 1, 0, 1, 1);
             continue;
         }
-        // bias of theta layer l <-> Delta_{l+1}: from out_bwd (l = L-1) or dx(g = l)
-        if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1);
+        // bias of theta layer l <-> Delta_{l+1}: from out_bwd (l = L-1) or dx(g = l); with the chain,
+        // layers l >= 1 from the tensor-core sums 1^T Delta_out of GEMM l-1
+        if (b.chain && l >= 1)
+            job(b.off_cb + (long)(l - 1) * b.npairs * WP, net.boff[l], wout, b.npairs, WP, 0, 1, 1);
+        else if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1);
         else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1);
         if (l == 0) {
             if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
@@ -1409,15 +1883,25 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         return CRVPINN_ENOMEM;
     }
     cudaMemcpy(b.jobs, jobs, sizeof(RedJob) * nj, cudaMemcpyHostToDevice);
-    if (WP == 64) set_attrs<64>(L);
-    else if (WP == 128) set_attrs<128>(L);
-    else if (WP == 192) { err = "hidden width 160/192 not supported by the tensor path"; return CRVPINN_EINVAL; }
-    else set_attrs<256>(L);
+    if (b.chain) {
+        const size_t rb = (size_t)b.npairs * (b.chain_S - 1) * BC_RS * KC * CHUNK_BYTES;
+        if (!al((void **)&b.ring, rb)) {
+            err = "cudaMalloc failed for the backward-chain ring";
+            return CRVPINN_ENOMEM;
+        }
+    }
     b.ready = 1;
     return CRVPINN_OK;
 }
 
 void tc_destroy(TcBufs &b) {
+    void *bufs[] = {b.Wf, b.WTf, b.W1p, b.bp, b.Wop, b.act, b.delta, b.gbar, b.partial, b.jobs, b.ring};
+    for (void *p : bufs)
+        if (p) cudaFree(p);
+    b.Wf = b.WTf = nullptr;
+    b.W1p = b.bp = b.Wop = b.gbar = b.partial = nullptr;
+    b.act = b.delta = b.ring = nullptr;
+    b.jobs = nullptr;
     for (auto &e : b.ev_fork)
         if (e) { cudaEventDestroy(e); e = nullptr; }
     if (b.ev_join) { cudaEventDestroy(b.ev_join); b.ev_join = nullptr; }
@@ -1478,7 +1962,44 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
                                                               b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob,
                                                               st);
-        for (int g = b.G - 1; g >= 0; --g) {
+        int g_next = b.G - 1;   // GEMMs above g_next are done by the chain
+        if (b.chain) {
+            constexpr int NS = B2<WP>::NS;
+            while (g_next >= 0) {
+                const int g0 = g_next;
+                const int Sl = b.chain_S < g0 + 1 ? b.chain_S : g0 + 1;
+                attr[0].val.clusterDim.x = Sl * NS;
+                cfg.gridDim = dim3(b.npairs * Sl * NS);
+                cfg.dynamicSmemBytes = BC<WP>::SMEM;
+                BwdcArgs a{net.N, b.ntiles, b.npairs, Sl, g0, b.delta + (size_t)(g0 + 1) * lay, b.act,
+                           b.delta + (size_t)(g0 - Sl + 1) * lay, b.ring, b.WTf, b.partial + b.off_dx,
+                           b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr};
+                static long long *ctrace = nullptr;
+                const char *te = getenv("CRVPINN_CHAIN_TRACE");   // debug: clock64 timeline -> file
+                if (te && g0 == b.G - 1) {
+                    if (!ctrace) cudaMalloc(&ctrace, 8 * 1024 * 8);
+                    cudaMemset(ctrace, 0, 8 * 1024 * 8);
+                    a.trace = ctrace;
+                }
+                cudaLaunchKernelEx(&cfg, k_tc_bwdc<WP>, a);
+                if (te && g0 == b.G - 1) {
+                    cudaStreamSynchronize(s);
+                    static long long h[8 * 1024];
+                    cudaMemcpy(h, ctrace, sizeof(h), cudaMemcpyDeviceToHost);
+                    FILE *f = fopen(te, "wb");
+                    if (f) { fwrite(h, 8, 8 * 1024, f); fclose(f); }
+                }
+                cudaEventRecord(b.ev_fork[g0], s);
+                cudaStreamWaitEvent(b.side, b.ev_fork[g0], 0);
+                for (int g = g0; g > g0 - Sl; --g)
+                    if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, b.nsm, b.side);
+                g_next = g0 - Sl;
+            }
+            attr[0].val.clusterDim.x = NS;
+            cfg.gridDim = dim3(b.npairs * NS);
+            cfg.dynamicSmemBytes = B2<WP>::SMEM;
+        }
+        for (int g = g_next; g >= 0; --g) {
             const bool outl = g == b.G - 1 && b.fuse_outl;
             // Launches alternate the direction of their tile walk, starting backwards: the forward
             // and every launch leave the most recently written tiles (t_L, Delta_in) in L2, and the
@@ -1536,12 +2057,20 @@ void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cud
     else bwd_launch<256>(net, b, st, grad, s);
 }
 
-int tc_launches(const Net &net) {
+int tc_launches(const Net &net, const TcBufs &b) {
     const int G = net.nl - 2;
-    const int wp = ((net.widths[1] + 63) / 64) * 64;
-    const char *e = getenv("CRVPINN_FUSE_OUTL");
-    const bool fused = wp >= 128 && !(e && e[0] == '0');
-    return 1 /*fwd*/ + (fused ? 0 : 1) /*out_bwd*/ + G /*fused dX+dW*/ + 1 /*reduce*/;   // Adam: crvpinn.cu
+    int bwd = G, side = 0;   // one launch per hidden GEMM, or the chain launches + remainder
+    if (b.chain) {
+        bwd = 0;
+        int g = G - 1;
+        while (g >= 0) {
+            const int Sl = b.chain_S < g + 1 ? b.chain_S : g + 1;
+            ++bwd;
+            g -= Sl;
+        }
+    }
+    for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
+    return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl ? 1 : 0) /*out_bwd*/ + bwd + side + 1 /*reduce*/;   // Adam: crvpinn.cu
 }
 
 }  // namespace crv

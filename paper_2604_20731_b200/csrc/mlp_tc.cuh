@@ -26,7 +26,7 @@ struct TcBufs {
     __half *delta = nullptr; // [L][ntiles][KC][128*64]  (scaled by DevState::gscale)
     float *gbar = nullptr;   // [P] dLOSS/dnet (unscaled)
     float *partial = nullptr;
-    long off_ob = 0, off_dx = 0, off_dw = 0;
+    long off_ob = 0, off_dx = 0, off_dw = 0, off_cb = 0;
     int grid_ob = 0, grid_dx = 0, grid_fwd = 0, grid_bwd = 0, npairs = 0;
     RedJob *jobs = nullptr;  // device copy
     int njobs = 0, max_count = 0, groups = 0;
@@ -34,17 +34,19 @@ struct TcBufs {
     RedJob wjobs[CRV_MAX_LAYERS];          // hidden-layer weight job of GEMM g
     bool wside[CRV_MAX_LAYERS] = {};       // ... reduced on the side stream (else inside jobs[0, njobs_deep))
     int nsm = 148;
+    int chain = 0, chain_S = 0;            // backward chain (k_tc_bwdc): on/off, stages per cluster
+    __half *ring = nullptr;                // its per-cluster Delta rings between stages
     cudaStream_t side = nullptr;           // side stream of the per-layer weight reductions
     cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr;
     const float *theta = nullptr;
 };
 
 int tc_create(const Net &net, TcBufs &b, std::string &err);
-void tc_destroy(TcBufs &b);   // side stream + events (device memory is owned by the context)
+void tc_destroy(TcBufs &b);   // device buffers, side stream, events
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
-int tc_launches(const Net &net);
+int tc_launches(const Net &net, const TcBufs &b);
 // A8 for the tensor path: Adam + write of the updated operand copies (one launch)
 void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
              DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s);

@@ -1,8 +1,10 @@
 #!/bin/bash
-# A/B: default build vs variants under build/ab/ (stage times from the profiled step graph)
+timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
+CRVPINN_BWD_CHAIN=0 timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
 for r in 1 2; do
-  for v in default clampn clampn_m6 clampn_m10 esleep; do
-    if [ $v = default ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
-    CRVPINN_LIB=$L timeout 120 python scripts/stage_time.py C5 5 2>&1 | tail -1 | sed "s|^|$v: |"
-  done
+for v in "CRVPINN_BWD_CHAIN=0" "CRVPINN_BWD_STAGES=4" "CRVPINN_BWD_STAGES=2" "CRVPINN_BWD_STAGES=1"; do
+  env $v timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
 done
+CRVPINN_LIB=build/ab/tlast/libcrvpinn.so CRVPINN_BWD_CHAIN=0 timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|tlast bwd2 |"
+done
+timeout -s KILL 120 python scripts/chain_trace.py C5 > /dev/null 2>&1

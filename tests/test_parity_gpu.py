@@ -268,3 +268,28 @@ def test_profiling_counts(crv):
     ms, n = g.profile(reset=True)
     assert n == 10 and all(x > 0 for x in ms)
     assert g.launches_per_iter > 5
+
+
+# ------------------------------------------------------------------ backward chain (opt-in path)
+@pytest.mark.parametrize("stages", ["1", "2", "4"])
+@pytest.mark.parametrize("N,widths,seed", [(64, (2, 256, 256, 256, 256, 256, 1), 11),
+                                           (32, (2, 128, 128, 128, 128, 128, 1), 12),
+                                           (64, (2, 256, 256, 256, 1), 13)])
+def test_backward_chain_vs_oracle(crv, monkeypatch, stages, N, widths, seed):
+    """k_tc_bwdc (CRVPINN_BWD_STAGES = S: S hidden GEMMs per launch, Delta handed between stages
+    through an L2-resident ring, bias gradients from tensor-core column sums) against the oracle
+    at the tensor-mode tolerance, and against the default per-GEMM backward."""
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    rl, rg = oracle.Oracle(N, widths, K, S, f, th).loss_grad()
+    monkeypatch.setenv("CRVPINN_BWD_STAGES", stages)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
+    loss, grad = g.loss_grad()
+    g.close()
+    monkeypatch.delenv("CRVPINN_BWD_STAGES")
+    tl, tg = TOL[0]
+    assert abs(loss - rl) <= tl * abs(rl)
+    assert grad_errors(widths, grad, rg).max() <= tg
+    d = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
+    _, grad_d = d.loss_grad()
+    assert grad_errors(widths, grad, grad_d.astype(np.float64)).max() <= 5e-3
