@@ -32,6 +32,9 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 ITERS_PER_STEP = 100
+# DRAM bytes per Adam iteration of the MLP kernels (forward + 4 backward GEMMs + weight-gradient
+# reductions), ncu --set full at C5: profiles/r01_v4_ncu_full_summary.md
+MLP_DRAM_BYTES_PER_ITER = 2.20e9
 
 
 def parse():
@@ -327,12 +330,13 @@ def run_ours(args, rank, world, local):
         "config": dict(workload_config(args.workload, args.precision), parallelism=f"replicas{world}"),
         "points_iters_per_s": value * w.points,
         "roofline": {"bound": bound, "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak, "traffic": None,
+                     "frac": achieved_tf / peak,
+                     "traffic": MLP_DRAM_BYTES_PER_ITER if args.workload == "C5" else None,
                      "kernel": "MLP forward + backward (A1, A6-A7), per Adam iteration",
                      "alg_flops_per_iter": flops, "peak_source": peak_note,
-                     "traffic_note": "per-iteration DRAM bytes of the MLP kernels (ncu --set full, C5): "
-                                     "2.12e9 (profiles/r01_v3_ncu_full_summary.md); activations pass "
-                                     "through HBM, so traffic >> the 20 MB algorithmic bytes"},
+                     "traffic_note": ("per-iteration DRAM bytes (read + write) of the MLP kernels from one ncu --set full "
+                                     "capture at C5 (profiles/r01_v4_ncu_full_summary.md): the fp16 activations pass "
+                                     "through HBM, so traffic >> the 20 MB algorithmic bytes; measured at C5 only")},
         "north_star_roofline": line_ns,
         "stage_ms_per_iter": {"mlp_fwd": stage_ms[0] / max(prof_iters, 1),
                               "stencil_gram_loss_adjoint": stage_ms[1] / max(prof_iters, 1),

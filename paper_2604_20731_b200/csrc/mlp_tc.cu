@@ -777,6 +777,14 @@ struct Bwd2Args {
     long long *trace;     // debug timeline (CTA 0), nullptr normally
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
+#ifndef CRV_B2_MMA_SLEEP
+#define CRV_B2_MMA_SLEEP 0
+#endif
+#if CRV_B2_MMA_SLEEP
+#define B2_MMA_WAIT mbar_wait_sleep
+#else
+#define B2_MMA_WAIT mbar_wait
+#endif
 
 #ifndef CRV_T_FIRST
 #define CRV_T_FIRST 0   // backward producers issue a tile's t_in load before its Delta chunks
@@ -866,9 +874,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             int dn = 0;   // running Delta chunk counter
             auto load_t = [&](int k, int tile) {
                 const int tb = k % NT;
-                BTRACE(k * 8 + 0);
+                BTRACE(k * 16 + 0);
                 mbar_wait_sleep(&tempty[tb], ((k / NT) & 1) ^ 1);
-                BTRACE(k * 8 + 1);
+                BTRACE(k * 16 + 1);
                 mbar_arrive_expect_tx(&tfull[tb], 2 * CHUNK_BYTES);
                 bulk_g2s(Tr + tb * 2 * CHUNK_BYTES,
                          (const uint8_t *)a.tin + ((size_t)tile * KC + 2 * rank) * CHUNK_BYTES, 2 * CHUNK_BYTES,
@@ -902,10 +910,10 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             for (int k = 0; k < nk; ++k) {
                 const int b = k & 1, tb = k % NT;
                 const int slot0 = dn % DS;
-                mbar_wait(&tfull[tb], (k / NT) & 1);
-                BTRACE(k * 8 + 2);
-                mbar_wait(&xempty[b], ((k >> 1) & 1) ^ 1);
-                BTRACE(k * 8 + 7);
+                B2_MMA_WAIT(&tfull[tb], (k / NT) & 1);
+                BTRACE(k * 16 + 2);
+                B2_MMA_WAIT(&xempty[b], ((k >> 1) & 1) ^ 1);
+                BTRACE(k * 16 + 7);
                 tc_fence_after();
                 const uint32_t accx = tmem + (uint32_t)(b * 128);
                 // chunk pairs (2h, 2h+1): dX over those K chunks, then the dW^T N-half h, then release
@@ -914,7 +922,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 for (int h = 0; h < KC / 2; ++h) {
                     const int sl = (slot0 + 2 * h) % DS;
                     for (int j = 2 * h; j < 2 * h + 2; ++j) {
-                        mbar_wait(a.outl ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
+                        B2_MMA_WAIT(a.outl ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
+                        BTRACE(k * 16 + 8 + j);
                         tc_fence_after();
 #pragma unroll
                         for (int kq = 0; kq < 4; ++kq) {
@@ -935,7 +944,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
                 }
                 mma_commit(&xfull[b]);
-                BTRACE(k * 8 + 3);
+                BTRACE(k * 16 + 3);
                 mma_commit(&tempty[tb]);
                 dn += KC;
             }
@@ -1037,9 +1046,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
-            if (warp == 2 && lane == 0) BTRACE(kk * 8 + 4);
+            if (warp == 2 && lane == 0) BTRACE(kk * 16 + 4);
             mbar_wait(&xfull[b], (kk >> 1) & 1);
-            if (warp == 2 && lane == 0) BTRACE(kk * 8 + 5);
+            if (warp == 2 && lane == 0) BTRACE(kk * 16 + 5);
             tc_fence_after();
 #pragma unroll
             for (int g2 = 0; g2 < CPW / 32; ++g2) {
@@ -1092,7 +1101,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (warp == 2) BTRACE(kk * 8 + 6);
+                if (warp == 2) BTRACE(kk * 16 + 6);
                 mbar_arrive(&xempty[b]);
                 mbar_arrive(&tempty[tb]);
             }
@@ -2013,7 +2022,9 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
-            if (te && g == b.G - 1) {
+            const char *tg = getenv("CRVPINN_BWD_TRACE_G");
+            const int trace_g = tg ? atoi(tg) : b.G - 1;
+            if (te && g == trace_g) {
                 if (!trace) cudaMalloc(&trace, 4096 * 8);
                 cudaMemset(trace, 0, 4096 * 8);
                 a.trace = trace;
@@ -2023,7 +2034,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             cudaEventRecord(b.ev_fork[g], s);
             cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
             if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, b.nsm, b.side);
-            if (te && g == b.G - 1) {
+            if (te && g == trace_g) {
                 cudaStreamSynchronize(s);
                 static long long h[4096];
                 cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);

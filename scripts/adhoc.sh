@@ -1,10 +1,9 @@
 #!/bin/bash
-timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
-CRVPINN_BWD_CHAIN=0 timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
-for r in 1 2; do
-for v in "CRVPINN_BWD_CHAIN=0" "CRVPINN_BWD_STAGES=4" "CRVPINN_BWD_STAGES=2" "CRVPINN_BWD_STAGES=1"; do
-  env $v timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
+for v in default msleep; do
+  if [ $v = default ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
+  CRVPINN_LIB=$L timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
+  for g in 3 2 0; do
+    CRVPINN_LIB=$L CRVPINN_BWD_TRACE=gpurun_out/b2_$v_$g.bin CRVPINN_BWD_TRACE_G=$g timeout -s KILL 120 python scripts/prof_once.py C5 2 > /dev/null 2>&1
+    echo "$v g=$g $(python scripts/bwd2_report.py gpurun_out/b2_$v_$g.bin)"
+  done
 done
-CRVPINN_LIB=build/ab/tlast/libcrvpinn.so CRVPINN_BWD_CHAIN=0 timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|tlast bwd2 |"
-done
-timeout -s KILL 120 python scripts/chain_trace.py C5 > /dev/null 2>&1

@@ -13,6 +13,6 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
     > gpurun_out/${TAG}_ncu_launches.log 2>&1
 timeout -s KILL 120 python scripts/prof_once.py C5 2 > gpurun_out/${TAG}_prof_plain.log 2>&1 && \
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_tc_forward|k_tc_bwd2|k_reduce|k_res_dst|k_tridiag|k_idst_loss|k_adj_final" -s 0 -c 9 \
+    -k regex:"k_tc_forward|k_tc_bwd2|k_reduce|k_res_dst|k_tridiag|k_idst_loss|k_adj_final|k_tc_adam" -s 0 -c 16 \
     -o gpurun_out/${TAG}_full python scripts/prof_once.py C5 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo round-done
