@@ -70,6 +70,12 @@ typedef struct {
     uint64_t seed;          /* Xavier init seed when theta0 == NULL */
     void *stream;           /* cudaStream_t to run on; NULL = the context creates its own */
     int device;             /* CUDA device ordinal, default 0 */
+    /* Gravity term of Eq. 23's RHS, grad+ . (g K ((1-S) rho_w/mu_w + S rho_g/mu_g)) (PAPER.md:370,
+     * SURVEY.md §8(f) f1), read non-dimensionally (R23): g = -gravity * y-hat and
+     * beta = (1-S) + M (rho_g/rho_w) S, so b_kl = h^2 f_kl + h gravity (gamma_{k,l+1} - gamma_{k,l}),
+     * gamma = K beta. Recomputed with alpha on every set_saturation. */
+    double gravity;         /* non-dimensional gravity number, default 0 (the configs have none, R11) */
+    double density_ratio;   /* rho_g/rho_w, default 479/1045 (Table 1) */
 } crvpinn_opts;
 
 /* Fill *o with the defaults listed above. */
@@ -107,6 +113,14 @@ int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist);
 /* Evaluate the network on the lattice: p_out (host, (N+1)^2 float32) = PINN_ij, exactly 0 on
  * the boundary (the hand-off to the IGA projection). */
 int crvpinn_eval(crvpinn_ctx *ctx, float *p_out);
+
+/* Continuous evaluation of the trained network with its hard cutoff at arbitrary points,
+ * p(x, y) = 16 x(1-x) y(1-y) net_theta(x, y), as the IGA L2 projection needs it at
+ * quadrature points (§6 step 4), in the
+ * context's precision mode (same kernels as the lattice forward). xy: host float32 [n][2] pairs
+ * (x, y); p_out: host float32 [n]. n == 0 is a no-op. EINVAL: n < 0 or a null pointer with n > 0;
+ * EDOMAIN: a non-finite coordinate (nothing is written). Synchronising. */
+int crvpinn_eval_points(crvpinn_ctx *ctx, long n, const float *xy, float *p_out);
 
 /* LOSS (Eq. 27) and dLOSS/dtheta at the current theta, no update. grad nullable. */
 int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad);

@@ -20,6 +20,7 @@ _SRC = os.path.join(_HERE, "crvpinn_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 MOBILITY_RATIO = 25.35 / 3.95   # Table 1
+DENSITY_RATIO = 479.0 / 1045.0   # rho_g / rho_w, Table 1
 
 
 def build(force: bool = False) -> str:
@@ -44,7 +45,7 @@ def lib():
         L.orc_create.restype = P
         L.orc_create.argtypes = [ctypes.c_int, ctypes.c_int, I, F, F, F, F, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                 ctypes.c_double, ctypes.c_int]
+                                 ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double]
         L.orc_destroy.argtypes = [P]
         L.orc_num_params.restype = ctypes.c_long
         L.orc_num_params.argtypes = [P]
@@ -52,6 +53,8 @@ def lib():
         L.orc_set_theta.argtypes = [P, D]
         L.orc_get_adam.argtypes = [P, D, D, ctypes.POINTER(ctypes.c_long)]
         L.orc_get_alpha.argtypes = [P, D]
+        L.orc_get_b.argtypes = [P, D]
+        L.orc_eval_points.argtypes = [P, D, ctypes.c_long, D, D]
         L.orc_set_saturation.argtypes = [P, F, F]
         L.orc_forward.argtypes = [P, D, D]
         L.orc_residual.argtypes = [P, D, D]
@@ -87,7 +90,7 @@ class Oracle:
 
     def __init__(self, N: int, widths, K, S, f, theta0=None, *, mobility: float = MOBILITY_RATIO,
                  lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
-                 factor_gram: bool = True):
+                 factor_gram: bool = True, gravity: float = 0.0, density_ratio: float = DENSITY_RATIO):
         L = lib()
         self.N, self.n = int(N), int(N) - 1
         self.widths = tuple(int(w) for w in widths)
@@ -96,7 +99,7 @@ class Oracle:
         th = None if theta0 is None else _f32(theta0)
         self._h = L.orc_create(self.N, len(self.widths) - 1, w, _fp(self._K), _fp(self._S),
                                _fp(self._f), None if th is None else _fp(th), mobility, lr,
-                               beta1, beta2, eps, 1 if factor_gram else 0)
+                               beta1, beta2, eps, 1 if factor_gram else 0, gravity, density_ratio)
         if not self._h:
             raise MemoryError("orc_create failed")
         self.np = int(L.orc_num_params(self._h))
@@ -126,6 +129,20 @@ class Oracle:
     def alpha(self) -> np.ndarray:
         out = np.empty((self.N + 1) ** 2)
         lib().orc_get_alpha(self._h, _dp(out))
+        return out
+
+    def rhs(self) -> np.ndarray:
+        """b = h^2 (f - grad+ . F) on the (N+1)^2 lattice (A0 with the gravity term)."""
+        out = np.empty((self.N + 1) ** 2)
+        lib().orc_get_b(self._h, _dp(out))
+        return out
+
+    def eval_points(self, xy, theta=None) -> np.ndarray:
+        """cutoff(x, y) * net(x, y) at arbitrary points xy (n, 2), fp64."""
+        th = self.theta if theta is None else np.ascontiguousarray(theta, dtype=np.float64)
+        xy = np.ascontiguousarray(np.asarray(xy, dtype=np.float64).reshape(-1, 2))
+        out = np.empty(xy.shape[0])
+        lib().orc_eval_points(self._h, _dp(th), int(xy.shape[0]), _dp(xy), _dp(out))
         return out
 
     def set_saturation(self, S, K=None):

@@ -8,7 +8,11 @@
  * What it computes, step by step in the paper's order (§5-§6, arXiv 2604.20731):
  *   A0  alpha_ij = ((1-S_ij)/mu_w + S_ij/mu_g) K_ij      PAPER.md:369 (Eq. 23), read
  *       non-dimensionally as K((1-S) + M S), M = mu_w/mu_g (reading R10);
- *       b_kl = h^2 f_kl, f the right side of -div(alpha grad p) = f (reading R1).
+ *       b_kl = h^2 f_kl, f the right side of -div(alpha grad p) = f (reading R1). With the
+ *       gravity term of Eq. 23's RHS (reading R23) the right
+ *       side is f - grad+ . F, F_ij = g K_ij ((1-S_ij) + M r S_ij), g = (0, -gravity),
+ *       r = rho_g/rho_w, grad+ . F = forward differences of Eq. 22.
+ *   eval_points: p(x,y) = cutoff(x,y) net_theta(x,y) at arbitrary points.
  *   A1  PINN_ij = 16 x(1-x) y(1-y) * net_theta(x_i, y_j), tanh MLP
  *       (architecture/cutoff: readings R5, R6).
  *   A2  RES_kl = (alpha grad+ PINN, grad+ delta_kl)_h - (RHS, delta_kl)_h   Eq. 25,
@@ -47,8 +51,10 @@ typedef struct orc_ctx {
     long np;                   /* parameter count */
     long woff[ORC_MAX_LAYERS], boff[ORC_MAX_LAYERS];
     double mobility;
+    double gravity, rho_ratio; /* gravity number and rho_g/rho_w (reading R23) */
     double *alpha;             /* (N+1)^2 nodes, [j*(N+1)+i] */
-    double *b;                 /* (N+1)^2 nodes: h^2 f */
+    double *f;                 /* (N+1)^2 nodes: the source f as given */
+    double *b;                 /* (N+1)^2 nodes: h^2 (f - grad+ . F) */
     double *U;                 /* band LU of G: n^2 rows x (n+1): U[r*(n+1)+d] = U(r, r+d) */
     double *theta, *m, *v;     /* parameters and Adam moments */
     long t;                    /* Adam step counter */
@@ -68,9 +74,41 @@ static void set_alpha(orc_ctx *c, const float *K, const float *S) {
     }
 }
 
+/* b = h^2 (f - grad+ . F): (RHS, delta_kl)_h of Eq. 24-25 with the sign of reading R1. F is the
+ * node field g K beta with g = (0, -gravity) and beta = (1-S) + M r S (non-dimensional form of
+ * (1-S) rho_w/mu_w + S rho_g/mu_g, divided by rho_w/mu_w); its x-component is zero. */
+static void set_rhs(orc_ctx *c, const float *K, const float *S) {
+    int N = c->N;
+    long nn = (long)(N + 1) * (N + 1);
+    double h = c->h;
+    double *Fx = (double *)calloc(nn, sizeof(double)), *Fy = (double *)calloc(nn, sizeof(double));
+    for (long p = 0; p < nn; ++p) {
+        double s = (double)S[p];
+        if (s < 0.0) s = 0.0;
+        if (s > 1.0) s = 1.0;
+        double beta = (1.0 - s) + c->mobility * c->rho_ratio * s;
+        Fx[p] = 0.0 * (double)K[p] * beta;              /* g_x = 0 */
+        Fy[p] = -c->gravity * (double)K[p] * beta;     /* g_y = -gravity */
+    }
+    for (int j = 0; j <= N; ++j)
+        for (int i = 0; i <= N; ++i) {
+            double div = 0.0;   /* grad+ . F at (i, j); defined where (i+1, j) and (i, j+1) exist */
+            if (i < N && j < N)
+                div = (Fx[idx(c, i + 1, j)] - Fx[idx(c, i, j)]) / h + (Fy[idx(c, i, j + 1)] - Fy[idx(c, i, j)]) / h;
+            c->b[idx(c, i, j)] = h * h * (c->f[idx(c, i, j)] - div);
+        }
+    free(Fx);
+    free(Fy);
+}
+
 int orc_set_saturation(orc_ctx *c, const float *K, const float *S) {
     set_alpha(c, K, S);
+    set_rhs(c, K, S);
     return 0;
+}
+
+void orc_get_b(const orc_ctx *c, double *out) {
+    memcpy(out, c->b, sizeof(double) * (long)(c->N + 1) * (c->N + 1));
 }
 
 /* ---------------------------------------------------------------- A3: factor G once */
@@ -148,11 +186,13 @@ void orc_gram_matvec(const orc_ctx *c, const double *v, double *out) {
 /* ---------------------------------------------------------------- context */
 orc_ctx *orc_create(int N, int nl, const int *widths, const float *K, const float *S,
                     const float *f, const float *theta0, double mobility, double lr,
-                    double beta1, double beta2, double eps, int factor_gram) {
+                    double beta1, double beta2, double eps, int factor_gram, double gravity,
+                    double rho_ratio) {
     if (N < 2 || nl < 1 || nl > ORC_MAX_LAYERS) return NULL;
     orc_ctx *c = (orc_ctx *)calloc(1, sizeof(orc_ctx));
     c->N = N; c->n = N - 1; c->h = 1.0 / N; c->nl = nl;
     c->mobility = mobility; c->lr = lr; c->beta1 = beta1; c->beta2 = beta2; c->eps = eps;
+    c->gravity = gravity; c->rho_ratio = rho_ratio;
     long np = 0;
     for (int l = 0; l <= nl; ++l) c->widths[l] = widths[l];
     for (int l = 0; l < nl; ++l) {
@@ -163,8 +203,10 @@ orc_ctx *orc_create(int N, int nl, const int *widths, const float *K, const floa
     long nn = (long)(N + 1) * (N + 1);
     c->alpha = (double *)malloc(sizeof(double) * nn);
     c->b = (double *)malloc(sizeof(double) * nn);
+    c->f = (double *)malloc(sizeof(double) * nn);
+    for (long p = 0; p < nn; ++p) c->f[p] = (double)f[p];
     set_alpha(c, K, S);
-    for (long p = 0; p < nn; ++p) c->b[p] = c->h * c->h * (double)f[p];
+    set_rhs(c, K, S);
     c->theta = (double *)calloc(np, sizeof(double));
     c->m = (double *)calloc(np, sizeof(double));
     c->v = (double *)calloc(np, sizeof(double));
@@ -173,7 +215,7 @@ orc_ctx *orc_create(int N, int nl, const int *widths, const float *K, const floa
     if (factor_gram) {
         long n2 = (long)c->n * c->n;
         c->U = (double *)malloc(sizeof(double) * n2 * (c->n + 1));
-        if (!c->U) { free(c->alpha); free(c->b); free(c->theta); free(c->m); free(c->v); free(c); return NULL; }
+        if (!c->U) { free(c->alpha); free(c->b); free(c->f); free(c->theta); free(c->m); free(c->v); free(c); return NULL; }
         gram_factor(c);
     }
     return c;
@@ -181,7 +223,7 @@ orc_ctx *orc_create(int N, int nl, const int *widths, const float *K, const floa
 
 void orc_destroy(orc_ctx *c) {
     if (!c) return;
-    free(c->alpha); free(c->b); free(c->U); free(c->theta); free(c->m); free(c->v);
+    free(c->alpha); free(c->b); free(c->f); free(c->U); free(c->theta); free(c->m); free(c->v);
     free(c);
 }
 
@@ -245,6 +287,20 @@ void orc_forward(const orc_ctx *c, const double *th, double *u) {
                 double x = (double)i / N, y = (double)j / N;
                 u[idx(c, i, j)] = cutoff(x, y) * net_point(c, th, x, y, act);
             }
+        free_act(c, act);
+    }
+}
+
+/* Continuous evaluation at arbitrary points: out[p] = cutoff(x_p, y_p) net(x_p, y_p). */
+void orc_eval_points(const orc_ctx *c, const double *th, long n, const double *xy, double *out) {
+#pragma omp parallel
+    {
+        double **act = alloc_act(c);
+#pragma omp for schedule(static)
+        for (long p = 0; p < n; ++p) {
+            double x = xy[2 * p], y = xy[2 * p + 1];
+            out[p] = cutoff(x, y) * net_point(c, th, x, y, act);
+        }
         free_act(c, act);
     }
 }

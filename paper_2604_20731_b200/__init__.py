@@ -21,7 +21,8 @@ PREC_TENSOR, PREC_FP32 = 0, 1
 # every symbol include/crvpinn.h declares
 EXPORTS = [
     "crvpinn_default_opts", "crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device",
-    "crvpinn_pretrain", "crvpinn_step", "crvpinn_eval", "crvpinn_loss_grad", "crvpinn_get_intermediates",
+    "crvpinn_pretrain", "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_loss_grad",
+    "crvpinn_get_intermediates",
     "crvpinn_num_params", "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
     "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter", "crvpinn_stream",
     "crvpinn_last_error", "crvpinn_destroy",
@@ -37,7 +38,8 @@ class CrvpinnError(RuntimeError):
 class Opts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
                 ("eps", ctypes.c_double), ("mobility_ratio", ctypes.c_double), ("precision", ctypes.c_int),
-                ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p), ("device", ctypes.c_int)]
+                ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p), ("device", ctypes.c_int),
+                ("gravity", ctypes.c_double), ("density_ratio", ctypes.c_double)]
 
 
 _lib = None
@@ -62,6 +64,7 @@ def load(path: str = LIB_PATH):
     L.crvpinn_step.argtypes = [P, I, D]
     L.crvpinn_eval.argtypes = [P, F]
     L.crvpinn_loss_grad.argtypes = [P, D, F]
+    L.crvpinn_eval_points.argtypes = [P, ctypes.c_long, F, F]
     L.crvpinn_get_intermediates.argtypes = [P, F, F, F, F]
     L.crvpinn_num_params.restype = ctypes.c_size_t
     L.crvpinn_num_params.argtypes = [P]
@@ -78,7 +81,7 @@ def load(path: str = LIB_PATH):
     L.crvpinn_last_error.argtypes = [P]
     L.crvpinn_destroy.argtypes = [P]
     for name in ["crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device", "crvpinn_pretrain",
-                 "crvpinn_step", "crvpinn_eval", "crvpinn_loss_grad", "crvpinn_get_intermediates",
+                 "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_loss_grad", "crvpinn_get_intermediates",
                  "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
                  "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter"]:
         getattr(L, name).restype = I
@@ -109,7 +112,7 @@ class Crvpinn:
     def __init__(self, N: int, widths: Sequence[int], K, S, f, theta0=None, *, precision: int = PREC_TENSOR,
                  lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  mobility_ratio: Optional[float] = None, seed: int = 0, stream: Optional[int] = None,
-                 device: int = 0):
+                 device: int = 0, gravity: float = 0.0, density_ratio: Optional[float] = None):
         L = load()
         self.N = int(N)
         self.widths = tuple(int(w) for w in widths)
@@ -119,6 +122,9 @@ class Crvpinn:
         if mobility_ratio is not None:
             o.mobility_ratio = mobility_ratio
         o.precision, o.seed, o.device = precision, seed, device
+        o.gravity = gravity
+        if density_ratio is not None:
+            o.density_ratio = density_ratio
         o.stream = stream
         w = (ctypes.c_int * len(self.widths))(*self.widths)
         K, S, f = _f32(K, nn), _f32(S, nn), _f32(f, nn)
@@ -167,6 +173,14 @@ class Crvpinn:
     def eval(self) -> np.ndarray:
         out = np.empty((self.N + 1) ** 2, np.float32)
         self._check(load().crvpinn_eval(self._h, _fp(out)))
+        return out
+
+    def eval_points(self, xy) -> np.ndarray:
+        """p(x, y) = cutoff * net at arbitrary points; xy: (n, 2) array-like -> (n,) float32."""
+        xy = np.ascontiguousarray(np.asarray(xy, dtype=np.float32).reshape(-1, 2))
+        out = np.empty(xy.shape[0], dtype=np.float32)
+        if xy.shape[0]:
+            self._check(load().crvpinn_eval_points(self._h, int(xy.shape[0]), _fp(xy), _fp(out)))
         return out
 
     def loss_grad(self, grad: bool = True):

@@ -97,7 +97,8 @@ __device__ __forceinline__ float cutoff(float x, float y) {
 namespace crv {
 // fields.cu
 void launch_alpha(const float *K, const float *S, float *alpha, int N, float mobility, cudaStream_t s);
-void launch_scale_b(const float *f, float *b, int N, cudaStream_t s);
+void launch_rhs(const float *K, const float *S, const float *f, float *b, int N, float mobility, float rho_ratio,
+                float gravity, cudaStream_t s);
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 void launch_begin_call(DevState *st, cudaStream_t s);
@@ -140,6 +141,8 @@ struct SimtBufs {
 };
 void simt_make_plan(const Net &net, MlpPlan &plan);
 void simt_forward(const Net &net, const float *theta, const SimtBufs &b, float *u, cudaStream_t s);
+void simt_eval_points(const Net &net, const float *theta, const SimtBufs &b, const float *xy, int npts,
+                      float *out, cudaStream_t s);
 void simt_backward(const Net &net, const MlpPlan &plan, const float *theta, const SimtBufs &b,
                    float *grad, cudaStream_t s);
 int simt_launches_fwd(const Net &net);

@@ -58,6 +58,9 @@ struct crvpinn_ctx {
     int64_t prof_iters = 0;
     std::string err;
     std::vector<void *> allocs;
+    // crvpinn_eval_points scratch (device xy [cap][2] + p [cap]), grown on demand
+    float *pts = nullptr;
+    long pts_cap = 0;
 };
 
 #define CK(call)                                                                 \
@@ -223,6 +226,8 @@ void crvpinn_default_opts(crvpinn_opts *o) {
     o->seed = 0;
     o->stream = nullptr;
     o->device = 0;
+    o->gravity = 0.0;
+    o->density_ratio = 479.0 / 1045.0;
 }
 
 const char *crvpinn_last_error(const crvpinn_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
@@ -240,6 +245,7 @@ void crvpinn_destroy(crvpinn_ctx *ctx) {
     drop_graphs(ctx);
     gram_free_constants(ctx->gram);
     tc_destroy(ctx->tc);
+    if (ctx->pts) cudaFree(ctx->pts);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_field) cudaFreeHost(ctx->h_field);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
@@ -328,7 +334,8 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     CK(cudaMemcpy(ctx->S, S, sizeof(float) * nn, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->f, f, sizeof(float) * nn, cudaMemcpyHostToDevice));
     launch_alpha(ctx->K, ctx->S, ctx->alpha, N, (float)ctx->opts.mobility_ratio, ctx->stream);
-    launch_scale_b(ctx->f, ctx->b, N, ctx->stream);
+    launch_rhs(ctx->K, ctx->S, ctx->f, ctx->b, N, (float)ctx->opts.mobility_ratio, (float)ctx->opts.density_ratio,
+               (float)ctx->opts.gravity, ctx->stream);
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
@@ -348,6 +355,8 @@ int crvpinn_create(crvpinn_ctx **out, int N, int n_widths, const int *widths, co
             return fail(nullptr, CRVPINN_EINVAL, "hidden widths must be multiples of 32 in [32, 256]");
     crvpinn_ctx *ctx = new crvpinn_ctx();
     if (opts) ctx->opts = *opts; else crvpinn_default_opts(&ctx->opts);
+    if (!std::isfinite(ctx->opts.gravity) || !std::isfinite(ctx->opts.density_ratio) || ctx->opts.density_ratio < 0.0)
+        return fail(nullptr, CRVPINN_EINVAL, "gravity / density_ratio must be finite (density_ratio >= 0)");
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) {
         for (int l = 2; l < n_widths - 1; ++l)
             if (widths[l] != widths[1]) {
@@ -379,6 +388,8 @@ int crvpinn_set_saturation(crvpinn_ctx *ctx, const float *S) {
     rc = upload_field(ctx, ctx->S, S);
     if (rc) return rc;
     launch_alpha(ctx->K, ctx->S, ctx->alpha, ctx->net.N, (float)ctx->opts.mobility_ratio, ctx->stream);
+    launch_rhs(ctx->K, ctx->S, ctx->f, ctx->b, ctx->net.N, (float)ctx->opts.mobility_ratio,
+               (float)ctx->opts.density_ratio, (float)ctx->opts.gravity, ctx->stream);
     CK(cudaGetLastError());
     return CRVPINN_OK;
 }
@@ -389,6 +400,8 @@ int crvpinn_set_saturation_device(crvpinn_ctx *ctx, const void *S_dev) {
     size_t bytes = sizeof(float) * (size_t)(ctx->net.N + 1) * (ctx->net.N + 1);
     CK(cudaMemcpyAsync(ctx->S, S_dev, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
     launch_alpha(ctx->K, ctx->S, ctx->alpha, ctx->net.N, (float)ctx->opts.mobility_ratio, ctx->stream);
+    launch_rhs(ctx->K, ctx->S, ctx->f, ctx->b, ctx->net.N, (float)ctx->opts.mobility_ratio,
+               (float)ctx->opts.density_ratio, (float)ctx->opts.gravity, ctx->stream);
     CK(cudaGetLastError());
     return CRVPINN_OK;
 }
@@ -444,6 +457,33 @@ int crvpinn_eval(crvpinn_ctx *ctx, float *p_out) {
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
     memcpy(p_out, ctx->h_field, sizeof(float) * nn);
+    return CRVPINN_OK;
+}
+
+int crvpinn_eval_points(crvpinn_ctx *ctx, long n, const float *xy, float *p_out) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    if (n < 0) return fail(ctx, CRVPINN_EINVAL, "n must be >= 0");
+    if (n == 0) return CRVPINN_OK;
+    if (!xy || !p_out) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    if (n > (1L << 30)) return fail(ctx, CRVPINN_EINVAL, "too many points in one call (max 2^30)");
+    for (long i = 0; i < 2 * n; ++i)
+        if (!std::isfinite(xy[i])) return fail(ctx, CRVPINN_EDOMAIN, "non-finite coordinate");
+    CK(cudaSetDevice(ctx->device));
+    if (n > ctx->pts_cap) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->pts) cudaFree(ctx->pts);
+        ctx->pts = nullptr;
+        ctx->pts_cap = 0;
+        CK(cudaMalloc(&ctx->pts, sizeof(float) * 3 * (size_t)n));
+        ctx->pts_cap = n;
+    }
+    float *dxy = ctx->pts, *dp = ctx->pts + 2 * n;
+    CK(cudaMemcpyAsync(dxy, xy, sizeof(float) * 2 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_eval_points(ctx->net, ctx->tc, dxy, (int)n, dp, ctx->stream);
+    else simt_eval_points(ctx->net, ctx->theta, ctx->simt, dxy, (int)n, dp, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(p_out, dp, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return CRVPINN_OK;
 }
 

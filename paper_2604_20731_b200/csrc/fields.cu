@@ -21,16 +21,30 @@ void launch_alpha(const float *K, const float *S, float *alpha, int N, float mob
     k_alpha<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(K, S, alpha, nn, mobility);
 }
 
-// b = h^2 f (reading R1: f is the right side of -div(alpha grad p) = f)
-__global__ void k_scale_b(const float *__restrict__ f, float *__restrict__ b, long nn, float h2) {
-    long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < nn) b[p] = h2 * f[p];
+// b = h^2 f_total, f_total = f - div+(g K beta) (reading R1: f_total is the right side of
+// -div(alpha grad p) = f_total; Eq. 23's RHS with the sign of R1). The gravity term (PAPER.md:370,
+// reading R23): g = -Gr y-hat, beta = (1-S) + M r S (r = rho_g/rho_w), so with gamma = K beta
+// -div+(g gamma)_{i,j} = Gr (gamma_{i,j+1} - gamma_{i,j}) / h (Eq. 22's forward difference in y).
+__device__ __forceinline__ float gamma_node(const float *K, const float *S, long p, float Mr) {
+    const float s = fminf(fmaxf(S[p], 0.0f), 1.0f);
+    return K[p] * ((1.0f - s) + Mr * s);
 }
 
-void launch_scale_b(const float *f, float *b, int N, cudaStream_t s) {
+__global__ void k_rhs(const float *__restrict__ K, const float *__restrict__ S, const float *__restrict__ f,
+                      float *__restrict__ b, int N, float h, float Mr, float Gr) {
+    const long nn = (long)(N + 1) * (N + 1);
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nn) return;
+    float v = h * h * f[p];
+    const int j = (int)(p / (N + 1));
+    if (Gr != 0.0f && j < N) v += h * Gr * (gamma_node(K, S, p + N + 1, Mr) - gamma_node(K, S, p, Mr));
+    b[p] = v;
+}
+
+void launch_rhs(const float *K, const float *S, const float *f, float *b, int N, float mobility, float rho_ratio,
+                float gravity, cudaStream_t s) {
     long nn = (long)(N + 1) * (N + 1);
-    float h = 1.0f / (float)N;
-    k_scale_b<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(f, b, nn, h * h);
+    k_rhs<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(K, S, f, b, N, 1.0f / (float)N, mobility * rho_ratio, gravity);
 }
 
 // A2-A5 (residual, Gram solve, loss, adjoint) live in gram.cu as one fused chain.

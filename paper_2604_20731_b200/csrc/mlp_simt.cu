@@ -75,6 +75,52 @@ void simt_forward(const Net &net, const float *theta, const SimtBufs &b, float *
 
 int simt_launches_fwd(const Net &net) { return 2 + (net.nl - 2); }
 
+// ---------------------------------------------------------------- continuous evaluation (f1)
+// The same network with cutoff at arbitrary points xy[p] = (x, y), p < npts (chunks of at most P
+// points, the capacity of the activation buffers).
+__global__ void k_input_layer_pts(const float *__restrict__ W0, const float *__restrict__ b0,
+                                  float *__restrict__ act, const float *__restrict__ xy, int npts, int w) {
+    long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long)npts * w) return;
+    int p = (int)(e / w), r = (int)(e % w);
+    const float x = xy[2 * (long)p], y = xy[2 * (long)p + 1];
+    act[e] = tanhf(fmaf(W0[2 * r], x, fmaf(W0[2 * r + 1], y, b0[r])));
+}
+
+__global__ void k_output_layer_pts(const float *__restrict__ act, const float *__restrict__ Wo,
+                                   const float *__restrict__ bo, const float *__restrict__ xy,
+                                   float *__restrict__ out, int npts, int w) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= npts) return;
+    const float *row = act + (long)warp * w;
+    float s = 0.0f;
+    for (int k = lane; k < w; k += 32) s = fmaf(Wo[k], row[k], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[warp] = cutoff(xy[2 * (long)warp], xy[2 * (long)warp + 1]) * (s + bo[0]);
+}
+
+void simt_eval_points(const Net &net, const float *theta, const SimtBufs &b, const float *xy, int npts,
+                      float *out, cudaStream_t s) {
+    const int nl = net.nl;
+    const float *th = theta;
+    for (int p0 = 0; p0 < npts; p0 += net.P) {
+        const int n = npts - p0 < net.P ? npts - p0 : net.P;
+        const float *xyc = xy + 2 * (long)p0;
+        int w1 = net.widths[1];
+        k_input_layer_pts<<<(unsigned)(((long)n * w1 + 255) / 256), 256, 0, s>>>(th + net.woff[0], th + net.boff[0],
+                                                                                act_ptr(net, b, 1), xyc, n, w1);
+        for (int l = 1; l <= nl - 2; ++l) {
+            int win = net.widths[l], wout = net.widths[l + 1];
+            sgemm<false, true>(n, wout, win, act_ptr(net, b, l), win, th + net.woff[l], win, 1,
+                               EpiTanh{act_ptr(net, b, l + 1), wout, th + net.boff[l]}, s);
+        }
+        int wL = net.widths[nl - 1];
+        k_output_layer_pts<<<ceil_div(n * 32, 256), 256, 0, s>>>(act_ptr(net, b, nl - 1), th + net.woff[nl - 1],
+                                                                  th + net.boff[nl - 1], xyc, out + p0, n, wL);
+    }
+}
+
 // ---------------------------------------------------------------- backward
 // delta_L = gbar * W_out (1 - t_L^2)
 __global__ void k_output_bwd(const float *__restrict__ act, const float *__restrict__ Wo,

@@ -77,8 +77,10 @@ struct FwdArgs {
     const __half *Wf;      // [G][KC] blocks
     const float *W1p, *bp, *Wop;
     __half *act;           // [L][ntiles][KC] blocks
-    float *u;              // lattice (N+1)^2
+    float *u;              // lattice (N+1)^2 (EVAL: [npts], one value per point)
     long long *trace;      // debug timeline (CTA 0), nullptr normally
+    const float *xy;       // EVAL only: point coordinates [npts][2]
+    int npts;              // EVAL only: number of points (ntiles = ceil(npts / 128), ragged tail)
 };
 #define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
@@ -121,7 +123,9 @@ __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
 // there is no block-wide barrier inside a tile. t_hi goes to HBM straight from registers
 // (one 32-byte sector per thread and chunk). (Pre-scaling the fp16 weights by 2 log2 e to save
 // the multiply in tanh was measured 3-4x less accurate in u on B200 and is not used.)
-template <int WP>
+// EVAL = true: the same network at arbitrary points a.xy (continuous evaluation, f1 / SPEC.md:493-501):
+// no activations are stored and u[p] = cutoff(x_p, y_p) net(x_p, y_p) for p < npts.
+template <int WP, bool EVAL = false>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   // 18 warps -> <= 96 regs (5 warps on SMSP 0/1)
     constexpr int KC = WP / 64;
     constexpr uint32_t WBLK = WP * 128;
@@ -194,9 +198,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         FWD_MMA_WAIT(&a_full[c], aph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 0);
                         // t_hi chunk c of layer g+1 -> HBM (the backward's operand)
-                        bulk_s2g(a.act + ((size_t)g * a.ntiles + tile) * (KC * CHUNK_HALVES) + c * CHUNK_HALVES,
-                                 A_hi + c * CHUNK_BYTES, CHUNK_BYTES);
-                        bulk_commit();
+                        if constexpr (!EVAL) {
+                            bulk_s2g(a.act + ((size_t)g * a.ntiles + tile) * (KC * CHUNK_HALVES) + c * CHUNK_HALVES,
+                                     A_hi + c * CHUNK_BYTES, CHUNK_BYTES);
+                            bulk_commit();
+                        }
                         FWD_MMA_WAIT(&w_full[stage], ph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
@@ -266,9 +272,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
         const int N = a.N;
         for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, par ^= 1) {
             const int p = tile * 128 + row;
-            int pi, pj;
-            point_ij(p, N, pi, pj);
-            const float x = (float)pi / (float)N, y = (float)pj / (float)N;
+            int pi = 0, pj = 0;
+            float x, y;
+            if constexpr (EVAL) {
+                const bool ok = p < a.npts;
+                x = ok ? __ldg(a.xy + 2 * (long)p) : 0.0f;
+                y = ok ? __ldg(a.xy + 2 * (long)p + 1) : 0.0f;
+            } else {
+                point_ij(p, N, pi, pj);
+                x = (float)pi / (float)N;
+                y = (float)pj / (float)N;
+            }
             float dot = 0.0f;
             for (int layer = 1; layer <= a.L; ++layer) {
                 const bool last = layer == a.L;
@@ -386,10 +400,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                             const float4 w4 = lds_f4(sWo + cc + k);
                             dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
                         }
-                        if (swap)
-                            st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
-                        else
-                            st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+                        if constexpr (!EVAL) {
+                            if (swap)
+                                st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
+                            else
+                                st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+                        }
                     }
                 }
             }
@@ -399,7 +415,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             if (wq == 0) {
                 const float *r = sRed + par * 4 * 128 + row;
                 const float net = ((r[0] + r[128]) + (r[256] + r[384])) + sWo[WP];
-                a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
+                if constexpr (EVAL) {
+                    if (p < a.npts) a.u[p] = cutoff(x, y) * net;
+                } else {
+                    a.u[(long)pj * (N + 1) + pi] = cutoff(x, y) * net;
+                }
             }
         }
     }
@@ -1708,6 +1728,7 @@ void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, 
 template <int WP>
 static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
+    cudaFuncSetAttribute(k_tc_forward<WP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
         cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
         cudaFuncSetAttribute(k_tc_bwdc<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, BC<WP>::SMEM);
@@ -1929,7 +1950,7 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
     static long long *trace = nullptr;
     const char *te = getenv("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
-    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr};
+    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0};
     if (te) {
         k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
         cudaStreamSynchronize(s);
@@ -1946,6 +1967,21 @@ void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
     if (b.WP == 64) fwd_launch<64>(net, b, u, s);
     else if (b.WP == 128) fwd_launch<128>(net, b, u, s);
     else fwd_launch<256>(net, b, u, s);
+}
+
+template <int WP>
+static void eval_launch(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s) {
+    const int ntiles = (npts + 127) / 128;
+    const int grid = ntiles < b.grid_fwd ? ntiles : b.grid_fwd;
+    FwdArgs a{net.N, ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, nullptr, out, nullptr, xy, npts};
+    k_tc_forward<WP, true><<<grid, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
+}
+
+void tc_eval_points(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s) {
+    if (npts <= 0) return;
+    if (b.WP == 64) eval_launch<64>(net, b, xy, npts, out, s);
+    else if (b.WP == 128) eval_launch<128>(net, b, xy, npts, out, s);
+    else eval_launch<256>(net, b, xy, npts, out, s);
 }
 
 template <int WP>

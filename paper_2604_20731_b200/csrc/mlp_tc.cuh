@@ -44,6 +44,8 @@ struct TcBufs {
 int tc_create(const Net &net, TcBufs &b, std::string &err);
 void tc_destroy(TcBufs &b);   // device buffers, side stream, events
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
+// the network with cutoff at arbitrary points: out[p] = cutoff(xy[2p], xy[2p+1]) net(...), device pointers
+void tc_eval_points(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s);
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
 int tc_launches(const Net &net, const TcBufs &b);

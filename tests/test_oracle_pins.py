@@ -461,3 +461,96 @@ def test_P13_zero_output_layer():
     b = f.astype(np.float64).reshape(N + 1, N + 1)[1:-1, 1:-1].reshape(-1) / N ** 2
     np.testing.assert_allclose(it["res"], -b, rtol=1e-15)
     assert abs(loss - b @ _gram_inv_dst(N, b)) <= 1e-11 * loss
+
+
+# --------------------------------------------------------------------------- P14: gravity term (f1)
+# Eq. 23's RHS carries grad+ . (g K ((1-S) rho_w/mu_w + S rho_g/mu_g)); reading R23
+# makes it non-dimensional: F = (0, -Gr) K ((1-S) + M r S), r = rho_g/rho_w, and b = h^2 (f - grad+.F).
+def _gamma(K, S, r=oracle.DENSITY_RATIO):
+    s = np.clip(S.astype(np.float64), 0.0, 1.0)
+    return K.astype(np.float64) * ((1.0 - s) + oracle.MOBILITY_RATIO * r * s)
+
+
+def test_P14_gravity_vanishes_for_homogeneous_medium():
+    """Constant K and S: F is constant, its forward-difference divergence is exactly 0."""
+    N = 16
+    nn = (N + 1) ** 2
+    K = np.full(nn, 2.5, np.float32)
+    S = np.full(nn, 0.25, np.float32)
+    f = W.random_fields(N, seed=3)[2]
+    b0 = _ctx(N, K=K, S=S, f=f).rhs()
+    b1 = _ctx(N, K=K, S=S, f=f, gravity=1.7).rhs()
+    assert np.array_equal(b0, b1)
+
+
+def test_P14_gravity_linear_permeability_is_a_constant_source():
+    """K = 1 + c y, S = 0: gamma_{k,l+1} - gamma_{k,l} = c h, so b(Gr) - b(0) = h^2 Gr c exactly on
+    every node with l < N; and the loss equals the gravity-free problem with f + Gr c."""
+    N, c, Gr = 16, 0.5, 0.75
+    j = np.repeat(np.arange(N + 1), N + 1)
+    K = (1.0 + c * j / N).astype(np.float32)        # exact in fp32
+    f = W.random_fields(N, seed=4)[2]
+    widths = (2, 8, 8, 1)
+    th = W.random_theta(widths, 4)
+    og = _ctx(N, widths, K=K, f=f, theta=th, gravity=Gr)
+    o0 = _ctx(N, widths, K=K, f=(f.astype(np.float64) + Gr * c).astype(np.float32), theta=th)
+    d = (og.rhs() - _ctx(N, widths, K=K, f=f, theta=th).rhs()).reshape(N + 1, N + 1)
+    np.testing.assert_allclose(d[:N, :N], Gr * c / N ** 2, rtol=1e-12)   # grad+ needs (i+1, j), (i, j+1)
+    assert abs(og.loss_grad()[0] - o0.loss_grad()[0]) <= 1e-6 * o0.loss_grad()[0]
+
+
+def test_P14_gravity_column_sums_telescope():
+    """sum over l = 1..N-1 of the gravity part of b at column k = h Gr (gamma_{k,N} - gamma_{k,1}):
+    catches a wrong sign, difference direction (forward vs backward) or power of h."""
+    N, Gr = 32, -1.3
+    K, S, f = W.random_fields(N, seed=5)
+    d = (_ctx(N, K=K, S=S, f=f, gravity=Gr).rhs() - _ctx(N, K=K, S=S, f=f).rhs()).reshape(N + 1, N + 1)
+    g = _gamma(K, S).reshape(N + 1, N + 1)
+    lhs = d[1:N, :].sum(axis=0)                      # rows = l (y), columns = k (x)
+    rhs = Gr / N * (g[N, :] - g[1, :])
+    np.testing.assert_allclose(lhs[1:N], rhs[1:N], rtol=1e-10, atol=1e-14)
+
+
+def test_P14_gravity_saturation_dependence_and_update():
+    """K = 1 and S = y/2: gamma steps by (M r - 1) h / 2 per row, so b(Gr) - b(0) = h^2 Gr (M r - 1)/2;
+    set_saturation must recompute it (the term depends on S through rho_g/rho_w)."""
+    N, Gr = 16, 0.9
+    nn = (N + 1) ** 2
+    j = np.repeat(np.arange(N + 1), N + 1)
+    S_lin = (0.5 * j / N).astype(np.float32)
+    o = _ctx(N, gravity=Gr)
+    b_S0 = o.rhs().copy()
+    o.set_saturation(S_lin)
+    d = (o.rhs() - b_S0).reshape(N + 1, N + 1)
+    expect = Gr * (oracle.MOBILITY_RATIO * oracle.DENSITY_RATIO - 1.0) / 2.0 / N ** 2
+    np.testing.assert_allclose(d[:N, :N], expect, rtol=1e-12)
+    assert np.all(d[N, :] == 0.0) and np.all(d[:, N] == 0.0)
+    assert np.allclose(_ctx(N, S=S_lin, gravity=Gr).rhs(), o.rhs(), rtol=0, atol=1e-15)
+    del nn
+
+
+# --------------------------------------------------------------------------- P15: continuous evaluation (f1)
+def test_P15_eval_points_boundary_zero_and_lattice_consistency():
+    N = 16
+    widths = (2, 8, 8, 1)
+    o = _ctx(N, widths, theta=W.random_theta(widths, 6))
+    t = np.linspace(0.0, 1.0, 23)
+    edge = np.concatenate([np.stack([np.zeros_like(t), t], 1), np.stack([np.ones_like(t), t], 1),
+                           np.stack([t, np.zeros_like(t)], 1), np.stack([t, np.ones_like(t)], 1)])
+    assert np.all(o.eval_points(edge) == 0.0)
+    i, j = np.meshgrid(np.arange(N + 1), np.arange(N + 1))
+    xy = np.stack([i.reshape(-1) / N, j.reshape(-1) / N], 1)
+    np.testing.assert_array_equal(o.eval_points(xy), o.forward())
+
+
+def test_P15_eval_points_closed_form_one_neuron():
+    """widths (2, 1, 1): p(x,y) = 16x(1-x)y(1-y) (w2 tanh(a x + b y + c) + d), numpy's tanh."""
+    a, b, c, w2, d = 0.7, -1.3, 0.2, 1.5, -0.4
+    th = np.array([a, b, c, w2, d], np.float32)
+    o = _ctx(8, (2, 1, 1), theta=th)
+    rng = np.random.default_rng(7)
+    xy = rng.uniform(-0.5, 1.5, size=(200, 2))      # outside the unit square too
+    x, y = xy[:, 0], xy[:, 1]
+    t64 = th.astype(np.float64)
+    ref = 16 * x * (1 - x) * y * (1 - y) * (t64[3] * np.tanh(t64[0] * x + t64[1] * y + t64[2]) + t64[4])
+    np.testing.assert_allclose(o.eval_points(xy), ref, rtol=1e-13, atol=1e-15)

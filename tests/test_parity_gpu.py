@@ -293,3 +293,64 @@ def test_backward_chain_vs_oracle(crv, monkeypatch, stages, N, widths, seed):
     d = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
     _, grad_d = d.loss_grad()
     assert grad_errors(widths, grad, grad_d.astype(np.float64)).max() <= 5e-3
+
+
+# ------------------------------------------------------------------ f1: gravity term and continuous evaluation
+@pytest.mark.parametrize("prec", PRECS)
+def test_gravity_term_vs_oracle(crv, prec):
+    """A0 with Eq. 23's gravity term (reading R23) against the oracle: the residual of the GPU's own u
+    (isolates b), loss and gradients, and again after set_saturation (the term depends on S)."""
+    N, widths, seed, Gr = 64, (2, 64, 64, 64, 1), 21, 0.8
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    ref = oracle.Oracle(N, widths, K, S, f, th, gravity=Gr)
+    rl, rg, _ = ref.loss_grad(intermediates=True)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=prec, gravity=Gr)
+    loss, grad = g.loss_grad()
+    im = g.intermediates()
+    r_own = ref.residual(im["u"])
+    assert np.max(np.abs(im["res"] - r_own)) <= 1e-5 * np.abs(r_own).max()
+    tl, tg = TOL[prec]
+    assert abs(loss - rl) <= tl * abs(rl), (loss, rl)
+    assert grad_errors(widths, grad, rg).max() <= tg
+    rl0 = oracle.Oracle(N, widths, K, S, f, th).loss_grad()[0]
+    assert abs(rl - rl0) > 100 * tl * abs(rl)            # the term is not negligible here
+    S2 = W.random_fields(N, seed + 1)[1]
+    g.set_saturation(S2)
+    ref.set_saturation(S2)
+    l2, r2 = g.loss_grad(grad=False), ref.loss_grad()[0]
+    assert abs(l2 - r2) <= tl * abs(r2), (l2, r2)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_eval_points_vs_oracle(crv, prec):
+    """crvpinn_eval_points (continuous evaluation for the IGA projection) against
+    the oracle at random points (ragged count, inside and outside the unit square), exact zeros on the
+    boundary, bitwise agreement with the lattice forward at the lattice nodes, more points than the
+    lattice holds, n = 0 and a non-finite coordinate."""
+    N, widths, seed = 32, (2, 128, 128, 128, 1), 22
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=prec)
+    ref = oracle.Oracle(N, widths, K, S, f, th)
+    rng = np.random.default_rng(seed)
+    xy = np.concatenate([rng.uniform(0, 1, (1000, 2)), rng.uniform(-0.25, 1.25, (77, 2))]).astype(np.float32)
+    p, pr = g.eval_points(xy), ref.eval_points(xy)
+    tol = (1e-5 if prec == 1 else 2e-3) * np.abs(pr).max()
+    assert np.max(np.abs(p - pr)) <= tol
+    t = np.linspace(0, 1, 37, dtype=np.float32)
+    edge = np.concatenate([np.stack([np.zeros_like(t), t], 1), np.stack([t, np.ones_like(t)], 1)])
+    assert np.all(g.eval_points(edge) == 0.0)
+    i, j = np.meshgrid(np.arange(N + 1), np.arange(N + 1))
+    lat = np.stack([i.reshape(-1) / N, j.reshape(-1) / N], 1).astype(np.float32)
+    np.testing.assert_array_equal(g.eval_points(lat), g.eval())
+    big = rng.uniform(0, 1, (N * N + 300, 2)).astype(np.float32)
+    pb = g.eval_points(big)
+    idx = rng.choice(big.shape[0], 200, replace=False)
+    assert np.max(np.abs(pb[idx] - ref.eval_points(big[idx]))) <= (1e-5 if prec == 1 else 2e-3) * np.abs(pr).max()
+    assert g.eval_points(np.zeros((0, 2), np.float32)).shape == (0,)
+    bad = xy[:5].copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(crv.CrvpinnError) as e:
+        g.eval_points(bad)
+    assert e.value.code == crv.CRVPINN_EDOMAIN
