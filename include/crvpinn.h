@@ -122,6 +122,17 @@ int crvpinn_eval(crvpinn_ctx *ctx, float *p_out);
  * EDOMAIN: a non-finite coordinate (nothing is written). Synchronising. */
 int crvpinn_eval_points(crvpinn_ctx *ctx, long n, const float *xy, float *p_out);
 
+/* the discrete system A(alpha) u = b itself -- the reference pressure the
+ * paper gets from MUMPS -- for the context's current alpha and b (K, S, f,
+ * gravity), solved on the GPU by conjugate gradients preconditioned with the exact Gram solve
+ * G^-1 of Eq. 26/28 (spectrally equivalent to A(alpha)), fp32 vectors, fp64
+ * dot products, starting from u = 0. Stops when ||r|| / ||b|| <= rtol (checked every 20
+ * iterations) or after max_iter iterations. u_out: host (N+1)^2 float32, boundary 0 (nullable);
+ * iters, rel_res (nullable): iterations used and the TRUE relative residual ||b - A u|| / ||b||
+ * of the returned u (fp64). EINVAL: rtol <= 0 or max_iter < 1; ENONFINITE: non-finite residual.
+ * Returns CRVPINN_OK also when rtol was not reached (check rel_res). Does not touch theta. */
+int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_out, int *iters, double *rel_res);
+
 /* LOSS (Eq. 27) and dLOSS/dtheta at the current theta, no update. grad nullable. */
 int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad);
 

@@ -54,6 +54,8 @@ def lib():
         L.orc_get_adam.argtypes = [P, D, D, ctypes.POINTER(ctypes.c_long)]
         L.orc_get_alpha.argtypes = [P, D]
         L.orc_get_b.argtypes = [P, D]
+        L.orc_direct_solve.restype = ctypes.c_int
+        L.orc_direct_solve.argtypes = [P, D]
         L.orc_eval_points.argtypes = [P, D, ctypes.c_long, D, D]
         L.orc_set_saturation.argtypes = [P, F, F]
         L.orc_forward.argtypes = [P, D, D]
@@ -135,6 +137,13 @@ class Oracle:
         """b = h^2 (f - grad+ . F) on the (N+1)^2 lattice (A0 with the gravity term)."""
         out = np.empty((self.N + 1) ** 2)
         lib().orc_get_b(self._h, _dp(out))
+        return out
+
+    def direct_solve(self) -> np.ndarray:
+        """u* with A(alpha) u* = b (band LU, fp64), (N+1)^2 lattice."""
+        out = np.empty((self.N + 1) ** 2)
+        if lib().orc_direct_solve(self._h, _dp(out)) != 0:
+            raise MemoryError("orc_direct_solve: allocation failed")
         return out
 
     def eval_points(self, xy, theta=None) -> np.ndarray:

@@ -111,6 +111,63 @@ void orc_get_b(const orc_ctx *c, double *out) {
     memcpy(out, c->b, sizeof(double) * (long)(c->N + 1) * (c->N + 1));
 }
 
+/* ---------------------------------------------------------------- f2: the discrete system itself */
+/* solve A(alpha) u = b directly -- the reference pressure the paper obtains
+ * with MUMPS. A(alpha) is read off the residual of Eq. 25 (RES = A u - b, stencil
+ * of A2 / reading R16): row (k,l) has diagonal alpha_{k-1,l} + alpha_{k,l-1} + 2 alpha_{k,l} and
+ * -alpha_{k-1,l}, -alpha_{k,l-1}, -alpha_{k,l}, -alpha_{k,l} for the neighbours (k-1,l), (k,l-1),
+ * (k+1,l), (k,l+1) (boundary neighbours drop out: u = 0 there). A is symmetric; it is factorised
+ * by banded Doolittle LU (half-bandwidth n, natural row-major order) and solved by forward/back
+ * substitution. u_out: (N+1)^2 lattice, boundary 0. Returns 0, or -1 on allocation failure. */
+int orc_direct_solve(const orc_ctx *c, double *u_out) {
+    int N = c->N, n = c->n;
+    long n2 = (long)n * n, bw = n + 1;
+    double *U = (double *)calloc((size_t)n2 * bw, sizeof(double));
+    double *z = (double *)malloc(sizeof(double) * n2);
+    if (!U || !z) { free(U); free(z); return -1; }
+    for (int l = 1; l <= n; ++l)
+        for (int k = 1; k <= n; ++k) {
+            long r = (long)(l - 1) * n + (k - 1);
+            U[r * bw + 0] = c->alpha[idx(c, k - 1, l)] + c->alpha[idx(c, k, l - 1)] + 2.0 * c->alpha[idx(c, k, l)];
+            if (k < n) U[r * bw + 1] = -c->alpha[idx(c, k, l)];   /* (k+1, l) */
+            if (l < n) U[r * bw + n] = -c->alpha[idx(c, k, l)];   /* (k, l+1) */
+        }
+    for (long k = 0; k < n2; ++k) {
+        const double *uk = U + k * bw;
+        long iend = k + n < n2 - 1 ? k + n : n2 - 1;
+#pragma omp parallel for schedule(static) if (n >= 48)
+        for (long i = k + 1; i <= iend; ++i) {
+            double lik = uk[i - k] / uk[0];   /* A symmetric: A(i,k) = U(k,i) before row k is used */
+            if (lik == 0.0) continue;
+            double *ui = U + i * bw;
+            for (long j = i; j <= iend; ++j) ui[j - i] -= lik * uk[j - k];
+        }
+    }
+    /* forward: L z = b (L_ik = U(k,i)/U(k,k)), backward: U u = z */
+    for (long i = 0; i < n2; ++i) {
+        int l = (int)(i / n) + 1, k = (int)(i % n) + 1;
+        double v = c->b[idx(c, k, l)];
+        long kbeg = i - n > 0 ? i - n : 0;
+        for (long kk = kbeg; kk < i; ++kk) v -= U[kk * bw + (i - kk)] / U[kk * bw] * z[kk];
+        z[i] = v;
+    }
+    long nn = (long)(N + 1) * (N + 1);
+    for (long p = 0; p < nn; ++p) u_out[p] = 0.0;
+    for (long i = n2 - 1; i >= 0; --i) {
+        double v = z[i];
+        long jend = i + n < n2 - 1 ? i + n : n2 - 1;
+        for (long j = i + 1; j <= jend; ++j) {
+            int lj = (int)(j / n) + 1, kj = (int)(j % n) + 1;
+            v -= U[i * bw + (j - i)] * u_out[idx(c, kj, lj)];
+        }
+        int l = (int)(i / n) + 1, k = (int)(i % n) + 1;
+        u_out[idx(c, k, l)] = v / U[i * bw];
+    }
+    free(U);
+    free(z);
+    return 0;
+}
+
 /* ---------------------------------------------------------------- A3: factor G once */
 /* Entry (r, r+d) of G (Eq. 26) for d >= 0, r = (l-1) n + (k-1). */
 static double gram_entry(const orc_ctx *c, long r, long d) {

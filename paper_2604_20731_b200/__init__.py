@@ -21,7 +21,8 @@ PREC_TENSOR, PREC_FP32 = 0, 1
 # every symbol include/crvpinn.h declares
 EXPORTS = [
     "crvpinn_default_opts", "crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device",
-    "crvpinn_pretrain", "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_loss_grad",
+    "crvpinn_pretrain", "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_direct_solve",
+    "crvpinn_loss_grad",
     "crvpinn_get_intermediates",
     "crvpinn_num_params", "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
     "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter", "crvpinn_stream",
@@ -65,6 +66,7 @@ def load(path: str = LIB_PATH):
     L.crvpinn_eval.argtypes = [P, F]
     L.crvpinn_loss_grad.argtypes = [P, D, F]
     L.crvpinn_eval_points.argtypes = [P, ctypes.c_long, F, F]
+    L.crvpinn_direct_solve.argtypes = [P, ctypes.c_double, I, F, ctypes.POINTER(ctypes.c_int), D]
     L.crvpinn_get_intermediates.argtypes = [P, F, F, F, F]
     L.crvpinn_num_params.restype = ctypes.c_size_t
     L.crvpinn_num_params.argtypes = [P]
@@ -81,7 +83,8 @@ def load(path: str = LIB_PATH):
     L.crvpinn_last_error.argtypes = [P]
     L.crvpinn_destroy.argtypes = [P]
     for name in ["crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device", "crvpinn_pretrain",
-                 "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_loss_grad", "crvpinn_get_intermediates",
+                 "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_direct_solve", "crvpinn_loss_grad",
+                 "crvpinn_get_intermediates",
                  "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
                  "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter"]:
         getattr(L, name).restype = I
@@ -182,6 +185,14 @@ class Crvpinn:
         if xy.shape[0]:
             self._check(load().crvpinn_eval_points(self._h, int(xy.shape[0]), _fp(xy), _fp(out)))
         return out
+
+    def direct_solve(self, rtol: float = 1e-5, max_iter: int = 20000):
+        """u with A(alpha) u = b (Gram-preconditioned CG) -> (u lattice (N+1)^2, iterations, rel. residual)."""
+        u = np.empty((self.N + 1) ** 2, dtype=np.float32)
+        it, rel = ctypes.c_int(0), ctypes.c_double(0.0)
+        self._check(load().crvpinn_direct_solve(self._h, float(rtol), int(max_iter), _fp(u), ctypes.byref(it),
+                                                ctypes.byref(rel)))
+        return u, int(it.value), float(rel.value)
 
     def loss_grad(self, grad: bool = True):
         loss = ctypes.c_double()

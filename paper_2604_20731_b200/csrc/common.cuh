@@ -122,6 +122,10 @@ int field_chain_loss_blocks(int N);
 void launch_field_chain(const float *u, const float *alpha, const float *b, float *res, float *q, float *gbar,
                         float *gu_lat, double *loss_part, const GramConsts &c, int N, DevState *st, int track_max,
                         double *hist, int n_hist, double beta1, double beta2, int advance, cudaStream_t s);
+// f2: A(alpha) u = b by Gram-preconditioned CG (u_lat: interior written, boundary untouched);
+// returns 0 / -1 (CUDA error); iterations used and the final true relative residual
+int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts &c, int N, double rtol, int max_iter,
+              int *iters_out, double *rel_out, cudaStream_t s);
 // mlp_simt.cu -- fp32 FFMA MLP path (CRVPINN_PREC_FP32)
 struct MlpPlan {
     long offW[CRV_MAX_LAYERS], offB[CRV_MAX_LAYERS];   // partial-buffer offsets per layer

@@ -487,6 +487,35 @@ int crvpinn_eval_points(crvpinn_ctx *ctx, long n, const float *xy, float *p_out)
     return CRVPINN_OK;
 }
 
+int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_out, int *iters, double *rel_res) {
+    if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
+    if (!(rtol > 0.0) || max_iter < 1) return fail(ctx, CRVPINN_EINVAL, "need rtol > 0 and max_iter >= 1");
+    CK(cudaSetDevice(ctx->device));
+    const int N = ctx->net.N;
+    const size_t nn = (size_t)(N + 1) * (N + 1);
+    float *ud = nullptr;   // lattice result (boundary 0); a temporary so that no training buffer changes
+    CK(cudaMalloc(&ud, sizeof(float) * nn));
+    cudaMemsetAsync(ud, 0, sizeof(float) * nn, ctx->stream);
+    int it = 0;
+    double rel = 0.0;
+    const int prc = pcg_solve(ctx->alpha, ctx->b, ud, ctx->gram, N, rtol, max_iter, &it, &rel, ctx->stream);
+    cudaError_t e = cudaSuccess;
+    if (prc == 0 && u_out) {
+        e = cudaMemcpyAsync(ctx->h_field, ud, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) memcpy(u_out, ctx->h_field, sizeof(float) * nn);
+    }
+    cudaFree(ud);
+    if (prc != 0 || e != cudaSuccess) {
+        ctx->err = std::string("direct solve: ") + cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError());
+        return CRVPINN_ECUDA;
+    }
+    if (iters) *iters = it;
+    if (rel_res) *rel_res = rel;
+    if (!std::isfinite(rel)) return fail(ctx, CRVPINN_ENONFINITE, "non-finite residual in the direct solve");
+    return CRVPINN_OK;
+}
+
 int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad) {
     if (!ctx || !loss) return fail(ctx, CRVPINN_EINVAL, "null argument");
     CK(cudaSetDevice(ctx->device));

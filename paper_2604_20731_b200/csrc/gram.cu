@@ -353,4 +353,242 @@ void launch_field_chain(const float *u, const float *alpha, const float *b, floa
                loss_part, rows, hist, n_hist, beta1, beta2, advance);
 }
 
+
+// ================================================================ f2: the discrete system itself
+// A(alpha) u = b (the system the paper solves with MUMPS)
+// by conjugate gradients preconditioned with the exact Gram solve G^-1 (the sine transform +
+// per-mode Thomas scans above; G is spectrally equivalent to A(alpha) with constants min/max alpha,
+// PAPER.md:384-395). Vectors are n x n interior arrays, row-major [j][k] like RES; dot products
+// are fp64 block partials summed in a fixed order by every consumer (deterministic, no atomics).
+namespace {
+struct PcgState {
+    double rz[2];   // r.z of iterations it (slot it & 1) and it - 1
+    double bb;      // ||b||^2
+};
+constexpr int PCG_MV_THREADS = 256;
+
+__device__ __forceinline__ double block_sum_f64(double v, double *sred) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+    __syncthreads();
+    return s;   // valid in thread 0
+}
+
+__device__ __forceinline__ double fixed_sum(const double *part, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    return s;
+}
+
+// DST-I of two rows of an n x n row-major array (the first stage of G^-1), mode-major output
+__global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat, const float2 *__restrict__ tw,
+                          int N, int logM, float scale) {
+    extern __shared__ float2 sa[];
+    const int n = N - 1, M = 2 * N;
+    float2 *stw = sa + M;
+    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    const int j0 = 2 * blockIdx.x;
+    const bool has1 = j0 + 1 < n;
+    const int shift = 32 - logM;
+    if (threadIdx.x == 0) {
+        sa[0] = make_float2(0.0f, 0.0f);
+        sa[__brev((unsigned)N) >> shift] = make_float2(0.0f, 0.0f);
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const float v1 = in[(long)j0 * n + k], v2 = has1 ? in[(long)(j0 + 1) * n + k] : 0.0f;
+        sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v1, v2);
+        sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v1, -v2);
+    }
+    __syncthreads();
+    fft_inplace(sa, stw, M, logM);
+    for (int k = threadIdx.x + 1; k <= n; k += blockDim.x) {
+        const float2 Y = sa[k];
+        rhat[(long)(k - 1) * n + j0] = -0.5f * Y.y * scale;
+        if (has1) rhat[(long)(k - 1) * n + j0 + 1] = 0.5f * Y.x * scale;
+    }
+}
+
+// y = A(alpha) v (the stencil of A2 without b; v = 0 off the interior), one block per row j, and
+// this block's part of v . y
+__global__ void k_pcg_matvec(const float *__restrict__ v, const float *__restrict__ alpha, float *__restrict__ y,
+                             double *__restrict__ part, int N) {
+    __shared__ double sred[32];
+    const int n = N - 1, j = blockIdx.x, l = j + 1;
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int i = k + 1;
+        const float vc = v[(long)j * n + k];
+        const float vw = k > 0 ? v[(long)j * n + k - 1] : 0.0f, ve = k + 1 < n ? v[(long)j * n + k + 1] : 0.0f;
+        const float vs = j > 0 ? v[(long)(j - 1) * n + k] : 0.0f, vn = j + 1 < n ? v[(long)(j + 1) * n + k] : 0.0f;
+        const float r = alpha[latx(i - 1, l, N)] * (vc - vw) + alpha[latx(i, l - 1, N)] * (vc - vs) +
+                        alpha[latx(i, l, N)] * ((vc - ve) + (vc - vn));
+        y[(long)j * n + k] = r;
+        acc += (double)vc * (double)r;
+    }
+    const double s = block_sum_f64(acc, sred);
+    if (threadIdx.x == 0) part[j] = s;
+}
+
+// x += a p, r -= a Ap with a = rz / (p . Ap); this block's part of r . r
+__global__ void k_pcg_xr(double *__restrict__ x, float *__restrict__ r, const float *__restrict__ p,
+                         const float *__restrict__ Ap, const double *__restrict__ part_pap, int npap,
+                         const PcgState *__restrict__ st, int it, double *__restrict__ part_rr, int n2) {
+    __shared__ double sred[32];
+    __shared__ float sa;
+    if (threadIdx.x == 0) {   // exact convergence (p = 0) leaves x and r unchanged
+        const double pap = fixed_sum(part_pap, npap);
+        sa = pap > 0.0 ? (float)(st->rz[it & 1] / pap) : 0.0f;
+    }
+    __syncthreads();
+    const float a = sa;
+    double acc = 0.0;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long)gridDim.x * blockDim.x) {
+        x[e] += (double)a * (double)p[e];
+        const float rn = fmaf(-a, Ap[e], r[e]);
+        r[e] = rn;
+        acc += (double)rn * (double)rn;
+    }
+    const double s = block_sum_f64(acc, sred);
+    if (threadIdx.x == 0) part_rr[blockIdx.x] = s;
+}
+
+// p = z + beta p, beta = rz_new / rz_old (beta = 0 on the first iteration); block 0 records rz_new
+__global__ void k_pcg_p(const float *__restrict__ z, float *__restrict__ p, const double *__restrict__ part_rz, int nrz,
+                        PcgState *st, int it, long n2) {
+    __shared__ double srz;
+    if (threadIdx.x == 0) srz = fixed_sum(part_rz, nrz);
+    __syncthreads();
+    const double rz = srz;
+    const double rz_old = it == 0 ? 0.0 : st->rz[(it - 1) & 1];
+    const float beta = rz_old > 0.0 ? (float)(rz / rz_old) : 0.0f;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long)gridDim.x * blockDim.x)
+        p[e] = beta == 0.0f ? z[e] : fmaf(beta, p[e], z[e]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->rz[it & 1] = rz;
+}
+
+// r = b on the interior (x = 0 start), this block's part of b . b
+__global__ void k_pcg_init(const float *__restrict__ b, double *__restrict__ x, float *__restrict__ r,
+                           double *__restrict__ part, int N) {
+    __shared__ double sred[32];
+    const int n = N - 1, j = blockIdx.x;
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const float v = b[latx(k + 1, j + 1, N)];
+        x[(long)j * n + k] = 0.0;
+        r[(long)j * n + k] = v;
+        acc += (double)v * (double)v;
+    }
+    const double s = block_sum_f64(acc, sred);
+    if (threadIdx.x == 0) part[j] = s;
+}
+
+__global__ void k_pcg_set_bb(PcgState *st, const double *part, int n) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) st->bb = fixed_sum(part, n);
+}
+
+// true residual of the fp64 iterate, r_true = b - A x in fp64: this block's part of ||r_true||^2
+// (row j); with r != nullptr it also replaces the recursive residual (residual replacement, which
+// keeps the fp32 recurrences from drifting away from the true residual), with u_lat != nullptr it
+// writes x (rounded to fp32) into the lattice
+__global__ void k_pcg_final(const double *__restrict__ x, const float *__restrict__ alpha, const float *__restrict__ b,
+                            float *__restrict__ r, float *__restrict__ u_lat, double *__restrict__ part, int N) {
+    __shared__ double sred[32];
+    const int n = N - 1, j = blockIdx.x, l = j + 1;
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int i = k + 1;
+        const double vc = x[(long)j * n + k];
+        const double vw = k > 0 ? x[(long)j * n + k - 1] : 0.0, ve = k + 1 < n ? x[(long)j * n + k + 1] : 0.0;
+        const double vs = j > 0 ? x[(long)(j - 1) * n + k] : 0.0, vn = j + 1 < n ? x[(long)(j + 1) * n + k] : 0.0;
+        const double ax = (double)alpha[latx(i - 1, l, N)] * (vc - vw) + (double)alpha[latx(i, l - 1, N)] * (vc - vs) +
+                          (double)alpha[latx(i, l, N)] * ((vc - ve) + (vc - vn));
+        const double d = (double)b[latx(i, l, N)] - ax;
+        acc += d * d;
+        if (r) r[(long)j * n + k] = (float)d;
+        if (u_lat) u_lat[latx(i, l, N)] = (float)vc;
+    }
+    const double s = block_sum_f64(acc, sred);
+    if (threadIdx.x == 0) part[j] = s;
+}
+}  // namespace
+
+int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts &c, int N, double rtol, int max_iter,
+              int *iters_out, double *rel_out, cudaStream_t s) {
+    const int n = N - 1, M = 2 * N;
+    const long n2 = (long)n * n;
+    const float h = 1.0f / (float)N;
+    const float nrm = sqrtf(2.0f / (float)N);
+    const int rows = (n + 1) / 2;
+    const int vblocks = 2 * 148;
+    float *buf = nullptr;
+    double *dpart = nullptr, *x = nullptr;
+    PcgState *st = nullptr;
+    if (cudaMalloc(&buf, sizeof(float) * 4 * n2) != cudaSuccess) return -1;
+    if (cudaMalloc(&x, sizeof(double) * n2) != cudaSuccess) { cudaFree(buf); return -1; }
+    if (cudaMalloc(&dpart, sizeof(double) * (3 * (size_t)n + vblocks)) != cudaSuccess) { cudaFree(buf); cudaFree(x); return -1; }
+    if (cudaMalloc(&st, sizeof(PcgState)) != cudaSuccess) { cudaFree(buf); cudaFree(x); cudaFree(dpart); return -1; }
+    float *r = buf, *z = buf + n2, *p = buf + 2 * n2, *Ap = buf + 3 * n2;
+    double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n, *part_rr = dpart + 3 * n;
+    float *rhat = c.work, *zhat = c.work + n2;
+    const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (M + M / 2));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_pcg_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+        attr = true;
+    }
+    auto precond = [&]() {   // z = G^-1 r (and the block parts of r . z)
+        k_pcg_dst<<<rows, fft_t, smem_fft, s>>>(r, rhat, c.tw, N, c.logM, nrm);
+        k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(
+            rhat, c.etab, zhat, n, c.seg, h * h);
+        k_idst_loss<<<rows, fft_t, smem_fft, s>>>(zhat, r, z, part_rz, c.tw, N, c.logM, nrm);
+    };
+    k_pcg_init<<<n, PCG_MV_THREADS, 0, s>>>(b, x, r, part_a, N);
+    k_pcg_set_bb<<<1, 32, 0, s>>>(st, part_a, n);
+    precond();
+    k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, 0, n2);
+    PcgState hs{};
+    std::vector<double> hf(n);
+    int it = 0;
+    double rel = 1.0;
+    constexpr int CHK = 20;
+    while (it < max_iter) {
+        const int upto = it + CHK < max_iter ? it + CHK : max_iter;
+        for (; it < upto; ++it) {
+            k_pcg_matvec<<<n, PCG_MV_THREADS, 0, s>>>(p, alpha, Ap, part_a, N);
+            k_pcg_xr<<<vblocks, 256, 0, s>>>(x, r, p, Ap, part_a, n, st, it, part_rr, n2);
+            precond();
+            k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, it + 1, n2);
+        }
+        // convergence on the TRUE residual of the fp64 iterate, which also replaces r
+        k_pcg_final<<<n, PCG_MV_THREADS, 0, s>>>(x, alpha, b, r, nullptr, part_fin, N);
+        if (cudaMemcpyAsync(&hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(hf.data(), part_fin, sizeof(double) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            break;
+        double rr = 0.0;
+        for (double v : hf) rr += v;
+        rel = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
+        if (!(rel > rtol)) break;   // converged (or NaN: stop)
+    }
+    // true residual of the returned iterate, x -> lattice (boundary stays as given: zeroed by the caller)
+    k_pcg_final<<<n, PCG_MV_THREADS, 0, s>>>(x, alpha, b, nullptr, u_lat, part_fin, N);
+    cudaMemcpyAsync(hf.data(), part_fin, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&hs, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    double rr = 0.0;
+    for (double v : hf) rr += v;
+    if (iters_out) *iters_out = it;
+    if (rel_out) *rel_out = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
+    cudaFree(buf);
+    cudaFree(x);
+    cudaFree(dpart);
+    cudaFree(st);
+    return e == cudaSuccess ? 0 : -1;
+}
+
 }  // namespace crv

@@ -1,0 +1,43 @@
+"""f2 measurement: crvpinn_direct_solve (Gram-preconditioned CG on the GPU) on C4 and C5 -- time to
+rtol 1e-6, iterations, true relative residual -- next to the oracle's band-LU direct solve (fp64,
+host cores), and the paper's accuracy comparison on C1 (CRVPINN pressure after 3000 Adam
+iterations vs the direct solution). usage: python scripts/bench_direct_solve.py [--no-oracle]"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2604_20731_b200 as crv  # noqa: E402
+import workloads as W  # noqa: E402
+
+res = {"op": "crvpinn_direct_solve"}
+for name in ("C4", "C5"):
+    F = W.make_fields(name)
+    w = F.workload
+    g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=0)
+    g.direct_solve(rtol=1e-3, max_iter=20)
+    t = time.perf_counter()
+    u, it, rel = g.direct_solve(rtol=1e-6, max_iter=50000)
+    dt = time.perf_counter() - t
+    e = {"N": w.N, "gpu_ms": dt * 1e3, "iterations": it, "rel_residual": rel, "us_per_iteration": dt * 1e6 / max(it, 1)}
+    if "--no-oracle" not in sys.argv:
+        import oracle
+        o = oracle.Oracle(w.N, w.widths, F.K, F.S, F.f, F.theta0, factor_gram=False)
+        t = time.perf_counter()
+        us = o.direct_solve()
+        e["oracle_band_lu_s"] = time.perf_counter() - t
+        e["oracle_threads"] = oracle.max_threads()
+        e["rel_error_vs_oracle"] = float(np.linalg.norm(u - us) / np.linalg.norm(us))
+    res[name] = e
+F = W.make_fields("C1")
+w = F.workload
+g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=0, lr=w.lr)
+ud, it, rel = g.direct_solve(rtol=1e-8, max_iter=1000)
+g.step(3000, history=False)
+up = g.eval()
+res["C1_crvpinn_vs_direct"] = {"adam_iterations": 3000, "rel_l2_error": float(np.linalg.norm(up - ud) / np.linalg.norm(ud))}
+print(json.dumps(res))

@@ -554,3 +554,38 @@ def test_P15_eval_points_closed_form_one_neuron():
     t64 = th.astype(np.float64)
     ref = 16 * x * (1 - x) * y * (1 - y) * (t64[3] * np.tanh(t64[0] * x + t64[1] * y + t64[2]) + t64[4])
     np.testing.assert_allclose(o.eval_points(xy), ref, rtol=1e-13, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- P16: direct solve (f2)
+def test_P16_direct_solve_zero_residual_and_dense_lapack():
+    """u* = A(alpha)^-1 b: RES(u*) = 0 by the literal residual (P3-pinned), LOSS(u*) = 0, and equal to a
+    dense LAPACK solve of the matrix assembled column by column from orc_residual (N = 8)."""
+    N = 8
+    K, S, f = W.random_fields(N, seed=16)
+    o = _ctx(N, K=K, S=S, f=f, gravity=0.6)
+    u = o.direct_solve()
+    U = u.reshape(N + 1, N + 1)
+    assert np.all(U[0] == 0) and np.all(U[-1] == 0) and np.all(U[:, 0] == 0) and np.all(U[:, -1] == 0)
+    res = o.residual(u)
+    assert np.max(np.abs(res)) <= 1e-12 * np.abs(o.rhs()).max()
+    n = N - 1
+    b = -o.residual(np.zeros((N + 1) ** 2))          # RES(0) = -b on the interior
+    A = np.empty((n * n, n * n))
+    for c in range(n * n):
+        e = np.zeros((N + 1) ** 2)
+        e[(c // n + 1) * (N + 1) + (c % n + 1)] = 1.0
+        A[:, c] = o.residual(e) + b                   # A e = RES(e) + b
+    x = np.linalg.solve(A, b)
+    np.testing.assert_allclose(U[1:-1, 1:-1].reshape(-1), x, rtol=1e-11, atol=1e-14)
+
+
+def test_P16_direct_solve_manufactured_polynomial():
+    """alpha = 1, f = 2[x(1-x) + y(1-y)]: the 5-point stencil is exact on quadratics, so u* = x(1-x)y(1-y)."""
+    N = 32
+    i, j = np.meshgrid(np.arange(N + 1), np.arange(N + 1))
+    x, y = (i / N).reshape(-1), (j / N).reshape(-1)
+    f = (2.0 * (x * (1 - x) + y * (1 - y))).astype(np.float32)
+    u = _ctx(N, f=f).direct_solve()
+    ustar = x * (1 - x) * y * (1 - y)
+    # f is rounded to fp32 on input: the solution error is that rounding propagated (~1e-8 rel)
+    np.testing.assert_allclose(u, ustar, rtol=0, atol=1e-8 * ustar.max())

@@ -354,3 +354,51 @@ def test_eval_points_vs_oracle(crv, prec):
     with pytest.raises(crv.CrvpinnError) as e:
         g.eval_points(bad)
     assert e.value.code == crv.CRVPINN_EDOMAIN
+
+
+# ------------------------------------------------------------------ f2: the discrete system by Gram-preconditioned CG
+@pytest.mark.parametrize("N,seed,Gr", [(32, 31, 0.0), (64, 32, 0.5), (128, 33, 0.0)])
+def test_direct_solve_vs_oracle(crv, N, seed, Gr):
+    """crvpinn_direct_solve against the oracle's band-LU solve of A(alpha) u = b:
+    the reported true residual (fp64 iterate) meets rtol, the oracle's residual of the returned fp32 u
+    is that plus fp32 rounding, and
+    the solution error is within the conditioning bound kappa * rtol (kappa <= max alpha / min alpha
+    times the Gram spectral bound, P6)."""
+    widths = (2, 32, 32, 1)
+    K, S, f = W.random_fields(N, seed)
+    g = crv.Crvpinn(N, widths, K, S, f, precision=1, gravity=Gr)
+    ref = oracle.Oracle(N, widths, K, S, f, gravity=Gr)
+    rtol = 1e-6
+    u, it, rel = g.direct_solve(rtol=rtol, max_iter=5000)
+    assert rel <= 2 * rtol and it < 5000, (it, rel)
+    U = u.reshape(N + 1, N + 1)
+    assert np.all(U[0] == 0) and np.all(U[-1] == 0) and np.all(U[:, 0] == 0) and np.all(U[:, -1] == 0)
+    b = -ref.residual(np.zeros((N + 1) ** 2))
+    # rel is the residual of the fp64 iterate; the returned u is its fp32 rounding
+    rel_o = np.linalg.norm(ref.residual(u.astype(np.float64))) / np.linalg.norm(b)
+    assert rel_o <= rel + 5e-5, (rel_o, rel)
+    ustar = ref.direct_solve()
+    a = ref.alpha().reshape(N + 1, N + 1)[:N, :N]
+    kappa = a.max() / a.min()
+    err = np.linalg.norm(u - ustar) / np.linalg.norm(ustar)
+    assert err <= 10 * kappa * rtol, (err, kappa)
+
+
+def test_direct_solve_edges(crv):
+    F = W.make_fields("C1")
+    w = F.workload
+    g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=0)
+    th = g.theta.copy()
+    with pytest.raises(crv.CrvpinnError):
+        g.direct_solve(rtol=0.0)
+    u, it, rel = g.direct_solve(rtol=1e-5, max_iter=1)
+    assert it == 1 and rel > 0
+    u, it, rel = g.direct_solve(rtol=1e-6)
+    assert rel <= 2e-6
+    # C1: alpha = 1, f = 2 pi^2 sin sin => u* = c_h sin sin exactly (P4), c_h = (pi h/2)^2 / sin^2(pi h/2)
+    N = w.N
+    i, j = np.meshgrid(np.arange(N + 1), np.arange(N + 1))
+    c_h = (np.pi / (2 * N)) ** 2 / np.sin(np.pi / (2 * N)) ** 2
+    ustar = c_h * np.sin(np.pi * i / N) * np.sin(np.pi * j / N)
+    assert np.max(np.abs(u - ustar.reshape(-1))) <= 1e-5 * ustar.max()
+    np.testing.assert_array_equal(g.theta, th)       # the solve leaves the network alone
