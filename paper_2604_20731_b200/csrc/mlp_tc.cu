@@ -806,8 +806,11 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_EARLY_T
+#define CRV_B2_EARLY_T 1   // bwd2 epilogue releases the t slot right after xfull (t values in registers)
+#endif
 #ifndef CRV_T_FIRST
-#define CRV_T_FIRST 0   // backward producers issue a tile's t_in load before its Delta chunks
+#define CRV_T_FIRST 1   // backward producers issue a tile's t_in load before its Delta chunks
 #endif
 #ifndef CRV_B2_EPI_WARPS
 #define CRV_B2_EPI_WARPS 8
@@ -1070,6 +1073,23 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(&xfull[b], (kk >> 1) & 1);
             if (warp == 2 && lane == 0) BTRACE(kk * 16 + 5);
             tc_fence_after();
+#if CRV_B2_EARLY_T
+            // the dW MMAs of this tile are complete (xfull follows them): take this warp's t values
+            // into registers and release the t slot now, so the next-but-one tile's t_in load starts
+            // a whole epilogue earlier (the MMA warp was waiting ~0.8K cycles per tile for it)
+            uint32_t tall[CPW / 32][4][4];
+#pragma unroll
+            for (int g2 = 0; g2 < CPW / 32; ++g2) {
+                const int col0 = wq * CPW + g2 * 32;
+                const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + (col0 >> 6)) * CHUNK_BYTES + row * 128);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    ld_shared_v4(tsm + (uint32_t)(((((col0 & 63) >> 3) + j) ^ (row & 7)) << 4), tall[g2][j][0],
+                                 tall[g2][j][1], tall[g2][j][2], tall[g2][j][3]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[tb]);
+#endif
 #pragma unroll
             for (int g2 = 0; g2 < CPW / 32; ++g2) {
                 const int col0 = wq * CPW + g2 * 32;     // local dX column (i - 128 rank)
@@ -1083,11 +1103,17 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int lg = lgb + j;
+#if CRV_B2_EARLY_T
+                    const uint32_t *tw = tall[g2][j];
+                    (void)lg;
+                    (void)tsm;
+#else
                     uint32_t tw[4];
                     ld_shared_v4(tsm + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
+#endif
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
-                        const float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&tw[mm]));
+                        const float2 tf = __half22float2(*reinterpret_cast<const __half2 *>(&tw[mm]));
                         v[8 * j + 2 * mm] *= (1.0f - tf.x * tf.x);
                         v[8 * j + 2 * mm + 1] *= (1.0f - tf.y * tf.y);
                         w[4 * j + mm] = pack_half2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
@@ -1123,7 +1149,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (lane == 0) {
                 if (warp == 2) BTRACE(kk * 16 + 6);
                 mbar_arrive(&xempty[b]);
+#if !CRV_B2_EARLY_T
                 mbar_arrive(&tempty[tb]);
+#endif
             }
         }
         // ---- end: all MMAs done -> the rings are free for the reductions
