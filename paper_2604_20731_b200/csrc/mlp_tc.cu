@@ -806,6 +806,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_DX_FIRST
+#define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
+#endif
 #ifndef CRV_B2_EARLY_T
 #define CRV_B2_EARLY_T 1   // bwd2 epilogue releases the t slot right after xfull (t values in registers)
 #endif
@@ -942,7 +945,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 // chunk pairs (2h, 2h+1): dX over those K chunks, then the dW^T N-half h, then release
                 // the two ring slots -- the next tile's loads refill them mid-tile. Pairs sit in
                 // consecutive slots (slot0 + 2h is even and <= DS - 2).
-                for (int h = 0; h < KC / 2; ++h) {
+                auto dx_pair = [&](int h) {
                     const int sl = (slot0 + 2 * h) % DS;
                     for (int j = 2 * h; j < 2 * h + 2; ++j) {
                         B2_MMA_WAIT(a.outl ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
@@ -955,6 +958,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                             mma_f16(accx, ad, bd, idesc_x, (j | kq) != 0);
                         }
                     }
+                };
+                auto dw_half = [&](int h) {
+                    const int sl = (slot0 + 2 * h) % DS;
 #pragma unroll
                     for (int ks = 0; ks < 8; ++ks) {
                         const uint64_t ad = sdesc_sw128(tr + tb * 2 * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
@@ -965,8 +971,19 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         if (NS == 1) mma_commit(&dempty[sl + j]);
                         else mma_commit_mc(&dempty[sl + j], MASK);
                     }
+                };
+#if CRV_B2_DX_FIRST
+                // all of dX first, committed before the dW MMAs: the epilogue drains it while dW runs
+                for (int h = 0; h < KC / 2; ++h) dx_pair(h);
+                mma_commit(&xfull[b]);
+                for (int h = 0; h < KC / 2; ++h) dw_half(h);
+#else
+                for (int h = 0; h < KC / 2; ++h) {
+                    dx_pair(h);
+                    dw_half(h);
                 }
                 mma_commit(&xfull[b]);
+#endif
                 BTRACE(k * 16 + 3);
                 mma_commit(&tempty[tb]);
                 dn += KC;
