@@ -781,6 +781,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
 // warps turn it into Delta_L = s*gbar*W_out (.) (1 - t_L^2) in place (the output-layer backward,
 // fused), reducing the output-layer gradients on the way. The last GEMM (g = 0) does not store
 // Delta_1 (only its column sums are needed: bias and first-layer weights).
+// SWIZZLE_NONE shared-memory descriptor (LBO/SBO in bytes); with LBO = SBO = 0 every core matrix
+// of the operand aliases one 128-byte block -- used for an all-ones A operand (column sums by MMA)
+__device__ __forceinline__ uint64_t sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
 struct Bwd2Args {
     int N, ntiles, npairs, first, outl;
     int rev;              // walk the tile sequence backwards (alternating launches: L2 reuse)
@@ -795,6 +806,7 @@ struct Bwd2Args {
     float *part_dw;       // [npairs][WP*WP]   rows = out features
     DevState *st;
     long long *trace;     // debug timeline (CTA 0), nullptr normally
+    float *part_cb;       // [npairs][WP] 1^T Delta_out (CRV_B2_MMA_CS): bias gradient of theta layer g+1
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 #ifndef CRV_B2_MMA_SLEEP
@@ -806,6 +818,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_MMA_CS
+#define CRV_B2_MMA_CS 0    // bias gradients from a tensor-core 1^T Delta_out (single-buffered dX accumulator)
+#endif
 #ifndef CRV_B2_DX_FIRST
 #define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
 #endif
@@ -828,7 +843,7 @@ struct B2 {
     static constexpr int KC = WP / 64;
     static constexpr int DS = KC + CRV_B2_DSX;   // Delta ring slots
     static constexpr int NT = CRV_B2_NT;         // t ring depth (tiles of 2 chunks)
-    static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 64 * 8;
+    static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
 template <int WP>
@@ -840,7 +855,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     uint8_t *Wt = smem;                          // [KC] x 16 KiB: W^T rows i in [128c, 128c+128)
     uint8_t *Dr = Wt + KC * CHUNK_BYTES;         // [DS] x 16 KiB
     uint8_t *Tr = Dr + DS * CHUNK_BYTES;         // [NT tiles][2 chunks] x 16 KiB
-    uint64_t *bars = (uint64_t *)(Tr + 2 * NT * CHUNK_BYTES);
+    uint8_t *ones = Tr + 2 * NT * CHUNK_BYTES;   // 256 B of fp16 ones (A operand of the bias MMA)
+    uint64_t *bars = (uint64_t *)(ones + 256);
     uint64_t *wfull = bars;
     uint64_t *dfull = bars + 1, *dempty = dfull + DS, *dready = dempty + DS;
     uint64_t *tfull = dready + DS, *tempty = tfull + NT, *xfull = tempty + NT, *xempty = xfull + 2;
@@ -868,6 +884,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         mbar_init(wdone, 1);
         fence_mbar_init();
     }
+    if (threadIdx.x < 64) reinterpret_cast<uint32_t *>(ones)[threadIdx.x] = 0x3C003C00u;   // fp16 1.0 pairs
+    fence_proxy_async_smem();
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     pdl_wait();   // inputs of this GEMM come from the previous launch
     pdl_trigger();
@@ -877,6 +895,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tm_w = tmem + 256;   // dW^T accumulator; dX accumulators at columns 0 / 128
+    [[maybe_unused]] const uint32_t tm_c = tmem + 128;   // CRV_B2_MMA_CS: 1^T Delta_out (dX single-buffered)
+    constexpr int XB = CRV_B2_MMA_CS ? 1 : 2;   // dX accumulator buffers
 
     if (warp == 0) {
         // ---------------- producer
@@ -934,11 +954,11 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(wfull, 0);
             int dn = 0;
             for (int k = 0; k < nk; ++k) {
-                const int b = k & 1, tb = k % NT;
+                const int b = k % XB, tb = k % NT;
                 const int slot0 = dn % DS;
                 B2_MMA_WAIT(&tfull[tb], (k / NT) & 1);
                 BTRACE(k * 16 + 2);
-                B2_MMA_WAIT(&xempty[b], ((k >> 1) & 1) ^ 1);
+                B2_MMA_WAIT(&xempty[b], ((k / XB) & 1) ^ 1);
                 BTRACE(k * 16 + 7);
                 tc_fence_after();
                 const uint32_t accx = tmem + (uint32_t)(b * 128);
@@ -967,6 +987,17 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
                     }
+#if CRV_B2_MMA_CS
+                    if (h == (int)rank) {   // 1^T Delta_out for this CTA's half of the output features
+                        constexpr uint32_t idesc_c = idesc_f16(128, 128, 0, 1);
+                        const uint64_t d1 = sdesc_none(smem_u32(ones), 0, 0);
+#pragma unroll
+                        for (int ks = 0; ks < 8; ++ks) {
+                            const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
+                            mma_f16(tm_c, d1, bd, idesc_c, (k | ks) != 0);
+                        }
+                    }
+#endif
                     for (int j = 0; j < 2; ++j) {
                         if (NS == 1) mma_commit(&dempty[sl + j]);
                         else mma_commit_mc(&dempty[sl + j], MASK);
@@ -1081,15 +1112,24 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             }
             if (k == 0) continue;
             // ---- dX epilogue of tile k-1
-            const int kk = k - 1, b = kk & 1, tb = kk % NT;
+            const int kk = k - 1, b = kk % XB, tb = kk % NT;
             const int tile = pair + (a.rev ? nk - 1 - kk : kk) * a.npairs;
             int pi, pj;
             point_ij(tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
             if (warp == 2 && lane == 0) BTRACE(kk * 16 + 4);
-            mbar_wait(&xfull[b], (kk >> 1) & 1);
+            mbar_wait(&xfull[b], (kk / XB) & 1);
             if (warp == 2 && lane == 0) BTRACE(kk * 16 + 5);
             tc_fence_after();
+#if CRV_B2_MMA_CS
+            // single dX buffer: drain it into registers and release it before any math
+            float vall[CPW / 32][32];
+#pragma unroll
+            for (int g2 = 0; g2 < CPW / 32; ++g2) tmem_ld32(tmem + t_lane + (uint32_t)(wq * CPW + g2 * 32), vall[g2]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xempty[b]);
+#endif
 #if CRV_B2_EARLY_T
             // the dW MMAs of this tile are complete (xfull follows them): take this warp's t values
             // into registers and release the t slot now, so the next-but-one tile's t_in load starts
@@ -1114,8 +1154,12 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 const int lgb = (col0 & 63) >> 3;        // first logical granule in the chunk
                 const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + hf) * CHUNK_BYTES + row * 128);
                 uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
+#if CRV_B2_MMA_CS
+                float(&v)[32] = vall[g2];
+#else
                 float v[32];
                 tmem_ld32(tmem + t_lane + (uint32_t)(b * 128 + col0), v);
+#endif
                 uint32_t w[16];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -1158,14 +1202,16 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     csx[g2] += vx[0];
                     csy[g2] += vy[0];
                 }
-                warp_reduce_scatter32(v, lane);
-                cs[g2] += v[0];
+                if (!CRV_B2_MMA_CS || a.first) {   // bias sums on the CUDA cores (else: tensor cores)
+                    warp_reduce_scatter32(v, lane);
+                    cs[g2] += v[0];
+                }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
                 if (warp == 2) BTRACE(kk * 16 + 6);
-                mbar_arrive(&xempty[b]);
+                if (!CRV_B2_MMA_CS) mbar_arrive(&xempty[b]);
 #if !CRV_B2_EARLY_T
                 mbar_arrive(&tempty[tb]);
 #endif
@@ -1236,6 +1282,26 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 }
             }
         }
+#if CRV_B2_MMA_CS
+        // 1^T Delta_out for the own output-feature half: every TMEM row holds the same sums
+        if (q == 0) {
+            float v[32];
+#pragma unroll 1
+            for (int c32 = wq * (128 / EWQ); c32 < (wq + 1) * (128 / EWQ); c32 += 32) {
+                if (nk > 0) {
+                    tmem_ld32(tm_c + t_lane + (uint32_t)c32, v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+                if (lane == 0) {
+                    float *pc = a.part_cb + (size_t)pair * WP + rank * 128 + c32;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) pc[e] = v[e];
+                }
+            }
+        }
+#endif
         // dW^T (rows i local = TMEM lanes, columns o) -> part_dw[pair][o][i], coalesced over i
         float *pw = a.part_dw + (size_t)pair * WP * WP + rank * 128 + row;
 #pragma unroll 1
@@ -1284,7 +1350,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 constexpr int BC_RS = CRV_BC_RS;   // global ring slots (tiles) per stage boundary
 template <int WP>
 struct BC {
-    static constexpr uint32_t SMEM = B2<WP>::SMEM + 256;   // + the all-ones core matrix
+    static constexpr uint32_t SMEM = B2<WP>::SMEM;   // includes the all-ones core matrix
 };
 struct BwdcArgs {
     int N, ntiles, nclus, S, g0;
@@ -1300,15 +1366,6 @@ struct BwdcArgs {
     long long *trace;     // debug timeline: CTAs 0..7 (cluster 0), 512 slots each; nullptr normally
 };
 #define CTRACE(slot) do { if (a.trace && blockIdx.x < 8 && (slot) < 1024) a.trace[blockIdx.x * 1024 + (slot)] = clock64(); } while (0)
-
-__device__ __forceinline__ uint64_t sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;
-}
 
 template <int WP>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
@@ -1881,7 +1938,8 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     b.off_dx = up64(b.off_ob + (long)b.grid_ob * (2 * WP + 1));
     b.off_dw = up64(b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP);
     b.off_cb = up64(b.off_dw + (long)(G > 0 ? G * b.npairs : 1) * WP * WP);
-    const long ptotal = b.off_cb + (b.chain ? (long)G * b.npairs * WP : 0);
+    b.cb_bias = WP >= 128 && (b.chain || CRV_B2_MMA_CS);   // hidden biases from the tensor-core column sums
+    const long ptotal = b.off_cb + (b.cb_bias ? (long)(G > 0 ? G : 1) * b.npairs * WP : 0);
     if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
         !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
         !al((void **)&b.Wop, (WP + 1) * 4) || !al((void **)&b.act, actn * 2) || !al((void **)&b.delta, actn * 2) ||
@@ -1910,7 +1968,7 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         }
         // bias of theta layer l <-> Delta_{l+1}: from out_bwd (l = L-1) or dx(g = l); with the chain,
         // layers l >= 1 from the tensor-core sums 1^T Delta_out of GEMM l-1
-        if (b.chain && l >= 1)
+        if (b.cb_bias && l >= 1)
             job(b.off_cb + (long)(l - 1) * b.npairs * WP, net.boff[l], wout, b.npairs, WP, 0, 1, 1);
         else if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1);
         else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1);
@@ -2100,7 +2158,8 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
                        b.gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
-                       b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr};
+                       b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
+                       b.partial + b.off_cb + (long)g * b.npairs * WP};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");

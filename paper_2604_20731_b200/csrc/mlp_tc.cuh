@@ -35,6 +35,7 @@ struct TcBufs {
     bool wside[CRV_MAX_LAYERS] = {};       // ... reduced on the side stream (else inside jobs[0, njobs_deep))
     int nsm = 148;
     int chain = 0, chain_S = 0;            // backward chain (k_tc_bwdc): on/off, stages per cluster
+    int cb_bias = 0;                       // hidden-layer bias gradients from the 1^T Delta partials (off_cb)
     __half *ring = nullptr;                // its per-cluster Delta rings between stages
     cudaStream_t side = nullptr;           // side stream of the per-layer weight reductions
     cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr;
