@@ -89,6 +89,10 @@ struct FwdArgs {
 #ifndef CRV_FWD_NSPLIT
 #define CRV_FWD_NSPLIT 1     // last K chunk of each GEMM issued and committed in two N halves
 #endif
+#ifndef CRV_FWD_NQ
+#define CRV_FWD_NQ 2         // N-parts of the last K chunk, each committed on its own barrier
+#endif
+constexpr int NQ = CRV_FWD_NQ;
 #ifndef CRV_FWD_MMA_SLEEP
 #define CRV_FWD_MMA_SLEEP 1  // MMA-issuer waits suspend (try_wait with a time hint) instead of polling
 #endif
@@ -141,8 +145,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
     uint64_t *w_full = bars, *w_empty = bars + NST_W;
     uint64_t *a_full = bars + 2 * NST_W;          // [KC]
-    uint64_t *acc_full = a_full + KC;             // [2 accumulators][2 N-halves]
-    uint32_t *tmem_slot = (uint32_t *)(acc_full + 4);
+    uint64_t *acc_full = a_full + KC;             // [2 accumulators][NQ N-parts]
+    uint32_t *tmem_slot = (uint32_t *)(acc_full + 2 * NQ);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             mbar_init(&w_empty[s], 1);
         }
         for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], FWD_EPI_WARPS);
-        for (int i = 0; i < 4; ++i) mbar_init(&acc_full[i], 1);
+        for (int i = 0; i < 2 * NQ; ++i) mbar_init(&acc_full[i], 1);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 2 * WP);
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
         // ---------------- MMA issuer (one thread)
         if (lane == 0 && a.G > 0) {
             constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
-            constexpr uint32_t idesc_h = idesc_f16(128, WP / 2, 0, 0);
+            constexpr uint32_t idesc_h = idesc_f16(128, WP / NQ, 0, 0);
             int stage = 0;
             uint32_t ph = 0, aph = 0;
             int gi = 0;   // running GEMM counter -> accumulator gi & 1
@@ -225,8 +229,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                                 mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
                                 mma_f16(acc, dl, bd, idesc, 1u);
                             }
-                            mma_commit(&acc_full[(gi & 1) * 2]);
-                            mma_commit(&acc_full[(gi & 1) * 2 + 1]);
+                            for (int hh = 0; hh < NQ; ++hh) mma_commit(&acc_full[(gi & 1) * NQ + hh]);
                         } else {
                             // last K chunk in two N halves, each committed on its own barrier: the
                             // next epilogue starts on output features [0, WP/2) while the MMAs for
@@ -235,16 +238,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                             // before the epilogue overwrites A_hi
                             bulk_wait_read0();
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
+                            for (int hh = 0; hh < NQ; ++hh) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk) {
-                                    uint64_t bd = sdesc_sw128(wr + stage * WBLK + hh * (WP / 2) * 128 + kk * 32, 16, 1024);
+                                    uint64_t bd = sdesc_sw128(wr + stage * WBLK + hh * (WP / NQ) * 128 + kk * 32, 16, 1024);
                                     uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
                                     uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                    mma_f16(acc + hh * (WP / 2), dh, bd, idesc_h, (c | kk) != 0);
-                                    mma_f16(acc + hh * (WP / 2), dl, bd, idesc_h, 1u);
+                                    mma_f16(acc + hh * (WP / NQ), dh, bd, idesc_h, (c | kk) != 0);
+                                    mma_f16(acc + hh * (WP / NQ), dl, bd, idesc_h, 1u);
                                 }
-                                mma_commit(&acc_full[(gi & 1) * 2 + hh]);
+                                mma_commit(&acc_full[(gi & 1) * NQ + hh]);
                             }
                         }
                         FTRACE(2048 + (gi * KC + c) * 4 + 2);
@@ -287,18 +290,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             for (int layer = 1; layer <= a.L; ++layer) {
                 const bool last = layer == a.L;
                 uint32_t acc = 0;
-                int ab = 0;          // acc_full barrier pair of this layer's accumulator
-                bool got1 = true;    // output half [WP/2, WP) available
+                int ab = 0;          // first acc_full barrier of this layer's accumulator
+                uint32_t got = ~0u;  // bit p: output part [p WP/NQ, (p+1) WP/NQ) available
                 if (layer > 1) {
                     const int ai = gi & 1;
-                    ab = ai * 2;
+                    ab = ai * NQ;
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 0);
                     FWD_EPI_WAIT(&acc_full[ab], (acc_ph >> ab) & 1u);
                     if (warp == 2 && lane == 0) FTRACE(gi * 16 + 1);
                     if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1)) * 16 + (warp - 2));
                     acc_ph ^= 1u << ab;
                     acc = (uint32_t)(ai * WP);
-                    got1 = false;
+                    got = 1u;
                     ++gi;
                     tc_fence_after();
                 }
@@ -310,11 +313,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 // issues no global stores there and its fence.proxy.async (a MEMBAR.ALL.CTA) does
                 // not wait on any; the last layer stores t_hi from registers.
                 uint32_t rbuf[16];
-                auto need_half1 = [&](int col) {
-                    if (col >= WP / 2 && !got1) {
-                        FWD_EPI_WAIT(&acc_full[ab + 1], (acc_ph >> (ab + 1)) & 1u);
-                        acc_ph ^= 1u << (ab + 1);
-                        got1 = true;
+                auto need_half1 = [&](int col) {   // wait for the N-part holding column col
+                    const int pp = col / (WP / NQ);
+                    if (!((got >> pp) & 1u)) {
+                        for (int q2 = 1; q2 <= pp; ++q2)
+                            if (!((got >> q2) & 1u)) {
+                                FWD_EPI_WAIT(&acc_full[ab + q2], (acc_ph >> (ab + q2)) & 1u);
+                                acc_ph ^= 1u << (ab + q2);
+                                got |= 1u << q2;
+                            }
                         tc_fence_after();
                     }
                 };
