@@ -17,6 +17,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "crvpinn_oracle.c")
+_SRC_IGA = os.path.join(_HERE, "iga_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 MOBILITY_RATIO = 25.35 / 3.95   # Table 1
@@ -25,8 +26,9 @@ DENSITY_RATIO = 479.0 / 1045.0   # rho_g / rho_w, Table 1
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain C, OpenMP)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+    if (force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
+            or os.path.getmtime(_LIB) < os.path.getmtime(_SRC_IGA)):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, _SRC_IGA, "-lm"])
     return _LIB
 
 
@@ -71,6 +73,23 @@ def lib():
         L.orc_train.restype = ctypes.c_int
         L.orc_train.argtypes = [P, ctypes.c_int, D]
         L.orc_max_threads.restype = ctypes.c_int
+        # IGA-ADS saturation step (iga_oracle.c)
+        L.iga_create.restype = P
+        L.iga_create.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.iga_destroy.argtypes = [P]
+        L.iga_num_basis.restype = ctypes.c_int
+        L.iga_num_basis.argtypes = [P]
+        L.iga_mass_1d.argtypes = [P, D]
+        L.iga_gauss.argtypes = [P, D, D]
+        L.iga_basis.restype = ctypes.c_int
+        L.iga_basis.argtypes = [P, ctypes.c_double, D, D]
+        L.iga_quad_points.argtypes = [P, D]
+        L.iga_kron_solve.argtypes = [P, D, D]
+        L.iga_load.argtypes = [P, D, D]
+        L.iga_project.argtypes = [P, D, D]
+        L.iga_eval.argtypes = [P, D, ctypes.c_long, D, D, D]
+        L.iga_saturation_step.argtypes = [P, D, D, D, D, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_double, D]
         _lib = L
     return _lib
 
@@ -224,3 +243,79 @@ class Oracle:
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+class IgaOracle:
+    """Tensor-product B-spline space of degree r on [0,1]^2 with ne elements per axis (iga_oracle.c):
+    the IGA-ADS saturation step of SURVEY.md §8(f) f3, fp64. Coefficient matrices are [l][k]
+    (row = y basis index, column = x basis index), nb = ne + r per axis."""
+
+    def __init__(self, ne: int, degree: int = 2):
+        self.ne, self.r = int(ne), int(degree)
+        self._h = lib().iga_create(self.ne, self.r)
+        if not self._h:
+            raise ValueError("iga_create: need ne >= 1 and 1 <= degree <= 8")
+        self.nb = int(lib().iga_num_basis(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().iga_destroy(self._h)
+            self._h = None
+
+    def mass_1d(self) -> np.ndarray:
+        out = np.empty((self.nb, self.nb))
+        lib().iga_mass_1d(self._h, _dp(out))
+        return out
+
+    def gauss(self):
+        x, w = np.empty(self.r + 1), np.empty(self.r + 1)
+        lib().iga_gauss(self._h, _dp(x), _dp(w))
+        return x, w
+
+    def basis(self, x: float):
+        val, der = np.empty(self.r + 1), np.empty(self.r + 1)
+        i0 = lib().iga_basis(self._h, float(x), _dp(val), _dp(der))
+        return int(i0), val, der
+
+    def quad_points(self) -> np.ndarray:
+        m = self.ne * (self.r + 1)
+        out = np.empty((m * m, 2))
+        lib().iga_quad_points(self._h, _dp(out))
+        return out
+
+    def kron_solve(self, L) -> np.ndarray:
+        L = np.ascontiguousarray(L, dtype=np.float64).reshape(self.nb, self.nb)
+        out = np.empty_like(L)
+        lib().iga_kron_solve(self._h, _dp(L), _dp(out))
+        return out
+
+    def load(self, fq) -> np.ndarray:
+        fq = np.ascontiguousarray(fq, dtype=np.float64).reshape(-1)
+        out = np.empty((self.nb, self.nb))
+        lib().iga_load(self._h, _dp(fq), _dp(out))
+        return out
+
+    def project(self, fq) -> np.ndarray:
+        fq = np.ascontiguousarray(fq, dtype=np.float64).reshape(-1)
+        out = np.empty((self.nb, self.nb))
+        lib().iga_project(self._h, _dp(fq), _dp(out))
+        return out
+
+    def eval(self, C, xy, grad: bool = False):
+        C = np.ascontiguousarray(C, dtype=np.float64).reshape(self.nb, self.nb)
+        xy = np.ascontiguousarray(np.asarray(xy, dtype=np.float64).reshape(-1, 2))
+        val = np.empty(xy.shape[0])
+        g = np.empty((xy.shape[0], 2)) if grad else None
+        lib().iga_eval(self._h, _dp(C), int(xy.shape[0]), _dp(xy), _dp(val), None if g is None else _dp(g))
+        return (val, g) if grad else val
+
+    def saturation_step(self, S, P, K, q, tau, phi=1.0, mobility=MOBILITY_RATIO, density_ratio=DENSITY_RATIO,
+                        gravity=0.0) -> np.ndarray:
+        S = np.ascontiguousarray(S, dtype=np.float64).reshape(self.nb, self.nb)
+        P = np.ascontiguousarray(P, dtype=np.float64).reshape(self.nb, self.nb)
+        K = np.ascontiguousarray(K, dtype=np.float64).reshape(self.ne, self.ne)
+        q = np.ascontiguousarray(q, dtype=np.float64).reshape(self.ne, self.ne)
+        out = np.empty((self.nb, self.nb))
+        lib().iga_saturation_step(self._h, _dp(S), _dp(P), _dp(K), _dp(q), float(tau), float(phi), float(mobility),
+                                  float(density_ratio), float(gravity), _dp(out))
+        return out

@@ -589,3 +589,111 @@ def test_P16_direct_solve_manufactured_polynomial():
     ustar = x * (1 - x) * y * (1 - y)
     # f is rounded to fp32 on input: the solution error is that rounding propagated (~1e-8 rel)
     np.testing.assert_allclose(u, ustar, rtol=0, atol=1e-8 * ustar.max())
+
+
+# --------------------------------------------------------------------------- P17-P19: IGA-ADS saturation step (f3)
+def test_P17_spline_space_basis_quadrature_mass():
+    """B-splines of degree r (Eq. 11): partition of unity, the cardinal quadratic at an interior element
+    midpoint (1/8, 3/4, 1/8 by hand), open-knot interpolation at x = 0; the Gauss rule integrates x^k
+    exactly for k <= 2r + 1; the mass matrix (Eq. 14) sums to 1, has bandwidth r, and for degree-1 hats
+    on 2 elements equals the hand integrals [[1/6, 1/12, 0], [1/12, 1/3, 1/12], [0, 1/12, 1/6]]."""
+    rng = np.random.default_rng(17)
+    for ne, r in [(5, 1), (8, 2), (7, 3)]:
+        o = oracle.IgaOracle(ne, r)
+        assert o.nb == ne + r
+        for x in rng.uniform(0, 1, 200):
+            i0, v, d = o.basis(x)
+            assert 0 <= i0 <= o.nb - r - 1 and np.all(v >= -1e-15)
+            assert abs(v.sum() - 1) <= 1e-13 and abs(d.sum()) <= 1e-10
+        i0, v, _ = o.basis(0.0)
+        assert i0 == 0 and v[0] == 1.0 and np.all(v[1:] == 0)
+        gx, gw = o.gauss()
+        for k in range(2 * r + 2):
+            assert abs(np.sum(gw * gx ** k) - 1.0 / (k + 1)) <= 1e-14
+        M = o.mass_1d()
+        assert abs(M.sum() - 1.0) <= 1e-13
+        i, k = np.indices(M.shape)
+        assert np.all(M[np.abs(i - k) > r] == 0.0)
+    _, v, d = oracle.IgaOracle(8, 2).basis(3.5 / 8)
+    np.testing.assert_allclose(v, [0.125, 0.75, 0.125], atol=1e-15)
+    np.testing.assert_allclose(oracle.IgaOracle(2, 1).mass_1d(),
+                               [[1 / 6, 1 / 12, 0], [1 / 12, 1 / 3, 1 / 12], [0, 1 / 12, 1 / 6]], atol=1e-15)
+
+
+def test_P18_kronecker_solve_and_projection():
+    """M = M^x (x) M^y (Eq. 14): the directional solves equal a dense solve of np.kron(M, M); a
+    constructed load M C0 M recovers C0; the L2 projection reproduces constants and x^2 + y^2 in the
+    quadratic space, preserves the integral, and eval's gradient matches central differences."""
+    rng = np.random.default_rng(18)
+    o = oracle.IgaOracle(4, 2)
+    M = o.mass_1d()
+    L = rng.standard_normal((o.nb, o.nb))
+    C = o.kron_solve(L)
+    x = np.linalg.solve(np.kron(M, M), L.reshape(-1))
+    np.testing.assert_allclose(C.reshape(-1), x, rtol=1e-10, atol=1e-10)
+    C0 = rng.standard_normal((o.nb, o.nb))
+    np.testing.assert_allclose(o.kron_solve(M @ C0 @ M), C0, atol=1e-9)
+    o = oracle.IgaOracle(16, 2)
+    q = o.quad_points()
+    np.testing.assert_allclose(o.project(np.ones(len(q))), 1.0, atol=1e-12)
+    f = q[:, 0] ** 2 + q[:, 1] ** 2
+    C = o.project(f)
+    pts = rng.uniform(0, 1, (100, 2))
+    np.testing.assert_allclose(o.eval(C, pts), pts[:, 0] ** 2 + pts[:, 1] ** 2, atol=1e-12)
+    g = np.sin(np.pi * q[:, 0]) * np.sin(np.pi * q[:, 1])
+    Cg = o.project(g)
+    m1 = o.mass_1d().sum(axis=0)                      # int B_k dx
+    assert abs(m1 @ Cg @ m1 - 4 / np.pi ** 2) <= 1e-6  # = int f (projection tested with v = 1)
+    val, grad = o.eval(Cg, pts, grad=True)
+    e = 1e-6
+    fdx = (o.eval(Cg, pts + [e, 0]) - o.eval(Cg, pts - [e, 0])) / (2 * e)
+    fdy = (o.eval(Cg, pts + [0, e]) - o.eval(Cg, pts - [0, e])) / (2 * e)
+    np.testing.assert_allclose(grad[:, 0], fdx, rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(grad[:, 1], fdy, rtol=1e-5, atol=1e-7)
+
+
+def _blob(o, cx=0.5, cy=0.4, w=0.1):
+    q = o.quad_points()
+    C = o.project(np.exp(-((q[:, 0] - cx) ** 2 + (q[:, 1] - cy) ** 2) / (2 * w * w)))
+    C[0, :] = C[-1, :] = C[:, 0] = C[:, -1] = 0.0
+    return C
+
+
+def test_P19_saturation_step_identities_and_source():
+    """Eq. 10: tau = 0, or grad p = 0 with no gravity and no source, is the identity on spline data
+    with zero boundary coefficients; a pure source adds exactly the projection of (tau/phi) q."""
+    o = oracle.IgaOracle(16, 2)
+    S = _blob(o)
+    ne = o.ne
+    K = np.random.default_rng(19).uniform(0.5, 2.0, (ne, ne))
+    P = np.random.default_rng(20).standard_normal((o.nb, o.nb))
+    np.testing.assert_allclose(o.saturation_step(S, P, K, np.zeros((ne, ne)), tau=0.0, gravity=1.0), S, atol=1e-12)
+    np.testing.assert_allclose(o.saturation_step(S, np.zeros_like(P), K, np.zeros((ne, ne)), tau=0.3), S, atol=1e-12)
+    q = np.zeros((ne, ne))
+    q[6:10, 6:10] = 2.0
+    tau, phi = 0.05, 0.4
+    d = o.saturation_step(np.zeros_like(S), np.zeros_like(P), K, q, tau=tau, phi=phi)
+    qq = o.quad_points()
+    qf = q[np.minimum((qq[:, 1] * ne).astype(int), ne - 1), np.minimum((qq[:, 0] * ne).astype(int), ne - 1)]
+    ref = o.project(tau / phi * qf)
+    ref[0, :] = ref[-1, :] = ref[:, 0] = ref[:, -1] = 0.0
+    np.testing.assert_allclose(d, ref, atol=1e-12)
+
+
+def test_P19_saturation_step_buoyancy_and_mass():
+    """Hydrostatic water pressure p = -Gr y (grad p = rho_w g, R23 units) and K = 1: the gas flux is
+    M S K Gr (1 - rho_g/rho_w) upward, so the blob's centroid rises (the sign that reading R24 fixes;
+    Eq. 9 as printed would make it sink) while the gas mass is conserved (interior blob, q = 0)."""
+    o = oracle.IgaOracle(32, 2)
+    S = _blob(o, cy=0.4)
+    q = o.quad_points()
+    Gr = 2.0
+    P = o.project(-Gr * q[:, 1])
+    ne = o.ne
+    S1 = o.saturation_step(S, P, np.ones((ne, ne)), np.zeros((ne, ne)), tau=2e-3, gravity=Gr)
+    g = np.stack(np.meshgrid(np.linspace(0, 1, 201), np.linspace(0, 1, 201)), -1).reshape(-1, 2)
+    s0, s1 = o.eval(S, g), o.eval(S1, g)
+    cy0, cy1 = (s0 * g[:, 1]).sum() / s0.sum(), (s1 * g[:, 1]).sum() / s1.sum()
+    assert cy1 > cy0 + 1e-4, (cy0, cy1)
+    m1 = o.mass_1d().sum(axis=0)
+    assert abs(m1 @ S1 @ m1 - m1 @ S @ m1) <= 1e-4 * (m1 @ S @ m1)   # blob tails reach the zeroed boundary
