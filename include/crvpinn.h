@@ -169,6 +169,48 @@ const char *crvpinn_last_error(const crvpinn_ctx *ctx);   /* ctx may be NULL (gl
 
 void crvpinn_destroy(crvpinn_ctx *ctx);
 
+/* ========================================================================== IGA-ADS (f3)
+ * the explicit saturation step of IGA-ADS on the GPU (§3-§4), the
+ * second half of the hybrid loop (§6 step 5 / §7). A crvpinn_iga is one tensor-product spline
+ * space on [0,1]^2: B-splines of degree r (C^{r-1}, Eq. 11) on open uniform
+ * knots with ne elements per axis, nb = ne + r functions per axis, Gauss-Legendre with r+1 points
+ * per element and axis (reading R27). Coefficient matrices are host float32 [nb][nb] indexed
+ * [l][k] (row = y basis index, column = x basis index); element fields [ne][ne] are [ey][ex].
+ * All calls are synchronous, take host buffers and return CRVPINN_* codes. */
+typedef struct crvpinn_iga crvpinn_iga;
+
+/* ne in [1, 8192], 1 <= degree <= 6. EINVAL on bad sizes, ECUDA without a device. */
+int crvpinn_iga_create(crvpinn_iga **out, int n_elements, int degree, int device);
+int crvpinn_iga_num_basis(const crvpinn_iga *g);            /* nb (per axis) */
+long crvpinn_iga_num_quad_points(const crvpinn_iga *g);     /* (ne (r+1))^2 */
+
+/* Tensor Gauss points, x fastest: xy[2p], xy[2p+1] for p = (ey(r+1)+qy) ne(r+1) + ex(r+1) + qx. */
+int crvpinn_iga_quad_points(crvpinn_iga *g, float *xy);
+
+/* Isogeometric L2 projection (Eq. 12-14): coef = (M^x (x) M^y)^-1 L, L_kl = (f, B_k B_l) by the
+ * tensor Gauss rule from f's values fq at the quadrature points (order of crvpinn_iga_quad_points;
+ * e.g. the CRVPINN pressure from crvpinn_eval_points, §6 step 4). The mass solve runs direction by
+ * direction with banded LDL^T factors (bandwidth r; the paper's Thomas algorithm). */
+int crvpinn_iga_project(crvpinn_iga *g, const float *fq, float *coef);
+
+/* One explicit step of Eq. 10 (readings R24-R26):
+ *   (S_out, v) = (S, v) + (tau/phi) ( -M S K (grad p . grad v + r Gr v_y) + q v )  for all v,
+ * then the boundary coefficients of S_out are set to 0 (zero Dirichlet saturation).
+ * S, P: coefficients of S^n and p^n; K_elem, q_elem: per-element permeability and gas source;
+ * M = mobility_ratio (mu_w/mu_g), r = density_ratio (rho_g/rho_w), Gr = gravity (R23). EINVAL:
+ * tau < 0, phi <= 0, non-finite parameters or null pointers. */
+int crvpinn_iga_saturation_step(crvpinn_iga *g, const float *S, const float *P, const float *K_elem,
+                                const float *q_elem, double tau, double phi, double mobility_ratio,
+                                double density_ratio, double gravity, float *S_out);
+
+/* Field value (and gradient, nullable: [n][2]) of coef at n points (clamped to [0,1]^2), e.g. the
+ * saturation at the CRVPINN collocation lattice (§6 step 7). */
+int crvpinn_iga_eval(crvpinn_iga *g, const float *coef, long n, const float *xy, float *val, float *grad);
+
+double crvpinn_iga_last_ms(const crvpinn_iga *g);   /* device time of the last project / step (ms) */
+const char *crvpinn_iga_last_error(const crvpinn_iga *g);
+void crvpinn_iga_destroy(crvpinn_iga *g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,9 @@ EXPORTS = [
     "crvpinn_num_params", "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
     "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter", "crvpinn_stream",
     "crvpinn_last_error", "crvpinn_destroy",
+    "crvpinn_iga_create", "crvpinn_iga_num_basis", "crvpinn_iga_num_quad_points", "crvpinn_iga_quad_points",
+    "crvpinn_iga_project", "crvpinn_iga_saturation_step", "crvpinn_iga_eval", "crvpinn_iga_last_ms",
+    "crvpinn_iga_last_error", "crvpinn_iga_destroy",
 ]
 
 
@@ -87,6 +90,24 @@ def load(path: str = LIB_PATH):
                  "crvpinn_get_intermediates",
                  "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
                  "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter"]:
+        getattr(L, name).restype = I
+    L.crvpinn_iga_create.argtypes = [ctypes.POINTER(P), I, I, I]
+    L.crvpinn_iga_create.restype = I
+    L.crvpinn_iga_num_basis.argtypes = [P]
+    L.crvpinn_iga_num_basis.restype = I
+    L.crvpinn_iga_num_quad_points.argtypes = [P]
+    L.crvpinn_iga_num_quad_points.restype = ctypes.c_long
+    L.crvpinn_iga_quad_points.argtypes = [P, F]
+    L.crvpinn_iga_project.argtypes = [P, F, F]
+    L.crvpinn_iga_saturation_step.argtypes = [P, F, F, F, F, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_double, F]
+    L.crvpinn_iga_eval.argtypes = [P, F, ctypes.c_long, F, F, F]
+    L.crvpinn_iga_last_ms.argtypes = [P]
+    L.crvpinn_iga_last_ms.restype = ctypes.c_double
+    L.crvpinn_iga_last_error.argtypes = [P]
+    L.crvpinn_iga_last_error.restype = ctypes.c_char_p
+    L.crvpinn_iga_destroy.argtypes = [P]
+    for name in ["crvpinn_iga_quad_points", "crvpinn_iga_project", "crvpinn_iga_saturation_step", "crvpinn_iga_eval"]:
         getattr(L, name).restype = I
     _lib = L
     return L
@@ -241,3 +262,67 @@ class Crvpinn:
     @property
     def stream(self) -> int:
         return int(load().crvpinn_stream(self._h) or 0)
+
+
+class Iga:
+    """Tensor-product B-spline space on [0,1]^2 on the GPU (crvpinn_iga): the IGA-ADS saturation step
+    (SURVEY.md §8(f) f3). Coefficients are (nb, nb) float32 arrays indexed [l][k] (row = y)."""
+
+    def __init__(self, n_elements: int, degree: int = 2, device: int = 0):
+        L = load()
+        h = ctypes.c_void_p()
+        rc = L.crvpinn_iga_create(ctypes.byref(h), int(n_elements), int(degree), int(device))
+        if rc != 0:
+            raise CrvpinnError(rc, "crvpinn_iga_create failed")
+        self._h = h
+        self.ne, self.r = int(n_elements), int(degree)
+        self.nb = int(L.crvpinn_iga_num_basis(h))
+        self.nq = int(L.crvpinn_iga_num_quad_points(h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            if load is None:
+                return
+            load().crvpinn_iga_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _check(self, rc):
+        if rc != 0:
+            raise CrvpinnError(rc, load().crvpinn_iga_last_error(self._h).decode())
+
+    def quad_points(self) -> np.ndarray:
+        out = np.empty((self.nq, 2), dtype=np.float32)
+        self._check(load().crvpinn_iga_quad_points(self._h, _fp(out)))
+        return out
+
+    def project(self, fq) -> np.ndarray:
+        fq = _f32(fq, self.nq)
+        out = np.empty((self.nb, self.nb), dtype=np.float32)
+        self._check(load().crvpinn_iga_project(self._h, _fp(fq), _fp(out)))
+        return out
+
+    def saturation_step(self, S, P, K_elem, q_elem, tau: float, phi: float = 1.0, mobility_ratio: float = 25.35 / 3.95,
+                        density_ratio: float = 479.0 / 1045.0, gravity: float = 0.0) -> np.ndarray:
+        n2, e2 = self.nb * self.nb, self.ne * self.ne
+        S, P, K, q = _f32(S, n2), _f32(P, n2), _f32(K_elem, e2), _f32(q_elem, e2)
+        out = np.empty((self.nb, self.nb), dtype=np.float32)
+        self._check(load().crvpinn_iga_saturation_step(self._h, _fp(S), _fp(P), _fp(K), _fp(q), float(tau), float(phi),
+                                                       float(mobility_ratio), float(density_ratio), float(gravity),
+                                                       _fp(out)))
+        return out
+
+    def eval(self, coef, xy, grad: bool = False):
+        C = _f32(coef, self.nb * self.nb)
+        xy = np.ascontiguousarray(np.asarray(xy, dtype=np.float32).reshape(-1, 2))
+        val = np.empty(xy.shape[0], dtype=np.float32)
+        g = np.empty((xy.shape[0], 2), dtype=np.float32) if grad else None
+        if xy.shape[0]:
+            self._check(load().crvpinn_iga_eval(self._h, _fp(C), int(xy.shape[0]), _fp(xy), _fp(val),
+                                                None if g is None else _fp(g)))
+        return (val, g) if grad else val
+
+    @property
+    def last_ms(self) -> float:
+        return float(load().crvpinn_iga_last_ms(self._h))

@@ -1,0 +1,554 @@
+// iga.cu -- SURVEY.md §8(f) f3: the IGA-ADS explicit saturation step on the GPU (§3-§4).
+//
+// Tensor-product B-splines of degree r (C^{r-1}, open uniform knots, ne elements per axis,
+// nb = ne + r functions per axis; Eq. 11), Gauss-Legendre with r+1 points per element and axis
+// (reading R27). One step of Eq. 10 (readings R24-R26):
+//   (S^{n+1}, v) = (S^n, v) + (tau/phi) ( -M S^n K (grad p . grad v + r Gr v_y) + q v )   for all v,
+//   M = M^x (x) M^y (Eq. 14)  =>  S^{n+1} = M^-1 (load), solved direction by direction,
+// then the boundary coefficients are set to 0 (zero Dirichlet saturation).
+// Kernels:
+//   k_iga_qp      one thread per quadrature point: S^n, grad p^n from the local (r+1)^2 coefficient
+//                 stencil; the integrand's weights for v, v_x, v_y (or f w for a plain projection)
+//   k_iga_gather  one thread per test function (k,l): sums its (r+1)^2 elements x (r+1)^2 points in a
+//                 fixed order (deterministic, no atomics) -> the load matrix L[l][k]
+//   k_iga_band    one thread per column (fp64): (LDL^T)^-1 along the row index with the precomputed band
+//                 factors of the 1D mass matrix (bandwidth r; the paper's "Thomas algorithm",
+//                 PAPER.md:209, generalised to bandwidth r); coalesced across threads
+//   k_iga_transpose, k_iga_dirichlet, k_iga_eval (field value/gradient at arbitrary points)
+// Coefficient matrices are [l][k] (row = y basis index). Host buffers at the C ABI.
+#include "common.cuh"
+#include "../../include/crvpinn.h"
+#include <cmath>
+#include <string>
+#include <vector>
+
+namespace crv {
+namespace {
+
+constexpr int IGA_MAX_R = 6;
+
+struct IgaDev {
+    int ne = 0, r = 0, nb = 0, m = 0;   // m = ne (r+1) quadrature points per axis
+    float *bv = nullptr, *bd = nullptr; // [ne][r+1 points][r+1 functions] values / x-derivatives
+    float *gw = nullptr;                // [m] weights (x quadrature incl. 1/ne), same for y
+    double *lf = nullptr;               // [nb][r] sub-diagonal band of the unit lower factor (row i: L_{i,i-1..i-r})
+    double *dinv = nullptr;             // [nb] 1/D of LDL^T
+    float *qv = nullptr;                // [3][m*m] integrand weights
+    double *A = nullptr, *B = nullptr;  // nb*nb work matrices: the mass solves run in fp64 (the degree-3
+                                        // mass matrix loses ~4 digits to conditioning in fp32)
+    float *outf = nullptr;              // nb*nb fp32 result
+    float *io = nullptr;                // staging for inputs/outputs (grown on demand)
+    size_t io_cap = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    float last_ms = 0.f;
+};
+
+// ---------------------------------------------------------------- host precomputation
+// Gauss-Legendre nodes/weights on [0,1]: Newton on the three-term recurrence of P_m.
+void gauss01(int m, std::vector<double> &x, std::vector<double> &w) {
+    x.assign(m, 0.0);
+    w.assign(m, 0.0);
+    for (int i = 0; i < m; ++i) {
+        double t = std::cos(M_PI * (4.0 * i + 3.0) / (4.0 * m + 2.0));
+        double dp = 1.0;
+        for (int it = 0; it < 64; ++it) {
+            double pm1 = 1.0, p = t;   // P_0, P_1
+            for (int n = 1; n < m; ++n) {
+                const double pn1 = ((2.0 * n + 1.0) * t * p - n * pm1) / (n + 1.0);
+                pm1 = p;
+                p = pn1;
+            }
+            dp = m * (pm1 - t * p) / (1.0 - t * t);   // P_m'
+            const double step = p / dp;
+            t -= step;
+            if (std::fabs(step) < 1e-16) break;
+        }
+        x[m - 1 - i] = 0.5 * (t + 1.0);
+        w[m - 1 - i] = 1.0 / ((1.0 - t * t) * dp * dp);
+    }
+}
+
+// The r+1 non-zero B-splines of degree r at x (uniform open knots, ne elements) and their
+// derivatives, by the triangular de Boor table (left/right differences); returns the first index.
+int bspline_local(int ne, int r, double x, double *val, double *der) {
+    auto knot = [&](int i) { return (double)std::min(std::max(i - r, 0), ne) / ne; };
+    int e = (int)std::floor(x * ne);
+    e = std::min(std::max(e, 0), ne - 1);
+    const int span = e + r;
+    std::vector<double> left(r + 1), right(r + 1);
+    std::vector<std::vector<double>> nd(r + 1, std::vector<double>(r + 1, 0.0));
+    nd[0][0] = 1.0;
+    for (int j = 1; j <= r; ++j) {
+        left[j] = x - knot(span + 1 - j);
+        right[j] = knot(span + j) - x;
+        double saved = 0.0;
+        for (int s = 0; s < j; ++s) {
+            const double den = right[s + 1] + left[j - s];
+            const double tmp = den != 0.0 ? nd[j - 1][s] / den : 0.0;
+            nd[j][s] = saved + right[s + 1] * tmp;
+            saved = left[j - s] * tmp;
+        }
+        nd[j][j] = saved;
+    }
+    for (int a = 0; a <= r; ++a) val[a] = nd[r][a];
+    // derivative: r (N_{i,r-1}/(u_{i+r}-u_i) - N_{i+1,r-1}/(u_{i+r+1}-u_{i+1}))
+    for (int a = 0; a <= r; ++a) {
+        const int i = span - r + a;
+        double d = 0.0;
+        if (a >= 1) {
+            const double den = knot(i + r) - knot(i);
+            if (den > 0.0) d += r * nd[r - 1][a - 1] / den;
+        }
+        if (a <= r - 1) {
+            const double den = knot(i + r + 1) - knot(i + 1);
+            if (den > 0.0) d -= r * nd[r - 1][a] / den;
+        }
+        der[a] = d;
+    }
+    return span - r;
+}
+
+// ---------------------------------------------------------------- kernels
+// mode 0: saturation integrand; mode 1: plain projection (f given at the points)
+__global__ void k_iga_qp(IgaDev g, const float *__restrict__ S, const float *__restrict__ P,
+                         const float *__restrict__ K, const float *__restrict__ q, const float *__restrict__ fq,
+                         int mode, float tau_phi, float mob, float grav_y) {
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long mm = (long)g.m * g.m;
+    if (p >= mm) return;
+    const int R1 = g.r + 1;
+    const int j = (int)(p / g.m), i = (int)(p % g.m);
+    const int ex = i / R1, qx = i % R1, ey = j / R1, qy = j % R1;
+    const float w = g.gw[i] * g.gw[j];
+    if (mode == 1) {
+        g.qv[p] = w * fq[p];
+        g.qv[mm + p] = 0.f;
+        g.qv[2 * mm + p] = 0.f;
+        return;
+    }
+    const float *bvx = g.bv + ((long)ex * R1 + qx) * R1, *bdx = g.bd + ((long)ex * R1 + qx) * R1;
+    const float *bvy = g.bv + ((long)ey * R1 + qy) * R1, *bdy = g.bd + ((long)ey * R1 + qy) * R1;
+    float s = 0.f, px = 0.f, py = 0.f;
+    for (int b = 0; b < R1; ++b) {
+        const float *srow = S + (long)(ey + b) * g.nb + ex, *prow = P + (long)(ey + b) * g.nb + ex;
+        float ss = 0.f, ppx = 0.f, ppy = 0.f;
+        for (int a = 0; a < R1; ++a) {
+            ss = fmaf(srow[a], bvx[a], ss);
+            ppx = fmaf(prow[a], bdx[a], ppx);
+            ppy = fmaf(prow[a], bvx[a], ppy);
+        }
+        s = fmaf(ss, bvy[b], s);
+        px = fmaf(ppx, bvy[b], px);
+        py = fmaf(ppy, bdy[b], py);
+    }
+    const long e = (long)ey * g.ne + ex;
+    const float flux = -tau_phi * mob * s * K[e];
+    g.qv[p] = w * (s + tau_phi * q[e]);
+    g.qv[mm + p] = w * flux * px;
+    g.qv[2 * mm + p] = w * flux * (py + grav_y);
+}
+
+__global__ void k_iga_gather(IgaDev g, double *__restrict__ L) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)g.nb * g.nb) return;
+    const int l = (int)(t / g.nb), k = (int)(t % g.nb);
+    const int R1 = g.r + 1;
+    const long mm = (long)g.m * g.m;
+    double acc = 0.0;
+    for (int ey = max(l - g.r, 0); ey <= min(l, g.ne - 1); ++ey) {
+        const int b = l - ey;
+        for (int qy = 0; qy < R1; ++qy) {
+            const float vy = g.bv[((long)ey * R1 + qy) * R1 + b], dy = g.bd[((long)ey * R1 + qy) * R1 + b];
+            const long row = (long)(ey * R1 + qy) * g.m;
+            for (int ex = max(k - g.r, 0); ex <= min(k, g.ne - 1); ++ex) {
+                const int a = k - ex;
+                for (int qx = 0; qx < R1; ++qx) {
+                    const float vx = g.bv[((long)ex * R1 + qx) * R1 + a], dx = g.bd[((long)ex * R1 + qx) * R1 + a];
+                    const long p = row + ex * R1 + qx;
+                    acc += (double)g.qv[p] * (double)(vx * vy) + (double)g.qv[mm + p] * (double)(dx * vy) +
+                           (double)g.qv[2 * mm + p] * (double)(vx * dy);
+                }
+            }
+        }
+    }
+    L[t] = acc;
+}
+
+// X = M^-1 X along the row index, one thread per column; M = L D L^T with unit lower band L
+__global__ void k_iga_band(IgaDev g, double *__restrict__ X) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.nb) return;
+    const int n = g.nb, r = g.r;
+    for (int i = 0; i < n; ++i) {   // L z = x
+        double v = X[(long)i * n + c];
+        for (int d = 1; d <= r && d <= i; ++d) v = fma(-g.lf[i * r + d - 1], X[(long)(i - d) * n + c], v);
+        X[(long)i * n + c] = v;
+    }
+    for (int i = 0; i < n; ++i) X[(long)i * n + c] *= g.dinv[i];
+    for (int i = n - 1; i >= 0; --i) {   // L^T x = y
+        double v = X[(long)i * n + c];
+        for (int d = 1; d <= r && i + d < n; ++d) v = fma(-g.lf[(i + d) * r + d - 1], X[(long)(i + d) * n + c], v);
+        X[(long)i * n + c] = v;
+    }
+}
+
+__global__ void k_iga_transpose(const double *__restrict__ in, double *__restrict__ out, int n) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int r = by + y, c = bx + threadIdx.x;
+        if (r < n && c < n) tile[y][threadIdx.x] = in[(long)r * n + c];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int r = bx + y, c = by + threadIdx.x;
+        if (r < n && c < n) out[(long)r * n + c] = tile[threadIdx.x][y];
+    }
+}
+
+__global__ void k_iga_dirichlet(double *X, int n) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    X[t] = 0.0;
+    X[(long)(n - 1) * n + t] = 0.0;
+    X[(long)t * n] = 0.0;
+    X[(long)t * n + n - 1] = 0.0;
+}
+
+__global__ void k_iga_to_f32(const double *__restrict__ in, float *__restrict__ out, long n) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = (float)in[t];
+}
+
+// value and gradient of the field C at arbitrary points (device de Boor per point)
+__global__ void k_iga_eval(IgaDev g, const float *__restrict__ C, const float *__restrict__ xy, long npts,
+                           float *__restrict__ val, float *__restrict__ grad) {
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npts) return;
+    const int r = g.r, ne = g.ne;
+    float v[2][IGA_MAX_R + 1], d[2][IGA_MAX_R + 1];
+    int i0[2];
+    for (int ax = 0; ax < 2; ++ax) {
+        const float x = fminf(fmaxf(xy[2 * p + ax], 0.f), 1.f);
+        int e = min(max((int)floorf(x * ne), 0), ne - 1);
+        const int span = e + r;
+        auto knot = [&](int i) { return (float)min(max(i - r, 0), ne) / (float)ne; };
+        float nd[IGA_MAX_R + 1][IGA_MAX_R + 1];
+        float left[IGA_MAX_R + 1], right[IGA_MAX_R + 1];
+        nd[0][0] = 1.f;
+        for (int j = 1; j <= r; ++j) {
+            left[j] = x - knot(span + 1 - j);
+            right[j] = knot(span + j) - x;
+            float saved = 0.f;
+            for (int s = 0; s < j; ++s) {
+                const float den = right[s + 1] + left[j - s];
+                const float tmp = den != 0.f ? nd[j - 1][s] / den : 0.f;
+                nd[j][s] = saved + right[s + 1] * tmp;
+                saved = left[j - s] * tmp;
+            }
+            nd[j][j] = saved;
+        }
+        for (int a = 0; a <= r; ++a) {
+            v[ax][a] = nd[r][a];
+            const int i = span - r + a;
+            float dd = 0.f;
+            if (a >= 1) {
+                const float den = knot(i + r) - knot(i);
+                if (den > 0.f) dd += r * nd[r - 1][a - 1] / den;
+            }
+            if (a <= r - 1) {
+                const float den = knot(i + r + 1) - knot(i + 1);
+                if (den > 0.f) dd -= r * nd[r - 1][a] / den;
+            }
+            d[ax][a] = dd;
+        }
+        i0[ax] = span - r;
+    }
+    float s = 0.f, gx = 0.f, gy = 0.f;
+    for (int b = 0; b <= r; ++b)
+        for (int a = 0; a <= r; ++a) {
+            const float c = C[(long)(i0[1] + b) * g.nb + i0[0] + a];
+            s = fmaf(c, v[0][a] * v[1][b], s);
+            gx = fmaf(c, d[0][a] * v[1][b], gx);
+            gy = fmaf(c, v[0][a] * d[1][b], gy);
+        }
+    val[p] = s;
+    if (grad) {
+        grad[2 * p] = gx;
+        grad[2 * p + 1] = gy;
+    }
+}
+
+// The same solve with a block's 32 columns staged in shared memory: the substitutions are serial in
+// i, so their latency (not bandwidth) bounds them, and shared memory has ~10x less of it than L2
+constexpr int IGA_BAND_COLS = 32;
+__global__ void k_iga_band_smem(IgaDev g, double *__restrict__ X) {
+    extern __shared__ double sx[];   // [nb][IGA_BAND_COLS]
+    const int n = g.nb, r = g.r;
+    const int c0 = blockIdx.x * IGA_BAND_COLS;
+    const int nc = min(IGA_BAND_COLS, n - c0);
+    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
+        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+        sx[e] = cc < nc ? X[(long)i * n + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < IGA_BAND_COLS) {
+        double *col = sx + threadIdx.x;
+        for (int i = 0; i < n; ++i) {   // L z = x
+            double v = col[i * IGA_BAND_COLS];
+            for (int d = 1; d <= r && d <= i; ++d) v = fma(-g.lf[i * r + d - 1], col[(i - d) * IGA_BAND_COLS], v);
+            col[i * IGA_BAND_COLS] = v;
+        }
+        for (int i = 0; i < n; ++i) col[i * IGA_BAND_COLS] *= g.dinv[i];
+        for (int i = n - 1; i >= 0; --i) {   // L^T x = D^-1 z
+            double v = col[i * IGA_BAND_COLS];
+            for (int d = 1; d <= r && i + d < n; ++d)
+                v = fma(-g.lf[(i + d) * r + d - 1], col[(i + d) * IGA_BAND_COLS], v);
+            col[i * IGA_BAND_COLS] = v;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
+        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+        if (cc < nc) X[(long)i * n + c0 + cc] = sx[e];
+    }
+}
+
+// L -> C = M^-1 L M^-1 (both directions), in place in g.A (g.B scratch)
+void kron_solve(IgaDev &g, cudaStream_t s) {
+    const int n = g.nb;
+    const dim3 tb(32, 8), tg((n + 31) / 32, (n + 31) / 32);
+    const size_t smem = sizeof(double) * (size_t)n * IGA_BAND_COLS;
+    if (smem <= 200 * 1024) {
+        static int attr_set = 0;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_iga_band_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr_set = 1;
+        }
+        k_iga_band_smem<<<ceil_div(n, IGA_BAND_COLS), 256, smem, s>>>(g, g.A);   // along l (rows)
+        k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
+        k_iga_band_smem<<<ceil_div(n, IGA_BAND_COLS), 256, smem, s>>>(g, g.B);   // along k
+    } else {   // very large spaces: straight from global memory
+        k_iga_band<<<ceil_div(n, 128), 128, 0, s>>>(g, g.A);
+        k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
+        k_iga_band<<<ceil_div(n, 128), 128, 0, s>>>(g, g.B);
+    }
+    k_iga_transpose<<<tg, tb, 0, s>>>(g.B, g.A, n);
+}
+
+}  // namespace
+}  // namespace crv
+
+// ================================================================ C ABI
+struct crvpinn_iga {
+    crv::IgaDev g;
+    int device = 0;
+    std::string err;
+};
+
+using crv::IgaDev;
+
+static int iga_fail(crvpinn_iga *h, int code, const std::string &m) {
+    if (h) h->err = m;
+    return code;
+}
+#define IGA_CK(call)                                                                      \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) return iga_fail(h, CRVPINN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+static int iga_stage(crvpinn_iga *h, size_t floats) {
+    IgaDev &g = h->g;
+    if (floats <= g.io_cap) return CRVPINN_OK;
+    if (g.io) cudaFree(g.io);
+    g.io = nullptr;
+    g.io_cap = 0;
+    IGA_CK(cudaMalloc(&g.io, sizeof(float) * floats));
+    g.io_cap = floats;
+    return CRVPINN_OK;
+}
+
+extern "C" {
+
+int crvpinn_iga_create(crvpinn_iga **out, int n_elements, int degree, int device) {
+    if (!out) return CRVPINN_EINVAL;
+    *out = nullptr;
+    if (n_elements < 1 || n_elements > 8192 || degree < 1 || degree > crv::IGA_MAX_R) return CRVPINN_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) return CRVPINN_ECUDA;
+    crvpinn_iga *h = new crvpinn_iga();
+    h->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) { delete h; return CRVPINN_ECUDA; }
+    IgaDev &g = h->g;
+    g.ne = n_elements; g.r = degree; g.nb = n_elements + degree; g.m = n_elements * (degree + 1);
+    const int R1 = degree + 1, nb = g.nb;
+    std::vector<double> gx, gw;
+    crv::gauss01(R1, gx, gw);
+    std::vector<float> bv((size_t)g.ne * R1 * R1), bd(bv.size()), w((size_t)g.m);
+    std::vector<double> mass((size_t)nb * (degree + 1), 0.0);   // mass[i][d] = M_{i, i+d}, d = 0..r
+    std::vector<double> val(R1), der(R1);
+    for (int e = 0; e < g.ne; ++e)
+        for (int q = 0; q < R1; ++q) {
+            const double x = (e + gx[q]) / g.ne, wq = gw[q] / g.ne;
+            const int i0 = crv::bspline_local(g.ne, degree, x, val.data(), der.data());
+            for (int a = 0; a < R1; ++a) {
+                bv[((size_t)e * R1 + q) * R1 + a] = (float)val[a];
+                bd[((size_t)e * R1 + q) * R1 + a] = (float)der[a];
+                for (int b = a; b < R1; ++b) mass[(size_t)(i0 + a) * R1 + (b - a)] += wq * val[a] * val[b];
+            }
+            w[(size_t)e * R1 + q] = (float)wq;
+        }
+    // banded LDL^T of the SPD mass matrix, fp64: lf[i][d-1] = L_{i,i-d}
+    std::vector<double> Lb((size_t)nb * degree, 0.0), D(nb, 0.0);
+    for (int i = 0; i < nb; ++i) {
+        for (int d = degree; d >= 1; --d) {   // L_{i,j}, j = i - d
+            const int j = i - d;
+            if (j < 0) continue;
+            double v = mass[(size_t)j * R1 + d];   // M_{j,i}
+            for (int t = 1; t <= degree && j - t >= 0; ++t) {
+                const int dl = i - (j - t);        // L_{i, j-t}
+                if (dl <= degree) v -= Lb[(size_t)i * degree + dl - 1] * Lb[(size_t)j * degree + t - 1] * D[j - t];
+            }
+            Lb[(size_t)i * degree + d - 1] = v / D[j];
+        }
+        double v = mass[(size_t)i * R1 + 0];
+        for (int d = 1; d <= degree && i - d >= 0; ++d) {
+            const double l = Lb[(size_t)i * degree + d - 1];
+            v -= l * l * D[i - d];
+        }
+        D[i] = v;
+    }
+    std::vector<double> lf(Lb), dinv(nb);
+    for (int i = 0; i < nb; ++i) dinv[i] = 1.0 / D[i];
+    const long mm = (long)g.m * g.m;
+    bool ok = cudaMalloc(&g.bv, sizeof(float) * bv.size()) == cudaSuccess &&
+              cudaMalloc(&g.bd, sizeof(float) * bd.size()) == cudaSuccess &&
+              cudaMalloc(&g.gw, sizeof(float) * w.size()) == cudaSuccess &&
+              cudaMalloc(&g.lf, sizeof(double) * (lf.size() ? lf.size() : 1)) == cudaSuccess &&
+              cudaMalloc(&g.dinv, sizeof(double) * nb) == cudaSuccess &&
+              cudaMalloc(&g.qv, sizeof(float) * 3 * mm) == cudaSuccess &&
+              cudaMalloc(&g.A, sizeof(double) * nb * nb) == cudaSuccess &&
+              cudaMalloc(&g.B, sizeof(double) * nb * nb) == cudaSuccess &&
+              cudaMalloc(&g.outf, sizeof(float) * nb * nb) == cudaSuccess &&
+              cudaEventCreate(&g.e0) == cudaSuccess && cudaEventCreate(&g.e1) == cudaSuccess;
+    if (ok)
+        ok = cudaMemcpy(g.bv, bv.data(), sizeof(float) * bv.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.bd, bd.data(), sizeof(float) * bd.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.gw, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.lf, lf.data(), sizeof(double) * lf.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.dinv, dinv.data(), sizeof(double) * nb, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+        crvpinn_iga_destroy(h);
+        return CRVPINN_ENOMEM;
+    }
+    *out = h;
+    return CRVPINN_OK;
+}
+
+int crvpinn_iga_num_basis(const crvpinn_iga *h) { return h ? h->g.nb : 0; }
+
+long crvpinn_iga_num_quad_points(const crvpinn_iga *h) { return h ? (long)h->g.m * h->g.m : 0; }
+
+int crvpinn_iga_quad_points(crvpinn_iga *h, float *xy) {
+    if (!h || !xy) return iga_fail(h, CRVPINN_EINVAL, "null argument");
+    const int R1 = h->g.r + 1;
+    std::vector<double> gx, gw;
+    crv::gauss01(R1, gx, gw);
+    const int m = h->g.m;
+    for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) {
+            const long p = (long)j * m + i;
+            xy[2 * p] = (float)((i / R1 + gx[i % R1]) / h->g.ne);
+            xy[2 * p + 1] = (float)((j / R1 + gx[j % R1]) / h->g.ne);
+        }
+    return CRVPINN_OK;
+}
+
+int crvpinn_iga_project(crvpinn_iga *h, const float *fq, float *coef) {
+    if (!h || !fq || !coef) return iga_fail(h, CRVPINN_EINVAL, "null argument");
+    IgaDev &g = h->g;
+    IGA_CK(cudaSetDevice(h->device));
+    const long mm = (long)g.m * g.m, n2 = (long)g.nb * g.nb;
+    int rc = iga_stage(h, (size_t)mm);
+    if (rc) return rc;
+    IGA_CK(cudaMemcpy(g.io, fq, sizeof(float) * mm, cudaMemcpyHostToDevice));
+    cudaEventRecord(g.e0, 0);
+    crv::k_iga_qp<<<crv::ceil_div(mm, 256), 256>>>(g, nullptr, nullptr, nullptr, nullptr, g.io, 1, 0.f, 0.f, 0.f);
+    crv::k_iga_gather<<<crv::ceil_div(n2, 256), 256>>>(g, g.A);
+    crv::kron_solve(g, 0);
+    crv::k_iga_to_f32<<<crv::ceil_div(n2, 256), 256>>>(g.A, g.outf, n2);
+    cudaEventRecord(g.e1, 0);
+    IGA_CK(cudaMemcpy(coef, g.outf, sizeof(float) * n2, cudaMemcpyDeviceToHost));
+    IGA_CK(cudaGetLastError());
+    cudaEventElapsedTime(&g.last_ms, g.e0, g.e1);
+    return CRVPINN_OK;
+}
+
+int crvpinn_iga_saturation_step(crvpinn_iga *h, const float *S, const float *P, const float *K_elem,
+                                const float *q_elem, double tau, double phi, double mobility_ratio,
+                                double density_ratio, double gravity, float *S_out) {
+    if (!h || !S || !P || !K_elem || !q_elem || !S_out) return iga_fail(h, CRVPINN_EINVAL, "null argument");
+    if (!(tau >= 0.0) || !(phi > 0.0) || !std::isfinite(mobility_ratio) || !std::isfinite(density_ratio) ||
+        !std::isfinite(gravity))
+        return iga_fail(h, CRVPINN_EINVAL, "need tau >= 0, phi > 0 and finite parameters");
+    IgaDev &g = h->g;
+    IGA_CK(cudaSetDevice(h->device));
+    const long n2 = (long)g.nb * g.nb, ne2 = (long)g.ne * g.ne, mm = (long)g.m * g.m;
+    int rc = iga_stage(h, (size_t)(2 * n2 + 2 * ne2));
+    if (rc) return rc;
+    float *dS = g.io, *dP = g.io + n2, *dK = g.io + 2 * n2, *dq = g.io + 2 * n2 + ne2;
+    IGA_CK(cudaMemcpy(dS, S, sizeof(float) * n2, cudaMemcpyHostToDevice));
+    IGA_CK(cudaMemcpy(dP, P, sizeof(float) * n2, cudaMemcpyHostToDevice));
+    IGA_CK(cudaMemcpy(dK, K_elem, sizeof(float) * ne2, cudaMemcpyHostToDevice));
+    IGA_CK(cudaMemcpy(dq, q_elem, sizeof(float) * ne2, cudaMemcpyHostToDevice));
+    cudaEventRecord(g.e0, 0);
+    crv::k_iga_qp<<<crv::ceil_div(mm, 256), 256>>>(g, dS, dP, dK, dq, nullptr, 0, (float)(tau / phi),
+                                                   (float)mobility_ratio, (float)(density_ratio * gravity));
+    crv::k_iga_gather<<<crv::ceil_div(n2, 256), 256>>>(g, g.A);
+    crv::kron_solve(g, 0);
+    crv::k_iga_dirichlet<<<crv::ceil_div(g.nb, 256), 256>>>(g.A, g.nb);
+    crv::k_iga_to_f32<<<crv::ceil_div(n2, 256), 256>>>(g.A, g.outf, n2);
+    cudaEventRecord(g.e1, 0);
+    IGA_CK(cudaMemcpy(S_out, g.outf, sizeof(float) * n2, cudaMemcpyDeviceToHost));
+    IGA_CK(cudaGetLastError());
+    cudaEventElapsedTime(&g.last_ms, g.e0, g.e1);
+    return CRVPINN_OK;
+}
+
+int crvpinn_iga_eval(crvpinn_iga *h, const float *coef, long n, const float *xy, float *val, float *grad) {
+    if (!h || n < 0) return iga_fail(h, CRVPINN_EINVAL, "bad argument");
+    if (n == 0) return CRVPINN_OK;
+    if (!coef || !xy || !val) return iga_fail(h, CRVPINN_EINVAL, "null argument");
+    IgaDev &g = h->g;
+    IGA_CK(cudaSetDevice(h->device));
+    const long n2 = (long)g.nb * g.nb;
+    int rc = iga_stage(h, (size_t)(n2 + 5 * n));
+    if (rc) return rc;
+    float *dC = g.io, *dxy = g.io + n2, *dv = dxy + 2 * n, *dg = dv + n;
+    IGA_CK(cudaMemcpy(dC, coef, sizeof(float) * n2, cudaMemcpyHostToDevice));
+    IGA_CK(cudaMemcpy(dxy, xy, sizeof(float) * 2 * n, cudaMemcpyHostToDevice));
+    crv::k_iga_eval<<<crv::ceil_div(n, 256), 256>>>(g, dC, dxy, n, dv, grad ? dg : nullptr);
+    IGA_CK(cudaMemcpy(val, dv, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    if (grad) IGA_CK(cudaMemcpy(grad, dg, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost));
+    IGA_CK(cudaGetLastError());
+    return CRVPINN_OK;
+}
+
+double crvpinn_iga_last_ms(const crvpinn_iga *h) { return h ? (double)h->g.last_ms : 0.0; }
+
+const char *crvpinn_iga_last_error(const crvpinn_iga *h) { return h ? h->err.c_str() : ""; }
+
+void crvpinn_iga_destroy(crvpinn_iga *h) {
+    if (!h) return;
+    IgaDev &g = h->g;
+    cudaSetDevice(h->device);
+    void *bufs[] = {g.bv, g.bd, g.gw, g.lf, g.dinv, g.qv, g.A, g.B, g.io, g.outf};
+    for (void *p : bufs)
+        if (p) cudaFree(p);
+    if (g.e0) cudaEventDestroy(g.e0);
+    if (g.e1) cudaEventDestroy(g.e1);
+    delete h;
+}
+
+}  // extern "C"

@@ -402,3 +402,103 @@ def test_direct_solve_edges(crv):
     ustar = c_h * np.sin(np.pi * i / N) * np.sin(np.pi * j / N)
     assert np.max(np.abs(u - ustar.reshape(-1))) <= 1e-5 * ustar.max()
     np.testing.assert_array_equal(g.theta, th)       # the solve leaves the network alone
+
+
+# ------------------------------------------------------------------ f3: IGA-ADS saturation step
+def _iga_pair(crv, ne, r):
+    return crv.Iga(ne, r), oracle.IgaOracle(ne, r)
+
+
+@pytest.mark.parametrize("ne,r", [(8, 1), (16, 2), (37, 2), (20, 3)])
+def test_iga_projection_and_eval_vs_oracle(crv, ne, r):
+    """crvpinn_iga_project / _eval against the fp64 oracle: quadrature points,
+    projected coefficients of a smooth function, exact reproduction of x^2 + y^2 (degree >= 2), and
+    values/gradients at random points."""
+    g, o = _iga_pair(crv, ne, r)
+    assert g.nb == o.nb == ne + r
+    q = g.quad_points()
+    np.testing.assert_allclose(q, o.quad_points(), atol=2e-7)
+    f = (np.sin(3 * q[:, 0]) * np.cos(2 * q[:, 1]) + q[:, 1]).astype(np.float32)
+    C, Co = g.project(f), o.project(f.astype(np.float64))
+    assert np.max(np.abs(C - Co)) <= 1e-5 * np.abs(Co).max()
+    rng = np.random.default_rng(ne)
+    pts = rng.uniform(0, 1, (500, 2)).astype(np.float32)
+    v, gr = g.eval(C, pts, grad=True)
+    vo, gro = o.eval(Co, pts, grad=True)
+    assert np.max(np.abs(v - vo)) <= 1e-5 * np.abs(vo).max()
+    assert np.max(np.abs(gr - gro)) <= 1e-4 * np.abs(gro).max()
+    if r >= 2:
+        C2 = g.project((q[:, 0] ** 2 + q[:, 1] ** 2).astype(np.float32))
+        np.testing.assert_allclose(g.eval(C2, pts), pts[:, 0] ** 2 + pts[:, 1] ** 2, atol=2e-6)
+
+
+@pytest.mark.parametrize("ne,r,Gr", [(16, 2, 0.0), (48, 2, 1.5), (33, 1, 0.7)])
+def test_iga_saturation_step_vs_oracle(crv, ne, r, Gr):
+    """One explicit step of Eq. 10 (readings R24-R26) on the GPU against the oracle, with
+    heterogeneous K, a source patch, a non-trivial pressure and gravity."""
+    g, o = _iga_pair(crv, ne, r)
+    q = g.quad_points().astype(np.float64)
+    S = o.project(np.exp(-((q[:, 0] - 0.5) ** 2 + (q[:, 1] - 0.45) ** 2) / 0.02))
+    S[0, :] = S[-1, :] = S[:, 0] = S[:, -1] = 0.0
+    P = o.project(np.cos(2 * q[:, 0]) * q[:, 1] - Gr * q[:, 1])
+    rng = np.random.default_rng(ne + r)
+    K = np.exp(rng.standard_normal((ne, ne)) * 0.5)
+    src = np.zeros((ne, ne))
+    src[ne // 3:ne // 2, ne // 3:ne // 2] = 1.0
+    args = dict(tau=0.02, phi=0.3, gravity=Gr)
+    S1 = g.saturation_step(S.astype(np.float32), P.astype(np.float32), K.astype(np.float32),
+                           src.astype(np.float32), **args)
+    S1o = o.saturation_step(S.astype(np.float32).astype(np.float64), P.astype(np.float32).astype(np.float64),
+                            K.astype(np.float32).astype(np.float64), src, **args)
+    assert np.max(np.abs(S1 - S1o)) <= 2e-5 * np.abs(S1o).max()
+    assert np.all(S1[0, :] == 0) and np.all(S1[-1, :] == 0) and np.all(S1[:, 0] == 0) and np.all(S1[:, -1] == 0)
+    assert g.last_ms > 0
+
+
+def test_iga_buoyancy_at_size_and_hybrid_loop(crv):
+    """At ne = 256 (the paper's scale of 100x100 IGA elements and above) the gas blob rises under a
+    hydrostatic water pressure (property of any size, reading R24), and one hybrid round trip runs
+    end to end: CRVPINN pressure at the Gauss points (f1) -> L2 projection -> saturation step ->
+    saturation at the collocation lattice -> crvpinn_set_saturation -> 100 Adam iterations."""
+    g = crv.Iga(256, 2)
+    q = g.quad_points()
+    S = g.project(np.exp(-((q[:, 0] - 0.5) ** 2 + (q[:, 1] - 0.4) ** 2) / 0.01).astype(np.float32))
+    S[0, :] = S[-1, :] = S[:, 0] = S[:, -1] = 0.0
+    Gr = 2.0
+    P = g.project((-Gr * q[:, 1]).astype(np.float32))
+    K = np.ones((256, 256), np.float32)
+    S1 = g.saturation_step(S, P, K, np.zeros_like(K), tau=1e-3, gravity=Gr)
+    grid = np.stack(np.meshgrid(np.linspace(0, 1, 257), np.linspace(0, 1, 257)), -1).reshape(-1, 2).astype(np.float32)
+    s0, s1 = g.eval(S, grid).astype(np.float64), g.eval(S1, grid).astype(np.float64)
+    assert (s1 * grid[:, 1]).sum() / s1.sum() > (s0 * grid[:, 1]).sum() / s0.sum()
+    F = W.make_fields("C3")
+    w = F.workload
+    c = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=0, lr=w.lr)
+    gi = crv.Iga(64, 2)
+    p_q = c.eval_points(gi.quad_points())
+    P = gi.project(p_q)
+    S0 = gi.project(np.zeros(gi.nq, np.float32))
+    Kq = np.ones((64, 64), np.float32)
+    src = np.zeros((64, 64), np.float32)
+    src[30:34, 30:34] = 5.0
+    S1 = gi.saturation_step(S0, P, Kq, src, tau=0.05)
+    N = w.N
+    i, j = np.meshgrid(np.arange(N + 1), np.arange(N + 1))
+    lat = np.stack([i.reshape(-1) / N, j.reshape(-1) / N], 1).astype(np.float32)
+    S_lat = np.clip(gi.eval(S1, lat), 0, 1)
+    c.set_saturation(S_lat)
+    hist = c.step(100)
+    assert np.all(np.isfinite(hist)) and S_lat.max() > 0
+
+
+def test_iga_edges(crv):
+    with pytest.raises(crv.CrvpinnError):
+        crv.Iga(0, 2)
+    with pytest.raises(crv.CrvpinnError):
+        crv.Iga(8, 7)
+    g = crv.Iga(8, 2)
+    z = np.zeros((g.nb, g.nb), np.float32)
+    e = np.zeros((8, 8), np.float32)
+    with pytest.raises(crv.CrvpinnError):
+        g.saturation_step(z, z, e, e, tau=-1.0)
+    assert g.eval(z, np.zeros((0, 2))).shape == (0,)
