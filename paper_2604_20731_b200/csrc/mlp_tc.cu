@@ -27,6 +27,9 @@
 #ifndef CRV_B2_NT
 #define CRV_B2_NT 2
 #endif
+#ifndef CRV_FWD_F32X2
+#define CRV_FWD_F32X2 0   // forward tanh epilogue in packed fp32 pairs (FFMA2 / FADD2)
+#endif
 #ifndef CRV_NEWTON_MASK
 #define CRV_NEWTON_MASK 0xAAAA   // which of a thread's 16 elements per chunk take the FMA-pipe reciprocal
 #endif
@@ -363,8 +366,51 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     // tanh(z) = 1 - 2 / (1 + 2^v) for 16 elements as a skewed pipeline:
                     // ex2 of element i, rcp of element i-2 and the finish (t, hi/lo split, fp16 pack)
                     // of pair (i-5, i-4) are issued together, so MUFU and ALU work interleave
-                    float e[16], r[16];
                     uint32_t hw[8], lw[8];
+#if CRV_FWD_F32X2
+                    float r[16];   // r[k] = 1/(1 + 2^v_k), even k: negated (from rcp(-(1 + 2^v)))
+                    {
+                        // pairs (2m, 2m+1): even elements take the MUFU reciprocal, odd ones Newton on the
+                        // FMA pipe, two odd elements (of pairs m, m+1) per packed FFMA2
+                        const f32x2_t M1 = pk2(-1.0f, -1.0f), ONE = pk2(1.0f, 1.0f);
+                        float nd[16];
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const float e0 = ex2_v(v[2 * m]), e1 = ex2_v(fminf(v[2 * m + 1], 60.0f));
+                            upk2(ffma2(pk2(e0, e1), M1, M1), nd[2 * m], nd[2 * m + 1]);   // -(1 + 2^v)
+                            r[2 * m] = rcp_v(nd[2 * m]);
+                        }
+#pragma unroll
+                        for (int m = 0; m < 8; m += 2) {
+                            const float a = nd[2 * m + 1], b = nd[2 * m + 3];
+                            // 1/d for d = -a: bit-trick seed from a's bits, 3 Newton steps e = 1 - d R, R += R e
+                            f32x2_t R = pk2(__int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(a))),
+                                            __int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(b))));
+                            const f32x2_t ND = pk2(a, b);
+#pragma unroll
+                            for (int it = 0; it < 3; ++it) {
+                                const f32x2_t E = ffma2(ND, R, ONE);
+                                R = ffma2(R, E, R);
+                            }
+                            upk2(R, r[2 * m + 1], r[2 * m + 3]);
+                        }
+                        const f32x2_t TW = pk2(2.0f, -2.0f);
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const f32x2_t t = ffma2(pk2(r[2 * m], r[2 * m + 1]), TW, ONE);   // 1 - 2/(1 + 2^v)
+                            float t0, t1;
+                            upk2(t, t0, t1);
+                            const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
+                            const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
+                            float l0, l1;
+                            upk2(fsub2(t, pk2(h0, h1)), l0, l1);
+                            hw[m] = pack_half2(h0, h1);
+                            lw[m] = pack_half2(l0, l1);
+                            if (last) { v[2 * m] = t0; v[2 * m + 1] = t1; }
+                        }
+                    }
+#else
+                    float e[16], r[16];
 #pragma unroll
                     for (int i = 0; i < 16 + 5; ++i) {
 #if CRV_TANH_MIX && CRV_CLAMP_NEWTON_ONLY
@@ -389,6 +435,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
 #pragma unroll
                         for (int k = 0; k < 16; ++k) v[k] = fmaf(-2.0f, r[k], 1.0f);
                     }
+#endif
                     if (!last) {
                         const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
                         st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);

@@ -225,6 +225,27 @@ __device__ __forceinline__ float rcp_newton(float d) {
     }
     return r;
 }
+// ---- packed fp32 pairs (sm_100 FFMA2 / FADD2: two elements per issue slot)
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pk2(float a, float b) {
+    f32x2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2_t x, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+}
+__device__ __forceinline__ f32x2_t ffma2(f32x2_t a, f32x2_t b, f32x2_t c) {
+    f32x2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f32x2_t fsub2(f32x2_t a, f32x2_t b) {
+    f32x2_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // t = 1 - 2 r for two elements, split t = hi + lo (hi: low 13 mantissa bits cleared, exact in
 // fp16; lo = t - hi exact in fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
 __device__ __forceinline__ void finish_pair(float r0, float r1, uint32_t &hw, uint32_t &lw) {
