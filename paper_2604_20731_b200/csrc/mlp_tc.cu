@@ -28,7 +28,7 @@
 #define CRV_B2_NT 2
 #endif
 #ifndef CRV_FWD_F32X2
-#define CRV_FWD_F32X2 0   // forward tanh epilogue in packed fp32 pairs (FFMA2 / FADD2)
+#define CRV_FWD_F32X2 2   // packed fp32 pairs (FFMA2) in the forward epilogue: 2 = v and the Newton reciprocals only, 1 = everything
 #endif
 #ifndef CRV_NEWTON_MASK
 #define CRV_NEWTON_MASK 0xAAAA   // which of a thread's 16 elements per chunk take the FMA-pipe reciprocal
@@ -351,10 +351,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
                             const float4 b4 = lds_f4(bias + cc + k);   // 2 log2(e) b
+#if CRV_FWD_F32X2 == 2
+                            const f32x2_t C2 = pk2(TANH_C, TANH_C);
+                            upk2(ffma2(pk2(__uint_as_float(rbuf[k]), __uint_as_float(rbuf[k + 1])), C2, pk2(b4.x, b4.y)),
+                                 v[k], v[k + 1]);
+                            upk2(ffma2(pk2(__uint_as_float(rbuf[k + 2]), __uint_as_float(rbuf[k + 3])), C2, pk2(b4.z, b4.w)),
+                                 v[k + 2], v[k + 3]);
+#else
                             v[k] = fmaf(__uint_as_float(rbuf[k]), TANH_C, b4.x);
                             v[k + 1] = fmaf(__uint_as_float(rbuf[k + 1]), TANH_C, b4.y);
                             v[k + 2] = fmaf(__uint_as_float(rbuf[k + 2]), TANH_C, b4.z);
                             v[k + 3] = fmaf(__uint_as_float(rbuf[k + 3]), TANH_C, b4.w);
+#endif
                         }
                         if (c + 1 < KC) {
                             need_half1(cc + 64);
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     // ex2 of element i, rcp of element i-2 and the finish (t, hi/lo split, fp16 pack)
                     // of pair (i-5, i-4) are issued together, so MUFU and ALU work interleave
                     uint32_t hw[8], lw[8];
-#if CRV_FWD_F32X2
+#if CRV_FWD_F32X2 == 1
                     float r[16];   // r[k] = 1/(1 + 2^v_k), even k: negated (from rcp(-(1 + 2^v)))
                     {
                         // pairs (2m, 2m+1): even elements take the MUFU reciprocal, odd ones Newton on the
@@ -419,7 +427,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
 #else
                         if (i < 16) e[i] = ex2_v(fminf(v[i], 60.0f));
 #endif
-#if CRV_TANH_MIX
+#if CRV_TANH_MIX && CRV_FWD_F32X2 == 2
+                        // odd elements take the reciprocal on the FMA pipe, two of them (k-2, k) per packed
+                        // Newton step (FFMA2) when k = 3 mod 4
+                        if (i >= 2 && i < 18) {
+                            const int k = i - 2;
+                            if ((k & 1) == 0) {
+                                r[k] = rcp_v(1.0f + e[k]);
+                            } else if ((k & 3) == 3) {
+                                const float da = 1.0f + e[k - 2], db = 1.0f + e[k];
+                                f32x2_t R = pk2(__int_as_float(0x7EF311C3 - __float_as_int(da)),
+                                                __int_as_float(0x7EF311C3 - __float_as_int(db)));
+                                const f32x2_t ND = pk2(-da, -db), ONE = pk2(1.0f, 1.0f);
+#pragma unroll
+                                for (int it = 0; it < 3; ++it) R = ffma2(R, ffma2(ND, R, ONE), R);
+                                upk2(R, r[k - 2], r[k]);
+                            }
+                        }
+#elif CRV_TANH_MIX
                         // odd elements take the reciprocal on the FMA pipe (MUFU : ALU balance)
                         if (i >= 2 && i < 18)
                             r[i - 2] = ((CRV_NEWTON_MASK >> (i - 2)) & 1) ? rcp_newton(1.0f + e[i - 2]) : rcp_v(1.0f + e[i - 2]);
@@ -872,6 +897,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_F32X2
+#define CRV_B2_F32X2 1     // bwd2 epilogue: (1 - t^2) v in packed fp32 pairs
+#endif
 #ifndef CRV_B2_MMA_CS
 #define CRV_B2_MMA_CS 0    // bias gradients from a tensor-core 1^T Delta_out (single-buffered dX accumulator)
 #endif
@@ -1229,8 +1257,18 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
                         const float2 tf = __half22float2(*reinterpret_cast<const __half2 *>(&tw[mm]));
+#if CRV_B2_F32X2
+                        {   // (1 - t^2) v for the pair in two packed FFMA2s
+                            const f32x2_t T = pk2(tf.x, tf.y);
+                            const f32x2_t V = pk2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
+                            const f32x2_t NTV = ffma2(T, pk2(-1.0f, -1.0f) , pk2(0.0f, 0.0f));   // -t
+                            const f32x2_t G = ffma2(NTV, T, pk2(1.0f, 1.0f));                 // 1 - t^2
+                            upk2(ffma2(G, V, pk2(0.0f, 0.0f)), v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
+                        }
+#else
                         v[8 * j + 2 * mm] *= (1.0f - tf.x * tf.x);
                         v[8 * j + 2 * mm + 1] *= (1.0f - tf.y * tf.y);
+#endif
                         w[4 * j + mm] = pack_half2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
                     }
                 }

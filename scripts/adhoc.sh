@@ -1,8 +1,8 @@
 #!/bin/bash
+CRVPINN_LIB=build/ab/b2f2/libcrvpinn.so timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
 timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
-timeout -s KILL 60 python scripts/outl_case.py 32 128 4 2>&1 | head -1
 for r in 1 2 3; do
-for v in default nof2; do
+for v in default b2f2; do
   if [ $v = default ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
   CRVPINN_LIB=$L timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
 done; done
