@@ -522,7 +522,9 @@ constexpr int OB_THREADS = 256;
 
 // Vectorised: thread T owns logical granule lg = T%8 (8 features) of chunk c = (T/8)%KC for the
 // rows r = rg, rg+NRG, ... (rg = T/(8 KC)); a warp covers whole 128-byte rows (coalesced).
-template <int WP>
+// STORE = false: only the output-layer gradient sums (dW_out, db_L, db_out), no Delta_L -- run on the
+// side stream next to the first k_tc_bwd2 launch, which then forms Delta_L without the sums
+template <int WP, bool STORE = true>
 __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __half *__restrict__ actL,
                                                            const float *__restrict__ gbar,
                                                            const float *__restrict__ Wop,
@@ -570,9 +572,9 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
                 aw[2 * m + 1] = fmaf(g, t.y, aw[2 * m + 1]);
                 ab[2 * m] += d0;
                 ab[2 * m + 1] += d1;
-                w[m] = pack_half2(d0, d1);
+                if constexpr (STORE) w[m] = pack_half2(d0, d1);
             }
-            *(uint4 *)(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
+            if constexpr (STORE) *(uint4 *)(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
     // fixed-order combination over row groups
@@ -886,6 +888,7 @@ struct Bwd2Args {
     DevState *st;
     long long *trace;     // debug timeline (CTA 0), nullptr normally
     float *part_cb;       // [npairs][WP] 1^T Delta_out (CRV_B2_MMA_CS): bias gradient of theta layer g+1
+    int outl_sums;        // outl: also reduce dW_out / db_L / db_out (else a side-stream k_tc_out_bwd does)
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 #ifndef CRV_B2_MMA_SLEEP
@@ -1176,7 +1179,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         for (int e = 0; e < 4; ++e) {
                             const __half2 t = *reinterpret_cast<__half2 *>(&w[e]);
                             const __half2 d = __hmul2(__hmul2(__hfma2(__hneg2(t), t, one2), wo2[j][e]), g2[m]);
-                            if (own && jj < 2) {
+                            if (a.outl_sums && own && jj < 2) {
                                 const float2 tf = __half22float2(t), df = __half22float2(d);
                                 aw[jj][2 * e] = fmaf(g[m], tf.x, aw[jj][2 * e]);
                                 aw[jj][2 * e + 1] = fmaf(g[m], tf.y, aw[jj][2 * e + 1]);
@@ -1324,7 +1327,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         // outl: pre-reduce the 4 row groups of a warp (lanes l, l^8, l^16, l^24 share olg) -> one
         // [2 kinds][128 own features] row per epilogue warp, then [EW] rows of g sums
         float *sob = sred + 12 * 128;
-        if (a.outl) {
+        if (a.outl && a.outl_sums) {
             const int ew = warp - 2;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj)
@@ -1358,7 +1361,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             pb[2 * ig] = sx;
             pb[2 * ig + 1] = sy;
             pb[2 * WP + ig] = sb;
-            if (a.outl) {
+            if (a.outl && a.outl_sums) {
                 float sw = 0.f, sbb = 0.f;
                 for (int r = 0; r < B2_EPI_WARPS; ++r) {
                     sw += sob[(r * 2 + 0) * 128 + col];
@@ -2014,7 +2017,11 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         // every stage of the chain
         const char *e = getenv("CRVPINN_FUSE_OUTL");   // tuning knob: fused output-layer backward
         b.fuse_outl = WP >= 128 && !b.chain && !(e && e[0] == '0');
-        b.grid_ob = WP >= 128 && b.fuse_outl ? b.npairs : (b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm);
+        // tuning knob (opt-in, measured slower: the sums kernel takes the SMs the first k_tc_bwd2
+        // launch needs, 0.59 vs 0.49 ms): output-layer sums on the side stream
+        const char *os = getenv("CRVPINN_OUTL_SIDE");
+        b.outl_side = b.fuse_outl && os && os[0] == '1';
+        b.grid_ob = WP >= 128 && b.fuse_outl && !b.outl_side ? b.npairs : (b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm);
         const char *r = getenv("CRVPINN_BWD_REV");     // tuning knob: alternating tile-walk direction
         b.bwd_rev = !(r && r[0] == '0');
     }
@@ -2094,7 +2101,9 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
     b.groups = reduce_groups(jobs, nj);
     b.groups_deep = reduce_groups(jobs, b.njobs_deep);
     if (cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&b.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&b.ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_pre, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_ob, cudaEventDisableTiming) != cudaSuccess) {
         err = "stream/event creation failed";
         return CRVPINN_ECUDA;
     }
@@ -2130,6 +2139,8 @@ void tc_destroy(TcBufs &b) {
     for (auto &e : b.ev_fork)
         if (e) { cudaEventDestroy(e); e = nullptr; }
     if (b.ev_join) { cudaEventDestroy(b.ev_join); b.ev_join = nullptr; }
+    if (b.ev_pre) { cudaEventDestroy(b.ev_pre); b.ev_pre = nullptr; }
+    if (b.ev_ob) { cudaEventDestroy(b.ev_ob); b.ev_ob = nullptr; }
     if (b.side) { cudaStreamDestroy(b.side); b.side = nullptr; }
 }
 
@@ -2239,6 +2250,15 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             cfg.gridDim = dim3(b.npairs * NS);
             cfg.dynamicSmemBytes = B2<WP>::SMEM;
         }
+        if (b.fuse_outl && b.outl_side && g_next == b.G - 1) {
+            // output-layer gradient sums on the side stream, concurrent with the fused first GEMM
+            cudaEventRecord(b.ev_pre, s);
+            cudaStreamWaitEvent(b.side, b.ev_pre, 0);
+            k_tc_out_bwd<WP, false><<<b.grid_ob, OB_THREADS, 0, b.side>>>(b.ntiles, b.act + (size_t)(L - 1) * lay,
+                                                                          b.gbar, b.Wop, nullptr,
+                                                                          b.partial + b.off_ob, st);
+            cudaEventRecord(b.ev_ob, b.side);   // the deep reduction below reads these sums
+        }
         for (int g = g_next; g >= 0; --g) {
             const bool outl = g == b.G - 1 && b.fuse_outl;
             // Launches alternate the direction of their tile walk, starting backwards: the forward
@@ -2251,7 +2271,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
-                       b.partial + b.off_cb + (long)g * b.npairs * WP};
+                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");
@@ -2286,6 +2306,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         }
     }
     if constexpr (WP >= 128) {
+        if (b.fuse_outl && b.outl_side) cudaStreamWaitEvent(s, b.ev_ob, 0);
         launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s);   // column sums, W1, W_out
         cudaEventRecord(b.ev_join, b.side);
         cudaStreamWaitEvent(s, b.ev_join, 0);
@@ -2313,7 +2334,8 @@ int tc_launches(const Net &net, const TcBufs &b) {
         }
     }
     for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
-    return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl ? 1 : 0) /*out_bwd*/ + bwd + side + 1 /*reduce*/;   // Adam: crvpinn.cu
+    return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl || b.outl_side ? 1 : 0) /*out_bwd (sums)*/ + bwd + side +
+           1 /*reduce*/;   // Adam: crvpinn.cu
 }
 
 }  // namespace crv
