@@ -900,6 +900,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_CS_DEFER
+#define CRV_B2_CS_DEFER 1  // bwd2 bias column sums: one butterfly level per tile, the rest once at the end
+#endif
 #ifndef CRV_B2_F32X2
 #define CRV_B2_F32X2 1     // bwd2 epilogue: (1 - t^2) v in packed fp32 pairs
 #endif
@@ -910,7 +913,7 @@ struct Bwd2Args {
 #define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
 #endif
 #ifndef CRV_B2_EARLY_T
-#define CRV_B2_EARLY_T 1   // bwd2 epilogue releases the t slot right after xfull (t values in registers)
+#define CRV_B2_EARLY_T 0   // bwd2 epilogue releases the t slot right after xfull (t values in registers)
 #endif
 #ifndef CRV_T_FIRST
 #define CRV_T_FIRST 1   // backward producers issue a tile's t_in load before its Delta chunks
@@ -1119,6 +1122,13 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         const uint32_t t_lane = (uint32_t)(q * 32) << 16;
         const int N = a.N;
         float cs[CPW / 32], csx[CPW / 32], csy[CPW / 32];
+#if CRV_B2_CS_DEFER
+        float csd[CPW / 32][16];   // column sums after the first butterfly level, over all tiles
+#pragma unroll
+        for (int g2 = 0; g2 < CPW / 32; ++g2)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) csd[g2][i] = 0.f;
+#endif
 #pragma unroll
         for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = csx[g2] = csy[g2] = 0.f;
         // output-layer transform state (outl). Thread -> granule lg (8 features) of every chunk,
@@ -1298,8 +1308,23 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     csy[g2] += vy[0];
                 }
                 if (!CRV_B2_MMA_CS || a.first) {   // bias sums on the CUDA cores (else: tensor cores)
-                    warp_reduce_scatter32(v, lane);
-                    cs[g2] += v[0];
+#if CRV_B2_CS_DEFER
+                    if (!a.first) {
+                        // first butterfly level only (lanes l, l^16), accumulated over tiles; the
+                        // other four levels run once at the end of the kernel
+                        const bool upper = (lane & 16) != 0;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float send = upper ? v[i] : v[i + 16];
+                            const float keep = upper ? v[i + 16] : v[i];
+                            csd[g2][i] += keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                        }
+                    } else
+#endif
+                    {
+                        warp_reduce_scatter32(v, lane);
+                        cs[g2] += v[0];
+                    }
                 }
             }
             tc_fence_before();
@@ -1312,6 +1337,25 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #endif
             }
         }
+#if CRV_B2_CS_DEFER
+        if (!a.first) {
+            // remaining butterfly levels (8, 4, 2, 1) of the deferred column sums: column = lane
+#pragma unroll
+            for (int g2 = 0; g2 < CPW / 32; ++g2) {
+#pragma unroll
+                for (int st = 8; st >= 1; st >>= 1) {
+                    const bool upper = (lane & st) != 0;
+#pragma unroll
+                    for (int i = 0; i < st; ++i) {
+                        const float send = upper ? csd[g2][i] : csd[g2][i + st];
+                        const float keep = upper ? csd[g2][i + st] : csd[g2][i];
+                        csd[g2][i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                    }
+                }
+                cs[g2] = csd[g2][0];
+            }
+        }
+#endif
         // ---- end: all MMAs done -> the rings are free for the reductions
         if (nk > 0) mbar_wait(wdone, 0);
         tc_fence_after();
