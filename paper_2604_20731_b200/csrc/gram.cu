@@ -556,13 +556,37 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     int it = 0;
     double rel = 1.0;
     constexpr int CHK = 20;
+    auto iteration = [&](int i) {
+        k_pcg_matvec<<<n, PCG_MV_THREADS, 0, s>>>(p, alpha, Ap, part_a, N);
+        k_pcg_xr<<<vblocks, 256, 0, s>>>(x, r, p, Ap, part_a, n, st, i, part_rr, n2);
+        precond();
+        k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, i + 1, n2);
+    };
+    // the kernels use only the parity of the iteration index (the rz ring) once it >= 1: a graph of
+    // two iterations (even, odd) replayed CHK / 2 times removes the per-kernel launch cost
+    cudaGraphExec_t gx = nullptr;
+    {
+        cudaGraph_t gr = nullptr;
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            iteration(0);
+            iteration(1);
+            if (cudaStreamEndCapture(s, &gr) == cudaSuccess && gr) {
+                if (cudaGraphInstantiate(&gx, gr, 0) != cudaSuccess) gx = nullptr;
+                cudaGraphDestroy(gr);
+            }
+        }
+        cudaGetLastError();
+    }
     while (it < max_iter) {
         const int upto = it + CHK < max_iter ? it + CHK : max_iter;
-        for (; it < upto; ++it) {
-            k_pcg_matvec<<<n, PCG_MV_THREADS, 0, s>>>(p, alpha, Ap, part_a, N);
-            k_pcg_xr<<<vblocks, 256, 0, s>>>(x, r, p, Ap, part_a, n, st, it, part_rr, n2);
-            precond();
-            k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, it + 1, n2);
+        while (it < upto) {
+            if (gx && it + 2 <= upto && (it & 1) == 0) {
+                cudaGraphLaunch(gx, s);
+                it += 2;
+            } else {
+                iteration(it);
+                ++it;
+            }
         }
         // convergence on the TRUE residual of the fp64 iterate, which also replaces r
         k_pcg_final<<<n, PCG_MV_THREADS, 0, s>>>(x, alpha, b, r, nullptr, part_fin, N);
@@ -584,6 +608,7 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     for (double v : hf) rr += v;
     if (iters_out) *iters_out = it;
     if (rel_out) *rel_out = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
+    if (gx) cudaGraphExecDestroy(gx);
     cudaFree(buf);
     cudaFree(x);
     cudaFree(dpart);
