@@ -2034,11 +2034,15 @@ int tc_create(const Net &net, TcBufs &b, std::string &err) {
         b.grid_dx = np_;              // rows of the column-sum partials
         b.grid_bwd = np_ * NS;        // CTAs per backward launch
         // backward chain (k_tc_bwdc): S stages of NS CTAs per cluster, clusters split the tiles
-        // (measured slower than one k_tc_bwd2 launch per GEMM at C5: opt-in only)
-        const char *ce = getenv("CRVPINN_BWD_CHAIN");       // tuning knob: 1 = backward chain
+        // Default: on for small problems (<= 4 tiles per SM: C4 measured 0.100 vs 0.120 ms backward,
+        // one launch instead of G amortises the per-launch fill/drain), off for large ones (C5:
+        // 0.60 vs 0.49 ms). CRVPINN_BWD_CHAIN=0/1 forces it.
+        const char *ce = getenv("CRVPINN_BWD_CHAIN");       // tuning knob: 0/1 = backward chain off/on
         const char *se = getenv("CRVPINN_BWD_STAGES");      // tuning knob: stages per cluster (implies chain)
+        const bool small = b.ntiles <= 4 * nsm;
+        const bool want = ce ? ce[0] == '1' : (se != nullptr || small);
         b.chain = 0;
-        if (WP >= 128 && G >= 2 && ((ce && ce[0] == '1') || se)) {
+        if (WP >= 128 && G >= 2 && want) {
             int S = se ? atoi(se) : 8 / NS;
             if (S > G) S = G;
             if (S * NS > 8) S = 8 / NS;
