@@ -536,11 +536,7 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n, *part_rr = dpart + 3 * n;
     float *rhat = c.work, *zhat = c.work + n2;
     const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (M + M / 2));
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_pcg_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-        attr = true;
-    }
+    cudaFuncSetAttribute(k_pcg_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);   // N = 2048: 48 KiB+
     auto precond = [&]() {   // z = G^-1 r (and the block parts of r . z)
         k_pcg_dst<<<rows, fft_t, smem_fft, s>>>(r, rhat, c.tw, N, c.logM, nrm);
         k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(

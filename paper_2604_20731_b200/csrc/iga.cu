@@ -320,11 +320,8 @@ void kron_solve(IgaDev &g, cudaStream_t s) {
     const dim3 tb(32, 8), tg((n + 31) / 32, (n + 31) / 32);
     const size_t smem = sizeof(double) * (size_t)n * IGA_BAND_COLS;
     if (smem <= 200 * 1024) {
-        static int attr_set = 0;
-        if (!attr_set) {
-            cudaFuncSetAttribute(k_iga_band_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr_set = 1;
-        }
+        // per device and cheap: set on every call (a process may use several devices)
+        cudaFuncSetAttribute(k_iga_band_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         k_iga_band_smem<<<ceil_div(n, IGA_BAND_COLS), 256, smem, s>>>(g, g.A);   // along l (rows)
         k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
         k_iga_band_smem<<<ceil_div(n, IGA_BAND_COLS), 256, smem, s>>>(g, g.B);   // along k
