@@ -502,3 +502,37 @@ def test_iga_edges(crv):
     with pytest.raises(crv.CrvpinnError):
         g.saturation_step(z, z, e, e, tau=-1.0)
     assert g.eval(z, np.zeros((0, 2))).shape == (0,)
+
+
+# ------------------------------------------------------------------ maximum size (N = 2048)
+def test_maximum_grid_properties(crv):
+    """N = 2048 (the largest grid the ABI accepts; 4.2 M MLP points, 21 GB of fp16 activations) with
+    the C5 network: the oracle cannot run the whole iteration at this size, so each step is checked
+    where it can be computed one by one -- u at 1000 sampled nodes against the oracle's evaluation
+    there, RES against the oracle's stencil on the GPU's own u, q through G q = RES (oracle stencil
+    form of G), dLOSS/du against the oracle's adjoint of the GPU's q -- plus exact boundary zeros."""
+    N, widths = 2048, (2, 256, 256, 256, 256, 256, 1)
+    K, S, f = W.random_fields(N, 2048)
+    th = W.random_theta(widths, 2048)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
+    loss, grad = g.loss_grad()
+    assert np.isfinite(loss) and loss > 0 and np.all(np.isfinite(grad))
+    im = g.intermediates()
+    U = im["u"].reshape(N + 1, N + 1)
+    assert np.all(U[0] == 0) and np.all(U[-1] == 0) and np.all(U[:, 0] == 0) and np.all(U[:, -1] == 0)
+    ref = oracle.Oracle(N, widths, K, S, f, th, factor_gram=False)
+    rng = np.random.default_rng(7)
+    idx = rng.choice((N + 1) ** 2, 1000, replace=False)
+    xy = np.stack([(idx % (N + 1)) / N, (idx // (N + 1)) / N], 1)
+    u_ref = ref.eval_points(xy)
+    assert np.max(np.abs(im["u"][idx] - u_ref)) <= 2e-3 * np.abs(u_ref).max()
+    r_own = ref.residual(im["u"])
+    assert np.max(np.abs(im["res"] - r_own)) <= 1e-5 * np.abs(r_own).max()
+    gq = ref.gram_matvec(im["q"].astype(np.float64))
+    assert np.linalg.norm(gq - im["res"]) <= 1e-3 * np.linalg.norm(im["res"])
+    gu_own = ref.residual_adjoint(2.0 * im["q"].astype(np.float64))
+    mask = np.zeros((N + 1, N + 1))
+    mask[1:-1, 1:-1] = 1
+    gu_own *= mask.reshape(-1)
+    assert np.max(np.abs(im["gu"] - gu_own)) <= 1e-5 * np.abs(gu_own).max()
+    g.close()
