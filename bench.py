@@ -190,7 +190,7 @@ def run_reference(args, rank, world):
         "unit": "Adam iters/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, "oracle"),
+        "config": dict(workload_config(args.workload, "oracle"), adam_iters_per_step=1),
         "cpu_baseline": {"value": value, "unit": "Adam iters/s", "cores": oracle.max_threads(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "Adam iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -1,5 +1,7 @@
 #!/bin/bash
-timeout -s KILL 700 python -m pytest tests -q -m gpu 2>&1 | tail -2
-for w in C3 C4 C5; do for v in "CRVPINN_BWD_CHAIN=0" "X=1"; do
-  env $v timeout -s KILL 120 python scripts/stage_time.py $w 5 2>&1 | tail -1 | sed "s|^|$w $v |"
+timeout -s KILL 60 python scripts/outl_case.py 64 256 5 2>&1 | head -1
+for r in 1 2 3; do
+for v in default old; do
+  if [ $v = default ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
+  CRVPINN_LIB=$L timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
 done; done
