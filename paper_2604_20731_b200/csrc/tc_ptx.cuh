@@ -204,14 +204,16 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // Volatile MUFU wrappers: their relative order is kept by the compiler, which lets a hand-skewed
 // loop interleave MUFU issue with the ALU work of other elements (4 warps per SMSP otherwise run
 // their MUFU phases in lockstep and leave the XU pipe idle during the ALU phases).
+// ex2_v / rcp_v / finish_pair are pure (non-volatile asm): the compiler may schedule them freely
+// and drops results nobody uses (the last layer's lo halves)
 __device__ __forceinline__ float ex2_v(float x) {
     float y;
-    asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 __device__ __forceinline__ float rcp_v(float x) {
     float y;
-    asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 // 1/d on the FMA pipe (d in [1, 2^60]): bit-trick seed (rel. error < 0.125) and three Newton
@@ -249,7 +251,7 @@ __device__ __forceinline__ f32x2_t fsub2(f32x2_t a, f32x2_t b) {
 // t = 1 - 2 r for two elements, split t = hi + lo (hi: low 13 mantissa bits cleared, exact in
 // fp16; lo = t - hi exact in fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
 __device__ __forceinline__ void finish_pair(float r0, float r1, uint32_t &hw, uint32_t &lw) {
-    asm volatile(
+    asm(
         "{\n\t.reg .f32 t0, t1, h0, h1, l0, l1;\n\t.reg .b32 b0, b1;\n\t"
         "fma.rn.f32 t0, %2, 0fC0000000, 0f3F800000;\n\t"
         "fma.rn.f32 t1, %3, 0fC0000000, 0f3F800000;\n\t"
