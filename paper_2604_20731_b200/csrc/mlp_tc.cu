@@ -900,6 +900,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_DEFER_FIRST
+#define CRV_B2_DEFER_FIRST 1   // the g = 0 launch defers its x-, y- and bias sums too (its own instantiation)
+#endif
 #ifndef CRV_B2_CS_DEFER
 #define CRV_B2_CS_DEFER 1  // bwd2 bias column sums: one butterfly level per tile, the rest once at the end
 #endif
@@ -913,7 +916,7 @@ struct Bwd2Args {
 #define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
 #endif
 #ifndef CRV_B2_EARLY_T
-#define CRV_B2_EARLY_T 0   // bwd2 epilogue releases the t slot right after xfull (t values in registers)
+#define CRV_B2_EARLY_T 1   // bwd2 (middle GEMMs only) releases the t slot right after xfull (t values in registers)
 #endif
 #ifndef CRV_T_FIRST
 #define CRV_T_FIRST 1   // backward producers issue a tile's t_in load before its Delta chunks
@@ -934,8 +937,14 @@ struct B2 {
     static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
-template <int WP>
+// MODE bit 0: the first launch (output layer fused, OUTL); bit 1: the last one (g = 0, FIRST).
+// Each mode is its own instantiation, so the registers the output-layer transform or the
+// first-layer sums need are not reserved in the others.
+template <int WP, int MODE>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
+    constexpr bool OUTL = (MODE & 1) != 0, FIRST = (MODE & 2) != 0;
+    constexpr bool EARLY_T = CRV_B2_EARLY_T && MODE == 0;
+    constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
     constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
     extern __shared__ uint8_t smem_raw[];
@@ -1056,7 +1065,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 auto dx_pair = [&](int h) {
                     const int sl = (slot0 + 2 * h) % DS;
                     for (int j = 2 * h; j < 2 * h + 2; ++j) {
-                        B2_MMA_WAIT(a.outl ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
+                        B2_MMA_WAIT(OUTL ? &dready[sl + j - 2 * h] : &dfull[sl + j - 2 * h], ((dn + j) / DS) & 1);
                         BTRACE(k * 16 + 8 + j);
                         tc_fence_after();
 #pragma unroll
@@ -1123,11 +1132,35 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         const int N = a.N;
         float cs[CPW / 32], csx[CPW / 32], csy[CPW / 32];
 #if CRV_B2_CS_DEFER
-        float csd[CPW / 32][16];   // column sums after the first butterfly level, over all tiles
+        // column sums after the first butterfly level (lanes l, l^16), accumulated over all tiles;
+        // the other four levels run once at the end (csdx/csdy: the g = 0 launch's x- and y-sums)
+        float csd[CPW / 32][16], csdx[CPW / 32][16], csdy[CPW / 32][16];
 #pragma unroll
         for (int g2 = 0; g2 < CPW / 32; ++g2)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) csd[g2][i] = 0.f;
+            for (int i = 0; i < 16; ++i) csd[g2][i] = csdx[g2][i] = csdy[g2][i] = 0.f;
+        auto level16 = [&](const float (&src)[32], float (&acc)[16], float scale) {
+            const bool upper = (lane & 16) != 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float send = (upper ? src[i] : src[i + 16]) * scale;
+                const float keep = (upper ? src[i + 16] : src[i]) * scale;
+                acc[i] += keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+        };
+        auto finish16 = [&](float (&acc)[16]) {
+#pragma unroll
+            for (int st = 8; st >= 1; st >>= 1) {
+                const bool upper = (lane & st) != 0;
+#pragma unroll
+                for (int i = 0; i < st; ++i) {
+                    const float send = upper ? acc[i] : acc[i + st];
+                    const float keep = upper ? acc[i + st] : acc[i];
+                    acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                }
+            }
+            return acc[0];
+        };
 #endif
 #pragma unroll
         for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = csx[g2] = csy[g2] = 0.f;
@@ -1142,7 +1175,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         __half2 wo2[KC][4];
         float aw[2][8], ab[2][8], ag = 0.f;
         float s = 1.0f;
-        if (a.outl) {
+        if (OUTL) {
             s = grad_scale(a.st);
             if (blockIdx.x == 0 && ep_tid == 0) {
                 a.st->gscale = s;
@@ -1160,7 +1193,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         }
         int dn = 0;
         for (int k = 0; k <= nk; ++k) {
-            if (a.outl && k < nk) {
+            if (OUTL && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
                 const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
                 float g[ORM];
@@ -1225,23 +1258,23 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&xempty[b]);
 #endif
-#if CRV_B2_EARLY_T
-            // the dW MMAs of this tile are complete (xfull follows them): take this warp's t values
-            // into registers and release the t slot now, so the next-but-one tile's t_in load starts
-            // a whole epilogue earlier (the MMA warp was waiting ~0.8K cycles per tile for it)
+            // EARLY_T: the dW MMAs of this tile are complete (xfull follows them): take this warp's t
+            // values into registers and release the t slot now, so the next-but-one tile's t_in load
+            // starts a whole epilogue earlier
             uint32_t tall[CPW / 32][4][4];
+            if constexpr (EARLY_T) {
 #pragma unroll
-            for (int g2 = 0; g2 < CPW / 32; ++g2) {
-                const int col0 = wq * CPW + g2 * 32;
-                const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + (col0 >> 6)) * CHUNK_BYTES + row * 128);
+                for (int g2 = 0; g2 < CPW / 32; ++g2) {
+                    const int col0 = wq * CPW + g2 * 32;
+                    const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + (col0 >> 6)) * CHUNK_BYTES + row * 128);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    ld_shared_v4(tsm + (uint32_t)(((((col0 & 63) >> 3) + j) ^ (row & 7)) << 4), tall[g2][j][0],
-                                 tall[g2][j][1], tall[g2][j][2], tall[g2][j][3]);
+                    for (int j = 0; j < 4; ++j)
+                        ld_shared_v4(tsm + (uint32_t)(((((col0 & 63) >> 3) + j) ^ (row & 7)) << 4), tall[g2][j][0],
+                                     tall[g2][j][1], tall[g2][j][2], tall[g2][j][3]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[tb]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[tb]);
-#endif
 #pragma unroll
             for (int g2 = 0; g2 < CPW / 32; ++g2) {
                 const int col0 = wq * CPW + g2 * 32;     // local dX column (i - 128 rank)
@@ -1259,14 +1292,13 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int lg = lgb + j;
-#if CRV_B2_EARLY_T
-                    const uint32_t *tw = tall[g2][j];
-                    (void)lg;
-                    (void)tsm;
-#else
                     uint32_t tw[4];
-                    ld_shared_v4(tsm + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
-#endif
+                    if constexpr (EARLY_T) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) tw[q4] = tall[g2][j][q4];
+                    } else {
+                        ld_shared_v4(tsm + (uint32_t)((lg ^ (row & 7)) << 4), tw[0], tw[1], tw[2], tw[3]);
+                    }
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
                         const float2 tf = __half22float2(*reinterpret_cast<const __half2 *>(&tw[mm]));
@@ -1285,7 +1317,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         w[4 * j + mm] = pack_half2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
                     }
                 }
-                if (!a.first) {
+                if (!FIRST) {
                     // logical granules (2m, 2m+1) occupy one 32-byte sector, swapped when row is odd
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
@@ -1298,27 +1330,27 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                             st_global_v8(drow + pos * 16, g0[0], g0[1], g0[2], g0[3], g1[0], g1[1], g1[2], g1[3]);
                     }
                 }
-                if (a.first) {
-                    float vx[32], vy[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
-                    warp_reduce_scatter32(vx, lane);
-                    warp_reduce_scatter32(vy, lane);
-                    csx[g2] += vx[0];
-                    csy[g2] += vy[0];
-                }
-                if (!CRV_B2_MMA_CS || a.first) {   // bias sums on the CUDA cores (else: tensor cores)
+                if (FIRST) {
 #if CRV_B2_CS_DEFER
-                    if (!a.first) {
-                        // first butterfly level only (lanes l, l^16), accumulated over tiles; the
-                        // other four levels run once at the end of the kernel
-                        const bool upper = (lane & 16) != 0;
+                    if constexpr (DEFER_FIRST) {
+                        level16(v, csdx[g2], x);
+                        level16(v, csdy[g2], y);
+                    } else
+#endif
+                    {
+                        float vx[32], vy[32];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float send = upper ? v[i] : v[i + 16];
-                            const float keep = upper ? v[i + 16] : v[i];
-                            csd[g2][i] += keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                        }
+                        for (int e = 0; e < 32; ++e) { vx[e] = v[e] * x; vy[e] = v[e] * y; }
+                        warp_reduce_scatter32(vx, lane);
+                        warp_reduce_scatter32(vy, lane);
+                        csx[g2] += vx[0];
+                        csy[g2] += vy[0];
+                    }
+                }
+                if (!CRV_B2_MMA_CS || FIRST) {   // bias sums on the CUDA cores (else: tensor cores)
+#if CRV_B2_CS_DEFER
+                    if (!FIRST || DEFER_FIRST) {
+                        level16(v, csd[g2], 1.0f);
                     } else
 #endif
                     {
@@ -1332,27 +1364,20 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (lane == 0) {
                 if (warp == 2) BTRACE(kk * 16 + 6);
                 if (!CRV_B2_MMA_CS) mbar_arrive(&xempty[b]);
-#if !CRV_B2_EARLY_T
-                mbar_arrive(&tempty[tb]);
-#endif
+                if constexpr (!EARLY_T) mbar_arrive(&tempty[tb]);
             }
         }
 #if CRV_B2_CS_DEFER
-        if (!a.first) {
-            // remaining butterfly levels (8, 4, 2, 1) of the deferred column sums: column = lane
+        // remaining butterfly levels (8, 4, 2, 1) of the deferred column sums: column = lane
+        if (!FIRST || DEFER_FIRST) {
+#pragma unroll
+            for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = finish16(csd[g2]);
+        }
+        if constexpr (DEFER_FIRST) {
 #pragma unroll
             for (int g2 = 0; g2 < CPW / 32; ++g2) {
-#pragma unroll
-                for (int st = 8; st >= 1; st >>= 1) {
-                    const bool upper = (lane & st) != 0;
-#pragma unroll
-                    for (int i = 0; i < st; ++i) {
-                        const float send = upper ? csd[g2][i] : csd[g2][i + st];
-                        const float keep = upper ? csd[g2][i + st] : csd[g2][i];
-                        csd[g2][i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
-                    }
-                }
-                cs[g2] = csd[g2][0];
+                csx[g2] = finish16(csdx[g2]);
+                csy[g2] = finish16(csdy[g2]);
             }
         }
 #endif
@@ -1371,7 +1396,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         // outl: pre-reduce the 4 row groups of a warp (lanes l, l^8, l^16, l^24 share olg) -> one
         // [2 kinds][128 own features] row per epilogue warp, then [EW] rows of g sums
         float *sob = sred + 12 * 128;
-        if (a.outl && a.outl_sums) {
+        if (OUTL && a.outl_sums) {
             const int ew = warp - 2;
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj)
@@ -1405,7 +1430,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             pb[2 * ig] = sx;
             pb[2 * ig + 1] = sy;
             pb[2 * WP + ig] = sb;
-            if (a.outl && a.outl_sums) {
+            if (OUTL && a.outl_sums) {
                 float sw = 0.f, sbb = 0.f;
                 for (int r = 0; r < B2_EPI_WARPS; ++r) {
                     sw += sob[(r * 2 + 0) * 128 + col];
@@ -1971,7 +1996,10 @@ static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     cudaFuncSetAttribute(k_tc_forward<WP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
-        cudaFuncSetAttribute(k_tc_bwd2<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
         cudaFuncSetAttribute(k_tc_bwdc<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, BC<WP>::SMEM);
     } else {
         cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
@@ -2329,7 +2357,11 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 cudaMemset(trace, 0, 4096 * 8);
                 a.trace = trace;
             }
-            cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP>, a);
+            const int mode = (outl ? 1 : 0) | (g == 0 ? 2 : 0);
+            if (mode == 0) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 0>, a);
+            else if (mode == 1) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 1>, a);
+            else if (mode == 2) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 2>, a);
+            else cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 3>, a);
             // dW of GEMM g is final: reduce it on the side stream while GEMM g-1 runs
             cudaEventRecord(b.ev_fork[g], s);
             cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
