@@ -900,6 +900,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_B2_EARLY_T_OUTL
+#define CRV_B2_EARLY_T_OUTL 0   // early t release in the fused output-layer launch too
+#endif
 #ifndef CRV_B2_DEFER_FIRST
 #define CRV_B2_DEFER_FIRST 1   // the g = 0 launch defers its x-, y- and bias sums too (its own instantiation)
 #endif
@@ -943,7 +946,7 @@ struct B2 {
 template <int WP, int MODE>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr bool OUTL = (MODE & 1) != 0, FIRST = (MODE & 2) != 0;
-    constexpr bool EARLY_T = CRV_B2_EARLY_T && MODE == 0;
+    constexpr bool EARLY_T = CRV_B2_EARLY_T && (MODE == 0 || (MODE == 1 && CRV_B2_EARLY_T_OUTL));
     constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
     constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
