@@ -900,6 +900,9 @@ struct Bwd2Args {
 #define B2_MMA_WAIT mbar_wait
 #endif
 
+#ifndef CRV_OUTL_H2SUM
+#define CRV_OUTL_H2SUM 1   // output-layer sums: rows of a granule column summed in half2 first
+#endif
 #ifndef CRV_B2_EARLY_T_OUTL
 #define CRV_B2_EARLY_T_OUTL 0   // early t release in the fused output-layer launch too
 #endif
@@ -1215,6 +1218,13 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     const uint32_t blk = smem_u32(Dr + slot * CHUNK_BYTES);
                     const bool own = NS == 1 || (j >> 1) == (int)rank;
                     const int jj = NS == 1 ? j : (j & 1);
+#if CRV_OUTL_H2SUM
+                    // the ORM rows of a granule column are first summed in half2 (g t and Delta_L are
+                    // fp16 values already), then added to the fp32 sums once
+                    __half2 haw[4], hab[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) haw[e] = hab[e] = __floats2half2_rn(0.0f, 0.0f);
+#endif
 #pragma unroll
                     for (int m = 0; m < ORM; ++m) {
                         const int r = orr + ORG * m;
@@ -1226,16 +1236,33 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                             const __half2 t = *reinterpret_cast<__half2 *>(&w[e]);
                             const __half2 d = __hmul2(__hmul2(__hfma2(__hneg2(t), t, one2), wo2[j][e]), g2[m]);
                             if (a.outl_sums && own && jj < 2) {
+#if CRV_OUTL_H2SUM
+                                haw[e] = __hfma2(g2[m], t, haw[e]);
+                                hab[e] = __hadd2(hab[e], d);
+#else
                                 const float2 tf = __half22float2(t), df = __half22float2(d);
                                 aw[jj][2 * e] = fmaf(g[m], tf.x, aw[jj][2 * e]);
                                 aw[jj][2 * e + 1] = fmaf(g[m], tf.y, aw[jj][2 * e + 1]);
                                 ab[jj][2 * e] += df.x;
                                 ab[jj][2 * e + 1] += df.y;
+#endif
                             }
                             w[e] = *reinterpret_cast<const uint32_t *>(&d);
                         }
                         st_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
                     }
+#if CRV_OUTL_H2SUM
+                    if (a.outl_sums && own && jj < 2) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 fw = __half22float2(haw[e]), fb = __half22float2(hab[e]);
+                            aw[jj][2 * e] += fw.x;
+                            aw[jj][2 * e + 1] += fw.y;
+                            ab[jj][2 * e] += fb.x;
+                            ab[jj][2 * e + 1] += fb.y;
+                        }
+                    }
+#endif
                     fence_proxy_async_smem();
                     mbar_arrive(&dready[slot]);   // count = B2_EPI_THREADS
                 }
