@@ -903,6 +903,9 @@ struct Bwd2Args {
 #ifndef CRV_OUTL_H2SUM
 #define CRV_OUTL_H2SUM 1   // output-layer sums: rows of a granule column summed in half2 first
 #endif
+#ifndef CRV_B2_OUTL_SWAP
+#define CRV_B2_OUTL_SWAP 0   // output-layer launch: early t release instead of the deferred bias sums
+#endif
 #ifndef CRV_B2_EARLY_T_OUTL
 #define CRV_B2_EARLY_T_OUTL 0   // early t release in the fused output-layer launch too
 #endif
@@ -949,7 +952,10 @@ struct B2 {
 template <int WP, int MODE>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr bool OUTL = (MODE & 1) != 0, FIRST = (MODE & 2) != 0;
-    constexpr bool EARLY_T = CRV_B2_EARLY_T && (MODE == 0 || (MODE == 1 && CRV_B2_EARLY_T_OUTL));
+    // the output-layer launch can trade the deferred bias sums for the early t release
+    constexpr bool OUTL_SWAP = MODE == 1 && CRV_B2_OUTL_SWAP;
+    constexpr bool EARLY_T = CRV_B2_EARLY_T && (MODE == 0 || (MODE == 1 && (CRV_B2_EARLY_T_OUTL || OUTL_SWAP)));
+    constexpr bool DEFER_CS = CRV_B2_CS_DEFER && !OUTL_SWAP;
     constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
     constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
@@ -1379,7 +1385,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 }
                 if (!CRV_B2_MMA_CS || FIRST) {   // bias sums on the CUDA cores (else: tensor cores)
 #if CRV_B2_CS_DEFER
-                    if (!FIRST || DEFER_FIRST) {
+                    if (DEFER_CS && (!FIRST || DEFER_FIRST)) {
                         level16(v, csd[g2], 1.0f);
                     } else
 #endif
@@ -1399,7 +1405,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         }
 #if CRV_B2_CS_DEFER
         // remaining butterfly levels (8, 4, 2, 1) of the deferred column sums: column = lane
-        if (!FIRST || DEFER_FIRST) {
+        if (DEFER_CS && (!FIRST || DEFER_FIRST)) {
 #pragma unroll
             for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = finish16(csd[g2]);
         }
