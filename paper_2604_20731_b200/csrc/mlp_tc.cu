@@ -903,6 +903,9 @@ struct Bwd2Args {
 #ifndef CRV_OUTL_H2SUM
 #define CRV_OUTL_H2SUM 1   // output-layer sums: rows of a granule column summed in half2 first
 #endif
+#ifndef CRV_B2_DEEP_DELTA
+#define CRV_B2_DEEP_DELTA 0   // middle and g = 0 launches: Delta ring of 2 tiles, t ring of 1 tile
+#endif
 #ifndef CRV_B2_OUTL_SWAP
 #define CRV_B2_OUTL_SWAP 0   // output-layer launch: early t release instead of the deferred bias sums
 #endif
@@ -937,12 +940,14 @@ constexpr int B2_EPI_WARPS = CRV_B2_EPI_WARPS;    // 8 or 16 (4 per TMEM lane qu
 constexpr int B2_EPI_THREADS = 32 * B2_EPI_WARPS;
 constexpr int B2_THREADS = 64 + B2_EPI_THREADS;
 
-template <int WP>
-struct B2 {
+template <int WP, int MODE = 1>
+struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch keeps 1.5 Delta tiles + 2 t tiles:
+              // with one t slot its transform would wait on Delta chunks queued behind t)
     static constexpr int NS = WP / 128;
     static constexpr int KC = WP / 64;
-    static constexpr int DS = KC + CRV_B2_DSX;   // Delta ring slots
-    static constexpr int NT = CRV_B2_NT;         // t ring depth (tiles of 2 chunks)
+    static constexpr bool DEEP = CRV_B2_DEEP_DELTA && (MODE & 1) == 0;
+    static constexpr int DS = KC + (DEEP ? KC : CRV_B2_DSX);   // Delta ring slots (DEEP: 2 tiles)
+    static constexpr int NT = DEEP ? 1 : CRV_B2_NT;           // t ring depth (tiles of 2 chunks)
     static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
@@ -956,8 +961,10 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr bool OUTL_SWAP = MODE == 1 && CRV_B2_OUTL_SWAP;
     constexpr bool EARLY_T = CRV_B2_EARLY_T && (MODE == 0 || (MODE == 1 && (CRV_B2_EARLY_T_OUTL || OUTL_SWAP)));
     constexpr bool DEFER_CS = CRV_B2_CS_DEFER && !OUTL_SWAP;
+    // with a single t slot the t load must not sit in front of the Delta chunks
+    constexpr bool T_FIRST = CRV_T_FIRST && B2<WP, MODE>::NT > 1;
     constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
-    constexpr int NS = B2<WP>::NS, KC = B2<WP>::KC, DS = B2<WP>::DS, NT = B2<WP>::NT;
+    constexpr int NS = B2<WP, MODE>::NS, KC = B2<WP, MODE>::KC, DS = B2<WP, MODE>::DS, NT = B2<WP, MODE>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -1041,7 +1048,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
                 prefetch(k + PD);
                 // t first: its ring is independent of the Delta ring, whose slots free up late
-                if (CRV_T_FIRST) load_t(k, tile);
+                if (T_FIRST) load_t(k, tile);
                 for (int j = 0; j < KC; ++j, ++dn) {
                     const int slot = dn % DS;
                     mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
@@ -1051,7 +1058,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     else if ((uint32_t)(j % NS) == rank)
                         bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], MASK);
                 }
-                if (!CRV_T_FIRST) load_t(k, tile);
+                if (!T_FIRST) load_t(k, tile);
             }
         }
     } else if (warp == 1) {
@@ -2032,10 +2039,10 @@ static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     cudaFuncSetAttribute(k_tc_forward<WP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
-        cudaFuncSetAttribute(k_tc_bwd2<WP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
-        cudaFuncSetAttribute(k_tc_bwd2<WP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
-        cudaFuncSetAttribute(k_tc_bwd2<WP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
-        cudaFuncSetAttribute(k_tc_bwd2<WP, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP, 0>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP, 1>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP, 2>::SMEM);
+        cudaFuncSetAttribute(k_tc_bwd2<WP, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP, 3>::SMEM);
         cudaFuncSetAttribute(k_tc_bwdc<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, BC<WP>::SMEM);
     } else {
         cudaFuncSetAttribute(k_tc_bwd_layer<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd_smem_bytes<WP>());
@@ -2394,10 +2401,10 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 a.trace = trace;
             }
             const int mode = (outl ? 1 : 0) | (g == 0 ? 2 : 0);
-            if (mode == 0) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 0>, a);
-            else if (mode == 1) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 1>, a);
-            else if (mode == 2) cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 2>, a);
-            else cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 3>, a);
+            if (mode == 0) { cfg.dynamicSmemBytes = B2<WP, 0>::SMEM; cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 0>, a); }
+            else if (mode == 1) { cfg.dynamicSmemBytes = B2<WP, 1>::SMEM; cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 1>, a); }
+            else if (mode == 2) { cfg.dynamicSmemBytes = B2<WP, 2>::SMEM; cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 2>, a); }
+            else { cfg.dynamicSmemBytes = B2<WP, 3>::SMEM; cudaLaunchKernelEx(&cfg, k_tc_bwd2<WP, 3>, a); }
             // dW of GEMM g is final: reduce it on the side stream while GEMM g-1 runs
             cudaEventRecord(b.ev_fork[g], s);
             cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
