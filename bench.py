@@ -9,8 +9,10 @@ Adam iterations per second on the named workload (default C5, 512^2 grid, MLP 2-
 value = Adam iterations of all ranks / max-over-ranks device time of the K timed steps,
 inputs resident in HBM (device-side S). e2e = the same metric through the C ABI with host
 buffers (H2D of S and D2H of the 100-entry loss history inside every step).
-Multi-GPU: the update does not shard across GPUs in this round ("replicas only",
-DESIGN.md §7): each rank runs an independent problem, scaling "weak".
+Multi-GPU: by default each rank runs an independent problem (replicas, scaling
+"weak"); --shard splits ONE problem's MLP points over the ranks with two
+in-graph NCCL all-reduces per Adam iteration (u after the forward, the gradient after the
+backward), scaling "strong".
 --impl reference times the fp64 CPU oracle (the reference arm of this tier) on the same config.
 """
 from __future__ import annotations
@@ -47,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one problem, MLP points split over the ranks (strong scaling, NCCL exchanges)")
     return ap.parse_args()
 
 
@@ -221,8 +225,13 @@ def run_ours(args, rank, world, local):
     F = W.make_fields(args.workload)
     w = F.workload
     stream = torch.cuda.Stream(device=torch.device("cuda", local))
+    shard_kw, tile_frac = {}, 1.0
+    if args.shard:
+        nid = crv.share_nccl_id() if dist else crv.nccl_unique_id()
+        shard_kw = dict(shard=(rank, world), nccl_id=nid)
+        tile_frac = crv.shard_tiles(w.N, rank, world)[1] / (w.N * w.N // 128)
     g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=prec, lr=w.lr, device=local,
-                    stream=stream.cuda_stream)
+                    stream=stream.cuda_stream, **shard_kw)
     S_dev = [torch.from_numpy(s).to(f"cuda:{local}") for s in F.S_steps]
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     torch.cuda.synchronize()
@@ -270,7 +279,7 @@ def run_ours(args, rank, world, local):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
-    iters_total = world * args.steps * ITERS_PER_STEP
+    iters_total = (1 if args.shard else world) * args.steps * ITERS_PER_STEP
     value = iters_total / (t_max / 1e3)
 
     # e2e through the public API with host buffers
@@ -298,7 +307,7 @@ def run_ours(args, rank, world, local):
         return 0
 
     peaks, peak_src = measured_peaks()
-    flops = alg_flops_per_iter(w)
+    flops = alg_flops_per_iter(w) * tile_frac     # this rank's share of the MLP points
     mlp_ms = (stage_ms[0] + stage_ms[2]) / max(prof_iters, 1)
     achieved_tf = flops / (mlp_ms * 1e-3) / 1e12
     if prec == crv.PREC_TENSOR:
@@ -325,13 +334,13 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": f"CRVPINN Adam iters/s ({args.workload})", "value": value, "unit": "Adam iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.shard else "weak", "vs_baseline": None,
         "dtype": "f16" if prec == crv.PREC_TENSOR else "f32", "data": "synthetic",
-        "config": dict(workload_config(args.workload, args.precision), parallelism=f"replicas{world}"),
+        "config": dict(workload_config(args.workload, args.precision), parallelism=f"points{world}" if args.shard else f"replicas{world}"),
         "points_iters_per_s": value * w.points,
         "roofline": {"bound": bound, "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak,
-                     "traffic": MLP_DRAM_BYTES_PER_ITER if args.workload == "C5" else None,
+                     "traffic": MLP_DRAM_BYTES_PER_ITER if args.workload == "C5" and not args.shard else None,
                      "kernel": "MLP forward + backward (A1, A6-A7), per Adam iteration",
                      "alg_flops_per_iter": flops, "peak_source": peak_note,
                      "traffic_note": ("per-iteration DRAM bytes (read + write) of the MLP kernels from one ncu --set full "

@@ -76,6 +76,24 @@ typedef struct {
      * gamma = K beta. Recomputed with alpha on every set_saturation. */
     double gravity;         /* non-dimensional gravity number, default 0 (the configs have none, R11) */
     double density_ratio;   /* rho_g/rho_w, default 479/1045 (Table 1) */
+    /* Point sharding across GPUs. The MLP points (the
+     * set the loss sums over) split into shard_world contiguous ranges of
+     * 128-point tiles (crvpinn_shard_tiles); this context runs the forward and backward of range
+     * shard_rank only. One Adam iteration then exchanges twice: an all-reduce (sum) of the
+     * lattice field u after the forward (each shard writes its own points into a zeroed field,
+     * so the sum is the whole field exactly), and an all-reduce (sum) of the gradient after the
+     * backward. Stencil, Gram solve, loss and Adam run replicated on every shard. Tensor path
+     * only. Default shard_rank 0, shard_world 1 (unsharded). */
+    int shard_rank;
+    int shard_world;
+    /* nccl = 1: the context creates an NCCL communicator (rank shard_rank of shard_world) from
+     * nccl_id (crvpinn_nccl_unique_id on one rank, shared by the caller) and issues the two
+     * all-reduces inside every iteration (and inside the captured graphs). Allowed at
+     * shard_world 1. nccl = 0 with shard_world > 1: the caller exchanges, using
+     * crvpinn_shard_forward / crvpinn_shard_backward; crvpinn_step and crvpinn_loss_grad then
+     * fail with EINVAL. libnccl.so.2 is loaded on first use (dlopen), not at library load. */
+    int nccl;
+    unsigned char nccl_id[128];
 } crvpinn_opts;
 
 /* Fill *o with the defaults listed above. */
@@ -168,6 +186,27 @@ void *crvpinn_stream(const crvpinn_ctx *ctx);
 const char *crvpinn_last_error(const crvpinn_ctx *ctx);   /* ctx may be NULL (global error) */
 
 void crvpinn_destroy(crvpinn_ctx *ctx);
+
+/* ------------------------------------------------------------ point sharding (f4) */
+/* Shard r of w over an N x N point set: tiles [*tile0, *tile0 + *ntiles) of T = N*N/128, the
+ * balanced split tile0 = floor(r T / w) (shards differ by at most one tile). Pure host
+ * arithmetic (no device needed). EINVAL unless N is a power of two in [16, 2048] and
+ * 0 <= r < w <= T. */
+int crvpinn_shard_tiles(int N, int rank, int world, long *tile0, long *ntiles);
+
+/* A fresh NCCL unique id (ncclGetUniqueId) for opts.nccl_id, to be created on one rank and sent
+ * to the others by the caller. ECUDA if libnccl.so.2 cannot be loaded. */
+int crvpinn_nccl_unique_id(unsigned char id[128]);
+
+/* The two halves of one iteration around the exchange, for callers that move the data
+ * themselves (and for single-GPU tests of a sharded decomposition). No collective is issued.
+ * shard_forward: u_part (host, (N+1)^2 floats) = this shard's points of u = cutoff * net, zero
+ * at every other node. shard_backward: given the whole field u_full (host, the sum of every
+ * shard's u_part), runs A2-A5 (replicated) and the backward of this shard's points: *loss = the
+ * loss of u_full, grad_part (host, num_params floats) = this shard's share of dLOSS/dtheta
+ * (the gradient is the sum of the shares). theta and the Adam state do not change. */
+int crvpinn_shard_forward(crvpinn_ctx *ctx, float *u_part);
+int crvpinn_shard_backward(crvpinn_ctx *ctx, const float *u_full, double *loss, float *grad_part);
 
 /* ========================================================================== IGA-ADS (f3)
  * the explicit saturation step of IGA-ADS on the GPU (§3-§4), the

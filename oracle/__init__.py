@@ -61,6 +61,8 @@ def lib():
         L.orc_eval_points.argtypes = [P, D, ctypes.c_long, D, D]
         L.orc_set_saturation.argtypes = [P, F, F]
         L.orc_forward.argtypes = [P, D, D]
+        L.orc_forward_rows.argtypes = [P, D, ctypes.c_int, ctypes.c_int, D]
+        L.orc_grad_rows.argtypes = [P, D, D, ctypes.c_int, ctypes.c_int, D]
         L.orc_residual.argtypes = [P, D, D]
         L.orc_residual_adjoint.argtypes = [P, D, D]
         L.orc_gram_solve.argtypes = [P, D, D]
@@ -185,6 +187,21 @@ class Oracle:
         u = np.empty((self.N + 1) ** 2)
         lib().orc_forward(self._h, _dp(th), _dp(u))
         return u
+
+    def forward_rows(self, j0: int, j1: int, theta=None) -> np.ndarray:
+        """u at the interior nodes of rows j in [j0, j1), zero elsewhere (one shard's forward)."""
+        th = self.theta if theta is None else np.ascontiguousarray(theta, dtype=np.float64)
+        u = np.empty((self.N + 1) ** 2)
+        lib().orc_forward_rows(self._h, _dp(th), int(j0), int(j1), _dp(u))
+        return u
+
+    def grad_rows(self, gu, j0: int, j1: int, theta=None) -> np.ndarray:
+        """dLOSS/dtheta over the MLP points of rows [j0, j1), given gu = dLOSS/du (one shard's backward)."""
+        th = self.theta if theta is None else np.ascontiguousarray(theta, dtype=np.float64)
+        gu = np.ascontiguousarray(gu, dtype=np.float64)
+        g = np.empty(self.np)
+        lib().orc_grad_rows(self._h, _dp(th), _dp(gu), int(j0), int(j1), _dp(g))
+        return g
 
     def residual(self, u) -> np.ndarray:
         u = np.ascontiguousarray(u, dtype=np.float64)

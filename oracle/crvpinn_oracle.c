@@ -330,16 +330,18 @@ static void free_act(const orc_ctx *c, double **a) {
     free(a);
 }
 
-/* u on the full (N+1)^2 lattice; boundary nodes are exactly 0 (cutoff). */
-void orc_forward(const orc_ctx *c, const double *th, double *u) {
+/* u at the interior nodes of rows j in [j0, j1) (clipped to [1, N-1]); every other node 0. */
+void orc_forward_rows(const orc_ctx *c, const double *th, int j0, int j1, double *u) {
     int N = c->N;
     long nn = (long)(N + 1) * (N + 1);
     for (long p = 0; p < nn; ++p) u[p] = 0.0;
+    if (j0 < 1) j0 = 1;
+    if (j1 > N) j1 = N;
 #pragma omp parallel
     {
         double **act = alloc_act(c);
 #pragma omp for schedule(static)
-        for (int j = 1; j < N; ++j)
+        for (int j = j0; j < j1; ++j)
             for (int i = 1; i < N; ++i) {
                 double x = (double)i / N, y = (double)j / N;
                 u[idx(c, i, j)] = cutoff(x, y) * net_point(c, th, x, y, act);
@@ -347,6 +349,9 @@ void orc_forward(const orc_ctx *c, const double *th, double *u) {
         free_act(c, act);
     }
 }
+
+/* u on the full (N+1)^2 lattice; boundary nodes are exactly 0 (cutoff). */
+void orc_forward(const orc_ctx *c, const double *th, double *u) { orc_forward_rows(c, th, 1, c->N, u); }
 
 /* Continuous evaluation at arbitrary points: out[p] = cutoff(x_p, y_p) net(x_p, y_p). */
 void orc_eval_points(const orc_ctx *c, const double *th, long n, const double *xy, double *out) {
@@ -427,6 +432,65 @@ double orc_loss_u(const orc_ctx *c, const double *u, double *res_out, double *q_
 }
 
 /* ---------------------------------------------------------------- A1-A6: loss and gradient */
+/* dLOSS/dtheta summed over the MLP points of rows j in [j0, j1) (clipped to [1, N-1]), given
+ * gu = dLOSS/du on the lattice: the chain rule through u = cutoff * net (A6, backpropagation). */
+void orc_grad_rows(const orc_ctx *c, const double *th, const double *gu, int j0, int j1, double *grad) {
+    int N = c->N;
+    if (j0 < 1) j0 = 1;
+    if (j1 > N) j1 = N;
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = omp_get_max_threads();
+#endif
+    long np = c->np;
+    double *part = (double *)calloc((size_t)nthr * np, sizeof(double));
+    int w = max_width(c);
+#pragma omp parallel num_threads(nthr)
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        double *g = part + (long)tid * np;
+        double **act = alloc_act(c);
+        double *dl = (double *)malloc(sizeof(double) * w);   /* delta of current layer */
+        double *dp = (double *)malloc(sizeof(double) * w);   /* delta of previous layer */
+#pragma omp for schedule(static)
+        for (int j = j0; j < j1; ++j)
+            for (int i = 1; i < N; ++i) {
+                double x = (double)i / N, y = (double)j / N;
+                net_point(c, th, x, y, act);
+                /* u = cutoff * net  =>  dLOSS/dnet = gu * cutoff */
+                dl[0] = gu[idx(c, i, j)] * cutoff(x, y);
+                for (int l = c->nl - 1; l >= 0; --l) {
+                    int fin = c->widths[l], fout = c->widths[l + 1];
+                    const double *W = th + c->woff[l];
+                    double *gW = g + c->woff[l], *gb = g + c->boff[l];
+                    for (int r = 0; r < fout; ++r) {
+                        gb[r] += dl[r];
+                        for (int k = 0; k < fin; ++k) gW[(long)r * fin + k] += dl[r] * act[l][k];
+                    }
+                    if (l > 0) {
+                        for (int k = 0; k < fin; ++k) {
+                            double s = 0.0;
+                            for (int r = 0; r < fout; ++r) s += W[(long)r * fin + k] * dl[r];
+                            dp[k] = s * (1.0 - act[l][k] * act[l][k]);   /* tanh' */
+                        }
+                        double *tmp = dl; dl = dp; dp = tmp;
+                    }
+                }
+            }
+        free(dl); free(dp);
+        free_act(c, act);
+    }
+    for (long k = 0; k < np; ++k) {
+        double s = 0.0;
+        for (int t = 0; t < nthr; ++t) s += part[(long)t * np + k];   /* thread order */
+        grad[k] = s;
+    }
+    free(part);
+}
+
 double orc_loss_grad(const orc_ctx *c, const double *th_in, double *grad,
                      double *u_out, double *res_out, double *q_out, double *gu_out) {
     int N = c->N;
@@ -443,59 +507,7 @@ double orc_loss_grad(const orc_ctx *c, const double *th_in, double *grad,
     for (long i = 0; i < n2; ++i) w2[i] = 2.0 * q[i];
     orc_residual_adjoint(c, w2, gu);
     free(w2);
-    if (grad) {
-        int nthr = 1;
-#ifdef _OPENMP
-        nthr = omp_get_max_threads();
-#endif
-        long np = c->np;
-        double *part = (double *)calloc((size_t)nthr * np, sizeof(double));
-        int w = max_width(c);
-#pragma omp parallel num_threads(nthr)
-        {
-            int tid = 0;
-#ifdef _OPENMP
-            tid = omp_get_thread_num();
-#endif
-            double *g = part + (long)tid * np;
-            double **act = alloc_act(c);
-            double *dl = (double *)malloc(sizeof(double) * w);   /* delta of current layer */
-            double *dp = (double *)malloc(sizeof(double) * w);   /* delta of previous layer */
-#pragma omp for schedule(static)
-            for (int j = 1; j < N; ++j)
-                for (int i = 1; i < N; ++i) {
-                    double x = (double)i / N, y = (double)j / N;
-                    net_point(c, th, x, y, act);
-                    /* u = cutoff * net  =>  dLOSS/dnet = gu * cutoff */
-                    dl[0] = gu[idx(c, i, j)] * cutoff(x, y);
-                    for (int l = c->nl - 1; l >= 0; --l) {
-                        int fin = c->widths[l], fout = c->widths[l + 1];
-                        const double *W = th + c->woff[l];
-                        double *gW = g + c->woff[l], *gb = g + c->boff[l];
-                        for (int r = 0; r < fout; ++r) {
-                            gb[r] += dl[r];
-                            for (int k = 0; k < fin; ++k) gW[(long)r * fin + k] += dl[r] * act[l][k];
-                        }
-                        if (l > 0) {
-                            for (int k = 0; k < fin; ++k) {
-                                double s = 0.0;
-                                for (int r = 0; r < fout; ++r) s += W[(long)r * fin + k] * dl[r];
-                                dp[k] = s * (1.0 - act[l][k] * act[l][k]);   /* tanh' */
-                            }
-                            double *tmp = dl; dl = dp; dp = tmp;
-                        }
-                    }
-                }
-            free(dl); free(dp);
-            free_act(c, act);
-        }
-        for (long k = 0; k < np; ++k) {
-            double s = 0.0;
-            for (int t = 0; t < nthr; ++t) s += part[(long)t * np + k];   /* thread order */
-            grad[k] = s;
-        }
-        free(part);
-    }
+    if (grad) orc_grad_rows(c, th, gu, 1, N, grad);
     if (!u_out) free(u);
     if (!res_out) free(res);
     if (!q_out) free(q);

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -27,6 +27,7 @@ EXPORTS = [
     "crvpinn_num_params", "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
     "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter", "crvpinn_stream",
     "crvpinn_last_error", "crvpinn_destroy",
+    "crvpinn_shard_tiles", "crvpinn_nccl_unique_id", "crvpinn_shard_forward", "crvpinn_shard_backward",
     "crvpinn_iga_create", "crvpinn_iga_num_basis", "crvpinn_iga_num_quad_points", "crvpinn_iga_quad_points",
     "crvpinn_iga_project", "crvpinn_iga_saturation_step", "crvpinn_iga_eval", "crvpinn_iga_last_ms",
     "crvpinn_iga_last_error", "crvpinn_iga_destroy",
@@ -43,7 +44,9 @@ class Opts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
                 ("eps", ctypes.c_double), ("mobility_ratio", ctypes.c_double), ("precision", ctypes.c_int),
                 ("seed", ctypes.c_uint64), ("stream", ctypes.c_void_p), ("device", ctypes.c_int),
-                ("gravity", ctypes.c_double), ("density_ratio", ctypes.c_double)]
+                ("gravity", ctypes.c_double), ("density_ratio", ctypes.c_double),
+                ("shard_rank", ctypes.c_int), ("shard_world", ctypes.c_int), ("nccl", ctypes.c_int),
+                ("nccl_id", ctypes.c_ubyte * 128)]
 
 
 _lib = None
@@ -85,11 +88,16 @@ def load(path: str = LIB_PATH):
     L.crvpinn_last_error.restype = ctypes.c_char_p
     L.crvpinn_last_error.argtypes = [P]
     L.crvpinn_destroy.argtypes = [P]
+    L.crvpinn_shard_tiles.argtypes = [I, I, I, ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)]
+    L.crvpinn_nccl_unique_id.argtypes = [ctypes.POINTER(ctypes.c_ubyte)]
+    L.crvpinn_shard_forward.argtypes = [P, F]
+    L.crvpinn_shard_backward.argtypes = [P, F, D, F]
     for name in ["crvpinn_create", "crvpinn_set_saturation", "crvpinn_set_saturation_device", "crvpinn_pretrain",
                  "crvpinn_step", "crvpinn_eval", "crvpinn_eval_points", "crvpinn_direct_solve", "crvpinn_loss_grad",
                  "crvpinn_get_intermediates",
                  "crvpinn_get_params", "crvpinn_set_params", "crvpinn_get_adam", "crvpinn_set_adam",
-                 "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter"]:
+                 "crvpinn_set_profiling", "crvpinn_get_profile", "crvpinn_launches_per_iter",
+                 "crvpinn_shard_tiles", "crvpinn_nccl_unique_id", "crvpinn_shard_forward", "crvpinn_shard_backward"]:
         getattr(L, name).restype = I
     L.crvpinn_iga_create.argtypes = [ctypes.POINTER(P), I, I, I]
     L.crvpinn_iga_create.restype = I
@@ -130,13 +138,41 @@ def default_opts() -> Opts:
     return o
 
 
+def shard_tiles(N: int, rank: int, world: int):
+    """(tile0, ntiles): shard `rank` of `world` over the N*N/128 MLP tiles (crvpinn_shard_tiles; host only)."""
+    t0, nt = ctypes.c_long(), ctypes.c_long()
+    rc = load().crvpinn_shard_tiles(int(N), int(rank), int(world), ctypes.byref(t0), ctypes.byref(nt))
+    if rc != 0:
+        raise CrvpinnError(rc, load().crvpinn_last_error(None).decode())
+    return int(t0.value), int(nt.value)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for Crvpinn(shard=..., nccl_id=...)."""
+    buf = (ctypes.c_ubyte * 128)()
+    rc = load().crvpinn_nccl_unique_id(buf)
+    if rc != 0:
+        raise CrvpinnError(rc, load().crvpinn_last_error(None).decode())
+    return bytes(buf)
+
+
+def share_nccl_id(group=None, src: int = 0, make_id=None) -> bytes:
+    """Rank `src` of the torch.distributed group creates the id, every rank returns it (plumbing only)."""
+    import torch.distributed as dist
+    obj = [(make_id or nccl_unique_id)() if dist.get_rank() == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
 class Crvpinn:
-    """One CRVPINN problem on one GPU (wraps crvpinn_ctx)."""
+    """One CRVPINN problem on one GPU (wraps crvpinn_ctx). shard=(rank, world) runs this GPU's share of
+    the MLP points; with nccl_id the context exchanges u and the gradient itself."""
 
     def __init__(self, N: int, widths: Sequence[int], K, S, f, theta0=None, *, precision: int = PREC_TENSOR,
                  lr: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  mobility_ratio: Optional[float] = None, seed: int = 0, stream: Optional[int] = None,
-                 device: int = 0, gravity: float = 0.0, density_ratio: Optional[float] = None):
+                 device: int = 0, gravity: float = 0.0, density_ratio: Optional[float] = None,
+                 shard: Optional[Tuple[int, int]] = None, nccl_id: Optional[bytes] = None):
         L = load()
         self.N = int(N)
         self.widths = tuple(int(w) for w in widths)
@@ -150,6 +186,14 @@ class Crvpinn:
         if density_ratio is not None:
             o.density_ratio = density_ratio
         o.stream = stream
+        if shard is not None:
+            o.shard_rank, o.shard_world = int(shard[0]), int(shard[1])
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            o.nccl = 1
+            ctypes.memmove(o.nccl_id, nccl_id, 128)
+        self.shard = (o.shard_rank, o.shard_world)
         w = (ctypes.c_int * len(self.widths))(*self.widths)
         K, S, f = _f32(K, nn), _f32(S, nn), _f32(f, nn)
         th = None if theta0 is None else _f32(theta0)
@@ -220,6 +264,20 @@ class Crvpinn:
         g = np.empty(self.np, np.float32) if grad else None
         self._check(load().crvpinn_loss_grad(self._h, ctypes.byref(loss), None if g is None else _fp(g)))
         return (loss.value, g) if grad else loss.value
+
+    def shard_forward(self) -> np.ndarray:
+        """This shard's points of u (zero elsewhere), lattice (N+1)^2; no collective."""
+        out = np.empty((self.N + 1) ** 2, np.float32)
+        self._check(load().crvpinn_shard_forward(self._h, _fp(out)))
+        return out
+
+    def shard_backward(self, u_full):
+        """(loss of u_full, this shard's share of the gradient); no collective."""
+        u = _f32(u_full, (self.N + 1) ** 2)
+        loss = ctypes.c_double()
+        g = np.empty(self.np, np.float32)
+        self._check(load().crvpinn_shard_backward(self._h, _fp(u), ctypes.byref(loss), _fp(g)))
+        return loss.value, g
 
     def intermediates(self):
         nn, n2 = (self.N + 1) ** 2, (self.N - 1) ** 2

@@ -4,10 +4,14 @@
 #include "common.cuh"
 #include "mlp_tc.cuh"
 
+#include <dlfcn.h>
+#include <nccl.h>   // types only: libnccl.so.2 is opened on first use (sharded contexts)
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -16,6 +20,50 @@ using namespace crv;
 namespace {
 
 std::string g_err;   // errors raised before a context exists
+
+// NCCL entry points, resolved from libnccl.so.2 at the first sharded create / unique-id call. The
+// library itself has no link-time NCCL dependency (a process that already loaded torch's NCCL gets
+// that same copy: dlopen matches the soname).
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string err;
+    ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char *(*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bool nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        const char *e = dlerror();
+        g_nccl.err = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+        return false;
+    }
+    g_nccl.get_unique_id = (decltype(g_nccl.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    g_nccl.comm_init_rank = (decltype(g_nccl.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    g_nccl.all_reduce = (decltype(g_nccl.all_reduce))dlsym(h, "ncclAllReduce");
+    g_nccl.comm_destroy = (decltype(g_nccl.comm_destroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.all_reduce && g_nccl.comm_destroy &&
+                g_nccl.error_string;
+    if (!g_nccl.ok) g_nccl.err = "libnccl.so.2 lacks ncclGetUniqueId/ncclCommInitRank/ncclAllReduce";
+    return g_nccl.ok;
+}
+
+// balanced split of T tiles over w shards (crvpinn_shard_tiles)
+void shard_split(long T, int r, int w, long &t0, long &nt) {
+    t0 = (long)((long long)r * T / w);
+    nt = (long)((long long)(r + 1) * T / w) - t0;
+}
 
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -61,6 +109,11 @@ struct crvpinn_ctx {
     // crvpinn_eval_points scratch (device xy [cap][2] + p [cap]), grown on demand
     float *pts = nullptr;
     long pts_cap = 0;
+    // point sharding (f4): this context's tiles, and the communicator of the two exchanges
+    long tile0 = 0, ntiles = 0;
+    bool sharded = false;          // shard_world > 1 or a communicator: u is zeroed before the forward
+    ncclComm_t comm = nullptr;
+    ncclResult_t nccl_rc = ncclSuccess;   // first failed NCCL call of a launch sequence
 };
 
 #define CK(call)                                                                 \
@@ -103,14 +156,33 @@ static int dalloc(crvpinn_ctx *ctx, T **p, size_t count) {
 // capture only expresses a dependency and is never executed as a timestamp).
 static void record(cudaEvent_t e, cudaStream_t s) { cudaEventRecordWithFlags(e, s, cudaEventRecordExternal); }
 
-static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool train, cudaEvent_t *ev) {
+// sum over the shards, in place, on the context stream (a no-op without a communicator)
+static void exchange(crvpinn_ctx *ctx, float *buf, size_t count) {
+    if (!ctx->comm) return;
+    ncclResult_t r = g_nccl.all_reduce(buf, buf, count, ncclFloat32, ncclSum, ctx->comm, ctx->stream);
+    if (r != ncclSuccess && ctx->nccl_rc == ncclSuccess) ctx->nccl_rc = r;
+}
+
+static size_t lattice_count(const crvpinn_ctx *ctx) { return (size_t)(ctx->net.N + 1) * (ctx->net.N + 1); }
+
+// A1 on this context's points (all of them unsharded); sharded: into a zeroed field
+static void launch_forward(crvpinn_ctx *ctx) {
+    cudaStream_t s = ctx->stream;
+    if (ctx->sharded) cudaMemsetAsync(ctx->u, 0, sizeof(float) * lattice_count(ctx), s);
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_forward(ctx->net, ctx->tc, ctx->u, s);
+    else simt_forward(ctx->net, ctx->theta, ctx->simt, ctx->u, s);
+}
+
+// fwd = false: u is already in place (crvpinn_shard_backward); xchg: the two all-reduces
+static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool train, cudaEvent_t *ev,
+                             bool fwd = true, bool xchg = true) {
     cudaStream_t s = ctx->stream;
     const Net &net = ctx->net;
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
     if (ev) record(ev[0], s);
-    // A1: network at every MLP point -> u on the lattice
-    if (tc) tc_forward(net, ctx->tc, ctx->u, s);
-    else simt_forward(net, ctx->theta, ctx->simt, ctx->u, s);
+    // A1: network at every MLP point of this shard -> u on the lattice; sharded: sum over shards
+    if (fwd) launch_forward(ctx);
+    if (fwd && xchg) exchange(ctx, ctx->u, lattice_count(ctx));
     if (ev) record(ev[1], s);
     // A2-A5: residual, Gram solve, loss, adjoint
     float *gbar = tc ? ctx->tc.gbar : ctx->simt.gbar;
@@ -120,6 +192,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
     // A6-A7: backward and deterministic weight-gradient reduction
     if (tc) tc_backward(net, ctx->tc, ctx->st, ctx->grad, s);
     else simt_backward(net, ctx->plan, ctx->theta, ctx->simt, ctx->grad, s);
+    if (xchg) exchange(ctx, ctx->grad, (size_t)ctx->np);   // each shard holds its points' share
     if (ev) record(ev[3], s);
     // A8: Adam (+ refresh of the tensor-core weight copies)
     if (train) {
@@ -137,6 +210,7 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
 static int launches_per_iter(const crvpinn_ctx *ctx) {
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
     int mlp = tc ? tc_launches(ctx->net, ctx->tc) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
+    // (sharded: + the memset of u and the two NCCL all-reduce kernels, which are not ours)
     return mlp + 4 /*residual+DST, tridiagonal, inverse DST+loss, adjoint+loss final*/ + 1 /*adam*/;
 }
 
@@ -177,6 +251,11 @@ static int get_graph(crvpinn_ctx *ctx, int n, GraphEntry **out) {
         launch_iteration(ctx, ge.hist, n, true, ctx->profiling ? &ge.ev[(size_t)5 * k] : nullptr);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     if (rc != CRVPINN_OK) return rc;
+    if (ctx->nccl_rc != ncclSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return fail(ctx, CRVPINN_ECUDA, std::string("NCCL all-reduce in graph capture: ") +
+                                            g_nccl.error_string(ctx->nccl_rc));
+    }
     if (e != cudaSuccess) return fail(ctx, CRVPINN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&ge.exec, g, 0);
     cudaGraphDestroy(g);
@@ -228,6 +307,10 @@ void crvpinn_default_opts(crvpinn_opts *o) {
     o->device = 0;
     o->gravity = 0.0;
     o->density_ratio = 479.0 / 1045.0;
+    o->shard_rank = 0;
+    o->shard_world = 1;
+    o->nccl = 0;
+    memset(o->nccl_id, 0, sizeof(o->nccl_id));
 }
 
 const char *crvpinn_last_error(const crvpinn_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
@@ -243,6 +326,7 @@ void crvpinn_destroy(crvpinn_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     drop_graphs(ctx);
+    if (ctx->comm) g_nccl.comm_destroy(ctx->comm);
     gram_free_constants(ctx->gram);
     tc_destroy(ctx->tc);
     if (ctx->pts) cudaFree(ctx->pts);
@@ -310,7 +394,7 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
         CK(cudaMemcpy(ctx->d_jobs, ctx->plan.jobs, sizeof(RedJob) * ctx->plan.njobs, cudaMemcpyHostToDevice));
         ctx->simt.jobs = ctx->d_jobs;
     } else {
-        int rc = tc_create(net, ctx->tc, ctx->err);
+        int rc = tc_create(net, ctx->tc, (int)ctx->tile0, (int)ctx->ntiles, ctx->err);
         if (rc != 0) return rc;
     }
     // ---- inputs, A0, Gram constants
@@ -339,6 +423,16 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
+    // ---- the shards' communicator (collective: every rank creates its context concurrently)
+    if (ctx->opts.nccl) {
+        ncclUniqueId id;
+        memcpy(&id, ctx->opts.nccl_id, sizeof(id) < 128 ? sizeof(id) : 128);
+        ncclResult_t r = g_nccl.comm_init_rank(&ctx->comm, ctx->opts.shard_world, id, ctx->opts.shard_rank);
+        if (r != ncclSuccess) {
+            ctx->comm = nullptr;
+            return fail(ctx, CRVPINN_ECUDA, std::string("ncclCommInitRank: ") + g_nccl.error_string(r));
+        }
+    }
     return CRVPINN_OK;
 }
 
@@ -355,6 +449,24 @@ int crvpinn_create(crvpinn_ctx **out, int N, int n_widths, const int *widths, co
             return fail(nullptr, CRVPINN_EINVAL, "hidden widths must be multiples of 32 in [32, 256]");
     crvpinn_ctx *ctx = new crvpinn_ctx();
     if (opts) ctx->opts = *opts; else crvpinn_default_opts(&ctx->opts);
+    {
+        const int w = ctx->opts.shard_world, r = ctx->opts.shard_rank;
+        const long T = (long)N * N / 128;
+        if (w < 1 || r < 0 || r >= w || w > T) {
+            delete ctx;
+            return fail(nullptr, CRVPINN_EINVAL, "need 0 <= shard_rank < shard_world <= N*N/128");
+        }
+        if (w > 1 && ctx->opts.precision != CRVPINN_PREC_TENSOR) {
+            delete ctx;
+            return fail(nullptr, CRVPINN_EINVAL, "point sharding needs the tensor path");
+        }
+        if (ctx->opts.nccl && !nccl_load()) {
+            delete ctx;
+            return fail(nullptr, CRVPINN_ECUDA, g_nccl.err);
+        }
+        shard_split(T, r, w, ctx->tile0, ctx->ntiles);
+        ctx->sharded = w > 1 || ctx->opts.nccl;
+    }
     if (!std::isfinite(ctx->opts.gravity) || !std::isfinite(ctx->opts.density_ratio) || ctx->opts.density_ratio < 0.0)
         return fail(nullptr, CRVPINN_EINVAL, "gravity / density_ratio must be finite (density_ratio >= 0)");
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) {
@@ -406,8 +518,12 @@ int crvpinn_set_saturation_device(crvpinn_ctx *ctx, const void *S_dev) {
     return CRVPINN_OK;
 }
 
+static bool needs_caller_exchange(const crvpinn_ctx *ctx) { return ctx->opts.shard_world > 1 && !ctx->comm; }
+
 int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist) {
     if (!ctx || n_adam < 1) return fail(ctx, CRVPINN_EINVAL, "n_adam must be >= 1");
+    if (needs_caller_exchange(ctx))
+        return fail(ctx, CRVPINN_EINVAL, "sharded context without a communicator: use crvpinn_shard_forward/backward");
     CK(cudaSetDevice(ctx->device));
     GraphEntry *ge = nullptr;
     int rc = get_graph(ctx, n_adam, &ge);
@@ -450,8 +566,11 @@ int crvpinn_pretrain(crvpinn_ctx *ctx, int n_iters, double *loss_hist) {
 int crvpinn_eval(crvpinn_ctx *ctx, float *p_out) {
     if (!ctx || !p_out) return fail(ctx, CRVPINN_EINVAL, "null argument");
     CK(cudaSetDevice(ctx->device));
-    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_forward(ctx->net, ctx->tc, ctx->u, ctx->stream);
-    else simt_forward(ctx->net, ctx->theta, ctx->simt, ctx->u, ctx->stream);
+    ctx->nccl_rc = ncclSuccess;
+    launch_forward(ctx);
+    exchange(ctx, ctx->u, lattice_count(ctx));
+    if (ctx->nccl_rc != ncclSuccess)
+        return fail(ctx, CRVPINN_ECUDA, std::string("NCCL all-reduce: ") + g_nccl.error_string(ctx->nccl_rc));
     size_t nn = (size_t)(ctx->net.N + 1) * (ctx->net.N + 1);
     CK(cudaMemcpyAsync(ctx->h_field, ctx->u, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -518,9 +637,14 @@ int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_o
 
 int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad) {
     if (!ctx || !loss) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    if (needs_caller_exchange(ctx))
+        return fail(ctx, CRVPINN_EINVAL, "sharded context without a communicator: use crvpinn_shard_forward/backward");
     CK(cudaSetDevice(ctx->device));
+    ctx->nccl_rc = ncclSuccess;
     launch_begin_call(ctx->st, ctx->stream);
     launch_iteration(ctx, nullptr, 0, false, nullptr);
+    if (ctx->nccl_rc != ncclSuccess)
+        return fail(ctx, CRVPINN_ECUDA, std::string("NCCL all-reduce: ") + g_nccl.error_string(ctx->nccl_rc));
     CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
     if (grad) CK(cudaMemcpyAsync(grad, ctx->grad, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -602,6 +726,57 @@ int crvpinn_get_profile(crvpinn_ctx *ctx, double *ms_sum, int64_t *n_iters, int 
         for (int s = 0; s < 4; ++s) ctx->prof_ms[s] = 0.0;
         ctx->prof_iters = 0;
     }
+    return CRVPINN_OK;
+}
+
+int crvpinn_shard_tiles(int N, int rank, int world, long *tile0, long *ntiles) {
+    if (!tile0 || !ntiles) return fail(nullptr, CRVPINN_EINVAL, "null argument");
+    if (!is_pow2(N) || N < 16 || N > 2048) return fail(nullptr, CRVPINN_EINVAL, "N must be a power of two in [16, 2048]");
+    const long T = (long)N * N / 128;
+    if (world < 1 || rank < 0 || rank >= world || world > T)
+        return fail(nullptr, CRVPINN_EINVAL, "need 0 <= rank < world <= N*N/128");
+    shard_split(T, rank, world, *tile0, *ntiles);
+    return CRVPINN_OK;
+}
+
+int crvpinn_nccl_unique_id(unsigned char id[128]) {
+    if (!id) return fail(nullptr, CRVPINN_EINVAL, "null argument");
+    if (!nccl_load()) return fail(nullptr, CRVPINN_ECUDA, g_nccl.err);
+    ncclUniqueId u;
+    ncclResult_t r = g_nccl.get_unique_id(&u);
+    if (r != ncclSuccess) return fail(nullptr, CRVPINN_ECUDA, std::string("ncclGetUniqueId: ") + g_nccl.error_string(r));
+    memset(id, 0, 128);
+    memcpy(id, &u, sizeof(u) < 128 ? sizeof(u) : 128);
+    return CRVPINN_OK;
+}
+
+int crvpinn_shard_forward(crvpinn_ctx *ctx, float *u_part) {
+    if (!ctx || !u_part) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    const size_t nn = lattice_count(ctx);
+    if (!ctx->sharded) CK(cudaMemsetAsync(ctx->u, 0, sizeof(float) * nn, ctx->stream));
+    launch_forward(ctx);
+    CK(cudaMemcpyAsync(ctx->h_field, ctx->u, sizeof(float) * nn, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    memcpy(u_part, ctx->h_field, sizeof(float) * nn);
+    return CRVPINN_OK;
+}
+
+int crvpinn_shard_backward(crvpinn_ctx *ctx, const float *u_full, double *loss, float *grad_part) {
+    if (!ctx || !u_full || !loss) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    int rc = upload_field(ctx, ctx->u, u_full);
+    if (rc) return rc;
+    launch_begin_call(ctx->st, ctx->stream);
+    launch_iteration(ctx, nullptr, 0, false, nullptr, /*fwd=*/false, /*xchg=*/false);
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    if (grad_part)
+        CK(cudaMemcpyAsync(grad_part, ctx->grad, sizeof(float) * ctx->np, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    *loss = ctx->h_state->loss;
+    if (!std::isfinite(*loss)) return fail(ctx, CRVPINN_ENONFINITE, "non-finite loss");
     return CRVPINN_OK;
 }
 

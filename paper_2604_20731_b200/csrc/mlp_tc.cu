@@ -84,6 +84,7 @@ struct FwdArgs {
     long long *trace;      // debug timeline (CTA 0), nullptr normally
     const float *xy;       // EVAL only: point coordinates [npts][2]
     int npts;              // EVAL only: number of points (ntiles = ceil(npts / 128), ragged tail)
+    int p0;                // first MLP point of this shard (tile0 * 128); 0 unsharded
 };
 #define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 x = ok ? __ldg(a.xy + 2 * (long)p) : 0.0f;
                 y = ok ? __ldg(a.xy + 2 * (long)p + 1) : 0.0f;
             } else {
-                point_ij(p, N, pi, pj);
+                point_ij(a.p0 + p, N, pi, pj);
                 x = (float)pi / (float)N;
                 y = (float)pj / (float)N;
             }
@@ -615,6 +616,7 @@ struct BwdArgs {
     const __half *WTf;    // [KC] blocks of W^T
     float *part_dx;       // [grid][3*WP]   column sums (xy-weighted | plain)
     float *part_dw;       // [npairs][WP*WP] rows = out features
+    int p0;               // first MLP point of this shard
 };
 
 template <int WP>
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
         for (int tile = pair; tile < a.ntiles; tile += a.npairs, ++i) {
             if (i % PF != kk_pf) continue;
             int pi, pj;
-            point_ij(tile * 128 + row, N, pi, pj);
+            point_ij(a.p0 + tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
             const uint8_t *trow = (const uint8_t *)a.tin + (size_t)tile * TILE_BYTES + row * 128;
             uint8_t *drow = (uint8_t *)a.din + (size_t)tile * TILE_BYTES + row * 128;
@@ -889,6 +891,7 @@ struct Bwd2Args {
     long long *trace;     // debug timeline (CTA 0), nullptr normally
     float *part_cb;       // [npairs][WP] 1^T Delta_out (CRV_B2_MMA_CS): bias gradient of theta layer g+1
     int outl_sums;        // outl: also reduce dW_out / db_L / db_out (else a side-stream k_tc_out_bwd does)
+    int p0;               // first MLP point of this shard (gbar is passed offset by it)
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 #ifndef CRV_B2_MMA_SLEEP
@@ -1286,7 +1289,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             const int kk = k - 1, b = kk % XB, tb = kk % NT;
             const int tile = pair + (a.rev ? nk - 1 - kk : kk) * a.npairs;
             int pi, pj;
-            point_ij(tile * 128 + row, N, pi, pj);
+            point_ij(a.p0 + tile * 128 + row, N, pi, pj);
             const float x = (float)pi / (float)N, y = (float)pj / (float)N;
             if (warp == 2 && lane == 0) BTRACE(kk * 16 + 4);
             mbar_wait(&xfull[b], (kk / XB) & 1);
@@ -1571,6 +1574,7 @@ struct BwdcArgs {
     float *part_cb;       // [G][nclus][WP]    1^T Delta_out of GEMM g (bias gradient of theta layer g+1)
     size_t lay;           // halves per activation layer
     long long *trace;     // debug timeline: CTAs 0..7 (cluster 0), 512 slots each; nullptr normally
+    int p0;               // first MLP point of this shard
 };
 #define CTRACE(slot) do { if (a.trace && blockIdx.x < 8 && (slot) < 1024) a.trace[blockIdx.x * 1024 + (slot)] = clock64(); } while (0)
 
@@ -1807,7 +1811,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
             float x = 0.f, y = 0.f;
             if (first) {
                 int pi, pj;
-                point_ij(tile * 128 + row, N, pi, pj);
+                point_ij(a.p0 + tile * 128 + row, N, pi, pj);
                 x = (float)pi / (float)N;
                 y = (float)pj / (float)N;
             }
@@ -2076,14 +2080,19 @@ static int chain_max_clusters(int csize) {
     }
 }
 
-int tc_create(const Net &net, TcBufs &b, std::string &err) {
+int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err) {
     const int L = net.nl - 1;
     int w = net.widths[1];
     b.WP = ((w + 63) / 64) * 64;
     b.KC = b.WP / 64;
     b.L = L;
     b.G = L - 1;
-    b.ntiles = net.P / 128;
+    if (tile0 < 0 || ntiles < 1 || tile0 + ntiles > net.P / 128) {
+        err = "shard tile range outside the MLP point set";
+        return CRVPINN_EINVAL;
+    }
+    b.tile0 = tile0;
+    b.ntiles = ntiles;
     const int WP = b.WP, KC = b.KC, G = b.G;
     if (fwd_smem_bytes<256>(L) > 232448 && WP == 256) {
         err = "too many layers for the shared-memory budget of the fused forward";
@@ -2275,7 +2284,7 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
     static long long *trace = nullptr;
     const char *te = getenv("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
-    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0};
+    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0, b.tile0 * 128};
     if (te) {
         k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
         cudaStreamSynchronize(s);
@@ -2297,8 +2306,8 @@ void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
 template <int WP>
 static void eval_launch(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s) {
     const int ntiles = (npts + 127) / 128;
-    const int grid = ntiles < b.grid_fwd ? ntiles : b.grid_fwd;
-    FwdArgs a{net.N, ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, nullptr, out, nullptr, xy, npts};
+    const int grid = ntiles < b.nsm ? ntiles : b.nsm;
+    FwdArgs a{net.N, ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, nullptr, out, nullptr, xy, npts, 0};
     k_tc_forward<WP, true><<<grid, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
 }
 
@@ -2313,6 +2322,8 @@ template <int WP>
 static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
     const size_t lay = (size_t)b.ntiles * b.KC * CHUNK_HALVES;
     const int L = b.L;
+    const int p0 = b.tile0 * 128;                    // this shard's first MLP point
+    const float *gbar = b.gbar + p0;               // gbar covers every point (replicated field chain)
     if constexpr (WP >= 128) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[2];
@@ -2329,7 +2340,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         cfg.attrs = attr;
         cfg.numAttrs = 2;
         if (!b.fuse_outl)
-            k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+            k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, gbar, b.Wop,
                                                               b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob,
                                                               st);
         int g_next = b.G - 1;   // GEMMs above g_next are done by the chain
@@ -2343,7 +2354,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 cfg.dynamicSmemBytes = BC<WP>::SMEM;
                 BwdcArgs a{net.N, b.ntiles, b.npairs, Sl, g0, b.delta + (size_t)(g0 + 1) * lay, b.act,
                            b.delta + (size_t)(g0 - Sl + 1) * lay, b.ring, b.WTf, b.partial + b.off_dx,
-                           b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr};
+                           b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr, p0};
                 static long long *ctrace = nullptr;
                 const char *te = getenv("CRVPINN_CHAIN_TRACE");   // debug: clock64 timeline -> file
                 if (te && g0 == b.G - 1) {
@@ -2374,7 +2385,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             cudaEventRecord(b.ev_pre, s);
             cudaStreamWaitEvent(b.side, b.ev_pre, 0);
             k_tc_out_bwd<WP, false><<<b.grid_ob, OB_THREADS, 0, b.side>>>(b.ntiles, b.act + (size_t)(L - 1) * lay,
-                                                                          b.gbar, b.Wop, nullptr,
+                                                                          gbar, b.Wop, nullptr,
                                                                           b.partial + b.off_ob, st);
             cudaEventRecord(b.ev_ob, b.side);   // the deep reduction below reads these sums
         }
@@ -2387,10 +2398,10 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             Bwd2Args a{net.N, b.ntiles, b.npairs, g == 0 ? 1 : 0, outl ? 1 : 0, rev,
                        outl ? b.act + (size_t)(L - 1) * lay : b.delta + (size_t)(g + 1) * lay,
                        b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
-                       b.gbar, b.Wop, b.partial + b.off_ob,
+                       gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
-                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1};
+                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1, p0};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");
@@ -2418,13 +2429,13 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             }
         }
     } else {
-        k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, b.gbar, b.Wop,
+        k_tc_out_bwd<WP><<<b.grid_ob, OB_THREADS, 0, s>>>(b.ntiles, b.act + (size_t)(L - 1) * lay, gbar, b.Wop,
                                                           b.delta + (size_t)(L - 1) * lay, b.partial + b.off_ob, st);
         for (int g = b.G - 1; g >= 0; --g) {
             BwdArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.npairs, b.delta + (size_t)(g + 1) * lay,
                       b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
                       b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
-                      b.partial + b.off_dw + (long)g * b.npairs * WP * WP};
+                      b.partial + b.off_dw + (long)g * b.npairs * WP * WP, p0};
             k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
         }
     }

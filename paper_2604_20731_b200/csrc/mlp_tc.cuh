@@ -16,7 +16,7 @@ struct TcBufs {
     int fuse_outl = 1;
     int bwd_rev = 1;         // alternate the backward launches' tile-walk direction (L2 reuse)
        // WP >= 128: output-layer backward fused into the first k_tc_bwd2 launch
-    int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0;
+    int WP = 0, KC = 0, L = 0, G = 0, ntiles = 0, tile0 = 0;   // this shard's tiles [tile0, tile0 + ntiles)
     __half *Wf = nullptr;    // [G][KC] blocks of WP rows x 128 B: B operand of the forward GEMMs
     __half *WTf = nullptr;   // [G][KC] blocks: B operand of the backward-dX GEMMs (W^T)
     float *W1p = nullptr;    // [WP][2]   first layer x 2 log2(e) (zero padded)
@@ -43,7 +43,9 @@ struct TcBufs {
     const float *theta = nullptr;
 };
 
-int tc_create(const Net &net, TcBufs &b, std::string &err);
+// tile0, ntiles: this shard's MLP tiles [tile0, tile0 + ntiles) of net.P / 128 (the whole set unsharded);
+// activations and partial sums are sized for the shard, gbar for all points
+int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err);
 void tc_destroy(TcBufs &b);   // device buffers, side stream, events
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 // the network with cutoff at arbitrary points: out[p] = cutoff(xy[2p], xy[2p+1]) net(...), device pointers

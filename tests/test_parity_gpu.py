@@ -295,6 +295,69 @@ def test_backward_chain_vs_oracle(crv, monkeypatch, stages, N, widths, seed):
     assert grad_errors(widths, grad, grad_d.astype(np.float64)).max() <= 5e-3
 
 
+# ------------------------------------------------------------------ f4: point sharding
+@pytest.mark.parametrize("chain", ["0", "1"])
+@pytest.mark.parametrize("N,widths,world,seed", [(64, (2, 128, 128, 128, 1), 3, 31),
+                                                 (128, (2, 256, 256, 256, 256, 1), 5, 32),
+                                                 (64, (2, 64, 64, 64, 1), 2, 33),
+                                                 (16, (2, 256, 256, 1), 2, 34)])
+def test_point_shards_vs_unsharded_and_oracle(crv, monkeypatch, chain, N, widths, world, seed):
+    """`world` shard contexts run one after another on this GPU (no rank waits
+    on another), each on its tile range (ragged splits, CTA pairs with odd tile counts); the caller
+    does the two exchanges. The summed u is the unsharded u bit for bit (the per-point arithmetic
+    does not depend on the tile range), every shard sees the unsharded loss, and the summed gradient
+    shares equal the unsharded gradient up to fp32 summation order and the oracle within north_star."""
+    monkeypatch.setenv("CRVPINN_BWD_CHAIN", chain)
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    full = crv.Crvpinn(N, widths, K, S, f, th)
+    u_ref = full.eval()
+    loss_d, grad_d = full.loss_grad()
+    full.close()
+    shards = [crv.Crvpinn(N, widths, K, S, f, th, shard=(r, world)) for r in range(world)]
+    parts = [s.shard_forward() for s in shards]
+    support = np.sum([p != 0 for p in parts], axis=0)
+    assert support.max() <= 1                                  # disjoint supports
+    u = np.sum(parts, axis=0, dtype=np.float32)
+    assert np.array_equal(u, u_ref)
+    outs = [s.shard_backward(u) for s in shards]
+    for loss, _ in outs:
+        assert loss == loss_d
+    grad = np.sum([g.astype(np.float64) for _, g in outs], axis=0)
+    assert grad_errors(widths, grad, grad_d.astype(np.float64)).max() <= 1e-4
+    rl, rg = oracle.Oracle(N, widths, K, S, f, th).loss_grad()
+    tl, tg = TOL[0]
+    assert abs(loss_d - rl) <= tl * abs(rl)
+    assert grad_errors(widths, grad, rg).max() <= tg
+    with pytest.raises(crv.CrvpinnError) as ei:                # no communicator: the caller exchanges
+        shards[0].step(1)
+    assert ei.value.code == crv.CRVPINN_EINVAL
+    for s in shards:
+        s.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_nccl_world1_matches_unsharded(crv, name):
+    """The in-graph exchange (memset of u, NCCL all-reduce of u and of the gradient, captured with the
+    100-iteration graph) on a one-rank communicator: the loss history and theta after 100 Adam steps
+    equal the unsharded context's bit for bit (a sum over one rank is the identity)."""
+    F = W.make_fields(name)
+    w = F.workload
+    a = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, lr=w.lr)
+    ha = a.step(100)
+    tha = a.theta
+    a.close()
+    b = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, lr=w.lr, shard=(0, 1), nccl_id=crv.nccl_unique_id())
+    hb = b.step(100)
+    assert np.array_equal(ha, hb)
+    assert np.array_equal(tha, b.theta)
+    loss, _ = b.loss_grad()
+    assert np.isfinite(loss)
+    u = b.eval()
+    assert np.isfinite(u).all() and np.abs(u).max() > 0
+    b.close()
+
+
 # ------------------------------------------------------------------ f1: gravity term and continuous evaluation
 @pytest.mark.parametrize("prec", PRECS)
 def test_gravity_term_vs_oracle(crv, prec):
