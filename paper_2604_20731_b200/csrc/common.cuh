@@ -114,6 +114,7 @@ struct GramConsts {
     float *etab = nullptr;  // per-mode Thomas pivots 1/w_j, mode-major [a][j]
     float *work = nullptr;  // 2 n^2 scratch (R^, Z^)
     int logM = 0, seg = 0;
+    void *pcg = nullptr;    // f2 workspace (vectors, CG state, the two-iteration graph), made on first use
 };
 GramConsts gram_make_constants(int N);
 void gram_free_constants(GramConsts &c);
@@ -124,7 +125,7 @@ void launch_field_chain(const float *u, const float *alpha, const float *b, floa
                         double *hist, int n_hist, double beta1, double beta2, int advance, cudaStream_t s);
 // f2: A(alpha) u = b by Gram-preconditioned CG (u_lat: interior written, boundary untouched);
 // returns 0 / -1 (CUDA error); iterations used and the final true relative residual
-int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts &c, int N, double rtol, int max_iter,
+int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, int N, double rtol, int max_iter,
               int *iters_out, double *rel_out, cudaStream_t s);
 // mlp_simt.cu -- fp32 FFMA MLP path (CRVPINN_PREC_FP32)
 struct MlpPlan {

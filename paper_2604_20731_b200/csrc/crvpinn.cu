@@ -109,6 +109,7 @@ struct crvpinn_ctx {
     // crvpinn_eval_points scratch (device xy [cap][2] + p [cap]), grown on demand
     float *pts = nullptr;
     long pts_cap = 0;
+    float *ds_u = nullptr;         // crvpinn_direct_solve's lattice result (first use)
     // point sharding (f4): this context's tiles, and the communicator of the two exchanges
     long tile0 = 0, ntiles = 0;
     bool sharded = false;          // shard_world > 1 or a communicator: u is zeroed before the forward
@@ -612,9 +613,9 @@ int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_o
     CK(cudaSetDevice(ctx->device));
     const int N = ctx->net.N;
     const size_t nn = (size_t)(N + 1) * (N + 1);
-    float *ud = nullptr;   // lattice result (boundary 0); a temporary so that no training buffer changes
-    CK(cudaMalloc(&ud, sizeof(float) * nn));
-    cudaMemsetAsync(ud, 0, sizeof(float) * nn, ctx->stream);
+    if (!ctx->ds_u) DALLOC(ctx->ds_u, nn);   // lattice result (boundary 0), apart from the training buffers
+    float *ud = ctx->ds_u;
+    CK(cudaMemsetAsync(ud, 0, sizeof(float) * nn, ctx->stream));
     int it = 0;
     double rel = 0.0;
     const int prc = pcg_solve(ctx->alpha, ctx->b, ud, ctx->gram, N, rtol, max_iter, &it, &rel, ctx->stream);
@@ -624,7 +625,6 @@ int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_o
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e == cudaSuccess) memcpy(u_out, ctx->h_field, sizeof(float) * nn);
     }
-    cudaFree(ud);
     if (prc != 0 || e != cudaSuccess) {
         ctx->err = std::string("direct solve: ") + cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError());
         return CRVPINN_ECUDA;

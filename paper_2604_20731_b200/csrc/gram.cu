@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include <cmath>
 #include <vector>
+#include <cstdlib>
+#include <cstring>
 
 namespace crv {
 
@@ -172,9 +174,10 @@ __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restric
 
 
 // Inverse DST of two rows of z (mode-major input) -> q (row-major), and this block's part of
-// LOSS = sum RES q.
+// LOSS = sum RES q. dsc != nullptr (the direct solve's preconditioner): q is scaled elementwise by it.
 __global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict__ res, float *__restrict__ q,
-                            double *__restrict__ part, const float2 *__restrict__ tw, int N, int logM, float scale) {
+                            double *__restrict__ part, const float2 *__restrict__ tw, int N, int logM, float scale,
+                            const float *__restrict__ dsc) {
     extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
     __shared__ double sred[32];
     const int n = N - 1, M = 2 * N;
@@ -199,7 +202,11 @@ __global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict
     double acc = 0.0;
     for (int k = threadIdx.x + 1; k <= n; k += blockDim.x) {
         const float2 Y = sa[k];
-        const float q1 = -0.5f * Y.y * scale, q2 = 0.5f * Y.x * scale;
+        float q1 = -0.5f * Y.y * scale, q2 = 0.5f * Y.x * scale;
+        if (dsc) {
+            q1 *= dsc[(long)j0 * n + (k - 1)];
+            if (has1) q2 *= dsc[(long)(j0 + 1) * n + (k - 1)];
+        }
         q[(long)j0 * n + (k - 1)] = q1;
         acc += (double)(res[(long)j0 * n + (k - 1)] * q1);
         if (has1) {
@@ -325,7 +332,12 @@ GramConsts gram_make_constants(int N) {
     return c;
 }
 
+struct PcgWork;
+static void pcg_work_free(PcgWork *w);
+
 void gram_free_constants(GramConsts &c) {
+    if (c.pcg) pcg_work_free((PcgWork *)c.pcg);
+    c.pcg = nullptr;
     cudaFree(c.tw);
     cudaFree(c.etab);
     cudaFree(c.work);
@@ -347,7 +359,7 @@ void launch_field_chain(const float *u, const float *alpha, const float *b, floa
     launch_pdl(k_tridiag, dim3(ceil_div(n, TRI_WARPS)), dim3(32 * TRI_WARPS), sizeof(float) * TRI_WARPS * 2 * 32 * c.seg,
                s, 1, rhat, c.etab, z, n, c.seg, h * h);
     launch_pdl(k_idst_loss, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (M + M / 2), s, 1, z, res, q, loss_part,
-               c.tw, N, c.logM, nrm);
+               c.tw, N, c.logM, nrm, (const float *)nullptr);
     const int P = N * N;
     launch_pdl(k_adj_final, dim3(ceil_div(P, 256)), dim3(256), 0, s, 1, q, alpha, gbar, gu_lat, N, st, track_max,
                loss_part, rows, hist, n_hist, beta1, beta2, advance);
@@ -387,7 +399,7 @@ __device__ __forceinline__ double fixed_sum(const double *part, int n) {
 
 // DST-I of two rows of an n x n row-major array (the first stage of G^-1), mode-major output
 __global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat, const float2 *__restrict__ tw,
-                          int N, int logM, float scale) {
+                          int N, int logM, float scale, const float *__restrict__ dsc) {
     extern __shared__ float2 sa[];
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
@@ -400,7 +412,11 @@ __global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat
         sa[__brev((unsigned)N) >> shift] = make_float2(0.0f, 0.0f);
     }
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const float v1 = in[(long)j0 * n + k], v2 = has1 ? in[(long)(j0 + 1) * n + k] : 0.0f;
+        float v1 = in[(long)j0 * n + k], v2 = has1 ? in[(long)(j0 + 1) * n + k] : 0.0f;
+        if (dsc) {
+            v1 *= dsc[(long)j0 * n + k];
+            if (has1) v2 *= dsc[(long)(j0 + 1) * n + k];
+        }
         sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v1, v2);
         sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v1, -v2);
     }
@@ -487,6 +503,17 @@ __global__ void k_pcg_init(const float *__restrict__ b, double *__restrict__ x, 
     if (threadIdx.x == 0) part[j] = s;
 }
 
+// Jacobi scaling of the Gram preconditioner: dsc = diag(A(alpha))^-1/2, the diagonal of the stencil
+// being alpha_{i-1,l} + alpha_{i,l-1} + 2 alpha_{i,l} (k_pcg_matvec's centre coefficient)
+__global__ void k_pcg_diag(const float *__restrict__ alpha, float *__restrict__ dsc, int N) {
+    const int n = N - 1, j = blockIdx.x, l = j + 1;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int i = k + 1;
+        const float d = alpha[latx(i - 1, l, N)] + alpha[latx(i, l - 1, N)] + 2.0f * alpha[latx(i, l, N)];
+        dsc[(long)j * n + k] = rsqrtf(d);
+    }
+}
+
 __global__ void k_pcg_set_bb(PcgState *st, const double *part, int n) {
     if (threadIdx.x == 0 && blockIdx.x == 0) st->bb = fixed_sum(part, n);
 }
@@ -517,7 +544,27 @@ __global__ void k_pcg_final(const double *__restrict__ x, const float *__restric
 }
 }  // namespace
 
-int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts &c, int N, double rtol, int max_iter,
+// f2 workspace, kept by the context between solves (the graph's kernel arguments point into it)
+struct PcgWork {
+    float *buf = nullptr;        // r, z, p, Ap, dsc   [5][n^2]
+    double *x = nullptr;         // fp64 iterate       [n^2]
+    double *dpart = nullptr;     // block partials     [3n + vblocks]
+    PcgState *st = nullptr;
+    cudaGraphExec_t gx = nullptr;   // iterations (even, odd)
+    bool scaled = true;          // Jacobi-scaled preconditioner
+};
+
+static void pcg_work_free(PcgWork *w) {
+    if (!w) return;
+    if (w->gx) cudaGraphExecDestroy(w->gx);
+    cudaFree(w->buf);
+    cudaFree(w->x);
+    cudaFree(w->dpart);
+    cudaFree(w->st);
+    delete w;
+}
+
+int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, int N, double rtol, int max_iter,
               int *iters_out, double *rel_out, cudaStream_t s) {
     const int n = N - 1, M = 2 * N;
     const long n2 = (long)n * n;
@@ -525,23 +572,38 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     const float nrm = sqrtf(2.0f / (float)N);
     const int rows = (n + 1) / 2;
     const int vblocks = 2 * 148;
-    float *buf = nullptr;
-    double *dpart = nullptr, *x = nullptr;
-    PcgState *st = nullptr;
-    if (cudaMalloc(&buf, sizeof(float) * 4 * n2) != cudaSuccess) return -1;
-    if (cudaMalloc(&x, sizeof(double) * n2) != cudaSuccess) { cudaFree(buf); return -1; }
-    if (cudaMalloc(&dpart, sizeof(double) * (3 * (size_t)n + vblocks)) != cudaSuccess) { cudaFree(buf); cudaFree(x); return -1; }
-    if (cudaMalloc(&st, sizeof(PcgState)) != cudaSuccess) { cudaFree(buf); cudaFree(x); cudaFree(dpart); return -1; }
+    PcgWork *w = (PcgWork *)c.pcg;
+    const bool fresh = w == nullptr;
+    if (fresh) {
+        w = new PcgWork();
+        if (cudaMalloc(&w->buf, sizeof(float) * 5 * n2) != cudaSuccess ||
+            cudaMalloc(&w->x, sizeof(double) * n2) != cudaSuccess ||
+            cudaMalloc(&w->dpart, sizeof(double) * (3 * (size_t)n + vblocks)) != cudaSuccess ||
+            cudaMalloc(&w->st, sizeof(PcgState)) != cudaSuccess) {
+            pcg_work_free(w);
+            return -1;
+        }
+        // preconditioner M^-1 = D^-1/2 G^-1 D^-1/2 (D = diag A): the Gram apply of A3 made aware of the
+        // coefficient's magnitude; CRVPINN_PCG_PRECOND=gram selects plain G^-1 (f2)
+        const char *pe = getenv("CRVPINN_PCG_PRECOND");
+        w->scaled = !(pe && strcmp(pe, "gram") == 0);
+        c.pcg = w;
+    }
+    float *buf = w->buf;
+    double *x = w->x, *dpart = w->dpart;
+    PcgState *st = w->st;
     float *r = buf, *z = buf + n2, *p = buf + 2 * n2, *Ap = buf + 3 * n2;
+    float *dsc = w->scaled ? buf + 4 * n2 : nullptr;
+    if (dsc) k_pcg_diag<<<n, PCG_MV_THREADS, 0, s>>>(alpha, dsc, N);   // alpha follows the saturation
     double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n, *part_rr = dpart + 3 * n;
     float *rhat = c.work, *zhat = c.work + n2;
     const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (M + M / 2));
     cudaFuncSetAttribute(k_pcg_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);   // N = 2048: 48 KiB+
-    auto precond = [&]() {   // z = G^-1 r (and the block parts of r . z)
-        k_pcg_dst<<<rows, fft_t, smem_fft, s>>>(r, rhat, c.tw, N, c.logM, nrm);
+    auto precond = [&]() {   // z = M^-1 r (and the block parts of r . z)
+        k_pcg_dst<<<rows, fft_t, smem_fft, s>>>(r, rhat, c.tw, N, c.logM, nrm, dsc);
         k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(
             rhat, c.etab, zhat, n, c.seg, h * h);
-        k_idst_loss<<<rows, fft_t, smem_fft, s>>>(zhat, r, z, part_rz, c.tw, N, c.logM, nrm);
+        k_idst_loss<<<rows, fft_t, smem_fft, s>>>(zhat, r, z, part_rz, c.tw, N, c.logM, nrm, dsc);
     };
     k_pcg_init<<<n, PCG_MV_THREADS, 0, s>>>(b, x, r, part_a, N);
     k_pcg_set_bb<<<1, 32, 0, s>>>(st, part_a, n);
@@ -560,8 +622,8 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     };
     // the kernels use only the parity of the iteration index (the rz ring) once it >= 1: a graph of
     // two iterations (even, odd) replayed CHK / 2 times removes the per-kernel launch cost
-    cudaGraphExec_t gx = nullptr;
-    {
+    cudaGraphExec_t gx = w->gx;
+    if (!gx) {
         cudaGraph_t gr = nullptr;
         if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
             iteration(0);
@@ -572,6 +634,7 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
             }
         }
         cudaGetLastError();
+        w->gx = gx;
     }
     while (it < max_iter) {
         const int upto = it + CHK < max_iter ? it + CHK : max_iter;
@@ -604,11 +667,6 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, const GramConsts
     for (double v : hf) rr += v;
     if (iters_out) *iters_out = it;
     if (rel_out) *rel_out = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
-    if (gx) cudaGraphExecDestroy(gx);
-    cudaFree(buf);
-    cudaFree(x);
-    cudaFree(dpart);
-    cudaFree(st);
     return e == cudaSuccess ? 0 : -1;
 }
 

@@ -19,11 +19,18 @@ for name in ("C4", "C5"):
     F = W.make_fields(name)
     w = F.workload
     g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=0)
-    g.direct_solve(rtol=1e-3, max_iter=20)
     t = time.perf_counter()
-    u, it, rel = g.direct_solve(rtol=1e-6, max_iter=50000)
-    dt = time.perf_counter() - t
-    e = {"N": w.N, "gpu_ms": dt * 1e3, "iterations": it, "rel_residual": rel, "us_per_iteration": dt * 1e6 / max(it, 1)}
+    g.direct_solve(rtol=1e-3, max_iter=20)     # first call: workspace + graph (kept by the context)
+    first_ms = (time.perf_counter() - t) * 1e3
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        u, it, rel = g.direct_solve(rtol=1e-6, max_iter=50000)
+        ts.append(time.perf_counter() - t)
+    dt = min(ts)
+    e = {"N": w.N, "gpu_ms": dt * 1e3, "iterations": it, "rel_residual": rel, "us_per_iteration": dt * 1e6 / max(it, 1),
+         "first_call_ms_20_iterations": first_ms, "timing": "end to end through the C ABI (host result), best of 3",
+         "preconditioner": os.environ.get("CRVPINN_PCG_PRECOND", "jacobi-scaled gram")}
     if "--no-oracle" not in sys.argv:
         import oracle
         o = oracle.Oracle(w.N, w.widths, F.K, F.S, F.f, F.theta0, factor_gram=False)
