@@ -391,19 +391,73 @@ __device__ __forceinline__ double block_sum_f64(double v, double *sred) {
     return s;   // valid in thread 0
 }
 
-__device__ __forceinline__ double fixed_sum(const double *part, int n) {
+// sum of n block partials by one full warp: lane l adds part[l], part[l+32], ... in order, then a
+// butterfly; the result of lane 0 is the same in every block and every run (a serial loop over the
+// partials in one thread costs ~40 ns each: L2 latency on a dependent chain)
+__device__ __forceinline__ double warp_fixed_sum(const double *part, int n) {
+    const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += part[i];
-    return s;
+    for (int i = lane; i < n; i += 32) s += part[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;   // use lane 0's
 }
 
-// DST-I of two rows of an n x n row-major array (the first stage of G^-1), mode-major output
-__global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat, const float2 *__restrict__ tw,
-                          int N, int logM, float scale, const float *__restrict__ dsc) {
+// Fused CG kernels (one iteration = k_pcg_pmv, k_pcg_xrdst, k_tridiag, k_idst_loss):
+// k_pcg_pmv, one block per row j: p_it = z + beta p_{it-1} (beta = rz_it / rz_{it-1}, 0 at it = 0 or
+// on exact convergence) for rows j-1, j, j+1 (p double-buffered by parity, so neighbours' old p is
+// never overwritten underneath), writes row j of p_it and of Ap = A(alpha) p_it and this block's
+// part of p . Ap; block 0 records rz_it.
+__global__ void k_pcg_pmv(const float *__restrict__ z, const float *__restrict__ p_prev, float *__restrict__ p_cur,
+                          const float *__restrict__ alpha, float *__restrict__ y, const double *__restrict__ part_rz,
+                          int nrz, PcgState *st, int it, double *__restrict__ part, int N) {
+    __shared__ double sred[32];
+    __shared__ float sbeta;
+    const int n = N - 1, j = blockIdx.x, l = j + 1;
+    if (threadIdx.x < 32) {
+        const double rz = warp_fixed_sum(part_rz, nrz);
+        if (threadIdx.x == 0) {
+            const double rz_old = it == 0 ? 0.0 : st->rz[(it - 1) & 1];
+            sbeta = rz_old > 0.0 ? (float)(rz / rz_old) : 0.0f;
+            if (j == 0) st->rz[it & 1] = rz;
+        }
+    }
+    __syncthreads();
+    const float beta = sbeta;
+    auto pv = [&](long e) { return beta == 0.0f ? z[e] : fmaf(beta, p_prev[e], z[e]); };
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int i = k + 1;
+        const long e = (long)j * n + k;
+        const float vc = pv(e);
+        const float vw = k > 0 ? pv(e - 1) : 0.0f, ve = k + 1 < n ? pv(e + 1) : 0.0f;
+        const float vs = j > 0 ? pv(e - n) : 0.0f, vn = j + 1 < n ? pv(e + n) : 0.0f;
+        const float r = alpha[latx(i - 1, l, N)] * (vc - vw) + alpha[latx(i, l - 1, N)] * (vc - vs) +
+                        alpha[latx(i, l, N)] * ((vc - ve) + (vc - vn));
+        p_cur[e] = vc;
+        y[e] = r;
+        acc += (double)vc * (double)r;
+    }
+    const double sm = block_sum_f64(acc, sred);
+    if (threadIdx.x == 0) part[j] = sm;
+}
+
+// k_pcg_xrdst, one block per row pair: x += a p, r -= a Ap (a = rz_it / p . Ap; update = 0: no update,
+// the initial preconditioner apply) on rows j0, j0+1, then the first stage of M^-1 on them: the DST-I
+// of dsc * r (mode-major output)
+__global__ void k_pcg_xrdst(double *__restrict__ x, float *__restrict__ r, const float *__restrict__ p,
+                            const float *__restrict__ Ap, const double *__restrict__ part_pap, int npap,
+                            const PcgState *__restrict__ st, int it, int update, float *__restrict__ rhat,
+                            const float2 *__restrict__ tw, int N, int logM, float scale, const float *__restrict__ dsc) {
     extern __shared__ float2 sa[];
+    __shared__ float s_a;
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
     for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    if (threadIdx.x < 32) {   // exact convergence (p = 0) leaves x and r unchanged
+        const double pap = update ? warp_fixed_sum(part_pap, npap) : 0.0;
+        if (threadIdx.x == 0) s_a = pap > 0.0 ? (float)(st->rz[it & 1] / pap) : 0.0f;
+    }
     const int j0 = 2 * blockIdx.x;
     const bool has1 = j0 + 1 < n;
     const int shift = 32 - logM;
@@ -411,14 +465,24 @@ __global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat
         sa[0] = make_float2(0.0f, 0.0f);
         sa[__brev((unsigned)N) >> shift] = make_float2(0.0f, 0.0f);
     }
+    __syncthreads();
+    const float a = s_a;
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        float v1 = in[(long)j0 * n + k], v2 = has1 ? in[(long)(j0 + 1) * n + k] : 0.0f;
-        if (dsc) {
-            v1 *= dsc[(long)j0 * n + k];
-            if (has1) v2 *= dsc[(long)(j0 + 1) * n + k];
+        float v[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !has1) break;
+            const long e = (long)(j0 + h) * n + k;
+            float rv = r[e];
+            if (update) {
+                x[e] += (double)a * (double)p[e];
+                rv = fmaf(-a, Ap[e], rv);
+                r[e] = rv;
+            }
+            v[h] = dsc ? rv * dsc[e] : rv;
         }
-        sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v1, v2);
-        sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v1, -v2);
+        sa[__brev((unsigned)(k + 1)) >> shift] = make_float2(v[0], v[1]);
+        sa[__brev((unsigned)(M - 1 - k)) >> shift] = make_float2(-v[0], -v[1]);
     }
     __syncthreads();
     fft_inplace(sa, stw, M, logM);
@@ -427,64 +491,6 @@ __global__ void k_pcg_dst(const float *__restrict__ in, float *__restrict__ rhat
         rhat[(long)(k - 1) * n + j0] = -0.5f * Y.y * scale;
         if (has1) rhat[(long)(k - 1) * n + j0 + 1] = 0.5f * Y.x * scale;
     }
-}
-
-// y = A(alpha) v (the stencil of A2 without b; v = 0 off the interior), one block per row j, and
-// this block's part of v . y
-__global__ void k_pcg_matvec(const float *__restrict__ v, const float *__restrict__ alpha, float *__restrict__ y,
-                             double *__restrict__ part, int N) {
-    __shared__ double sred[32];
-    const int n = N - 1, j = blockIdx.x, l = j + 1;
-    double acc = 0.0;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const int i = k + 1;
-        const float vc = v[(long)j * n + k];
-        const float vw = k > 0 ? v[(long)j * n + k - 1] : 0.0f, ve = k + 1 < n ? v[(long)j * n + k + 1] : 0.0f;
-        const float vs = j > 0 ? v[(long)(j - 1) * n + k] : 0.0f, vn = j + 1 < n ? v[(long)(j + 1) * n + k] : 0.0f;
-        const float r = alpha[latx(i - 1, l, N)] * (vc - vw) + alpha[latx(i, l - 1, N)] * (vc - vs) +
-                        alpha[latx(i, l, N)] * ((vc - ve) + (vc - vn));
-        y[(long)j * n + k] = r;
-        acc += (double)vc * (double)r;
-    }
-    const double s = block_sum_f64(acc, sred);
-    if (threadIdx.x == 0) part[j] = s;
-}
-
-// x += a p, r -= a Ap with a = rz / (p . Ap); this block's part of r . r
-__global__ void k_pcg_xr(double *__restrict__ x, float *__restrict__ r, const float *__restrict__ p,
-                         const float *__restrict__ Ap, const double *__restrict__ part_pap, int npap,
-                         const PcgState *__restrict__ st, int it, double *__restrict__ part_rr, int n2) {
-    __shared__ double sred[32];
-    __shared__ float sa;
-    if (threadIdx.x == 0) {   // exact convergence (p = 0) leaves x and r unchanged
-        const double pap = fixed_sum(part_pap, npap);
-        sa = pap > 0.0 ? (float)(st->rz[it & 1] / pap) : 0.0f;
-    }
-    __syncthreads();
-    const float a = sa;
-    double acc = 0.0;
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long)gridDim.x * blockDim.x) {
-        x[e] += (double)a * (double)p[e];
-        const float rn = fmaf(-a, Ap[e], r[e]);
-        r[e] = rn;
-        acc += (double)rn * (double)rn;
-    }
-    const double s = block_sum_f64(acc, sred);
-    if (threadIdx.x == 0) part_rr[blockIdx.x] = s;
-}
-
-// p = z + beta p, beta = rz_new / rz_old (beta = 0 on the first iteration); block 0 records rz_new
-__global__ void k_pcg_p(const float *__restrict__ z, float *__restrict__ p, const double *__restrict__ part_rz, int nrz,
-                        PcgState *st, int it, long n2) {
-    __shared__ double srz;
-    if (threadIdx.x == 0) srz = fixed_sum(part_rz, nrz);
-    __syncthreads();
-    const double rz = srz;
-    const double rz_old = it == 0 ? 0.0 : st->rz[(it - 1) & 1];
-    const float beta = rz_old > 0.0 ? (float)(rz / rz_old) : 0.0f;
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long)gridDim.x * blockDim.x)
-        p[e] = beta == 0.0f ? z[e] : fmaf(beta, p[e], z[e]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->rz[it & 1] = rz;
 }
 
 // r = b on the interior (x = 0 start), this block's part of b . b
@@ -504,7 +510,7 @@ __global__ void k_pcg_init(const float *__restrict__ b, double *__restrict__ x, 
 }
 
 // Jacobi scaling of the Gram preconditioner: dsc = diag(A(alpha))^-1/2, the diagonal of the stencil
-// being alpha_{i-1,l} + alpha_{i,l-1} + 2 alpha_{i,l} (k_pcg_matvec's centre coefficient)
+// being alpha_{i-1,l} + alpha_{i,l-1} + 2 alpha_{i,l} (k_pcg_pmv's centre coefficient)
 __global__ void k_pcg_diag(const float *__restrict__ alpha, float *__restrict__ dsc, int N) {
     const int n = N - 1, j = blockIdx.x, l = j + 1;
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -515,7 +521,8 @@ __global__ void k_pcg_diag(const float *__restrict__ alpha, float *__restrict__ 
 }
 
 __global__ void k_pcg_set_bb(PcgState *st, const double *part, int n) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) st->bb = fixed_sum(part, n);
+    const double bb = warp_fixed_sum(part, n);
+    if (threadIdx.x == 0 && blockIdx.x == 0) st->bb = bb;
 }
 
 // true residual of the fp64 iterate, r_true = b - A x in fp64: this block's part of ||r_true||^2
@@ -546,9 +553,9 @@ __global__ void k_pcg_final(const double *__restrict__ x, const float *__restric
 
 // f2 workspace, kept by the context between solves (the graph's kernel arguments point into it)
 struct PcgWork {
-    float *buf = nullptr;        // r, z, p, Ap, dsc   [5][n^2]
+    float *buf = nullptr;        // r, z, p (2, by parity), Ap, dsc   [6][n^2]
     double *x = nullptr;         // fp64 iterate       [n^2]
-    double *dpart = nullptr;     // block partials     [3n + vblocks]
+    double *dpart = nullptr;     // block partials     [3n]
     PcgState *st = nullptr;
     cudaGraphExec_t gx = nullptr;   // iterations (even, odd)
     bool scaled = true;          // Jacobi-scaled preconditioner
@@ -571,14 +578,13 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
     const float h = 1.0f / (float)N;
     const float nrm = sqrtf(2.0f / (float)N);
     const int rows = (n + 1) / 2;
-    const int vblocks = 2 * 148;
     PcgWork *w = (PcgWork *)c.pcg;
     const bool fresh = w == nullptr;
     if (fresh) {
         w = new PcgWork();
-        if (cudaMalloc(&w->buf, sizeof(float) * 5 * n2) != cudaSuccess ||
+        if (cudaMalloc(&w->buf, sizeof(float) * 6 * n2) != cudaSuccess ||
             cudaMalloc(&w->x, sizeof(double) * n2) != cudaSuccess ||
-            cudaMalloc(&w->dpart, sizeof(double) * (3 * (size_t)n + vblocks)) != cudaSuccess ||
+            cudaMalloc(&w->dpart, sizeof(double) * 3 * (size_t)n) != cudaSuccess ||
             cudaMalloc(&w->st, sizeof(PcgState)) != cudaSuccess) {
             pcg_work_free(w);
             return -1;
@@ -592,42 +598,41 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
     float *buf = w->buf;
     double *x = w->x, *dpart = w->dpart;
     PcgState *st = w->st;
-    float *r = buf, *z = buf + n2, *p = buf + 2 * n2, *Ap = buf + 3 * n2;
-    float *dsc = w->scaled ? buf + 4 * n2 : nullptr;
+    float *r = buf, *z = buf + n2, *pb[2] = {buf + 2 * n2, buf + 3 * n2}, *Ap = buf + 4 * n2;
+    float *dsc = w->scaled ? buf + 5 * n2 : nullptr;
     if (dsc) k_pcg_diag<<<n, PCG_MV_THREADS, 0, s>>>(alpha, dsc, N);   // alpha follows the saturation
-    double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n, *part_rr = dpart + 3 * n;
+    double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n;
     float *rhat = c.work, *zhat = c.work + n2;
     const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (M + M / 2));
-    cudaFuncSetAttribute(k_pcg_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);   // N = 2048: 48 KiB+
-    auto precond = [&]() {   // z = M^-1 r (and the block parts of r . z)
-        k_pcg_dst<<<rows, fft_t, smem_fft, s>>>(r, rhat, c.tw, N, c.logM, nrm, dsc);
+    cudaFuncSetAttribute(k_pcg_xrdst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);   // N = 2048: 48 KiB+
+    // one CG iteration it: p_it and A p_it, then x, r, and z = M^-1 r (with the parts of r . z)
+    auto iteration = [&](int i, bool update) {
+        if (update) {
+            k_pcg_pmv<<<n, PCG_MV_THREADS, 0, s>>>(z, pb[(i + 1) & 1], pb[i & 1], alpha, Ap, part_rz, rows, st, i,
+                                                   part_a, N);
+        }
+        k_pcg_xrdst<<<rows, fft_t, smem_fft, s>>>(x, r, pb[i & 1], Ap, part_a, n, st, i, update ? 1 : 0, rhat, c.tw,
+                                                  N, c.logM, nrm, dsc);
         k_tridiag<<<ceil_div(n, TRI_WARPS), 32 * TRI_WARPS, sizeof(float) * TRI_WARPS * 2 * 32 * c.seg, s>>>(
             rhat, c.etab, zhat, n, c.seg, h * h);
         k_idst_loss<<<rows, fft_t, smem_fft, s>>>(zhat, r, z, part_rz, c.tw, N, c.logM, nrm, dsc);
     };
     k_pcg_init<<<n, PCG_MV_THREADS, 0, s>>>(b, x, r, part_a, N);
     k_pcg_set_bb<<<1, 32, 0, s>>>(st, part_a, n);
-    precond();
-    k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, 0, n2);
+    iteration(0, false);   // z_0 = M^-1 b
     PcgState hs{};
     std::vector<double> hf(n);
     int it = 0;
     double rel = 1.0;
     constexpr int CHK = 20;
-    auto iteration = [&](int i) {
-        k_pcg_matvec<<<n, PCG_MV_THREADS, 0, s>>>(p, alpha, Ap, part_a, N);
-        k_pcg_xr<<<vblocks, 256, 0, s>>>(x, r, p, Ap, part_a, n, st, i, part_rr, n2);
-        precond();
-        k_pcg_p<<<vblocks, 256, 0, s>>>(z, p, part_rz, rows, st, i + 1, n2);
-    };
-    // the kernels use only the parity of the iteration index (the rz ring) once it >= 1: a graph of
-    // two iterations (even, odd) replayed CHK / 2 times removes the per-kernel launch cost
+    // kernels use the iteration index only through its parity and it == 0: a graph of iterations
+    // (2, 3) replays every even-odd pair from 2 on and removes the per-kernel launch cost
     cudaGraphExec_t gx = w->gx;
     if (!gx) {
         cudaGraph_t gr = nullptr;
         if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-            iteration(0);
-            iteration(1);
+            iteration(2, true);
+            iteration(3, true);
             if (cudaStreamEndCapture(s, &gr) == cudaSuccess && gr) {
                 if (cudaGraphInstantiate(&gx, gr, 0) != cudaSuccess) gx = nullptr;
                 cudaGraphDestroy(gr);
@@ -639,11 +644,11 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
     while (it < max_iter) {
         const int upto = it + CHK < max_iter ? it + CHK : max_iter;
         while (it < upto) {
-            if (gx && it + 2 <= upto && (it & 1) == 0) {
+            if (gx && it >= 2 && it + 2 <= upto && (it & 1) == 0) {
                 cudaGraphLaunch(gx, s);
                 it += 2;
             } else {
-                iteration(it);
+                iteration(it, true);
                 ++it;
             }
         }
