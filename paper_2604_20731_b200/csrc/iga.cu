@@ -18,6 +18,8 @@
 // Coefficient matrices are [l][k] (row = y basis index). Host buffers at the C ABI.
 #include "common.cuh"
 #include "../../include/crvpinn.h"
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -314,12 +316,128 @@ __global__ void k_iga_band_smem(IgaDev g, double *__restrict__ X) {
     }
 }
 
+// The substitutions with the band recurrence carried in registers: the last R values of the chain
+// never go back through shared memory (its load-after-store latency set the step time of
+// k_iga_band_smem); the band and 1/D are staged once per block (zero-padded, no bounds tests in the
+// chain), and 1/D is folded into the forward pass.
+template <int R>
+__global__ void k_iga_band_reg(IgaDev g, double *__restrict__ X) {
+    extern __shared__ double sx[];   // [nb][IGA_BAND_COLS] columns, [nb + R][R] band, [nb] 1/D
+    const int n = g.nb;
+    double *slf = sx + (size_t)n * IGA_BAND_COLS, *sdi = slf + (size_t)(n + R) * R;
+    const int c0 = blockIdx.x * IGA_BAND_COLS;
+    const int nc = min(IGA_BAND_COLS, n - c0);
+    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
+        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+        sx[e] = cc < nc ? X[(long)i * n + c0 + cc] : 0.0;
+    }
+    for (int e = threadIdx.x; e < (n + R) * R; e += blockDim.x) {
+        const int i = e / R, d = e % R + 1;
+        slf[e] = (i < n && d <= i) ? g.lf[(long)i * g.r + d - 1] : 0.0;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sdi[i] = g.dinv[i];
+    __syncthreads();
+    if (threadIdx.x < IGA_BAND_COLS) {
+        // U steps per batch: their loads are issued together, then the recurrence runs with one
+        // DFMA on the critical path per step (the terms of older values are added first)
+        constexpr int U = 8;
+        double *col = sx + threadIdx.x;
+        double z[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) z[d] = 0.0;
+        for (int i0 = 0; i0 < n; i0 += U) {   // L z = x, then y = D^-1 z
+            double xv[U], di[U], lv[U][R];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = min(i0 + u, n - 1);
+                xv[u] = col[i * IGA_BAND_COLS];
+                di[u] = sdi[i];
+#pragma unroll
+                for (int d = 0; d < R; ++d) lv[u][d] = slf[i * R + d];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                double v = xv[u];
+#pragma unroll
+                for (int d = R; d >= 1; --d) v = fma(-lv[u][d - 1], z[d - 1], v);
+#pragma unroll
+                for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
+                z[0] = v;
+                xv[u] = v * di[u];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + u < n) col[(i0 + u) * IGA_BAND_COLS] = xv[u];
+        }
+#pragma unroll
+        for (int d = 0; d < R; ++d) z[d] = 0.0;
+        for (int i0 = n - 1; i0 >= 0; i0 -= U) {   // L^T x = y
+            double yv[U], lv[U][R];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = max(i0 - u, 0);
+                yv[u] = col[i * IGA_BAND_COLS];
+#pragma unroll
+                for (int d = 1; d <= R; ++d) lv[u][d - 1] = slf[(i + d) * R + d - 1];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                double v = yv[u];
+#pragma unroll
+                for (int d = R; d >= 1; --d) v = fma(-lv[u][d - 1], z[d - 1], v);
+#pragma unroll
+                for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
+                z[0] = v;
+                yv[u] = v;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 - u >= 0) col[(i0 - u) * IGA_BAND_COLS] = yv[u];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
+        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+        if (cc < nc) X[(long)i * n + c0 + cc] = sx[e];
+    }
+}
+
+template <int R>
+static size_t band_reg_smem(int n) { return sizeof(double) * ((size_t)n * IGA_BAND_COLS + (size_t)(n + R) * R + n); }
+
+template <int R>
+static bool band_reg_launch(IgaDev &g, double *X, cudaStream_t s) {
+    const size_t smem = band_reg_smem<R>(g.nb);
+    if (smem > 200 * 1024) return false;
+    // per device and cheap: set on every call (a process may use several devices)
+    cudaFuncSetAttribute(k_iga_band_reg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_iga_band_reg<R><<<ceil_div(g.nb, IGA_BAND_COLS), 256, smem, s>>>(g, X);
+    return true;
+}
+
+static bool band_reg(IgaDev &g, double *X, cudaStream_t s) {
+    switch (g.r) {
+        case 1: return band_reg_launch<1>(g, X, s);
+        case 2: return band_reg_launch<2>(g, X, s);
+        case 3: return band_reg_launch<3>(g, X, s);
+        case 4: return band_reg_launch<4>(g, X, s);
+        case 5: return band_reg_launch<5>(g, X, s);
+        default: return band_reg_launch<6>(g, X, s);
+    }
+}
+
 // L -> C = M^-1 L M^-1 (both directions), in place in g.A (g.B scratch)
 void kron_solve(IgaDev &g, cudaStream_t s) {
     const int n = g.nb;
     const dim3 tb(32, 8), tg((n + 31) / 32, (n + 31) / 32);
     const size_t smem = sizeof(double) * (size_t)n * IGA_BAND_COLS;
-    if (smem <= 200 * 1024) {
+    const char *bv = getenv("CRVPINN_IGA_BAND");   // tuning knob: "smem" = k_iga_band_smem
+    const bool reg = !(bv && strcmp(bv, "smem") == 0) && band_reg_smem<6>(n) <= 200 * 1024;
+    if (reg) {
+        band_reg(g, g.A, s);                       // along l (rows)
+        k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
+        band_reg(g, g.B, s);                       // along k
+    } else if (smem <= 200 * 1024) {
         // per device and cheap: set on every call (a process may use several devices)
         cudaFuncSetAttribute(k_iga_band_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         k_iga_band_smem<<<ceil_div(n, IGA_BAND_COLS), 256, smem, s>>>(g, g.A);   // along l (rows)

@@ -1,4 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "direct_solve" > gpurun_out/pt.log 2>&1; tail -3 gpurun_out/pt.log
-timeout -s KILL 600 python scripts/bench_direct_solve.py > gpurun_out/ds.json 2>gpurun_out/ds.err; tail -c 1500 gpurun_out/ds.json; tail -3 gpurun_out/ds.err
+timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "iga" > gpurun_out/pt.log 2>&1; tail -3 gpurun_out/pt.log
+timeout -s KILL 600 python scripts/bench_iga.py > gpurun_out/iga.json 2>gpurun_out/iga.err; tail -c 900 gpurun_out/iga.json; tail -3 gpurun_out/iga.err
+CRVPINN_IGA_BAND=smem timeout -s KILL 600 python scripts/bench_iga.py > gpurun_out/iga_smem.json 2>&1; tail -c 900 gpurun_out/iga_smem.json
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/iga_launches.csv python scripts/prof_iga.py > gpurun_out/ncu.log 2>&1
