@@ -512,11 +512,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
 // Delta_L = s * gbar * W_out (.) (1 - t_L^2) (fp16, tile-chunk format), with
 // s = 2^(7 - ceil(log2 max|gbar|)) so max|s gbar| is in (64, 128].
 // Partials per block: [WP] sum s*gbar*t_L (dW_out) | [WP] sum Delta_L (db) | [1] sum s*gbar (db_out).
-__device__ __forceinline__ float grad_scale(const DevState *st) {
+// ew = ceil(log2 max|W_out|) (0 for a zero output layer): Delta_L = s gbar W_out (1 - t_L^2) then has
+// max |Delta_L| <= 128 whatever the magnitudes of gbar and W_out (fp16 holds 65504)
+__device__ __forceinline__ int wout_exp(float womax) {
+    return (womax > 0.0f && isfinite(womax)) ? (int)ceilf(log2f(womax)) : 0;
+}
+__device__ __forceinline__ float grad_scale(const DevState *st, int ew) {
     float gm = __uint_as_float(st->gmax_bits);
     if (!(gm > 0.0f) || !isfinite(gm)) return 1.0f;
-    int e = (int)ceilf(log2f(gm));
-    return exp2f((float)(7 - e));
+    int e = 7 - (int)ceilf(log2f(gm)) - ew;
+    e = e < -126 ? -126 : (e > 126 ? 126 : e);
+    return exp2f((float)e);
 }
 
 constexpr int OB_THREADS = 256;
@@ -537,10 +543,19 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
     __shared__ float sg[128];
     __shared__ float sred[2][NRG][WP];
     __shared__ float sgsum[NRG];
+    __shared__ float swo;
     const int T = threadIdx.x;
     const int lg = T & 7, c = (T >> 3) % KC, rg = T / (8 * KC);
     const int f0 = c * 64 + lg * 8;
-    const float s = grad_scale(st);
+    if (T < 32) {   // max |W_out| (order-independent: every block gets the same value)
+        float m = 0.0f;
+        for (int f = T; f < WP; f += 32) m = fmaxf(m, fabsf(Wop[f]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (T == 0) swo = m;
+    }
+    __syncthreads();
+    const float s = grad_scale(st, wout_exp(swo));
     if (blockIdx.x == 0 && T == 0) {
         st->gscale = s;
         st->inv_gscale = 1.0f / s;
@@ -1197,17 +1212,29 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         __half2 wo2[KC][4];
         float aw[2][8], ab[2][8], ag = 0.f;
         float s = 1.0f;
+        float wboost = 1.0f;   // 2^ew: Delta_L = (s gbar 2^ew) (W_out 2^-ew) (1 - t_L^2), both factors fp16-safe
         if (OUTL) {
-            s = grad_scale(a.st);
+            float wm = 0.0f;
+#pragma unroll
+            for (int j = 0; j < KC; ++j)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) wm = fmaxf(wm, fabsf(a.Wop[j * 64 + olg * 8 + e]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));   // lanes: all 8 granules
+            const int ew = wout_exp(wm);
+            wboost = exp2f((float)ew);
+            s = grad_scale(a.st, ew);
             if (blockIdx.x == 0 && ep_tid == 0) {
                 a.st->gscale = s;
                 a.st->inv_gscale = 1.0f / s;
             }
+            const float wsc = 1.0f / wboost;
 #pragma unroll
             for (int j = 0; j < KC; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    wo2[j][e] = __floats2half2_rn(a.Wop[j * 64 + olg * 8 + 2 * e], a.Wop[j * 64 + olg * 8 + 2 * e + 1]);
+                    wo2[j][e] = __floats2half2_rn(a.Wop[j * 64 + olg * 8 + 2 * e] * wsc,
+                                                  a.Wop[j * 64 + olg * 8 + 2 * e + 1] * wsc);
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
@@ -1223,7 +1250,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                 for (int m = 0; m < ORM; ++m) {
                     g[m] = s * __ldg(a.gbar + (size_t)tile * 128 + orr + ORG * m);
-                    g2[m] = __floats2half2_rn(g[m], g[m]);
+                    g2[m] = __floats2half2_rn(g[m] * wboost, g[m] * wboost);
                     if (olg == 0) ag += g[m];
                 }
                 const __half2 one2 = __floats2half2_rn(1.0f, 1.0f);
@@ -1272,8 +1299,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 fw = __half22float2(haw[e]), fb = __half22float2(hab[e]);
-                            aw[jj][2 * e] += fw.x;
-                            aw[jj][2 * e + 1] += fw.y;
+                            aw[jj][2 * e] = fmaf(fw.x, 1.0f / wboost, aw[jj][2 * e]);   // haw is in g 2^ew units
+                            aw[jj][2 * e + 1] = fmaf(fw.y, 1.0f / wboost, aw[jj][2 * e + 1]);
                             ab[jj][2 * e] += fb.x;
                             ab[jj][2 * e + 1] += fb.y;
                         }

@@ -1,6 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "iga" > gpurun_out/pt.log 2>&1; tail -3 gpurun_out/pt.log
-timeout -s KILL 600 python scripts/bench_iga.py > gpurun_out/iga.json 2>gpurun_out/iga.err; tail -c 900 gpurun_out/iga.json; tail -3 gpurun_out/iga.err
-CRVPINN_IGA_BAND=smem timeout -s KILL 600 python scripts/bench_iga.py > gpurun_out/iga_smem.json 2>&1; tail -c 900 gpurun_out/iga_smem.json
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/iga_launches.csv python scripts/prof_iga.py > gpurun_out/ncu.log 2>&1
+timeout -s KILL 900 python -m pytest tests -x -q -m gpu > gpurun_out/pt.log 2>&1; tail -15 gpurun_out/pt.log
+for r in 1 2; do timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1; done

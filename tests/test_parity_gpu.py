@@ -295,6 +295,49 @@ def test_backward_chain_vs_oracle(crv, monkeypatch, stages, N, widths, seed):
     assert grad_errors(widths, grad, grad_d.astype(np.float64)).max() <= 5e-3
 
 
+# ------------------------------------------------------------------ degenerate and extreme-scale inputs
+@pytest.mark.parametrize("prec", PRECS)
+def test_zero_problem_is_a_fixed_point(crv, prec):
+    """f = 0 and a network whose output layer is zero: u = 0, RES = 0, so LOSS = 0 and every gradient is
+    exactly 0 (the zero gradient-scale path: max|gbar| = 0), and Adam leaves theta unchanged bit for bit
+    (m = v = 0, so the update is 0 / (0 + eps))."""
+    N, widths = 32, (2, 64, 64, 64, 1)
+    K, S, _ = W.random_fields(N, 41)
+    f = np.zeros_like(K)
+    th = W.random_theta(widths, 41)
+    off, shape = W.theta_slices(widths)[-2]
+    th[off:off + int(np.prod(shape)) + 1] = 0.0               # W_out and b_out
+    rl, rg = oracle.Oracle(N, widths, K, S, f, th).loss_grad()
+    assert rl == 0.0 and not np.any(rg)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=prec)
+    loss, grad = g.loss_grad()
+    assert loss == 0.0 and not np.any(grad)
+    assert not np.any(g.eval())
+    hist = g.step(5)
+    assert not np.any(hist)
+    assert np.array_equal(g.theta, th)
+
+
+@pytest.mark.parametrize("scale", [1e-9, 1e6])
+def test_gradient_scale_extremes(crv, scale):
+    """The tensor path keeps Delta in fp16 with a power-of-two scale s = 2^(7 - ceil(log2 max|gbar|)):
+    gradients many orders of magnitude below fp16's normal range or above its maximum (f scaled by
+    1e-9 / 1e6, so RES and gbar scale with it) still match the oracle at the tensor-mode tolerance."""
+    N, widths, seed = 64, (2, 128, 128, 128, 1), 42
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    off, shape = W.theta_slices(widths)[-2]
+    th[off:off + int(np.prod(shape)) + 1] *= scale            # keep u on the scale of b
+    f = (f * scale).astype(np.float32)
+    rl, rg = oracle.Oracle(N, widths, K, S, f, th).loss_grad()
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
+    loss, grad = g.loss_grad()
+    tl, tg = TOL[0]
+    assert np.isfinite(loss) and abs(loss - rl) <= tl * abs(rl), (loss, rl)
+    assert np.all(np.isfinite(grad))
+    assert grad_errors(widths, grad, rg).max() <= tg
+
+
 # ------------------------------------------------------------------ f4: point sharding
 @pytest.mark.parametrize("chain", ["0", "1"])
 @pytest.mark.parametrize("N,widths,world,seed", [(64, (2, 128, 128, 128, 1), 3, 31),
