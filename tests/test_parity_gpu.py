@@ -338,6 +338,27 @@ def test_gradient_scale_extremes(crv, scale):
     assert grad_errors(widths, grad, rg).max() <= tg
 
 
+@pytest.mark.parametrize("N,widths,wscale,seed", [(64, (2,) + (128,) * 10 + (1,), 1.0, 43),
+                                                  (64, (2,) + (256,) * 4 + (1,), 3.0, 44),
+                                                  (32, (2,) + (64,) * 15 + (1,), 1.0, 45)])
+def test_deep_and_saturated_networks(crv, N, widths, wscale, seed):
+    """Depth (9 and 14 hidden GEMMs: the fp16 Delta passes through every one of them under one scale)
+    and weights 3x the Xavier range (saturated tanh, large pre-activations for the hi/lo split) on the
+    tensor path, against the oracle at the tensor-mode tolerance, at theta and after 20 Adam steps."""
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed, scale=wscale)
+    ref = oracle.Oracle(N, widths, K, S, f, th)
+    rl, rg = ref.loss_grad()
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=0)
+    loss, grad = g.loss_grad()
+    tl, tg = TOL[0]
+    assert abs(loss - rl) <= tl * abs(rl), (loss, rl)
+    assert grad_errors(widths, grad, rg).max() <= tg
+    hist = g.step(20)
+    rh = ref.train(20)
+    assert abs(hist[-1] - rh[-1]) <= 0.02 * abs(rh[-1]), (hist[-1], rh[-1])
+
+
 # ------------------------------------------------------------------ f4: point sharding
 @pytest.mark.parametrize("chain", ["0", "1"])
 @pytest.mark.parametrize("N,widths,world,seed", [(64, (2, 128, 128, 128, 1), 3, 31),
