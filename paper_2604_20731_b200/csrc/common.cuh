@@ -110,7 +110,7 @@ void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int nj
                    const DevState *st, cudaStream_t s);
 // gram.cu
 struct GramConsts {
-    float2 *tw = nullptr;   // FFT twiddles exp(-2 pi i k / 2N), k < N
+    float2 *tw = nullptr;   // FFT twiddles per stage: [hs + pos] = exp(-2 pi i pos / 2hs), 2N entries
     float *etab = nullptr;  // per-mode Thomas pivots 1/w_j, mode-major [a][j]
     float *work = nullptr;  // 2 n^2 scratch (R^, Z^)
     int logM = 0, seg = 0;

@@ -34,15 +34,16 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ long latx(int i, int j, int N) { return (long)j * (N + 1) + i; }
 
-// In-place radix-2 FFT of sa[0..M) (input already in bit-reversed order).
+// In-place radix-2 FFT of sa[0..M) (input already in bit-reversed order). Twiddles per stage,
+// contiguous: tw[hs + pos] = exp(-2 pi i pos / (2 hs)), so a warp's consecutive butterflies read
+// consecutive entries (one table indexed pos * M / (2 hs) put stages 4-8 on one bank)
 __device__ __forceinline__ void fft_inplace(float2 *sa, const float2 *tw, int M, int logM) {
     for (int lh = 0; lh < logM; ++lh) {
         const int hs = 1 << lh;
-        const int tstride = M >> (lh + 1);
         for (int b = threadIdx.x; b < M / 2; b += blockDim.x) {
             const int pos = b & (hs - 1);
             const int i0 = ((b >> lh) << (lh + 1)) + pos, i1 = i0 + hs;
-            const float2 w = tw[pos * tstride];
+            const float2 w = tw[hs + pos];
             const float2 u = sa[i0], v = cmul(sa[i1], w);
             sa[i0] = make_float2(u.x + v.x, u.y + v.y);
             sa[i1] = make_float2(u.x - v.x, u.y - v.y);
@@ -61,7 +62,7 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
     extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
+    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
     pdl_wait();
     pdl_trigger();
     const int j0 = 2 * blockIdx.x;
@@ -182,7 +183,7 @@ __global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict
     __shared__ double sred[32];
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];
     pdl_wait();
     pdl_trigger();
     const int j0 = 2 * blockIdx.x;
@@ -303,11 +304,12 @@ GramConsts gram_make_constants(int N) {
     c.logM = logM;
     c.seg = (n + 31) / 32;
     if ((c.seg & 1) == 0) c.seg += 1;
-    std::vector<float2> tw((size_t)M / 2);
-    for (int k = 0; k < M / 2; ++k) {
-        const double ang = -2.0 * M_PI * (double)k / (double)M;
-        tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-    }
+    std::vector<float2> tw((size_t)M, make_float2(0.0f, 0.0f));   // per-stage tables, see fft_inplace
+    for (int hs = 1; hs < M; hs <<= 1)
+        for (int pos = 0; pos < hs; ++pos) {
+            const double ang = -M_PI * (double)pos / (double)hs;
+            tw[hs + pos] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        }
     // Thomas pivots e[a][j] = 1/w_j of the (lam_a + 2, -1) tridiagonal, mode-major
     std::vector<float> e((size_t)n * n);
     for (int a = 0; a < n; ++a) {
@@ -324,7 +326,7 @@ GramConsts gram_make_constants(int N) {
     cudaMalloc(&c.work, sizeof(float) * 2 * (size_t)n * n);
     cudaMemcpy(c.tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(c.etab, e.data(), sizeof(float) * e.size(), cudaMemcpyHostToDevice);
-    const int smem_fft = (int)(sizeof(float2) * (M + M / 2));
+    const int smem_fft = (int)(sizeof(float2) * (2 * M));
     cudaFuncSetAttribute(k_res_dst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);
     cudaFuncSetAttribute(k_idst_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);
     cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -354,11 +356,11 @@ void launch_field_chain(const float *u, const float *alpha, const float *b, floa
     const float nrm = sqrtf(2.0f / (float)N);
     float *rhat = c.work, *z = c.work + (size_t)n * n;
     const int rows = (n + 1) / 2;
-    launch_pdl(k_res_dst, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (M + M / 2), s, 1, u, alpha, b, res, rhat,
+    launch_pdl(k_res_dst, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (2 * M), s, 1, u, alpha, b, res, rhat,
                c.tw, N, c.logM, nrm, st);
     launch_pdl(k_tridiag, dim3(ceil_div(n, TRI_WARPS)), dim3(32 * TRI_WARPS), sizeof(float) * TRI_WARPS * 2 * 32 * c.seg,
                s, 1, rhat, c.etab, z, n, c.seg, h * h);
-    launch_pdl(k_idst_loss, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (M + M / 2), s, 1, z, res, q, loss_part,
+    launch_pdl(k_idst_loss, dim3(rows), dim3(fft_threads(N)), sizeof(float2) * (2 * M), s, 1, z, res, q, loss_part,
                c.tw, N, c.logM, nrm, (const float *)nullptr);
     const int P = N * N;
     launch_pdl(k_adj_final, dim3(ceil_div(P, 256)), dim3(256), 0, s, 1, q, alpha, gbar, gu_lat, N, st, track_max,
@@ -453,7 +455,7 @@ __global__ void k_pcg_xrdst(double *__restrict__ x, float *__restrict__ r, const
     __shared__ float s_a;
     const int n = N - 1, M = 2 * N;
     float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M / 2; k += blockDim.x) stw[k] = tw[k];
+    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];
     if (threadIdx.x < 32) {   // exact convergence (p = 0) leaves x and r unchanged
         const double pap = update ? warp_fixed_sum(part_pap, npap) : 0.0;
         if (threadIdx.x == 0) s_a = pap > 0.0 ? (float)(st->rz[it & 1] / pap) : 0.0f;
@@ -603,7 +605,7 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
     if (dsc) k_pcg_diag<<<n, PCG_MV_THREADS, 0, s>>>(alpha, dsc, N);   // alpha follows the saturation
     double *part_a = dpart, *part_rz = dpart + n, *part_fin = dpart + 2 * n;
     float *rhat = c.work, *zhat = c.work + n2;
-    const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (M + M / 2));
+    const int fft_t = fft_threads(N), smem_fft = (int)(sizeof(float2) * (2 * M));
     cudaFuncSetAttribute(k_pcg_xrdst, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fft);   // N = 2048: 48 KiB+
     // one CG iteration it: p_it and A p_it, then x, r, and z = M^-1 r (with the parts of r . z)
     auto iteration = [&](int i, bool update) {
