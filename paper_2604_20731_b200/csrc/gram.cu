@@ -34,19 +34,37 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ long latx(int i, int j, int N) { return (long)j * (N + 1) + i; }
 
-// In-place radix-2 FFT of sa[0..M) (input already in bit-reversed order). Twiddles per stage,
+// In-place FFT of sa[0..M) (input already in bit-reversed order), radix-4 passes. Twiddles per stage,
 // contiguous: tw[hs + pos] = exp(-2 pi i pos / (2 hs)), so a warp's consecutive butterflies read
 // consecutive entries (one table indexed pos * M / (2 hs) put stages 4-8 on one bank)
 __device__ __forceinline__ void fft_inplace(float2 *sa, const float2 *tw, int M, int logM) {
-    for (int lh = 0; lh < logM; ++lh) {
-        const int hs = 1 << lh;
+    int lh = 0;
+    if (logM & 1) {   // odd log2(M): one radix-2 stage first (its twiddles are all 1)
         for (int b = threadIdx.x; b < M / 2; b += blockDim.x) {
-            const int pos = b & (hs - 1);
-            const int i0 = ((b >> lh) << (lh + 1)) + pos, i1 = i0 + hs;
-            const float2 w = tw[hs + pos];
-            const float2 u = sa[i0], v = cmul(sa[i1], w);
-            sa[i0] = make_float2(u.x + v.x, u.y + v.y);
-            sa[i1] = make_float2(u.x - v.x, u.y - v.y);
+            const float2 u = sa[2 * b], v = sa[2 * b + 1];
+            sa[2 * b] = make_float2(u.x + v.x, u.y + v.y);
+            sa[2 * b + 1] = make_float2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+        lh = 1;
+    }
+    // radix-4: stages lh and lh+1 in one pass (half the barriers and shared-memory round trips)
+    for (; lh < logM; lh += 2) {
+        const int hs = 1 << lh;
+        for (int q = threadIdx.x; q < M / 4; q += blockDim.x) {
+            const int pos = q & (hs - 1);
+            const int i0 = ((q >> lh) << (lh + 2)) + pos;
+            const float2 w1 = tw[hs + pos], w2 = tw[2 * hs + pos];
+            const float2 x0 = sa[i0], x1 = cmul(sa[i0 + hs], w1), x2 = sa[i0 + 2 * hs], x3 = cmul(sa[i0 + 3 * hs], w1);
+            const float2 a0 = make_float2(x0.x + x1.x, x0.y + x1.y), a1 = make_float2(x0.x - x1.x, x0.y - x1.y);
+            const float2 a2 = make_float2(x2.x + x3.x, x2.y + x3.y), a3 = make_float2(x2.x - x3.x, x2.y - x3.y);
+            const float2 b2 = cmul(a2, w2);
+            const float2 c3 = cmul(a3, w2);
+            const float2 b3 = make_float2(c3.y, -c3.x);   // (-i) w2 a3
+            sa[i0] = make_float2(a0.x + b2.x, a0.y + b2.y);
+            sa[i0 + 2 * hs] = make_float2(a0.x - b2.x, a0.y - b2.y);
+            sa[i0 + hs] = make_float2(a1.x + b3.x, a1.y + b3.y);
+            sa[i0 + 3 * hs] = make_float2(a1.x - b3.x, a1.y - b3.y);
         }
         __syncthreads();
     }
