@@ -176,6 +176,127 @@ __global__ void k_iga_gather(IgaDev g, double *__restrict__ L) {
     L[t] = acc;
 }
 
+// Fused integrand + load assembly (replaces k_iga_qp + k_iga_gather): a block owns TB x TB test
+// functions (k, l), computes the integrand of k_iga_qp at every Gauss point of the elements their
+// supports touch (a halo of r elements) into shared memory, and then each thread sums its test
+// function's load, factorised by Gauss rows (fp32 row sums of at most (r+1)^2 terms, fp64 across
+// rows). The 3 x m^2 integrand array never goes through HBM.
+template <int TB>
+__global__ void __launch_bounds__(TB * TB) k_iga_assemble(IgaDev g, const float *__restrict__ S,
+                                                          const float *__restrict__ P, const float *__restrict__ K,
+                                                          const float *__restrict__ q, const float *__restrict__ fq,
+                                                          int mode, float tau_phi, float mob, float grav_y,
+                                                          double *__restrict__ L) {
+    extern __shared__ float sq[];   // [3][QW][QW] integrand of the block's Gauss points
+    const int r = g.r, R1 = r + 1, ne = g.ne, nb = g.nb, m = g.m;
+    const int k0 = blockIdx.x * TB, l0 = blockIdx.y * TB;
+    const int ex0 = max(k0 - r, 0), ey0 = max(l0 - r, 0);                          // first element
+    const int ex1 = min(k0 + TB - 1, ne - 1), ey1 = min(l0 + TB - 1, ne - 1);      // last element
+    const int QX = (ex1 - ex0 + 1) * R1, QY = (ey1 - ey0 + 1) * R1;
+    const int QW = (TB + r) * R1;
+    for (int t = threadIdx.x; t < QX * QY; t += blockDim.x) {
+        const int jy = t / QX, ix = t % QX;
+        const int i = ex0 * R1 + ix, j = ey0 * R1 + jy;   // global Gauss point indices
+        const long p = (long)j * m + i;
+        const int ex = i / R1, qx = i % R1, ey = j / R1, qy = j % R1;
+        const float w = g.gw[i] * g.gw[j];
+        float v0, v1, v2;
+        if (mode == 1) {
+            v0 = w * fq[p];
+            v1 = v2 = 0.f;
+        } else {
+            const float *bvx = g.bv + ((long)ex * R1 + qx) * R1, *bdx = g.bd + ((long)ex * R1 + qx) * R1;
+            const float *bvy = g.bv + ((long)ey * R1 + qy) * R1, *bdy = g.bd + ((long)ey * R1 + qy) * R1;
+            float sv = 0.f, px = 0.f, py = 0.f;
+            for (int b = 0; b < R1; ++b) {
+                const float *srow = S + (long)(ey + b) * nb + ex, *prow = P + (long)(ey + b) * nb + ex;
+                float ss = 0.f, ppx = 0.f, ppy = 0.f;
+                for (int a = 0; a < R1; ++a) {
+                    ss = fmaf(srow[a], bvx[a], ss);
+                    ppx = fmaf(prow[a], bdx[a], ppx);
+                    ppy = fmaf(prow[a], bvx[a], ppy);
+                }
+                sv = fmaf(ss, bvy[b], sv);
+                px = fmaf(ppx, bvy[b], px);
+                py = fmaf(ppy, bdy[b], py);
+            }
+            const long e = (long)ey * ne + ex;
+            const float flux = -tau_phi * mob * sv * K[e];
+            v0 = w * (sv + tau_phi * q[e]);
+            v1 = w * flux * px;
+            v2 = w * flux * (py + grav_y);
+        }
+        const int o = jy * QW + ix;
+        sq[o] = v0;
+        sq[QW * QW + o] = v1;
+        sq[2 * QW * QW + o] = v2;
+    }
+    __syncthreads();
+    const int k = k0 + (int)(threadIdx.x % TB), l = l0 + (int)(threadIdx.x / TB);
+    if (k >= nb || l >= nb) return;
+    // the x-direction test-function factors of this k, in Gauss-point order (at most (r+1)^2 each)
+    float vxs[(IGA_MAX_R + 1) * (IGA_MAX_R + 1)], dxs[(IGA_MAX_R + 1) * (IGA_MAX_R + 1)];
+    const int exa = max(k - r, 0), exb = min(k, ne - 1);
+    int nx = 0;
+    for (int ex = exa; ex <= exb; ++ex)
+        for (int qx = 0; qx < R1; ++qx, ++nx) {
+            vxs[nx] = g.bv[((long)ex * R1 + qx) * R1 + (k - ex)];
+            dxs[nx] = g.bd[((long)ex * R1 + qx) * R1 + (k - ex)];
+        }
+    // per Gauss row: A = sum_x (q0 vx + q1 dx), B = sum_x q2 vx in fp32 (at most (r+1)^2 terms),
+    // then L += vy A + dy B in fp64 (two conversions per row instead of six per point)
+    double acc = 0.0;
+    const int xo = (exa - ex0) * R1;
+    for (int ey = max(l - r, 0); ey <= min(l, ne - 1); ++ey) {
+        const int b = l - ey;
+        for (int qy = 0; qy < R1; ++qy) {
+            const float vy = g.bv[((long)ey * R1 + qy) * R1 + b], dy = g.bd[((long)ey * R1 + qy) * R1 + b];
+            const float *r0 = sq + ((ey - ey0) * R1 + qy) * QW + xo;
+            float A = 0.f, B = 0.f;
+            for (int t = 0; t < nx; ++t) {
+                A = fmaf(r0[t], vxs[t], A);
+                A = fmaf(r0[QW * QW + t], dxs[t], A);
+                B = fmaf(r0[2 * QW * QW + t], vxs[t], B);
+            }
+            acc = fma((double)vy, (double)A, acc);
+            acc = fma((double)dy, (double)B, acc);
+        }
+    }
+    L[(long)l * nb + k] = acc;
+}
+
+static bool assemble_split() {   // tuning knob: CRVPINN_IGA_ASSEMBLY=split -> k_iga_qp + k_iga_gather
+    const char *e = getenv("CRVPINN_IGA_ASSEMBLY");
+    return e && strcmp(e, "split") == 0;
+}
+
+// the load vector L (fp64, nb x nb) of mode 0 (saturation step) or 1 (projection of fq)
+static void assemble(IgaDev &g, const float *S, const float *P, const float *K, const float *q, const float *fq,
+                     int mode, float tau_phi, float mob, float grav_y, cudaStream_t s) {
+    const long mm = (long)g.m * g.m, n2 = (long)g.nb * g.nb;
+    if (assemble_split()) {
+        k_iga_qp<<<ceil_div(mm, 256), 256, 0, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y);
+        k_iga_gather<<<ceil_div(n2, 256), 256, 0, s>>>(g, g.A);
+        return;
+    }
+    const int R1 = g.r + 1;
+    if (g.r <= 3) {
+        constexpr int TB = 16;
+        const int QW = (TB + g.r) * R1;
+        const size_t smem = sizeof(float) * 3 * QW * QW;
+        cudaFuncSetAttribute(k_iga_assemble<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const dim3 grid(ceil_div(g.nb, TB), ceil_div(g.nb, TB));
+        k_iga_assemble<TB><<<grid, TB * TB, smem, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, g.A);
+    } else {
+        constexpr int TB = 8;
+        const int QW = (TB + g.r) * R1;
+        const size_t smem = sizeof(float) * 3 * QW * QW;
+        cudaFuncSetAttribute(k_iga_assemble<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const dim3 grid(ceil_div(g.nb, TB), ceil_div(g.nb, TB));
+        k_iga_assemble<TB><<<grid, TB * TB, smem, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, g.A);
+    }
+}
+
 // X = M^-1 X along the row index, one thread per column; M = L D L^T with unit lower band L
 __global__ void k_iga_band(IgaDev g, double *__restrict__ X) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -589,8 +710,7 @@ int crvpinn_iga_project(crvpinn_iga *h, const float *fq, float *coef) {
     if (rc) return rc;
     IGA_CK(cudaMemcpy(g.io, fq, sizeof(float) * mm, cudaMemcpyHostToDevice));
     cudaEventRecord(g.e0, 0);
-    crv::k_iga_qp<<<crv::ceil_div(mm, 256), 256>>>(g, nullptr, nullptr, nullptr, nullptr, g.io, 1, 0.f, 0.f, 0.f);
-    crv::k_iga_gather<<<crv::ceil_div(n2, 256), 256>>>(g, g.A);
+    crv::assemble(g, nullptr, nullptr, nullptr, nullptr, g.io, 1, 0.f, 0.f, 0.f, 0);
     crv::kron_solve(g, 0);
     crv::k_iga_to_f32<<<crv::ceil_div(n2, 256), 256>>>(g.A, g.outf, n2);
     cudaEventRecord(g.e1, 0);
@@ -609,7 +729,7 @@ int crvpinn_iga_saturation_step(crvpinn_iga *h, const float *S, const float *P, 
         return iga_fail(h, CRVPINN_EINVAL, "need tau >= 0, phi > 0 and finite parameters");
     IgaDev &g = h->g;
     IGA_CK(cudaSetDevice(h->device));
-    const long n2 = (long)g.nb * g.nb, ne2 = (long)g.ne * g.ne, mm = (long)g.m * g.m;
+    const long n2 = (long)g.nb * g.nb, ne2 = (long)g.ne * g.ne;
     int rc = iga_stage(h, (size_t)(2 * n2 + 2 * ne2));
     if (rc) return rc;
     float *dS = g.io, *dP = g.io + n2, *dK = g.io + 2 * n2, *dq = g.io + 2 * n2 + ne2;
@@ -618,9 +738,8 @@ int crvpinn_iga_saturation_step(crvpinn_iga *h, const float *S, const float *P, 
     IGA_CK(cudaMemcpy(dK, K_elem, sizeof(float) * ne2, cudaMemcpyHostToDevice));
     IGA_CK(cudaMemcpy(dq, q_elem, sizeof(float) * ne2, cudaMemcpyHostToDevice));
     cudaEventRecord(g.e0, 0);
-    crv::k_iga_qp<<<crv::ceil_div(mm, 256), 256>>>(g, dS, dP, dK, dq, nullptr, 0, (float)(tau / phi),
-                                                   (float)mobility_ratio, (float)(density_ratio * gravity));
-    crv::k_iga_gather<<<crv::ceil_div(n2, 256), 256>>>(g, g.A);
+    crv::assemble(g, dS, dP, dK, dq, nullptr, 0, (float)(tau / phi), (float)mobility_ratio,
+                  (float)(density_ratio * gravity), 0);
     crv::kron_solve(g, 0);
     crv::k_iga_dirichlet<<<crv::ceil_div(g.nb, 256), 256>>>(g.A, g.nb);
     crv::k_iga_to_f32<<<crv::ceil_div(n2, 256), 256>>>(g.A, g.outf, n2);
