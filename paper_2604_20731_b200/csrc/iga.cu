@@ -35,6 +35,10 @@ struct IgaDev {
     float *gw = nullptr;                // [m] weights (x quadrature incl. 1/ne), same for y
     double *lf = nullptr;               // [nb][r] sub-diagonal band of the unit lower factor (row i: L_{i,i-1..i-r})
     double *dinv = nullptr;             // [nb] 1/D of LDL^T
+    int nseg = 0;                       // k_iga_band_seg: segments per column (0: not used)
+    int *seg0 = nullptr;                // [nseg + 1] segment starts
+    double *cfw = nullptr, *cbw = nullptr;   // [nb][r] homogeneous responses of the forward / backward
+                                             // substitution to the state at the segment's entry
     float *qv = nullptr;                // [3][m*m] integrand weights
     double *A = nullptr, *B = nullptr;  // nb*nb work matrices: the mass solves run in fp64 (the degree-3
                                         // mass matrix loses ~4 digits to conditioning in fp32)
@@ -181,36 +185,81 @@ __global__ void k_iga_gather(IgaDev g, double *__restrict__ L) {
 // supports touch (a halo of r elements) into shared memory, and then each thread sums its test
 // function's load, factorised by Gauss rows (fp32 row sums of at most (r+1)^2 terms, fp64 across
 // rows). The 3 x m^2 integrand array never goes through HBM.
-template <int TB>
+template <int TB, int RD>   // RD: the spline degree r (compile time: the per-point loops unroll)
 __global__ void __launch_bounds__(TB * TB) k_iga_assemble(IgaDev g, const float *__restrict__ S,
                                                           const float *__restrict__ P, const float *__restrict__ K,
                                                           const float *__restrict__ q, const float *__restrict__ fq,
                                                           int mode, float tau_phi, float mob, float grav_y,
                                                           double *__restrict__ L) {
-    extern __shared__ float sq[];   // [3][QW][QW] integrand of the block's Gauss points
-    const int r = g.r, R1 = r + 1, ne = g.ne, nb = g.nb, m = g.m;
+    extern __shared__ float sq[];   // [3][QW][QW] integrand of the block's Gauss points, then the staged inputs
+    constexpr int r = RD, R1 = RD + 1, RR = R1 * R1, QW = (TB + r) * R1;
+    const int ne = g.ne, nb = g.nb, m = g.m;
     const int k0 = blockIdx.x * TB, l0 = blockIdx.y * TB;
     const int ex0 = max(k0 - r, 0), ey0 = max(l0 - r, 0);                          // first element
     const int ex1 = min(k0 + TB - 1, ne - 1), ey1 = min(l0 + TB - 1, ne - 1);      // last element
-    const int QX = (ex1 - ex0 + 1) * R1, QY = (ey1 - ey0 + 1) * R1;
-    const int QW = (TB + r) * R1;
+    const int EX = ex1 - ex0 + 1, EY = ey1 - ey0 + 1;
+    const int QX = EX * R1, QY = EY * R1;
+    // staged inputs (one batched pass over global memory; every later read is shared memory):
+    // basis values / x-derivatives of the x and y elements, Gauss weights, and (mode 0) the S and P
+    // coefficient tiles and the element fields K, q; (mode 1) the values fq at the block's Gauss points
+    float *sbx = sq + 3 * QW * QW, *sdx = sbx + EX * RR, *sby = sdx + EX * RR, *sdy = sby + EY * RR;
+    float *sgx = sdy + EY * RR, *sgy = sgx + QX;
+    const int CX = EX + r, CY = EY + r;
+    float *sS = sgy + QY, *sP = sS + CX * CY, *sK = sP + CX * CY, *sQ = sK + EX * EY;
+    float *sF = sS;   // mode 1: [QY][QX] in place of the mode-0 arrays
+    {
+        const int n1 = EX * RR, n2 = n1 + EX * RR, n3 = n2 + EY * RR, n4 = n3 + EY * RR, n5 = n4 + QX, n6 = n5 + QY;
+        const int n7 = n6 + (mode == 1 ? 0 : CX * CY), n8 = n7 + (mode == 1 ? 0 : CX * CY);
+        const int n9 = n8 + (mode == 1 ? 0 : EX * EY), n10 = n9 + (mode == 1 ? QX * QY : EX * EY);
+        auto src = [&](int e) -> float {
+            if (mode == 1 && e >= n6) {
+                const int t = e - n6;
+                return fq[(long)(ey0 * R1 + t / QX) * m + ex0 * R1 + t % QX];
+            }
+            if (e < n1) return g.bv[(long)ex0 * RR + e];
+            if (e < n2) return g.bd[(long)ex0 * RR + (e - n1)];
+            if (e < n3) return g.bv[(long)ey0 * RR + (e - n2)];
+            if (e < n4) return g.bd[(long)ey0 * RR + (e - n3)];
+            if (e < n5) return g.gw[ex0 * R1 + (e - n4)];
+            if (e < n6) return g.gw[ey0 * R1 + (e - n5)];
+            if (e < n8) {
+                const int t = e < n7 ? e - n6 : e - n7;
+                const int cy = t / CX, cx = t % CX;
+                const int gy = min(ey0 + cy, nb - 1), gx = min(ex0 + cx, nb - 1);
+                return (e < n7 ? S : P)[(long)gy * nb + gx];
+            }
+            const int t = e < n9 ? e - n8 : e - n9;
+            const long el = (long)(ey0 + t / EX) * ne + ex0 + t % EX;
+            return e < n9 ? K[el] : q[el];
+        };
+        const int step = (int)blockDim.x;
+        for (int e0 = threadIdx.x; e0 < n10; e0 += 4 * step) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = e0 + u * step < n10 ? src(e0 + u * step) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (e0 + u * step < n10) sbx[e0 + u * step] = v[u];   // the staged arrays are contiguous
+        }
+    }
+    __syncthreads();
     for (int t = threadIdx.x; t < QX * QY; t += blockDim.x) {
         const int jy = t / QX, ix = t % QX;
-        const int i = ex0 * R1 + ix, j = ey0 * R1 + jy;   // global Gauss point indices
-        const long p = (long)j * m + i;
-        const int ex = i / R1, qx = i % R1, ey = j / R1, qy = j % R1;
-        const float w = g.gw[i] * g.gw[j];
+        const int lex = ix / R1, qx = ix % R1, ley = jy / R1, qy = jy % R1;
+        const float w = sgx[ix] * sgy[jy];
         float v0, v1, v2;
         if (mode == 1) {
-            v0 = w * fq[p];
+            v0 = w * sF[jy * QX + ix];
             v1 = v2 = 0.f;
         } else {
-            const float *bvx = g.bv + ((long)ex * R1 + qx) * R1, *bdx = g.bd + ((long)ex * R1 + qx) * R1;
-            const float *bvy = g.bv + ((long)ey * R1 + qy) * R1, *bdy = g.bd + ((long)ey * R1 + qy) * R1;
+            const float *bvx = sbx + (lex * R1 + qx) * R1, *bdx = sdx + (lex * R1 + qx) * R1;
+            const float *bvy = sby + (ley * R1 + qy) * R1, *bdy = sdy + (ley * R1 + qy) * R1;
             float sv = 0.f, px = 0.f, py = 0.f;
+#pragma unroll
             for (int b = 0; b < R1; ++b) {
-                const float *srow = S + (long)(ey + b) * nb + ex, *prow = P + (long)(ey + b) * nb + ex;
+                const float *srow = sS + (ley + b) * CX + lex, *prow = sP + (ley + b) * CX + lex;
                 float ss = 0.f, ppx = 0.f, ppy = 0.f;
+#pragma unroll
                 for (int a = 0; a < R1; ++a) {
                     ss = fmaf(srow[a], bvx[a], ss);
                     ppx = fmaf(prow[a], bdx[a], ppx);
@@ -220,9 +269,9 @@ __global__ void __launch_bounds__(TB * TB) k_iga_assemble(IgaDev g, const float 
                 px = fmaf(ppx, bvy[b], px);
                 py = fmaf(ppy, bdy[b], py);
             }
-            const long e = (long)ey * ne + ex;
-            const float flux = -tau_phi * mob * sv * K[e];
-            v0 = w * (sv + tau_phi * q[e]);
+            const int el = ley * EX + lex;
+            const float flux = -tau_phi * mob * sv * sK[el];
+            v0 = w * (sv + tau_phi * sQ[el]);
             v1 = w * flux * px;
             v2 = w * flux * (py + grav_y);
         }
@@ -234,30 +283,42 @@ __global__ void __launch_bounds__(TB * TB) k_iga_assemble(IgaDev g, const float 
     __syncthreads();
     const int k = k0 + (int)(threadIdx.x % TB), l = l0 + (int)(threadIdx.x / TB);
     if (k >= nb || l >= nb) return;
-    // the x-direction test-function factors of this k, in Gauss-point order (at most (r+1)^2 each)
-    float vxs[(IGA_MAX_R + 1) * (IGA_MAX_R + 1)], dxs[(IGA_MAX_R + 1) * (IGA_MAX_R + 1)];
-    const int exa = max(k - r, 0), exb = min(k, ne - 1);
-    int nx = 0;
-    for (int ex = exa; ex <= exb; ++ex)
-        for (int qx = 0; qx < R1; ++qx, ++nx) {
-            vxs[nx] = g.bv[((long)ex * R1 + qx) * R1 + (k - ex)];
-            dxs[nx] = g.bd[((long)ex * R1 + qx) * R1 + (k - ex)];
+    // the x-direction test-function factors of this k in registers: element ex = exa + de of its
+    // support (exa = max(k - r, 0)), Gauss point qx; zero where the support leaves the mesh
+    const int exa = max(k - r, 0), nex = min(k, ne - 1) - exa + 1;
+    float vxs[R1][R1], dxs[R1][R1];
+#pragma unroll
+    for (int de = 0; de < R1; ++de)
+#pragma unroll
+        for (int qx = 0; qx < R1; ++qx) {
+            const bool ok = de < nex;
+            const int o = ((ok ? exa + de - ex0 : 0) * R1 + qx) * R1 + (ok ? k - exa - de : 0);
+            vxs[de][qx] = ok ? sbx[o] : 0.f;
+            dxs[de][qx] = ok ? sdx[o] : 0.f;
         }
     // per Gauss row: A = sum_x (q0 vx + q1 dx), B = sum_x q2 vx in fp32 (at most (r+1)^2 terms),
     // then L += vy A + dy B in fp64 (two conversions per row instead of six per point)
     double acc = 0.0;
     const int xo = (exa - ex0) * R1;
-    for (int ey = max(l - r, 0); ey <= min(l, ne - 1); ++ey) {
-        const int b = l - ey;
+    const int eya = max(l - r, 0), ney = min(l, ne - 1) - eya + 1;
+#pragma unroll
+    for (int de = 0; de < R1; ++de) {
+        if (de >= ney) break;
+        const int ey = eya + de, b = l - ey;
+#pragma unroll
         for (int qy = 0; qy < R1; ++qy) {
-            const float vy = g.bv[((long)ey * R1 + qy) * R1 + b], dy = g.bd[((long)ey * R1 + qy) * R1 + b];
+            const float vy = sby[((ey - ey0) * R1 + qy) * R1 + b], dy = sdy[((ey - ey0) * R1 + qy) * R1 + b];
             const float *r0 = sq + ((ey - ey0) * R1 + qy) * QW + xo;
             float A = 0.f, B = 0.f;
-            for (int t = 0; t < nx; ++t) {
-                A = fmaf(r0[t], vxs[t], A);
-                A = fmaf(r0[QW * QW + t], dxs[t], A);
-                B = fmaf(r0[2 * QW * QW + t], vxs[t], B);
-            }
+#pragma unroll
+            for (int dx2 = 0; dx2 < R1; ++dx2)
+#pragma unroll
+                for (int qx = 0; qx < R1; ++qx) {
+                    const int t = (dx2 < nex ? dx2 : 0) * R1 + qx;   // zero factors beyond the mesh
+                    A = fmaf(r0[t], vxs[dx2][qx], A);
+                    A = fmaf(r0[QW * QW + t], dxs[dx2][qx], A);
+                    B = fmaf(r0[2 * QW * QW + t], vxs[dx2][qx], B);
+                }
             acc = fma((double)vy, (double)A, acc);
             acc = fma((double)dy, (double)B, acc);
         }
@@ -270,6 +331,17 @@ static bool assemble_split() {   // tuning knob: CRVPINN_IGA_ASSEMBLY=split -> k
     return e && strcmp(e, "split") == 0;
 }
 
+template <int TB, int RD>
+static void assemble_launch(IgaDev &g, const float *S, const float *P, const float *K, const float *q, const float *fq,
+                            int mode, float tau_phi, float mob, float grav_y, cudaStream_t s) {
+    constexpr int R1 = RD + 1, QW = (TB + RD) * R1, E = TB + RD, RR = R1 * R1;
+    constexpr size_t smem = sizeof(float) * (3 * QW * QW + 4 * E * RR + 2 * E * R1 +
+                                             2 * (E + RD) * (E + RD) + 2 * E * E + E * R1 * E * R1);
+    cudaFuncSetAttribute(k_iga_assemble<TB, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 grid(ceil_div(g.nb, TB), ceil_div(g.nb, TB));
+    k_iga_assemble<TB, RD><<<grid, TB * TB, smem, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, g.A);
+}
+
 // the load vector L (fp64, nb x nb) of mode 0 (saturation step) or 1 (projection of fq)
 static void assemble(IgaDev &g, const float *S, const float *P, const float *K, const float *q, const float *fq,
                      int mode, float tau_phi, float mob, float grav_y, cudaStream_t s) {
@@ -279,21 +351,13 @@ static void assemble(IgaDev &g, const float *S, const float *P, const float *K, 
         k_iga_gather<<<ceil_div(n2, 256), 256, 0, s>>>(g, g.A);
         return;
     }
-    const int R1 = g.r + 1;
-    if (g.r <= 3) {
-        constexpr int TB = 16;
-        const int QW = (TB + g.r) * R1;
-        const size_t smem = sizeof(float) * 3 * QW * QW;
-        cudaFuncSetAttribute(k_iga_assemble<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const dim3 grid(ceil_div(g.nb, TB), ceil_div(g.nb, TB));
-        k_iga_assemble<TB><<<grid, TB * TB, smem, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, g.A);
-    } else {
-        constexpr int TB = 8;
-        const int QW = (TB + g.r) * R1;
-        const size_t smem = sizeof(float) * 3 * QW * QW;
-        cudaFuncSetAttribute(k_iga_assemble<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const dim3 grid(ceil_div(g.nb, TB), ceil_div(g.nb, TB));
-        k_iga_assemble<TB><<<grid, TB * TB, smem, s>>>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, g.A);
+    switch (g.r) {
+        case 1: assemble_launch<16, 1>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
+        case 2: assemble_launch<16, 2>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
+        case 3: assemble_launch<16, 3>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
+        case 4: assemble_launch<8, 4>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
+        case 5: assemble_launch<8, 5>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
+        default: assemble_launch<8, 6>(g, S, P, K, q, fq, mode, tau_phi, mob, grav_y, s); break;
     }
 }
 
@@ -405,15 +469,30 @@ __global__ void k_iga_eval(IgaDev g, const float *__restrict__ C, const float *_
 // The same solve with a block's 32 columns staged in shared memory: the substitutions are serial in
 // i, so their latency (not bandwidth) bounds them, and shared memory has ~10x less of it than L2
 constexpr int IGA_BAND_COLS = 32;
+// a block's 32 columns -> shared memory [n][32], eight loads in flight per thread (a load-store
+// loop keeps one: its global-load latency was most of the band kernels' time)
+__device__ __forceinline__ void stage_cols(double *sx, const double *__restrict__ X, int n, int c0, int nc) {
+    const int total = n * IGA_BAND_COLS, step = (int)blockDim.x;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * step) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * step;
+            const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+            v[u] = (e < total && cc < nc) ? X[(long)i * n + c0 + cc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (e0 + u * step < total) sx[e0 + u * step] = v[u];
+    }
+}
+
 __global__ void k_iga_band_smem(IgaDev g, double *__restrict__ X) {
     extern __shared__ double sx[];   // [nb][IGA_BAND_COLS]
     const int n = g.nb, r = g.r;
     const int c0 = blockIdx.x * IGA_BAND_COLS;
     const int nc = min(IGA_BAND_COLS, n - c0);
-    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
-        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
-        sx[e] = cc < nc ? X[(long)i * n + c0 + cc] : 0.0;
-    }
+    stage_cols(sx, X, n, c0, nc);
     __syncthreads();
     if (threadIdx.x < IGA_BAND_COLS) {
         double *col = sx + threadIdx.x;
@@ -448,10 +527,7 @@ __global__ void k_iga_band_reg(IgaDev g, double *__restrict__ X) {
     double *slf = sx + (size_t)n * IGA_BAND_COLS, *sdi = slf + (size_t)(n + R) * R;
     const int c0 = blockIdx.x * IGA_BAND_COLS;
     const int nc = min(IGA_BAND_COLS, n - c0);
-    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
-        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
-        sx[e] = cc < nc ? X[(long)i * n + c0 + cc] : 0.0;
-    }
+    stage_cols(sx, X, n, c0, nc);
     for (int e = threadIdx.x; e < (n + R) * R; e += blockDim.x) {
         const int i = e / R, d = e % R + 1;
         slf[e] = (i < n && d <= i) ? g.lf[(long)i * g.r + d - 1] : 0.0;
@@ -523,6 +599,188 @@ __global__ void k_iga_band_reg(IgaDev g, double *__restrict__ X) {
     }
 }
 
+// The substitutions of k_iga_band_reg split along the chain: NSEG segments of every column run at
+// once. A substitution is linear, so a segment's values are its particular solution from a zero
+// entry state (phase A) plus the response to the true entry state (the R values before it; phase
+// C), whose coefficients (cfw / cbw, the homogeneous solutions inside the segment) depend only on
+// the mass matrix and are precomputed in fp64 at create. Only the entry states are carried from
+// segment to segment, one short step per segment (phase B). 1028 dependent steps per column become
+// 2 x (n / NSEG + NSEG).
+template <int R>
+__global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
+    extern __shared__ double sx[];   // [nb][32] columns, [nb + R][R] band, [nb] 1/D, [nseg][R][32] entry
+                                     // states, [nb][R] forward and backward responses
+    const int n = g.nb, S = g.nseg;
+    double *slf = sx + (size_t)n * IGA_BAND_COLS, *sdi = slf + (size_t)(n + R) * R;
+    double *sst = sdi + n;
+    double *scf = sst + (size_t)S * R * IGA_BAND_COLS, *scb = scf + (size_t)n * R;
+    for (int e = threadIdx.x; e < n * R; e += blockDim.x) {   // (global loads in phase B were its latency)
+        scf[e] = g.cfw[e];
+        scb[e] = g.cbw[e];
+    }
+    const int c0 = blockIdx.x * IGA_BAND_COLS;
+    const int nc = min(IGA_BAND_COLS, n - c0);
+    stage_cols(sx, X, n, c0, nc);
+    for (int e = threadIdx.x; e < (n + R) * R; e += blockDim.x) {
+        const int i = e / R, d = e % R + 1;
+        slf[e] = (i < n && d <= i) ? g.lf[(long)i * g.r + d - 1] : 0.0;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sdi[i] = g.dinv[i];
+    __syncthreads();
+    const int col = threadIdx.x % IGA_BAND_COLS, sg = threadIdx.x / IGA_BAND_COLS;
+    const bool act = sg < S;
+    const int a = act ? g.seg0[sg] : 0, b = act ? g.seg0[sg + 1] : 0;
+    double *cx = sx + col;
+    // ---- forward: L z = x from a zero entry state
+    if (act) {
+        double z[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) z[d] = 0.0;
+        for (int i = a; i < b; ++i) {
+            double v = cx[i * IGA_BAND_COLS];
+#pragma unroll
+            for (int d = R; d >= 1; --d) v = fma(-slf[i * R + d - 1], z[d - 1], v);
+#pragma unroll
+            for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
+            z[0] = v;
+            cx[i * IGA_BAND_COLS] = v;
+        }
+    }
+    __syncthreads();
+    if (sg == 0) {   // entry states: st_s[c] = z_{a_s - 1 - c}
+        double st[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) st[c] = 0.0;
+        for (int s2 = 0; s2 < S; ++s2) {
+#pragma unroll
+            for (int c = 0; c < R; ++c) sst[((size_t)s2 * R + c) * IGA_BAND_COLS + col] = st[c];
+            if (s2 + 1 == S) break;
+            const int e2 = g.seg0[s2 + 1];
+            double nx[R];
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                const int j = e2 - 1 - c;
+                double v = cx[j * IGA_BAND_COLS];
+#pragma unroll
+                for (int c2 = 0; c2 < R; ++c2) v = fma(scf[j * R + c2], st[c2], v);
+                nx[c] = v;
+            }
+#pragma unroll
+            for (int c = 0; c < R; ++c) st[c] = nx[c];
+        }
+    }
+    __syncthreads();
+    if (act) {   // z = particular + response to the entry state, then y = D^-1 z
+        double st[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) st[c] = sst[((size_t)sg * R + c) * IGA_BAND_COLS + col];
+        for (int i = a; i < b; ++i) {
+            double v = cx[i * IGA_BAND_COLS];
+#pragma unroll
+            for (int c = 0; c < R; ++c) v = fma(scf[i * R + c], st[c], v);
+            cx[i * IGA_BAND_COLS] = v * sdi[i];
+        }
+    }
+    __syncthreads();
+    // ---- backward: L^T x = y from a zero exit state
+    if (act) {
+        double z[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) z[d] = 0.0;
+        for (int i = b - 1; i >= a; --i) {
+            double v = cx[i * IGA_BAND_COLS];
+#pragma unroll
+            for (int d = R; d >= 1; --d) v = fma(-slf[(i + d) * R + d - 1], z[d - 1], v);
+#pragma unroll
+            for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
+            z[0] = v;
+            cx[i * IGA_BAND_COLS] = v;
+        }
+    }
+    __syncthreads();
+    if (sg == 0) {   // exit states: st_s[c] = x_{b_s + c}
+        double st[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) st[c] = 0.0;
+        for (int s2 = S - 1; s2 >= 0; --s2) {
+#pragma unroll
+            for (int c = 0; c < R; ++c) sst[((size_t)s2 * R + c) * IGA_BAND_COLS + col] = st[c];
+            if (s2 == 0) break;
+            const int e2 = g.seg0[s2];
+            double nx[R];
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                const int j = e2 + c;
+                double v = cx[j * IGA_BAND_COLS];
+#pragma unroll
+                for (int c2 = 0; c2 < R; ++c2) v = fma(scb[j * R + c2], st[c2], v);
+                nx[c] = v;
+            }
+#pragma unroll
+            for (int c = 0; c < R; ++c) st[c] = nx[c];
+        }
+    }
+    __syncthreads();
+    if (act) {
+        double st[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) st[c] = sst[((size_t)sg * R + c) * IGA_BAND_COLS + col];
+        for (int i = a; i < b; ++i) {
+            double v = cx[i * IGA_BAND_COLS];
+#pragma unroll
+            for (int c = 0; c < R; ++c) v = fma(scb[i * R + c], st[c], v);
+            cx[i * IGA_BAND_COLS] = v;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
+        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+        if (cc < nc) X[(long)i * n + c0 + cc] = sx[e];
+    }
+}
+
+template <int R>
+static size_t band_seg_smem(int n, int nseg) {
+    return sizeof(double) * ((size_t)n * IGA_BAND_COLS + (size_t)(n + R) * R + n + (size_t)nseg * R * IGA_BAND_COLS +
+                             2 * (size_t)n * R);
+}
+
+template <int R>
+static bool band_seg_launch(IgaDev &g, double *X, cudaStream_t s) {
+    const size_t smem = band_seg_smem<R>(g.nb, g.nseg);
+    if (g.nseg < 2 || smem > 200 * 1024) return false;
+    cudaFuncSetAttribute(k_iga_band_seg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_iga_band_seg<R><<<ceil_div(g.nb, IGA_BAND_COLS), IGA_BAND_COLS * g.nseg, smem, s>>>(g, X);
+    return true;
+}
+
+static bool band_seg_ok(const IgaDev &g) {
+    const char *bv = getenv("CRVPINN_IGA_BAND");   // tuning knob: "reg" / "smem" = the serial kernels
+    if (bv && (strcmp(bv, "reg") == 0 || strcmp(bv, "smem") == 0)) return false;
+    if (g.nseg < 2) return false;
+    size_t sm;
+    switch (g.r) {
+        case 1: sm = band_seg_smem<1>(g.nb, g.nseg); break;
+        case 2: sm = band_seg_smem<2>(g.nb, g.nseg); break;
+        case 3: sm = band_seg_smem<3>(g.nb, g.nseg); break;
+        case 4: sm = band_seg_smem<4>(g.nb, g.nseg); break;
+        case 5: sm = band_seg_smem<5>(g.nb, g.nseg); break;
+        default: sm = band_seg_smem<6>(g.nb, g.nseg); break;
+    }
+    return sm <= 200 * 1024;
+}
+
+static bool band_seg(IgaDev &g, double *X, cudaStream_t s) {
+    switch (g.r) {
+        case 1: return band_seg_launch<1>(g, X, s);
+        case 2: return band_seg_launch<2>(g, X, s);
+        case 3: return band_seg_launch<3>(g, X, s);
+        case 4: return band_seg_launch<4>(g, X, s);
+        case 5: return band_seg_launch<5>(g, X, s);
+        default: return band_seg_launch<6>(g, X, s);
+    }
+}
+
 template <int R>
 static size_t band_reg_smem(int n) { return sizeof(double) * ((size_t)n * IGA_BAND_COLS + (size_t)(n + R) * R + n); }
 
@@ -554,7 +812,11 @@ void kron_solve(IgaDev &g, cudaStream_t s) {
     const size_t smem = sizeof(double) * (size_t)n * IGA_BAND_COLS;
     const char *bv = getenv("CRVPINN_IGA_BAND");   // tuning knob: "smem" = k_iga_band_smem
     const bool reg = !(bv && strcmp(bv, "smem") == 0) && band_reg_smem<6>(n) <= 200 * 1024;
-    if (reg) {
+    if (band_seg_ok(g)) {
+        band_seg(g, g.A, s);
+        k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);   // along l (rows), then along k
+        band_seg(g, g.B, s);
+    } else if (reg) {
         band_reg(g, g.A, s);                       // along l (rows)
         k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
         band_reg(g, g.B, s);                       // along k
@@ -657,12 +919,47 @@ int crvpinn_iga_create(crvpinn_iga **out, int n_elements, int degree, int device
     }
     std::vector<double> lf(Lb), dinv(nb);
     for (int i = 0; i < nb; ++i) dinv[i] = 1.0 / D[i];
+    // chain segments of k_iga_band_seg (balanced, each >= max(degree, 8) rows) and the homogeneous
+    // responses of both substitutions to a segment's entry state
+    int nseg = nb / 32 > 0 ? (nb + 31) / 32 : 1;
+    if (nseg > 32) nseg = 32;
+    while (nseg > 1 && nb / nseg < (degree > 8 ? degree : 8)) --nseg;
+    std::vector<int> seg0(nseg + 1);
+    for (int s2 = 0; s2 <= nseg; ++s2) seg0[s2] = (int)((long)s2 * nb / nseg);
+    std::vector<double> cfw((size_t)nb * degree, 0.0), cbw((size_t)nb * degree, 0.0);
+    for (int s2 = 0; s2 < nseg; ++s2) {
+        const int a = seg0[s2], b = seg0[s2 + 1];
+        for (int c = 0; c < degree; ++c) {
+            std::vector<double> z((size_t)(b - a + degree), 0.0);   // z[degree + (i - a)]; entry z[degree-1-c] = 1
+            z[(size_t)(degree - 1 - c)] = 1.0;
+            for (int i = a; i < b; ++i) {
+                double v = 0.0;
+                for (int d = 1; d <= degree; ++d)
+                    if (i - d >= 0) v -= Lb[(size_t)i * degree + d - 1] * z[(size_t)(degree + i - a - d)];
+                z[(size_t)(degree + i - a)] = v;
+                cfw[(size_t)i * degree + c] = v;
+            }
+            std::vector<double> x((size_t)(b - a + degree), 0.0);   // x[i - a]; exit x[b - a + c] = 1
+            x[(size_t)(b - a + c)] = 1.0;
+            for (int i = b - 1; i >= a; --i) {
+                double v = 0.0;
+                for (int d = 1; d <= degree; ++d)
+                    if (i + d < nb) v -= Lb[(size_t)(i + d) * degree + d - 1] * x[(size_t)(i - a + d)];
+                x[(size_t)(i - a)] = v;
+                cbw[(size_t)i * degree + c] = v;
+            }
+        }
+    }
+    g.nseg = nseg;
     const long mm = (long)g.m * g.m;
     bool ok = cudaMalloc(&g.bv, sizeof(float) * bv.size()) == cudaSuccess &&
               cudaMalloc(&g.bd, sizeof(float) * bd.size()) == cudaSuccess &&
               cudaMalloc(&g.gw, sizeof(float) * w.size()) == cudaSuccess &&
               cudaMalloc(&g.lf, sizeof(double) * (lf.size() ? lf.size() : 1)) == cudaSuccess &&
               cudaMalloc(&g.dinv, sizeof(double) * nb) == cudaSuccess &&
+              cudaMalloc(&g.seg0, sizeof(int) * seg0.size()) == cudaSuccess &&
+              cudaMalloc(&g.cfw, sizeof(double) * cfw.size()) == cudaSuccess &&
+              cudaMalloc(&g.cbw, sizeof(double) * cbw.size()) == cudaSuccess &&
               cudaMalloc(&g.qv, sizeof(float) * 3 * mm) == cudaSuccess &&
               cudaMalloc(&g.A, sizeof(double) * nb * nb) == cudaSuccess &&
               cudaMalloc(&g.B, sizeof(double) * nb * nb) == cudaSuccess &&
@@ -673,7 +970,10 @@ int crvpinn_iga_create(crvpinn_iga **out, int n_elements, int degree, int device
              cudaMemcpy(g.bd, bd.data(), sizeof(float) * bd.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
              cudaMemcpy(g.gw, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
              cudaMemcpy(g.lf, lf.data(), sizeof(double) * lf.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
-             cudaMemcpy(g.dinv, dinv.data(), sizeof(double) * nb, cudaMemcpyHostToDevice) == cudaSuccess;
+             cudaMemcpy(g.dinv, dinv.data(), sizeof(double) * nb, cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.seg0, seg0.data(), sizeof(int) * seg0.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.cfw, cfw.data(), sizeof(double) * cfw.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+             cudaMemcpy(g.cbw, cbw.data(), sizeof(double) * cbw.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) {
         crvpinn_iga_destroy(h);
         return CRVPINN_ENOMEM;
@@ -777,7 +1077,7 @@ void crvpinn_iga_destroy(crvpinn_iga *h) {
     if (!h) return;
     IgaDev &g = h->g;
     cudaSetDevice(h->device);
-    void *bufs[] = {g.bv, g.bd, g.gw, g.lf, g.dinv, g.qv, g.A, g.B, g.io, g.outf};
+    void *bufs[] = {g.bv, g.bd, g.gw, g.lf, g.dinv, g.seg0, g.cfw, g.cbw, g.qv, g.A, g.B, g.io, g.outf};
     for (void *p : bufs)
         if (p) cudaFree(p);
     if (g.e0) cudaEventDestroy(g.e0);
