@@ -606,12 +606,15 @@ __global__ void k_iga_band_reg(IgaDev g, double *__restrict__ X) {
 // the mass matrix and are precomputed in fp64 at create. Only the entry states are carried from
 // segment to segment, one short step per segment (phase B). 1028 dependent steps per column become
 // 2 x (n / NSEG + NSEG).
-template <int R>
+// TR = false: the block's 32 columns of X (solve along the row index); TR = true: 32 rows of X (solve
+// along the column index, X^T staged on the fly: no transposes around the second direction)
+template <int R, bool TR>
 __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
+    constexpr int CS = TR ? IGA_BAND_COLS + 1 : IGA_BAND_COLS;   // odd stride: the transposed staging is conflict-light
     extern __shared__ double sx[];   // [nb][32] columns, [nb + R][R] band, [nb] 1/D, [nseg][R][32] entry
                                      // states, [nb][R] forward and backward responses
     const int n = g.nb, S = g.nseg;
-    double *slf = sx + (size_t)n * IGA_BAND_COLS, *sdi = slf + (size_t)(n + R) * R;
+    double *slf = sx + (size_t)n * CS, *sdi = slf + (size_t)(n + R) * R;
     double *sst = sdi + n;
     double *scf = sst + (size_t)S * R * IGA_BAND_COLS, *scb = scf + (size_t)n * R;
     for (int e = threadIdx.x; e < n * R; e += blockDim.x) {   // (global loads in phase B were its latency)
@@ -620,7 +623,24 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
     }
     const int c0 = blockIdx.x * IGA_BAND_COLS;
     const int nc = min(IGA_BAND_COLS, n - c0);
-    stage_cols(sx, X, n, c0, nc);
+    if (TR) {
+        const int total = n * IGA_BAND_COLS, step = (int)blockDim.x;
+        for (int e0 = threadIdx.x; e0 < total; e0 += 8 * step) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * step, cc = e / n, i = e % n;
+                v[u] = (e < total && cc < nc) ? X[(long)(c0 + cc) * n + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * step;
+                if (e < total) sx[(e % n) * CS + e / n] = v[u];
+            }
+        }
+    } else {
+        stage_cols(sx, X, n, c0, nc);
+    }
     for (int e = threadIdx.x; e < (n + R) * R; e += blockDim.x) {
         const int i = e / R, d = e % R + 1;
         slf[e] = (i < n && d <= i) ? g.lf[(long)i * g.r + d - 1] : 0.0;
@@ -637,13 +657,13 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
         for (int d = 0; d < R; ++d) z[d] = 0.0;
         for (int i = a; i < b; ++i) {
-            double v = cx[i * IGA_BAND_COLS];
+            double v = cx[i * CS];
 #pragma unroll
             for (int d = R; d >= 1; --d) v = fma(-slf[i * R + d - 1], z[d - 1], v);
 #pragma unroll
             for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
             z[0] = v;
-            cx[i * IGA_BAND_COLS] = v;
+            cx[i * CS] = v;
         }
     }
     __syncthreads();
@@ -660,7 +680,7 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
             for (int c = 0; c < R; ++c) {
                 const int j = e2 - 1 - c;
-                double v = cx[j * IGA_BAND_COLS];
+                double v = cx[j * CS];
 #pragma unroll
                 for (int c2 = 0; c2 < R; ++c2) v = fma(scf[j * R + c2], st[c2], v);
                 nx[c] = v;
@@ -675,10 +695,10 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
         for (int c = 0; c < R; ++c) st[c] = sst[((size_t)sg * R + c) * IGA_BAND_COLS + col];
         for (int i = a; i < b; ++i) {
-            double v = cx[i * IGA_BAND_COLS];
+            double v = cx[i * CS];
 #pragma unroll
             for (int c = 0; c < R; ++c) v = fma(scf[i * R + c], st[c], v);
-            cx[i * IGA_BAND_COLS] = v * sdi[i];
+            cx[i * CS] = v * sdi[i];
         }
     }
     __syncthreads();
@@ -688,13 +708,13 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
         for (int d = 0; d < R; ++d) z[d] = 0.0;
         for (int i = b - 1; i >= a; --i) {
-            double v = cx[i * IGA_BAND_COLS];
+            double v = cx[i * CS];
 #pragma unroll
             for (int d = R; d >= 1; --d) v = fma(-slf[(i + d) * R + d - 1], z[d - 1], v);
 #pragma unroll
             for (int d = R - 1; d > 0; --d) z[d] = z[d - 1];
             z[0] = v;
-            cx[i * IGA_BAND_COLS] = v;
+            cx[i * CS] = v;
         }
     }
     __syncthreads();
@@ -711,7 +731,7 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
             for (int c = 0; c < R; ++c) {
                 const int j = e2 + c;
-                double v = cx[j * IGA_BAND_COLS];
+                double v = cx[j * CS];
 #pragma unroll
                 for (int c2 = 0; c2 < R; ++c2) v = fma(scb[j * R + c2], st[c2], v);
                 nx[c] = v;
@@ -726,31 +746,42 @@ __global__ void k_iga_band_seg(IgaDev g, double *__restrict__ X) {
 #pragma unroll
         for (int c = 0; c < R; ++c) st[c] = sst[((size_t)sg * R + c) * IGA_BAND_COLS + col];
         for (int i = a; i < b; ++i) {
-            double v = cx[i * IGA_BAND_COLS];
+            double v = cx[i * CS];
 #pragma unroll
             for (int c = 0; c < R; ++c) v = fma(scb[i * R + c], st[c], v);
-            cx[i * IGA_BAND_COLS] = v;
+            cx[i * CS] = v;
         }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < n * IGA_BAND_COLS; e += blockDim.x) {
-        const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
-        if (cc < nc) X[(long)i * n + c0 + cc] = sx[e];
+        if (TR) {
+            const int cc = e / n, i = e % n;
+            if (cc < nc) X[(long)(c0 + cc) * n + i] = sx[i * CS + cc];
+        } else {
+            const int i = e / IGA_BAND_COLS, cc = e % IGA_BAND_COLS;
+            if (cc < nc) X[(long)i * n + c0 + cc] = sx[e];
+        }
     }
 }
 
 template <int R>
 static size_t band_seg_smem(int n, int nseg) {
-    return sizeof(double) * ((size_t)n * IGA_BAND_COLS + (size_t)(n + R) * R + n + (size_t)nseg * R * IGA_BAND_COLS +
+    return sizeof(double) * ((size_t)n * (IGA_BAND_COLS + 1) + (size_t)(n + R) * R + n + (size_t)nseg * R * IGA_BAND_COLS +
                              2 * (size_t)n * R);
 }
 
 template <int R>
-static bool band_seg_launch(IgaDev &g, double *X, cudaStream_t s) {
+static bool band_seg_launch(IgaDev &g, double *X, bool tr, cudaStream_t s) {
     const size_t smem = band_seg_smem<R>(g.nb, g.nseg);
     if (g.nseg < 2 || smem > 200 * 1024) return false;
-    cudaFuncSetAttribute(k_iga_band_seg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k_iga_band_seg<R><<<ceil_div(g.nb, IGA_BAND_COLS), IGA_BAND_COLS * g.nseg, smem, s>>>(g, X);
+    const dim3 grid(ceil_div(g.nb, IGA_BAND_COLS)), block(IGA_BAND_COLS * g.nseg);
+    if (tr) {
+        cudaFuncSetAttribute(k_iga_band_seg<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        k_iga_band_seg<R, true><<<grid, block, smem, s>>>(g, X);
+    } else {
+        cudaFuncSetAttribute(k_iga_band_seg<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        k_iga_band_seg<R, false><<<grid, block, smem, s>>>(g, X);
+    }
     return true;
 }
 
@@ -770,14 +801,14 @@ static bool band_seg_ok(const IgaDev &g) {
     return sm <= 200 * 1024;
 }
 
-static bool band_seg(IgaDev &g, double *X, cudaStream_t s) {
+static bool band_seg(IgaDev &g, double *X, bool tr, cudaStream_t s) {
     switch (g.r) {
-        case 1: return band_seg_launch<1>(g, X, s);
-        case 2: return band_seg_launch<2>(g, X, s);
-        case 3: return band_seg_launch<3>(g, X, s);
-        case 4: return band_seg_launch<4>(g, X, s);
-        case 5: return band_seg_launch<5>(g, X, s);
-        default: return band_seg_launch<6>(g, X, s);
+        case 1: return band_seg_launch<1>(g, X, tr, s);
+        case 2: return band_seg_launch<2>(g, X, tr, s);
+        case 3: return band_seg_launch<3>(g, X, tr, s);
+        case 4: return band_seg_launch<4>(g, X, tr, s);
+        case 5: return band_seg_launch<5>(g, X, tr, s);
+        default: return band_seg_launch<6>(g, X, tr, s);
     }
 }
 
@@ -813,9 +844,9 @@ void kron_solve(IgaDev &g, cudaStream_t s) {
     const char *bv = getenv("CRVPINN_IGA_BAND");   // tuning knob: "smem" = k_iga_band_smem
     const bool reg = !(bv && strcmp(bv, "smem") == 0) && band_reg_smem<6>(n) <= 200 * 1024;
     if (band_seg_ok(g)) {
-        band_seg(g, g.A, s);
-        k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);   // along l (rows), then along k
-        band_seg(g, g.B, s);
+        band_seg(g, g.A, false, s);   // along l (rows)
+        band_seg(g, g.A, true, s);    // along k, in place: the result is already in g.A
+        return;
     } else if (reg) {
         band_reg(g, g.A, s);                       // along l (rows)
         k_iga_transpose<<<tg, tb, 0, s>>>(g.A, g.B, n);
