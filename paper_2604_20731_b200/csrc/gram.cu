@@ -140,9 +140,22 @@ __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restric
     float *se = sr + stride;
     const float *r = rhat + (size_t)a * n;
     const float *e = etab + (size_t)a * n;
-    for (int j = lane; j < n; j += 32) {
-        sr[j] = h2 * r[j];
-        se[j] = e[j];
+    for (int j0 = lane; j0 < n; j0 += 8 * 32) {   // eight loads of each row in flight per lane
+        float rv[8], ev[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 32 * u;
+            rv[u] = j < n ? r[j] : 0.0f;
+            ev[u] = j < n ? e[j] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 32 * u;
+            if (j < n) {
+                sr[j] = h2 * rv[u];
+                se[j] = ev[u];
+            }
+        }
     }
     __syncwarp();
     const int j0 = lane * seg, j1 = min(n, j0 + seg);
