@@ -106,9 +106,12 @@ struct crvpinn_ctx {
     int64_t prof_iters = 0;
     std::string err;
     std::vector<void *> allocs;
-    // crvpinn_eval_points scratch (device xy [cap][2] + p [cap]), grown on demand
-    float *pts = nullptr;
-    long pts_cap = 0;
+    // crvpinn_eval_points: two chunks in flight, each with device xy + p, pinned host xy + p, and
+    // events; a copy stream moves chunk c+1 in and chunk c-1 out while chunk c computes
+    float *pts = nullptr;                 // device [2][3 * EP_CHUNK]
+    float *pts_h = nullptr;               // pinned [2][3 * EP_CHUNK]
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ep_in[2] = {}, ep_done[2] = {}, ep_out[2] = {};
     float *ds_u = nullptr;         // crvpinn_direct_solve's lattice result (first use)
     // point sharding (f4): this context's tiles, and the communicator of the two exchanges
     long tile0 = 0, ntiles = 0;
@@ -330,7 +333,15 @@ void crvpinn_destroy(crvpinn_ctx *ctx) {
     if (ctx->comm) g_nccl.comm_destroy(ctx->comm);
     gram_free_constants(ctx->gram);
     tc_destroy(ctx->tc);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
     if (ctx->pts) cudaFree(ctx->pts);
+    if (ctx->pts_h) cudaFreeHost(ctx->pts_h);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->ep_in[b]) cudaEventDestroy(ctx->ep_in[b]);
+        if (ctx->ep_done[b]) cudaEventDestroy(ctx->ep_done[b]);
+        if (ctx->ep_out[b]) cudaEventDestroy(ctx->ep_out[b]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_field) cudaFreeHost(ctx->h_field);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
@@ -580,30 +591,68 @@ int crvpinn_eval(crvpinn_ctx *ctx, float *p_out) {
     return CRVPINN_OK;
 }
 
+constexpr long EP_CHUNK = 1L << 18;   // points per chunk (a multiple of the 128-point tile)
+
 int crvpinn_eval_points(crvpinn_ctx *ctx, long n, const float *xy, float *p_out) {
     if (!ctx) return fail(ctx, CRVPINN_EINVAL, "null ctx");
     if (n < 0) return fail(ctx, CRVPINN_EINVAL, "n must be >= 0");
     if (n == 0) return CRVPINN_OK;
     if (!xy || !p_out) return fail(ctx, CRVPINN_EINVAL, "null argument");
     if (n > (1L << 30)) return fail(ctx, CRVPINN_EINVAL, "too many points in one call (max 2^30)");
-    for (long i = 0; i < 2 * n; ++i)
-        if (!std::isfinite(xy[i])) return fail(ctx, CRVPINN_EDOMAIN, "non-finite coordinate");
-    CK(cudaSetDevice(ctx->device));
-    if (n > ctx->pts_cap) {
-        CK(cudaStreamSynchronize(ctx->stream));
-        if (ctx->pts) cudaFree(ctx->pts);
-        ctx->pts = nullptr;
-        ctx->pts_cap = 0;
-        CK(cudaMalloc(&ctx->pts, sizeof(float) * 3 * (size_t)n));
-        ctx->pts_cap = n;
+    {   // branch-free scan (vectorises): a float is non-finite iff its exponent bits are all set
+        const uint32_t *w = reinterpret_cast<const uint32_t *>(xy);
+        uint32_t bad = 0;
+        for (long i = 0; i < 2 * n; ++i) bad |= (uint32_t)((w[i] & 0x7f800000u) == 0x7f800000u);
+        if (bad) return fail(ctx, CRVPINN_EDOMAIN, "non-finite coordinate");
     }
-    float *dxy = ctx->pts, *dp = ctx->pts + 2 * n;
-    CK(cudaMemcpyAsync(dxy, xy, sizeof(float) * 2 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
-    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_eval_points(ctx->net, ctx->tc, dxy, (int)n, dp, ctx->stream);
-    else simt_eval_points(ctx->net, ctx->theta, ctx->simt, dxy, (int)n, dp, ctx->stream);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(p_out, dp, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->pts) {
+        CK(cudaMalloc(&ctx->pts, sizeof(float) * 6 * (size_t)EP_CHUNK));
+        CK(cudaMallocHost(&ctx->pts_h, sizeof(float) * 6 * (size_t)EP_CHUNK));
+        CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&ctx->ep_in[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ep_done[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ep_out[b], cudaEventDisableTiming));
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));   // the weights of any queued training are final
+    const long nch = (n + EP_CHUNK - 1) / EP_CHUNK;
+    auto drain = [&](long c) -> int {          // chunk c's values -> p_out (host)
+        const int b = (int)(c & 1);
+        const long c0 = c * EP_CHUNK, cn = n - c0 < EP_CHUNK ? n - c0 : EP_CHUNK;
+        CK(cudaEventSynchronize(ctx->ep_out[b]));
+        memcpy(p_out + c0, ctx->pts_h + (size_t)b * 3 * EP_CHUNK + 2 * EP_CHUNK, sizeof(float) * cn);
+        return CRVPINN_OK;
+    };
+    for (long c = 0; c < nch; ++c) {
+        const int b = (int)(c & 1);
+        const long c0 = c * EP_CHUNK, cn = n - c0 < EP_CHUNK ? n - c0 : EP_CHUNK;
+        float *hb = ctx->pts_h + (size_t)b * 3 * EP_CHUNK, *db = ctx->pts + (size_t)b * 3 * EP_CHUNK;
+        if (c >= 2) {   // buffer b last held chunk c-2: its result must be out before it is reused
+            int rc = drain(c - 2);
+            if (rc) return rc;
+        }
+        memcpy(hb, xy + 2 * c0, sizeof(float) * 2 * cn);   // pageable -> pinned, overlapping the GPU
+        CK(cudaMemcpyAsync(db, hb, sizeof(float) * 2 * cn, cudaMemcpyHostToDevice, ctx->copy_stream));
+        CK(cudaEventRecord(ctx->ep_in[b], ctx->copy_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ep_in[b], 0));
+        if (ctx->opts.precision == CRVPINN_PREC_TENSOR)
+            tc_eval_points(ctx->net, ctx->tc, db, (int)cn, db + 2 * EP_CHUNK, ctx->stream);
+        else
+            simt_eval_points(ctx->net, ctx->theta, ctx->simt, db, (int)cn, db + 2 * EP_CHUNK, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ep_done[b], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ep_done[b], 0));
+        CK(cudaMemcpyAsync(hb + 2 * EP_CHUNK, db + 2 * EP_CHUNK, sizeof(float) * cn, cudaMemcpyDeviceToHost,
+                           ctx->copy_stream));
+        CK(cudaEventRecord(ctx->ep_out[b], ctx->copy_stream));
+    }
+    for (long c = nch >= 2 ? nch - 2 : 0; c < nch; ++c) {
+        int rc = drain(c);
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(ctx->copy_stream));
     return CRVPINN_OK;
 }
 
