@@ -35,7 +35,7 @@ import workloads as W  # noqa: E402
 
 ITERS_PER_STEP = 100
 # DRAM bytes per Adam iteration of the MLP kernels (forward + 4 backward GEMMs + weight-gradient
-# reductions), ncu --set full at C5: profiles/r01_v6_ncu_full_summary.md
+# reductions), ncu --set full at C5: profiles/r01_v8_ncu_full_summary.md (2.19e9 in v6-v8)
 MLP_DRAM_BYTES_PER_ITER = 2.19e9
 
 
@@ -344,7 +344,7 @@ def run_ours(args, rank, world, local):
                      "kernel": "MLP forward + backward (A1, A6-A7), per Adam iteration",
                      "alg_flops_per_iter": flops, "peak_source": peak_note,
                      "traffic_note": ("per-iteration DRAM bytes (read + write) of the MLP kernels from one ncu --set full "
-                                     "capture at C5 (profiles/r01_v6_ncu_full_summary.md): the fp16 activations pass "
+                                     "capture at C5 (profiles/r01_v8_ncu_full_summary.md): the fp16 activations pass "
                                      "through HBM, so traffic >> the 20 MB algorithmic bytes; measured at C5 only")},
         "north_star_roofline": line_ns,
         "stage_ms_per_iter": {"mlp_fwd": stage_ms[0] / max(prof_iters, 1),
