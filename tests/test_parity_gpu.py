@@ -483,6 +483,39 @@ def test_eval_points_vs_oracle(crv, prec):
     assert e.value.code == crv.CRVPINN_EDOMAIN
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_eval_points_chunk_pipeline(crv, prec):
+    """crvpinn_eval_points streams its points through two 2^18-point chunk buffers (pinned staging, copy
+    stream): 2 chunks + a ragged tail give the same values bit for bit as evaluating every piece on its
+    own (the per-point arithmetic does not depend on the chunk), sampled points match the oracle, the
+    output of a non-finite call is untouched (nothing is written), and training in between is seen."""
+    N, widths, seed = 32, (2, 128, 128, 128, 1), 23
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=prec)
+    ref = oracle.Oracle(N, widths, K, S, f, th)
+    rng = np.random.default_rng(seed)
+    C = 1 << 18
+    n = 2 * C + 12345
+    xy = rng.uniform(-0.1, 1.1, (n, 2)).astype(np.float32)
+    p = g.eval_points(xy)
+    pieces = np.concatenate([g.eval_points(xy[a:b]) for a, b in ((0, 1000), (1000, C + 7), (C + 7, n))])
+    np.testing.assert_array_equal(p, pieces)
+    idx = np.concatenate([rng.choice(n, 200, replace=False), [0, C - 1, C, 2 * C - 1, 2 * C, n - 1]])
+    pr = ref.eval_points(xy[idx])
+    assert np.max(np.abs(p[idx] - pr)) <= (1e-5 if prec == 1 else 2e-3) * np.abs(pr).max()
+    out = np.full(n, 7.0, np.float32)
+    bad = xy.copy()
+    bad[C + 5, 0] = np.inf
+    rc = crv.load().crvpinn_eval_points(g._h, n, crv._fp(bad), crv._fp(out))   # the raw call: out is ours
+    assert rc == crv.CRVPINN_EDOMAIN
+    assert np.all(out == 7.0)
+    g.step(3)
+    p2 = g.eval_points(xy[:5000])
+    np.testing.assert_array_equal(p2, g.eval_points(xy[:5000]))
+    assert not np.array_equal(p2, p[:5000])
+
+
 # ------------------------------------------------------------------ f2: the discrete system by Gram-preconditioned CG
 @pytest.mark.parametrize("N,seed,Gr", [(32, 31, 0.0), (64, 32, 0.5), (128, 33, 0.0)])
 def test_direct_solve_vs_oracle(crv, N, seed, Gr):
