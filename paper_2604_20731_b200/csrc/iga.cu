@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "../../include/crvpinn.h"
 #include <cstdlib>
+#include <type_traits>
 #include <cstring>
 #include <cmath>
 #include <string>
@@ -309,15 +310,18 @@ __global__ void __launch_bounds__(TB * TB) k_iga_assemble(IgaDev g, const float 
         for (int qy = 0; qy < R1; ++qy) {
             const float vy = sby[((ey - ey0) * R1 + qy) * R1 + b], dy = sdy[((ey - ey0) * R1 + qy) * R1 + b];
             const float *r0 = sq + ((ey - ey0) * R1 + qy) * QW + xo;
-            float A = 0.f, B = 0.f;
+            // degree >= 4: the row sums in fp64 too (the mass matrix's condition number, ~5e3 in 2-D at
+            // degree 4 and 2e5 at 6, amplifies the rounding of (r+1)^2-term fp32 sums visibly)
+            using acc_t = typename std::conditional<(RD >= 4), double, float>::type;
+            acc_t A = 0, B = 0;
 #pragma unroll
             for (int dx2 = 0; dx2 < R1; ++dx2)
 #pragma unroll
                 for (int qx = 0; qx < R1; ++qx) {
                     const int t = (dx2 < nex ? dx2 : 0) * R1 + qx;   // zero factors beyond the mesh
-                    A = fmaf(r0[t], vxs[dx2][qx], A);
-                    A = fmaf(r0[QW * QW + t], dxs[dx2][qx], A);
-                    B = fmaf(r0[2 * QW * QW + t], vxs[dx2][qx], B);
+                    A = fma((acc_t)r0[t], (acc_t)vxs[dx2][qx], A);
+                    A = fma((acc_t)r0[QW * QW + t], (acc_t)dxs[dx2][qx], A);
+                    B = fma((acc_t)r0[2 * QW * QW + t], (acc_t)vxs[dx2][qx], B);
                 }
             acc = fma((double)vy, (double)A, acc);
             acc = fma((double)dy, (double)B, acc);

@@ -569,7 +569,22 @@ def _iga_pair(crv, ne, r):
     return crv.Iga(ne, r), oracle.IgaOracle(ne, r)
 
 
-@pytest.mark.parametrize("ne,r", [(8, 1), (16, 2), (37, 2), (20, 3)])
+def _mass_dense(o):
+    """The oracle's 1-D mass matrix as a dense array (banded storage [nb][r+1]: M_{j,j+d})."""
+    M = np.asarray(o.mass_1d())
+    nb, r = o.nb, o.r
+    if M.ndim == 2 and M.shape == (nb, nb):
+        return M
+    B = M.reshape(nb, r + 1)
+    F = np.zeros((nb, nb))
+    for j in range(nb):
+        for d in range(r + 1):
+            if j + d < nb:
+                F[j, j + d] = F[j + d, j] = B[j, d]
+    return F
+
+
+@pytest.mark.parametrize("ne,r", [(8, 1), (16, 2), (37, 2), (20, 3), (100, 3), (64, 4), (70, 5), (40, 6)])
 def test_iga_projection_and_eval_vs_oracle(crv, ne, r):
     """crvpinn_iga_project / _eval against the fp64 oracle: quadrature points,
     projected coefficients of a smooth function, exact reproduction of x^2 + y^2 (degree >= 2), and
@@ -580,7 +595,12 @@ def test_iga_projection_and_eval_vs_oracle(crv, ne, r):
     np.testing.assert_allclose(q, o.quad_points(), atol=2e-7)
     f = (np.sin(3 * q[:, 0]) * np.cos(2 * q[:, 1]) + q[:, 1]).astype(np.float32)
     C, Co = g.project(f), o.project(f.astype(np.float64))
-    assert np.max(np.abs(C - Co)) <= 1e-5 * np.abs(Co).max()
+    # the fp32 load vector's rounding is amplified by the 2-D mass matrix's condition number
+    # (1e2 at degree 2, 7e2 at 3, 5e3 at 4, 3e4 at 5, 2e5 at 6; DESIGN.md §9 f3): 5e-9 kappa, 12x
+    # below the worst case 2^-24 kappa, floored at 1e-5
+    M1 = _mass_dense(o)
+    tol = max(1e-5, 5e-9 * np.linalg.cond(M1) ** 2)
+    assert np.max(np.abs(C - Co)) <= tol * np.abs(Co).max()
     rng = np.random.default_rng(ne)
     pts = rng.uniform(0, 1, (500, 2)).astype(np.float32)
     v, gr = g.eval(C, pts, grad=True)
@@ -592,7 +612,8 @@ def test_iga_projection_and_eval_vs_oracle(crv, ne, r):
         np.testing.assert_allclose(g.eval(C2, pts), pts[:, 0] ** 2 + pts[:, 1] ** 2, atol=2e-6)
 
 
-@pytest.mark.parametrize("ne,r,Gr", [(16, 2, 0.0), (48, 2, 1.5), (33, 1, 0.7)])
+@pytest.mark.parametrize("ne,r,Gr", [(16, 2, 0.0), (48, 2, 1.5), (33, 1, 0.7), (100, 3, 0.4), (64, 4, 1.0),
+                                     (70, 5, 0.0), (40, 6, 0.8)])
 def test_iga_saturation_step_vs_oracle(crv, ne, r, Gr):
     """One explicit step of Eq. 10 (readings R24-R26) on the GPU against the oracle, with
     heterogeneous K, a source patch, a non-trivial pressure and gravity."""
