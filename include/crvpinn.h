@@ -91,7 +91,11 @@ typedef struct {
      * all-reduces inside every iteration (and inside the captured graphs). Allowed at
      * shard_world 1. nccl = 0 with shard_world > 1: the caller exchanges, using
      * crvpinn_shard_forward / crvpinn_shard_backward; crvpinn_step and crvpinn_loss_grad then
-     * fail with EINVAL. libnccl.so.2 is loaded on first use (dlopen), not at library load. */
+     * fail with EINVAL. libnccl.so.2 is loaded on first use (dlopen), not at library load.
+     * θ, the Adam state and the fields are replicated: every rank of a group must make the same
+     * calls with the same arguments (create, set_saturation, step, set_params, set_adam), and
+     * crvpinn_step / crvpinn_loss_grad / crvpinn_eval are collective (each rank calls them once,
+     * in the same order). */
     int nccl;
     unsigned char nccl_id[128];
 } crvpinn_opts;
