@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         if (i >= 2 && i < 18) {
                             const int k = i - 2;
                             if ((k & 1) == 0) {
-                                r[k] = rcp_v(1.0f + e[k]);
+                                // (CRV_NEWTON_MASK 0xEEEE: elements 2 mod 4 take a scalar Newton reciprocal too)
+                                r[k] = ((CRV_NEWTON_MASK >> k) & 1) ? rcp_newton(1.0f + e[k]) : rcp_v(1.0f + e[k]);
                             } else if ((k & 3) == 3) {
                                 const float da = 1.0f + e[k - 2], db = 1.0f + e[k];
                                 f32x2_t R = pk2(__int_as_float(0x7EF311C3 - __float_as_int(da)),

@@ -1,4 +1,6 @@
 #!/bin/bash
-mkdir -p gpurun_out
-timeout -s KILL 900 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "eval_points or iga_buoyancy or gravity" > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
-timeout -s KILL 600 python scripts/bench_eval_points.py > gpurun_out/ep.json 2>&1; tail -c 600 gpurun_out/ep.json
+CRVPINN_LIB=build/ab/n34/libcrvpinn.so timeout -s KILL 300 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "workload_theta0 or intermediates" 2>&1 | tail -1
+for r in 1 2 3; do
+for v in base n34 n78; do
+  CRVPINN_LIB=build/ab/$v/libcrvpinn.so timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
+done; done
