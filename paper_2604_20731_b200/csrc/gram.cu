@@ -657,7 +657,10 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
     std::vector<double> hf(n);
     int it = 0;
     double rel = 1.0;
-    constexpr int CHK = 20;
+    // convergence checks (a host round trip each) every chk iterations: 20 at first, then ~80 % of
+    // the iterations the observed convergence rate predicts are still needed (20..200)
+    int chk = 20, it_prev = 0;
+    double rel_prev = 1.0;
     // kernels use the iteration index only through its parity and it == 0: a graph of iterations
     // (2, 3) replays every even-odd pair from 2 on and removes the per-kernel launch cost
     cudaGraphExec_t gx = w->gx;
@@ -675,7 +678,7 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
         w->gx = gx;
     }
     while (it < max_iter) {
-        const int upto = it + CHK < max_iter ? it + CHK : max_iter;
+        const int upto = it + chk < max_iter ? it + chk : max_iter;
         while (it < upto) {
             if (gx && it >= 2 && it + 2 <= upto && (it & 1) == 0) {
                 cudaGraphLaunch(gx, s);
@@ -695,6 +698,17 @@ int pcg_solve(const float *alpha, const float *b, float *u_lat, GramConsts &c, i
         for (double v : hf) rr += v;
         rel = hs.bb > 0.0 ? std::sqrt(rr / hs.bb) : 0.0;
         if (!(rel > rtol)) break;   // converged (or NaN: stop)
+        if (rel < rel_prev && it > it_prev) {
+            const double lr = std::log(rel / rel_prev) / (double)(it - it_prev);   // log rate per iteration
+            const double need = std::log(rtol / rel) / lr;
+            int c = (int)(0.8 * need);
+            c = c < 20 ? 20 : (c > 200 ? 200 : c);
+            chk = c & ~1;
+        } else {
+            chk = 20;
+        }
+        it_prev = it;
+        rel_prev = rel;
     }
     // true residual of the returned iterate, x -> lattice (boundary stays as given: zeroed by the caller)
     k_pcg_final<<<n, PCG_MV_THREADS, 0, s>>>(x, alpha, b, nullptr, u_lat, part_fin, N);
