@@ -1,6 +1,7 @@
 #!/bin/bash
-CRVPINN_LIB=build/ab/n34/libcrvpinn.so timeout -s KILL 300 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "workload_theta0 or intermediates" 2>&1 | tail -1
+timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "workload_100 or nonfinite or checkpoint or zero_problem or composition" 2>&1 | tail -1
 for r in 1 2 3; do
-for v in base n34 n78; do
-  CRVPINN_LIB=build/ab/$v/libcrvpinn.so timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
+for v in base new; do
+  if [ $v = new ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
+  CRVPINN_LIB=$L timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
 done; done
