@@ -330,7 +330,8 @@ static void free_act(const orc_ctx *c, double **a) {
     free(a);
 }
 
-/* u at the interior nodes of rows j in [j0, j1) (clipped to [1, N-1]); every other node 0. */
+/* u at the interior nodes of rows j in [j0, j1) (clipped to [1, N-1]); every other node 0. One shard's
+ * forward of the point-sharded iteration; pinned by P20 (additivity). */
 void orc_forward_rows(const orc_ctx *c, const double *th, int j0, int j1, double *u) {
     int N = c->N;
     long nn = (long)(N + 1) * (N + 1);
@@ -433,7 +434,8 @@ double orc_loss_u(const orc_ctx *c, const double *u, double *res_out, double *q_
 
 /* ---------------------------------------------------------------- A1-A6: loss and gradient */
 /* dLOSS/dtheta summed over the MLP points of rows j in [j0, j1) (clipped to [1, N-1]), given
- * gu = dLOSS/du on the lattice: the chain rule through u = cutoff * net (A6, backpropagation). */
+ * gu = dLOSS/du on the lattice: the chain rule through u = cutoff * net (A6, backpropagation).
+ * One shard's backward; pinned by P20 (the shares sum to the gradient). */
 void orc_grad_rows(const orc_ctx *c, const double *th, const double *gu, int j0, int j1, double *grad) {
     int N = c->N;
     if (j0 < 1) j0 = 1;
