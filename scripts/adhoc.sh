@@ -1,7 +1,4 @@
 #!/bin/bash
-timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "workload_100 or nonfinite or checkpoint or zero_problem or composition" 2>&1 | tail -1
-for r in 1 2 3; do
-for v in base new; do
-  if [ $v = new ]; then L=paper_2604_20731_b200/libcrvpinn.so; else L=build/ab/$v/libcrvpinn.so; fi
-  CRVPINN_LIB=$L timeout -s KILL 120 python scripts/stage_time.py C5 3 2>&1 | tail -1 | sed "s|^|$v |"
-done; done
+timeout -s KILL 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -k "iga" 2>&1 | tail -1
+timeout -s KILL 600 python scripts/bench_iga.py 2>&1 | tail -c 330
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/iga_launches.csv python scripts/prof_iga.py > gpurun_out/ncu.log 2>&1
