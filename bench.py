@@ -216,11 +216,19 @@ def run_ours(args, rank, world, local):
     import torch
     import paper_2604_20731_b200 as crv
 
+    # plumbing test hook: CRVPINN_BENCH_BACKEND=gloo lets several ranks share one GPU (functional check
+    # of the multi-rank path only; such a run is not a measurement)
+    backend = os.environ.get("CRVPINN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     prec = crv.PREC_TENSOR if args.precision == "tensor" else crv.PREC_FP32
     F = W.make_fields(args.workload)
     w = F.workload
@@ -275,7 +283,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     stage_ms, prof_iters = g.profile(reset=True)
     g.set_profiling(False)
-    t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+    red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"   # where the max-over-ranks reductions run
+    t = torch.tensor([t_ms], dtype=torch.float64, device=red_dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
@@ -295,7 +304,7 @@ def run_ours(args, rank, world, local):
             g.set_saturation(F.S_steps[k % len(F.S_steps)])
             g.step(ITERS_PER_STEP, history=True)
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         if dist:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": iters_total / float(tt.item()), "unit": "Adam iters/s",
