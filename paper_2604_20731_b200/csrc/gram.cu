@@ -74,18 +74,15 @@ __device__ __forceinline__ void fft_inplace(float2 *sa, const float2 *tw, int M,
 // Y = -2i X1 + 2 X2  =>  X1_k = -Im(Y_k)/2, X2_k = Re(Y_k)/2.
 // Stage 1: RES_kl = a_{k-1,l}(u_kl-u_{k-1,l}) + a_{k,l-1}(u_kl-u_{k,l-1}) + a_kl(2u_kl-u_{k+1,l}-u_{k,l+1}) - b_kl
 // (the closed form of (alpha grad+ u, grad+ delta_kl)_h - (RHS, delta_kl)_h, reading R16).
-__global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__ alpha, const float *__restrict__ bvec,
-                          float *__restrict__ res, float *__restrict__ rhat, const float2 *__restrict__ tw, int N,
-                          int logM, float scale, DevState *st) {
-    extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
+// stencil residual of row pair `pair` and its DST-I (stage 1 of G^-1); sa: [M] block scratch,
+// stw: the per-stage twiddles (already in shared memory)
+__device__ __forceinline__ void res_dst_pair(int pair, const float *__restrict__ u, const float *__restrict__ alpha,
+                                             const float *__restrict__ bvec, float *__restrict__ res,
+                                             float *__restrict__ rhat, float2 *sa, const float2 *stw, int N, int logM,
+                                             float scale) {
     const int n = N - 1, M = 2 * N;
-    float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
-    pdl_wait();
-    pdl_trigger();
-    const int j0 = 2 * blockIdx.x;
+    const int j0 = 2 * pair;
     const bool has1 = j0 + 1 < n;
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->gmax_bits = 0u;   // k_adj_final folds this iteration's max
     // odd extension y_m: y_0 = y_N = 0, y_{k+1} = RES_k, y_{M-1-k} = -RES_k (bit-reversed slots)
     const int shift = 32 - logM;
     if (threadIdx.x == 0) {
@@ -119,6 +116,20 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
     }
 }
 
+
+__global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__ alpha, const float *__restrict__ bvec,
+                          float *__restrict__ res, float *__restrict__ rhat, const float2 *__restrict__ tw, int N,
+                          int logM, float scale, DevState *st) {
+    extern __shared__ float2 sa[];   // [M] data, then [M] twiddles
+    const int M = 2 * N;
+    float2 *stw = sa + M;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->gmax_bits = 0u;   // k_adj_final folds this iteration's max
+    res_dst_pair(blockIdx.x, u, alpha, bvec, res, rhat, sa, stw, N, logM, scale);
+}
+
 // One warp per mode a: Thomas elimination of (lam_a I + T) z = h2 * r written as two first-order
 // linear recurrences (forward g_j = e_{j-1} g_{j-1} + r_j; backward z_j = e_j z_{j+1} + e_j g_j,
 // e_j = 1/w_j the precomputed pivots) and evaluated as warp-level affine scans: each lane owns a
@@ -127,16 +138,12 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
 // conflicts). R^, Z^ and the pivot table are mode-major ([a][j]) so each warp's row is contiguous.
 constexpr int TRI_WARPS = 4;
 
-__global__ void k_tridiag(const float *__restrict__ rhat, const float *__restrict__ etab, float *__restrict__ z,
-                          int n, int seg, float h2) {
-    pdl_wait();
-    pdl_trigger();
-    extern __shared__ float sm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int a = blockIdx.x * TRI_WARPS + warp;
-    if (a >= n) return;
+// Thomas scans of mode a by one warp; sm: the warp's 2 * 32 * seg floats of shared memory
+__device__ __forceinline__ void tridiag_mode(int a, const float *__restrict__ rhat, const float *__restrict__ etab,
+                                             float *__restrict__ z, int n, int seg, float h2, float *sm) {
+    const int lane = threadIdx.x & 31;
     const int stride = 32 * seg;
-    float *sr = sm + (size_t)warp * 2 * stride;   // r, then g, then z
+    float *sr = sm;   // this warp's [2][32 seg]: r, then g, then z
     float *se = sr + stride;
     const float *r = rhat + (size_t)a * n;
     const float *e = etab + (size_t)a * n;
@@ -204,20 +211,29 @@ __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restric
     for (int j = lane; j < n; j += 32) zo[j] = sr[j];
 }
 
+__global__ void k_tridiag(const float *__restrict__ rhat, const float *__restrict__ etab, float *__restrict__ z,
+                          int n, int seg, float h2) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ float sm[];
+    const int warp = threadIdx.x >> 5;
+    const int a = blockIdx.x * TRI_WARPS + warp;
+    if (a >= n) return;
+    tridiag_mode(a, rhat, etab, z, n, seg, h2, sm + (size_t)warp * 2 * 32 * seg);
+}
+
 
 // Inverse DST of two rows of z (mode-major input) -> q (row-major), and this block's part of
 // LOSS = sum RES q. dsc != nullptr (the direct solve's preconditioner): q is scaled elementwise by it.
-__global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict__ res, float *__restrict__ q,
-                            double *__restrict__ part, const float2 *__restrict__ tw, int N, int logM, float scale,
-                            const float *__restrict__ dsc) {
-    extern __shared__ float2 sa[];   // [M] data, then [M/2] twiddles
+// inverse DST of row pair `pair` (mode-major z -> row-major q, optionally scaled by dsc) and its
+// part of LOSS = sum RES q (fp64, written to part[pair]); sa / stw as in res_dst_pair
+__device__ __forceinline__ void idst_pair(int pair, const float *__restrict__ z, const float *__restrict__ res,
+                                          float *__restrict__ q, double *__restrict__ part, float2 *sa,
+                                          const float2 *stw, int N, int logM, float scale,
+                                          const float *__restrict__ dsc) {
     __shared__ double sred[32];
     const int n = N - 1, M = 2 * N;
-    float2 *stw = sa + M;
-    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];
-    pdl_wait();
-    pdl_trigger();
-    const int j0 = 2 * blockIdx.x;
+    const int j0 = 2 * pair;
     const bool has1 = j0 + 1 < n;
     const int shift = 32 - logM;
     if (threadIdx.x == 0) {
@@ -253,8 +269,20 @@ __global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
-        part[blockIdx.x] = s;
+        part[pair] = s;
     }
+}
+
+__global__ void k_idst_loss(const float *__restrict__ z, const float *__restrict__ res, float *__restrict__ q,
+                            double *__restrict__ part, const float2 *__restrict__ tw, int N, int logM, float scale,
+                            const float *__restrict__ dsc) {
+    extern __shared__ float2 sa[];   // [M] data, then [M] twiddles
+    const int M = 2 * N;
+    float2 *stw = sa + M;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];
+    pdl_wait();
+    pdl_trigger();
+    idst_pair(blockIdx.x, z, res, q, part, sa, stw, N, logM, scale, dsc);
 }
 
 // g_u = dLOSS/du = 2 A(alpha) q (A symmetric: the same stencil on q, q = 0 off the interior),
