@@ -967,6 +967,9 @@ struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch ke
     static constexpr bool DEEP = CRV_B2_DEEP_DELTA && (MODE & 1) == 0;
     static constexpr int DS = KC + (DEEP ? KC : CRV_B2_DSX);   // Delta ring slots (DEEP: 2 tiles)
     static constexpr int NT = DEEP ? 1 : CRV_B2_NT;           // t ring depth (tiles of 2 chunks)
+    // measured: CRV_B2_DSX = 1 (a 5-slot Delta ring at WP = 256) hangs the launches (like NT = 1 with
+    // the output layer fused) -- the ring must hold the tile in flight plus the next pair of chunks
+    static_assert(DEEP || CRV_B2_DSX >= 2, "CRV_B2_DSX < 2 deadlocks k_tc_bwd2");
     static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
