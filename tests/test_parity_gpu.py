@@ -400,6 +400,25 @@ def test_point_shards_vs_unsharded_and_oracle(crv, monkeypatch, chain, N, widths
         s.close()
 
 
+def test_shard_halves_on_an_unsharded_context(crv):
+    """crvpinn_shard_forward / _backward on a world-1 context (no communicator) are the two halves
+    of loss_grad: the whole u, then the loss and the whole gradient, bit for bit; theta and the Adam
+    state do not move."""
+    N, widths, seed = 64, (2, 128, 128, 128, 1), 35
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    g = crv.Crvpinn(N, widths, K, S, f, th)
+    loss, grad = g.loss_grad()
+    u = g.intermediates()["u"]
+    up = g.shard_forward()
+    np.testing.assert_array_equal(up, u)
+    l2, g2 = g.shard_backward(up)
+    assert l2 == loss
+    np.testing.assert_array_equal(g2, grad)
+    np.testing.assert_array_equal(g.theta, th)
+    assert g.adam_state()[2] == 0
+
+
 @pytest.mark.parametrize("name", ["C1", "C4"])
 def test_nccl_world1_matches_unsharded(crv, name):
     """The in-graph exchange (memset of u, NCCL all-reduce of u and of the gradient, captured with the
