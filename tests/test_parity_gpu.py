@@ -216,6 +216,25 @@ def test_set_saturation_matches_oracle(crv, prec):
     assert grad_errors(widths, grad, rg).max() <= TOL[prec][1]
 
 
+def test_set_saturation_device_matches_host(crv):
+    """crvpinn_set_saturation_device (the bench's device-resident S update) and the host call give the
+    same alpha and RHS: 5 Adam steps after each update agree bit for bit, with and without gravity."""
+    import torch
+    N, widths, seed = 64, (2, 64, 64, 64, 1), 36
+    K, S, f = W.random_fields(N, seed)
+    th = W.random_theta(widths, seed)
+    S2 = W.random_fields(N, seed + 1)[1]
+    for Gr in (0.0, 0.7):
+        a = crv.Crvpinn(N, widths, K, S, f, th, gravity=Gr)
+        b = crv.Crvpinn(N, widths, K, S, f, th, gravity=Gr)
+        a.set_saturation(S2)
+        dS = torch.from_numpy(np.ascontiguousarray(S2, dtype=np.float32)).cuda()
+        torch.cuda.synchronize()
+        b.set_saturation_device(dS.data_ptr())
+        np.testing.assert_array_equal(a.step(5), b.step(5))
+        np.testing.assert_array_equal(a.theta, b.theta)
+
+
 def test_eval_boundary_and_values(crv):
     N, widths = 32, (2, 64, 64, 1)
     K, S, f = W.random_fields(N, 5)
