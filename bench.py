@@ -34,9 +34,6 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 ITERS_PER_STEP = 100
-# DRAM bytes per Adam iteration of the MLP kernels (forward + 4 backward GEMMs + weight-gradient
-# reductions), ncu --set full at C5: profiles/r01_v8_ncu_full_summary.md (2.19e9 in v6-v8)
-MLP_DRAM_BYTES_PER_ITER = 2.19e9
 
 
 def parse():
@@ -49,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-per-workload", action="store_true", help="skip the C1-C5 table (per_workload)")
     ap.add_argument("--shard", action="store_true",
                     help="one problem, MLP points split over the ranks (strong scaling, NCCL exchanges)")
     return ap.parse_args()
@@ -134,28 +132,6 @@ def alg_bytes_per_iter(w: W.Workload) -> float:
     return 40.0 * w.points + 36.0 * w.n_params
 
 
-def measure_tf32_peak(device: int) -> float:
-    """TF32 dense tensor peak of this GPU in TFLOP/s (torch.matmul 8192^3, TF32, best of 10)."""
-    import torch
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        a = torch.randn(8192, 8192, device=f"cuda:{device}")
-        b = torch.randn(8192, 8192, device=f"cuda:{device}")
-        best = float("inf")
-        for _ in range(12):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            torch.matmul(a, b)
-            e1.record()
-            torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1) / 1e3)
-        del a, b
-        return 2.0 * 8192 ** 3 / best / 1e12
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-
-
 # ------------------------------------------------------------------ the oracle (CPU) arm
 def time_oracle(name: str, iters: int):
     import oracle
@@ -187,16 +163,17 @@ def run_reference(args, rank, world):
         o.train(1)
     dt = time.perf_counter() - t0
     value = args.steps / dt
-    sample = (f"{args.steps} full Adam iterations of {args.workload} (1 per step) after {args.warmup} warm-up; "
+    sample = (f"{args.steps} full Adam iterations of {args.workload} (1 per step: a bounded sample of the 100-iteration "
+              f"pressure update of the config) after {args.warmup} warm-up; "
               f"one-time banded-LU factorisation of G ({t_factor:.1f}s) excluded")
     line = {
         "impl": "reference", "metric": f"CRVPINN Adam iters/s ({args.workload})", "value": value,
         "unit": "Adam iters/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args.workload, "oracle"), adam_iters_per_step=1),
+        "config": dict(workload_config(args.workload, args.precision), parallelism="replicas1"),
         "cpu_baseline": {"value": value, "unit": "Adam iters/s", "cores": oracle.max_threads(), "kind": "oracle",
-                         "sample": sample},
+                         "cpu": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "Adam iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -212,6 +189,85 @@ def workload_config(name: str, precision: str):
 
 
 # ------------------------------------------------------------------ our arm
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def set_oracle_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's parallel regions (libgomp ICV of this thread)."""
+    import ctypes
+    import oracle
+    oracle.lib()
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+
+
+# oracle Adam iterations timed per workload in the per-workload table (bounded samples, DESIGN.md §8)
+ORACLE_ITERS = {"C1": 50, "C2": 10, "C3": 3, "C4": 1, "C5": 1}
+
+
+def time_oracle_table(names, one_thread=("C1", "C2", "C3")):
+    import oracle
+    out = {}
+    nmax = oracle.max_threads()
+    for name in names:
+        v, cores, _ = time_oracle(name, ORACLE_ITERS[name])
+        row = {"value": v, "unit": "Adam iters/s", "cores": cores, "iters_timed": ORACLE_ITERS[name]}
+        if name in one_thread:
+            set_oracle_threads(1)
+            try:
+                row["value_1thread"] = time_oracle(name, ORACLE_ITERS[name])[0]
+            finally:
+                set_oracle_threads(nmax)
+        out[name] = row
+    return out
+
+
+def roofline_frac(w, ms_per_iter, peak_tf):
+    ach = alg_flops_per_iter(w) / (ms_per_iter * 1e-3) / 1e12
+    return ach, ach / peak_tf
+
+
+def measured_traffic():
+    """Per-iteration DRAM bytes of the whole Adam iteration per workload, from one ncu --set full capture
+    (profiles/r02_traffic.json, written by scripts/ncu_traffic.py); None where not captured."""
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if not os.path.exists(path):
+        return {}, None
+    with open(path) as fh:
+        d = json.load(fh)
+    return d.get("bytes_per_iter", {}), d.get("source")
+
+
+def time_steps(torch, g, S_dev, stream, flush, steps, warmup):
+    """Device time (ms) of `steps` pressure updates (set_saturation + 100-iteration graph), L2 flushed
+    between them outside the events."""
+    def one_step(k):
+        g.set_saturation_device(S_dev[k % len(S_dev)].data_ptr())
+        g.step(ITERS_PER_STEP, history=False)
+    for k in range(warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    evs = []
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(k))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        one_step(k)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs), one_step
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2604_20731_b200 as crv
@@ -244,36 +300,18 @@ def run_ours(args, rank, world, local):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     torch.cuda.synchronize()
 
-    def one_step(k):
-        g.set_saturation_device(S_dev[k % len(S_dev)].data_ptr())
-        g.step(ITERS_PER_STEP, history=False)
-
-    for k in range(args.warmup):
-        one_step(k)
-    torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    evs = []
-    for k in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.fill_(float(k))            # L2 flush (outside the timed events)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        one_step(k)
-        e1.record(stream)
-        evs.append((e0, e1))
-    torch.cuda.synchronize()
+    t_ms, one_step = time_steps(torch, g, S_dev, stream, flush, args.steps, args.warmup)
     if dist:
         dist.barrier()
     sampler.stop()
-    t_ms = sum(a.elapsed_time(b) for a, b in evs)
-    # per-stage device times (roofline "achieved"): the same graph with CUDA event nodes between the
-    # stages (cudaEventRecordExternal on the library stream), run right after the timed region --
+    # per-stage device times (the dominant kernel's share): the same graph with CUDA event nodes between
+    # the stages (cudaEventRecordExternal on the library stream), run right after the timed region --
     # the event nodes are kept out of the timed graph because they break kernel-to-kernel overlap
     g.set_profiling(True)
     one_step(0)                      # capture the profiled graph
@@ -309,68 +347,98 @@ def run_ours(args, rank, world, local):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": iters_total / float(tt.item()), "unit": "Adam iters/s",
                "h2d_bytes_per_step": s_bytes, "d2h_bytes_per_step": hist_bytes}
+    launches = args.steps * (ITERS_PER_STEP * g.launches_per_iter + 1)
 
     if rank != 0:
+        g.close()
         if dist:
             dist.destroy_process_group()
         return 0
 
     peaks, peak_src = measured_peaks()
+    traffic, traffic_src = measured_traffic()
     flops = alg_flops_per_iter(w) * tile_frac     # this rank's share of the MLP points
-    mlp_ms = (stage_ms[0] + stage_ms[2]) / max(prof_iters, 1)
-    achieved_tf = flops / (mlp_ms * 1e-3) / 1e12
+    ms_iter = t_max / (args.steps * ITERS_PER_STEP)
     if prec == crv.PREC_TENSOR:
-        # fp16 operands run at the bf16 rate; the MLP is timed inside a long step -> sustained
+        # fp16 operands run at the bf16 rate; every kernel runs inside a long step -> the sustained figure
         peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-        bound, peak_note = "tensor", f"{peak_src} bf16 sustained (fp16 = bf16 rate)"
+        bound, peak_note = "tensor", f"{peak_src} bf16 sustained (fp16 = bf16 rate), MEASURED_PEAKS.json"
     else:
-        peak = 148 * 128 * 2 * 1.965e9 / 1e12   # FFMA fp32: SMs x lanes x 2 x max clock (DESIGN.md §6)
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12   # FFMA fp32: SMs x lanes x 2 x max clock (DESIGN.md §5.4)
         bound, peak_note = "alu", "derived FP32 FFMA peak 74.4 TFLOP/s (148 SM x 128 x 2 x 1965 MHz)"
+    achieved = flops / (ms_iter * 1e-3) / 1e12
+    pi = max(prof_iters, 1)
+    st = {"mlp_fwd": stage_ms[0] / pi, "stencil_gram_loss_adjoint": stage_ms[1] / pi,
+          "mlp_bwd_reduce": stage_ms[2] / pi, "adam": stage_ms[3] / pi}
+    # the dominant kernel: the fused forward (A1), one launch per Adam iteration; its algorithmic flops
+    # are the forward third of SURVEY.md §8's count
+    hid, Lh = w.widths[1], len(w.widths) - 2
+    fwd_flops = 2.0 * (2 * hid + (Lh - 1) * hid * hid + hid) * w.points * tile_frac
     clocks = sampler.summary()
-    # north_star / SURVEY.md §8(d) roofline: the method's precision class is TF32 (the fp16 operands
-    # here have TF32's 10-bit mantissa), so its denominator is the TF32 tensor peak -- measured here
-    # like MEASURED_PEAKS measures bf16 (torch.matmul 8192^3, TF32 enabled, best of 10) -- and the
-    # whole Adam iteration is compared with max(GEMM flops / TF32 peak, algorithmic bytes / HBM).
-    tf32 = measure_tf32_peak(local) if prec == crv.PREC_TENSOR else None
-    step_s = (t_max / 1e3) / (args.steps * ITERS_PER_STEP)
-    alg_bytes = alg_bytes_per_iter(w)
-    line_ns = None
-    if tf32:
-        t_roof = max(flops / (tf32 * 1e12), alg_bytes / (float(peaks["hbm_gbs"]) * 1e9))
-        line_ns = {"denominator": "TF32 tensor peak measured in this run (torch.matmul 8192^3, best of 10)",
-                   "tf32_tflops": tf32, "t_roof_us": t_roof * 1e6, "step_us": step_s * 1e6,
-                   "frac": t_roof / step_s}
     line = {
         "metric": f"CRVPINN Adam iters/s ({args.workload})", "value": value, "unit": "Adam iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
         "higher_is_better": True, "scaling": "strong" if args.shard else "weak", "vs_baseline": None,
         "dtype": "f16" if prec == crv.PREC_TENSOR else "f32", "data": "synthetic",
-        "config": dict(workload_config(args.workload, args.precision), parallelism=f"points{world}" if args.shard else f"replicas{world}"),
+        "config": dict(workload_config(args.workload, args.precision),
+                       parallelism=f"points{world}" if args.shard else f"replicas{world}"),
         "points_iters_per_s": value * w.points,
-        "roofline": {"bound": bound, "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak,
-                     "traffic": MLP_DRAM_BYTES_PER_ITER if args.workload == "C5" and not args.shard else None,
-                     "kernel": "MLP forward + backward (A1, A6-A7), per Adam iteration",
-                     "alg_flops_per_iter": flops, "peak_source": peak_note,
-                     "traffic_note": ("per-iteration DRAM bytes (read + write) of the MLP kernels from one ncu --set full "
-                                     "capture at C5 (profiles/r01_v8_ncu_full_summary.md): the fp16 activations pass "
-                                     "through HBM, so traffic >> the 20 MB algorithmic bytes; measured at C5 only")},
-        "north_star_roofline": line_ns,
-        "stage_ms_per_iter": {"mlp_fwd": stage_ms[0] / max(prof_iters, 1),
-                              "stencil_gram_loss_adjoint": stage_ms[1] / max(prof_iters, 1),
-                              "mlp_bwd_reduce": stage_ms[2] / max(prof_iters, 1),
-                              "adam": stage_ms[3] / max(prof_iters, 1)},
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak,
+                     "traffic": traffic.get(args.workload) if not args.shard else None,
+                     "scope": "whole Adam iteration (A1-A8): SURVEY.md §8 algorithmic MLP flops per iteration / "
+                              "device time per iteration of the timed region",
+                     "alg_flops_per_iter": flops, "ms_per_iter": ms_iter, "peak_source": peak_note,
+                     "traffic_source": traffic_src},
+        "roofline_dominant_kernel": {
+            "kernel": "k_tc_forward (A1, fused forward)" if prec == crv.PREC_TENSOR else "MLP forward (SIMT)",
+            "achieved": fwd_flops / (st["mlp_fwd"] * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+            "frac": fwd_flops / (st["mlp_fwd"] * 1e-3) / 1e12 / peak, "alg_flops_per_launch": fwd_flops,
+            "us_per_launch": st["mlp_fwd"] * 1e3, "share_of_step": st["mlp_fwd"] / max(sum(st.values()), 1e-12),
+            "timing": "CUDA event nodes on the library stream in a profiled replay of the same graph"},
+        "stage_ms_per_iter": st,
         "clocks": clocks,
         "e2e": e2e,
-        "gpu_launches": args.steps * (ITERS_PER_STEP * g.launches_per_iter + 1),
+        "gpu_launches": launches,
     }
-    if world == 1 and not args.no_cpu_baseline:
-        v, cores, t_factor = time_oracle(args.workload, 1)
-        line["cpu_baseline"] = {"value": v, "unit": "Adam iters/s", "cores": cores, "kind": "oracle",
-                                "sample": f"1 full Adam iteration of {args.workload} (fp64 oracle, OpenMP); "
-                                          f"one-time LU factorisation ({t_factor:.1f}s) excluded"}
-    print(json.dumps(line), flush=True)
     g.close()
+    del S_dev
+    if world == 1 and not args.shard and not args.no_per_workload:
+        # C1..C5 (north_star: report every workload): device-timed it/s, points.it/s, ms/iter, roofline
+        # fraction; the other four configs are timed with the same protocol, fewer steps
+        per = {}
+        for name in W.WORKLOADS:
+            if name == args.workload:
+                per[name] = {"it_s": value, "ms_per_iter": ms_iter}
+            else:
+                Fn = W.make_fields(name)
+                wn = Fn.workload
+                gn = crv.Crvpinn(wn.N, wn.widths, Fn.K, Fn.S, Fn.f, Fn.theta0, precision=prec, lr=wn.lr,
+                                 device=local, stream=stream.cuda_stream)
+                Sn = [torch.from_numpy(s).to(f"cuda:{local}") for s in Fn.S_steps]
+                steps_n = max(3, min(args.steps, 10))
+                tn, _ = time_steps(torch, gn, Sn, stream, flush, steps_n, max(3, min(args.warmup, 5)))
+                gn.close()
+                per[name] = {"it_s": steps_n * ITERS_PER_STEP / (tn / 1e3), "ms_per_iter": tn / (steps_n * ITERS_PER_STEP)}
+            wn = W.WORKLOADS[name]
+            per[name]["points_it_s"] = per[name]["it_s"] * wn.points
+            ach, frac = roofline_frac(wn, per[name]["ms_per_iter"], peak)
+            per[name]["roofline"] = {"achieved_tflops": ach, "frac": frac, "bound": bound,
+                                     "traffic": traffic.get(name)}
+        if not args.no_cpu_baseline:
+            orc = time_oracle_table(list(W.WORKLOADS))
+            for name, row in orc.items():
+                per[name]["oracle"] = row
+        line["per_workload"] = per
+    if world == 1 and not args.no_cpu_baseline:
+        n_or = 2
+        v, cores, t_factor = time_oracle(args.workload, n_or)
+        line["cpu_baseline"] = {"value": v, "unit": "Adam iters/s", "cores": cores, "kind": "oracle",
+                                "cpu": cpu_model(),
+                                "sample": f"{n_or} full Adam iterations of {args.workload} (fp64 oracle, OpenMP, "
+                                          f"{cores} threads, right after the one-time LU factorisation "
+                                          f"({t_factor:.1f}s, excluded))"}
+    print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0

@@ -104,7 +104,11 @@ typedef struct {
 void crvpinn_default_opts(crvpinn_opts *o);
 
 /* Create a problem on grid N (power of two, 16 <= N <= 2048) with layer widths
- * widths[0..n_widths-1] = {2, w, ..., w, 1} (hidden widths multiples of 32, <= 256).
+ * widths[0..n_widths-1] = {2, w, ..., w, 1} (hidden widths multiples of 32, <= 256, at most
+ * 16 layers). CRVPINN_PREC_TENSOR further requires (else EINVAL): at least two hidden layers
+ * (one hidden-to-hidden GEMM), all hidden widths equal, and w in {32, 64, 96, 128, 224, 256}
+ * (w is zero-padded to WP = 64 ceil(w/64) in {64, 128, 256}; WP = 192, i.e. w = 160 or 192, has
+ * no kernel instantiation). CRVPINN_PREC_FP32 takes every width set above.
  * K, S, f: host (N+1)^2 float32 fields (K > 0; S is clamped to [0,1]).
  * theta0: host float32 of crvpinn_num_params entries, or NULL for Xavier-uniform (biases 0).
  * Runs step A0 (alpha, b) and builds the Gram-solve constants (Eq. 28 "factorization performed

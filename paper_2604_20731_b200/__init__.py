@@ -196,7 +196,9 @@ class Crvpinn:
         self.shard = (o.shard_rank, o.shard_world)
         w = (ctypes.c_int * len(self.widths))(*self.widths)
         K, S, f = _f32(K, nn), _f32(S, nn), _f32(f, nn)
-        th = None if theta0 is None else _f32(theta0)
+        wd = self.widths
+        n_params = sum(wd[l + 1] * (wd[l] + 1) for l in range(len(wd) - 1))
+        th = None if theta0 is None else _f32(theta0, n_params)   # the C side reads exactly n_params floats
         h = ctypes.c_void_p()
         rc = L.crvpinn_create(ctypes.byref(h), self.N, len(self.widths), w, _fp(K), _fp(S), _fp(f),
                               None if th is None else _fp(th), ctypes.byref(o))

@@ -403,7 +403,8 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
         DALLOC(ctx->simt.gbar, net.P);
         DALLOC(ctx->simt.partial, ctx->plan.partial_floats);
         DALLOC(ctx->d_jobs, ctx->plan.njobs);
-        CK(cudaMemcpy(ctx->d_jobs, ctx->plan.jobs, sizeof(RedJob) * ctx->plan.njobs, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ctx->d_jobs, ctx->plan.jobs, sizeof(RedJob) * ctx->plan.njobs, cudaMemcpyHostToDevice,
+                           ctx->stream));
         ctx->simt.jobs = ctx->d_jobs;
     } else {
         int rc = tc_create(net, ctx->tc, (int)ctx->tile0, (int)ctx->ntiles, ctx->err);
@@ -425,10 +426,13 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
             for (int k = 0; k < fout; ++k) th[net.boff[l] + k] = 0.0f;
         }
     }
-    CK(cudaMemcpy(ctx->theta, th.data(), sizeof(float) * np, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->K, K, sizeof(float) * nn, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->S, S, sizeof(float) * nn, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->f, f, sizeof(float) * nn, cudaMemcpyHostToDevice));
+    // pageable sources: the copies are staged and ordered on the context stream, ahead of the
+    // kernels that read them (a plain cudaMemcpy runs on the legacy stream, which a non-blocking
+    // context stream does not wait for)
+    CK(cudaMemcpyAsync(ctx->theta, th.data(), sizeof(float) * np, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->K, K, sizeof(float) * nn, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->S, S, sizeof(float) * nn, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->f, f, sizeof(float) * nn, cudaMemcpyHostToDevice, ctx->stream));
     launch_alpha(ctx->K, ctx->S, ctx->alpha, N, (float)ctx->opts.mobility_ratio, ctx->stream);
     launch_rhs(ctx->K, ctx->S, ctx->f, ctx->b, N, (float)ctx->opts.mobility_ratio, (float)ctx->opts.density_ratio,
                (float)ctx->opts.gravity, ctx->stream);
@@ -479,8 +483,10 @@ int crvpinn_create(crvpinn_ctx **out, int N, int n_widths, const int *widths, co
         shard_split(T, r, w, ctx->tile0, ctx->ntiles);
         ctx->sharded = w > 1 || ctx->opts.nccl;
     }
-    if (!std::isfinite(ctx->opts.gravity) || !std::isfinite(ctx->opts.density_ratio) || ctx->opts.density_ratio < 0.0)
+    if (!std::isfinite(ctx->opts.gravity) || !std::isfinite(ctx->opts.density_ratio) || ctx->opts.density_ratio < 0.0) {
+        delete ctx;
         return fail(nullptr, CRVPINN_EINVAL, "gravity / density_ratio must be finite (density_ratio >= 0)");
+    }
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) {
         for (int l = 2; l < n_widths - 1; ++l)
             if (widths[l] != widths[1]) {
@@ -565,6 +571,10 @@ int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist) {
     if (ctx->h_state->nonfinite) {
         rc = snapshot_copies(ctx, false);
         if (rc) return rc;
+        // the tensor path computes only from its fp16 weight copies, which every Adam step of the
+        // call rewrote: rebuild them from the restored theta
+        if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->stream);
+        CK(cudaGetLastError());
         CK(cudaStreamSynchronize(ctx->stream));
         return fail(ctx, CRVPINN_ENONFINITE, "non-finite loss or gradient; theta and Adam state restored");
     }
@@ -577,6 +587,8 @@ int crvpinn_pretrain(crvpinn_ctx *ctx, int n_iters, double *loss_hist) {
 
 int crvpinn_eval(crvpinn_ctx *ctx, float *p_out) {
     if (!ctx || !p_out) return fail(ctx, CRVPINN_EINVAL, "null argument");
+    if (needs_caller_exchange(ctx))
+        return fail(ctx, CRVPINN_EINVAL, "sharded context without a communicator: use crvpinn_shard_forward");
     CK(cudaSetDevice(ctx->device));
     ctx->nccl_rc = ncclSuccess;
     launch_forward(ctx);
@@ -726,8 +738,7 @@ int crvpinn_get_params(crvpinn_ctx *ctx, float *theta) {
 int crvpinn_set_params(crvpinn_ctx *ctx, const float *theta) {
     if (!ctx || !theta) return fail(ctx, CRVPINN_EINVAL, "null argument");
     CK(cudaSetDevice(ctx->device));
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(ctx->theta, theta, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->theta, theta, sizeof(float) * ctx->np, cudaMemcpyHostToDevice, ctx->stream));
     if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     return CRVPINN_OK;
@@ -747,12 +758,13 @@ int crvpinn_get_adam(crvpinn_ctx *ctx, float *m, float *v, int64_t *t) {
 int crvpinn_set_adam(crvpinn_ctx *ctx, const float *m, const float *v, int64_t t) {
     if (!ctx || !m || !v || t < 0) return fail(ctx, CRVPINN_EINVAL, "bad argument");
     CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(ctx->m, m, sizeof(float) * ctx->np, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->v, v, sizeof(float) * ctx->np, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(ctx->m, m, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->v, v, sizeof(float) * ctx->np, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->h_state, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     ctx->h_state->t = t;
-    CK(cudaMemcpy(ctx->st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return CRVPINN_OK;
 }
 

@@ -9,11 +9,12 @@
 //    (SURVEY.md key finding 4); weights are rounded once to fp16 (10-bit mantissa, as TF32).
 //    Epilogue warps read TMEM, add bias, apply tanh, split, write the next A operand into
 //    shared memory (SWIZZLE_128B K-major) and stream t_hi to HBM with bulk copies.
-//  * backward: Delta_{a} = (Delta_{a+1} W) (.) (1 - t_a^2) on tcgen05 (k_tc_dx, one layer per
-//    launch, W^T streamed as the B operand), and dW = sum_p Delta^T t as a split-K tcgen05
-//    GEMM over points with MN-major operands read straight from the stored tiles (k_tc_dw).
-//    Delta is stored in fp16 after a power-of-two scaling of dLOSS/dnet (DevState::gscale)
-//    so that it stays in fp16's normal range; partial sums are unscaled in the reduction.
+//  * backward: Delta_{a} = (Delta_{a+1} W) (.) (1 - t_a^2) and dW = sum_p Delta^T t, both on
+//    tcgen05 in one launch per hidden GEMM (k_tc_bwd2: CTA pairs, Delta multicast, W^T resident),
+//    or all hidden GEMMs in one spatial-pipeline launch (k_tc_bwdc, small problems), or
+//    k_tc_out_bwd + k_tc_bwd_layer for WP = 64. Delta is stored in fp16 after a power-of-two
+//    scaling of dLOSS/dnet (DevState::gscale) so that it stays in fp16's normal range; partial
+//    sums are unscaled in the reduction.
 // Weights are streamed into shared memory by cp.async.bulk (the TMA engine) from fp16 copies
 // that k_tc_refresh re-lays out after every Adam step (zero-padded to WP = 64*ceil(w/64)).
 #include "mlp_tc.cuh"

@@ -1,0 +1,99 @@
+"""Long oracle runs for the multi-step parity fixtures (tests/golden/), oracle only (fp64).
+
+Calls only oracle/ and the seeded input generators (workloads/); nothing here touches the CUDA
+path. Each sub-command writes one .npz under tests/golden/.
+
+  c4sched                 C4's full schedule (§6 step 7; BASELINE.json configs[3]):
+                          10 time steps x 100 Adam iterations, warm-started weights and Adam state,
+                          S advanced between steps (S_steps[k] for step k) -> C4_sched10x100.npz
+  c3 <seed> <iters>       C3's pretraining + updates with fixed S (configs[2]):
+                          <iters> Adam iterations from theta0 (seed 0) or from theta0 moved by one fp32
+                          ulp per entry (seed > 0, the recipe of scripts/c3_sensitivity.py)
+                          -> C3_run<iters>_s<seed>.npz
+  c3 <seed> <iters> --noise SIGMA
+                          the same with a seeded Gaussian perturbation of the gradient before every
+                          Adam step, g + SIGMA (|g|_2 / sqrt(n)) xi (reading R28: the
+                          oracle driven at a given per-iteration gradient-error level)
+                          -> C3_run<iters>_s<seed>_noise<SIGMA>.npz
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+import workloads as W  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def ulp_perturbed(theta0, seed):
+    t0 = np.asarray(theta0, dtype=np.float32)
+    if seed == 0:
+        return t0
+    rng = np.random.default_rng(seed)
+    return np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
+
+
+def c4sched():
+    F = W.make_fields("C4")
+    w = F.workload
+    t = time.time()
+    o = oracle.Oracle(w.N, w.widths, F.K, F.S_steps[0], F.f, F.theta0, lr=w.lr)
+    hist = np.zeros((w.n_steps, w.n_adam))
+    step_end = np.zeros(w.n_steps)
+    thetas = {}
+    for k in range(w.n_steps):
+        if k > 0:
+            o.set_saturation(F.S_steps[k])
+        hist[k] = o.train(w.n_adam)
+        step_end[k] = o.loss_grad()[0]      # LOSS(theta after step k) on S_steps[k]
+        if k in (0, w.n_steps - 1):
+            thetas[f"theta_step{k + 1}"] = o.theta.astype(np.float32)
+        print(f"C4 step {k + 1}: {hist[k, 0]:.6e} -> {hist[k, -1]:.6e} end {step_end[k]:.6e} "
+              f"({time.time() - t:.0f}s)", flush=True)
+    np.savez_compressed(os.path.join(OUT, "C4_sched10x100.npz"), hist=hist, step_end=step_end,
+                        threads=oracle.max_threads(), **thetas)
+
+
+def c3(seed, iters, noise):
+    F = W.make_fields("C3")
+    w = F.workload
+    t = time.time()
+    o = oracle.Oracle(w.N, w.widths, F.K, F.S, F.f, ulp_perturbed(F.theta0, seed), lr=w.lr)
+    if noise > 0:
+        rng = np.random.Generator(np.random.PCG64(1000 + seed))
+        hist = np.zeros(iters)
+        for i in range(iters):
+            loss, g = o.loss_grad()
+            hist[i] = loss
+            xi = rng.standard_normal(g.shape)
+            o.adam_step(g + noise * (np.linalg.norm(g) / np.sqrt(g.size)) * xi)
+            if (i + 1) % 500 == 0:
+                print(f"C3 s{seed} noise {noise:g}: it {i + 1} loss {loss:.6e} ({time.time() - t:.0f}s)", flush=True)
+        name = f"C3_run{iters}_s{seed}_noise{noise:g}.npz"
+    else:
+        chunks = []
+        for i0 in range(0, iters, 500):
+            chunks.append(o.train(min(500, iters - i0)))
+            print(f"C3 s{seed}: it {i0 + len(chunks[-1])} loss {chunks[-1][-1]:.6e} ({time.time() - t:.0f}s)",
+                  flush=True)
+        hist = np.concatenate(chunks)
+        name = f"C3_run{iters}_s{seed}.npz"
+    np.savez_compressed(os.path.join(OUT, name), hist=hist, final_loss=np.float64(o.loss_grad()[0]),
+                        theta=o.theta.astype(np.float32), seed=seed, noise=noise, threads=oracle.max_threads())
+    print(f"wrote {name} ({time.time() - t:.0f}s)", flush=True)
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1]
+    if cmd == "c4sched":
+        c4sched()
+    elif cmd == "c3":
+        noise = float(sys.argv[sys.argv.index("--noise") + 1]) if "--noise" in sys.argv else 0.0
+        c3(int(sys.argv[2]), int(sys.argv[3]), noise)
+    else:
+        raise SystemExit(__doc__)

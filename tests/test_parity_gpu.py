@@ -265,6 +265,29 @@ def test_nonfinite_restores_state(crv):
     assert t == t5 and np.array_equal(m, m5) and np.array_equal(v, v5)
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_nonfinite_mid_call_restores_computation(crv, prec):
+    """A divergence after several Adam steps of one call (lr = 1e38: the first update moves every
+    weight by ~1e38, the next forward overflows): ENONFINITE, and the context computes exactly as at
+    call entry afterwards -- theta, the Adam state and, on the tensor path, the fp16 weight copies
+    the kernels read (rewritten by every Adam step of the call) are all restored."""
+    N, widths = 32, (2, 64, 64, 64, 1)
+    K, S, f = W.random_fields(N, 8)
+    th = W.random_theta(widths, 8)
+    g = crv.Crvpinn(N, widths, K, S, f, th, precision=prec, lr=1e38)
+    l0, g0 = g.loss_grad()
+    p0 = g.eval()
+    with pytest.raises(crv.CrvpinnError) as ei:
+        g.step(10)
+    assert ei.value.code == crv.CRVPINN_ENONFINITE
+    assert np.array_equal(g.theta, th)
+    m, v, t = g.adam_state()
+    assert t == 0 and not np.any(m) and not np.any(v)
+    l1, g1 = g.loss_grad()
+    assert l1 == l0 and np.array_equal(g1, g0)
+    assert np.array_equal(g.eval(), p0)
+
+
 def test_checkpoint_roundtrip(crv):
     N, widths = 32, (2, 32, 32, 1)
     K, S, f = W.random_fields(N, 7)
