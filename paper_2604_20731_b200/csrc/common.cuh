@@ -20,6 +20,12 @@ struct DevState {
     float inv_gscale;
     unsigned gmax_bits;   // max |dLOSS/dnet| of the current iteration (float bits, atomicMax)
     int pad;
+    // Tensor path, per hidden GEMM g: the fp16 weight copies hold W_g 2^-wexp[g]
+    // (max |.| <= 2^14 for the whole call), and the backward stores Delta one level down with an extra
+    // factor 2^-fexp[g] (fexp = round(log2(|W_g|_F / sqrt(fan_in))), 0 for Xavier-scaled weights), so
+    // fp16 holds weights and Delta of any magnitude. Set per call by k_wscale.
+    int wexp[CRV_MAX_LAYERS];
+    int fexp[CRV_MAX_LAYERS];
 };
 
 // Geometry and network description passed by value to kernels.
@@ -43,8 +49,19 @@ struct RedJob {
     int nsplit;
     int cols, ld;  // transposed layout parameters
     int transposed;
-    int scaled;    // multiply by DevState::inv_gscale (tensor backward partials)
+    int scaled;    // tensor backward partials: multiply by DevState::inv_gscale x 2^(sum_{g_lo <= g < g_hi}
+                   // fexp[g] - 14 tsc) (the Delta level's cumulative scale; tsc: the partials carry one
+                   // activation factor t' = 2^14 t)
+    int g_lo, g_hi, tsc;
 };
+
+// unscale factor of a reduction job (RedJob::scaled)
+__device__ __forceinline__ float red_scale(const RedJob &j, const DevState *st) {
+    if (!j.scaled) return 1.0f;
+    int e = j.tsc ? -14 : 0;
+    for (int g = j.g_lo; g < j.g_hi; ++g) e += st->fexp[g];
+    return st->inv_gscale * exp2f((float)e);
+}
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 

@@ -251,6 +251,9 @@ static int get_graph(crvpinn_ctx *ctx, int n, GraphEntry **out) {
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     launch_begin_call(ctx->st, ctx->stream);
     int rc = snapshot_copies(ctx, true);
+    // the fp16 weight copies' exponents for this call: room for n Adam steps
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR)
+        tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->st, (float)(4.0 * n * ctx->opts.lr), ctx->stream);
     for (int k = 0; k < n && rc == CRVPINN_OK; ++k)
         launch_iteration(ctx, ge.hist, n, true, ctx->profiling ? &ge.ev[(size_t)5 * k] : nullptr);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
@@ -409,6 +412,7 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     } else {
         int rc = tc_create(net, ctx->tc, (int)ctx->tile0, (int)ctx->ntiles, ctx->err);
         if (rc != 0) return rc;
+        ctx->tc.st = ctx->st;
     }
     // ---- inputs, A0, Gram constants
     std::vector<float> th((size_t)np);
@@ -436,7 +440,7 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
     launch_alpha(ctx->K, ctx->S, ctx->alpha, N, (float)ctx->opts.mobility_ratio, ctx->stream);
     launch_rhs(ctx->K, ctx->S, ctx->f, ctx->b, N, (float)ctx->opts.mobility_ratio, (float)ctx->opts.density_ratio,
                (float)ctx->opts.gravity, ctx->stream);
-    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->stream);
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(net, ctx->tc, ctx->theta, ctx->st, 0.0f, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
     // ---- the shards' communicator (collective: every rank creates its context concurrently)
@@ -573,7 +577,7 @@ int crvpinn_step(crvpinn_ctx *ctx, int n_adam, double *loss_hist) {
         if (rc) return rc;
         // the tensor path computes only from its fp16 weight copies, which every Adam step of the
         // call rewrote: rebuild them from the restored theta
-        if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->stream);
+        if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->st, 0.0f, ctx->stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(ctx->stream));
         return fail(ctx, CRVPINN_ENONFINITE, "non-finite loss or gradient; theta and Adam state restored");
@@ -739,7 +743,7 @@ int crvpinn_set_params(crvpinn_ctx *ctx, const float *theta) {
     if (!ctx || !theta) return fail(ctx, CRVPINN_EINVAL, "null argument");
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(ctx->theta, theta, sizeof(float) * ctx->np, cudaMemcpyHostToDevice, ctx->stream));
-    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->stream);
+    if (ctx->opts.precision == CRVPINN_PREC_TENSOR) tc_refresh_weights(ctx->net, ctx->tc, ctx->theta, ctx->st, 0.0f, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     return CRVPINN_OK;
 }

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
     while (j < njobs && g >= red_groups(jobs[j])) { g -= red_groups(jobs[j]); ++j; }
     if (j >= njobs) return;
     const RedJob jb = jobs[j];
-    const float sc = jb.scaled ? st->inv_gscale : 1.0f;
+    const float sc = red_scale(jb, st);
     if (red_wide(jb)) {
         const int o = g * RED_THREADS + threadIdx.x;
         if (o >= jb.count) return;
@@ -131,7 +131,7 @@ constexpr int RW_THREADS = 64;
 __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restrict__ partial,
                                                             float *__restrict__ grad, RedJob jb,
                                                             const DevState *st) {
-    const float sc = jb.scaled ? st->inv_gscale : 1.0f;
+    const float sc = red_scale(jb, st);
     const int n4 = jb.count >> 2;
     for (int q = blockIdx.x * RW_THREADS + threadIdx.x; q < n4; q += gridDim.x * RW_THREADS) {
         const float4 *src = reinterpret_cast<const float4 *>(partial + jb.src + red_off(jb, 4 * q));

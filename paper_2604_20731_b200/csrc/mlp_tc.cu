@@ -22,23 +22,12 @@
 #include "../../include/crvpinn.h"
 #include <math.h>
 #include <cstdlib>
+#include <type_traits>
 #ifndef CRV_B2_DSX
 #define CRV_B2_DSX 2
 #endif
 #ifndef CRV_B2_NT
 #define CRV_B2_NT 2
-#endif
-#ifndef CRV_FWD_F32X2
-#define CRV_FWD_F32X2 2   // packed fp32 pairs (FFMA2) in the forward epilogue: 2 = v and the Newton reciprocals only, 1 = everything
-#endif
-#ifndef CRV_NEWTON_MASK
-#define CRV_NEWTON_MASK 0xAAAA   // which of a thread's 16 elements per chunk take the FMA-pipe reciprocal
-#endif
-#ifndef CRV_CLAMP_NEWTON_ONLY
-#define CRV_CLAMP_NEWTON_ONLY 1
-#endif
-#ifndef CRV_TANH_MIX
-#define CRV_TANH_MIX 1
 #endif
 
 namespace crv {
@@ -86,6 +75,7 @@ struct FwdArgs {
     const float *xy;       // EVAL only: point coordinates [npts][2]
     int npts;              // EVAL only: number of points (ntiles = ceil(npts / 128), ragged tail)
     int p0;                // first MLP point of this shard (tile0 * 128); 0 unsharded
+    const DevState *st;    // per-GEMM weight exponents (wexp, written by k_wscale)
 };
 #define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 
@@ -116,12 +106,17 @@ constexpr int NQ = CRV_FWD_NQ;
 #endif
 
 constexpr float TANH_C = 2.8853900817779268f;   // 2 log2(e): tanh(z) = 1 - 2 / (1 + 2^(TANH_C z))
+// activation scale of every fp16 activation operand and stored activation: t' = 2^14 t
+constexpr float ACT_INV = 1.0f / 16384.0f;
+// the backward's factor on (Delta_out W~)(.)(1 - t^2) for GEMM g: 2^(wexp - fexp), and with t' = 2^14 t,
+// k (1 - t^2) = k - (k 2^-28) t'^2
+__device__ __forceinline__ float bwd_k(const DevState *st, int g) { return ldexpf(1.0f, st->wexp[g] - st->fexp[g]); }
 constexpr int FWD_EPI_WARPS = 16;                       // 4 per TMEM lane quarter
 constexpr int FWD_THREADS = 64 + 32 * FWD_EPI_WARPS;     // producer warp + MMA warp + epilogue
 
 template <int WP>
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
-    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128) * 4 +
+    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128 + 2 * L) * 4 +
            40 * 8 + 16;
 }
 
@@ -147,7 +142,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     float *sB = sW1 + 2 * WP;
     float *sWo = sB + a.L * WP;          // WP + 1 (bias last)
     float *sRed = sWo + WP + 1;          // [2 parity][4][128]
-    uint64_t *bars = (uint64_t *)(((uintptr_t)(sRed + 2 * 4 * 128) + 7) & ~(uintptr_t)7);
+    float *sC = sRed + 2 * 4 * 128;      // [G] epilogue factor of GEMM g: 2 log2(e) 2^(wexp[g] - 14)
+    int *sAcc = (int *)(sC + a.L);       // [L] layer l's tanh must be accurate for small |t| (next GEMM's gain >= 16)
+    uint64_t *bars = (uint64_t *)(((uintptr_t)(sAcc + a.L) + 7) & ~(uintptr_t)7);
     uint64_t *w_full = bars, *w_empty = bars + NST_W;
     uint64_t *a_full = bars + 2 * NST_W;          // [KC]
     uint64_t *acc_full = a_full + KC;             // [2 accumulators][NQ N-parts]
@@ -171,6 +168,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
     for (int i = threadIdx.x; i < 2 * WP; i += blockDim.x) sW1[i] = a.W1p[i];
     for (int i = threadIdx.x; i < a.L * WP; i += blockDim.x) sB[i] = a.bp[i];
     for (int i = threadIdx.x; i < WP + 1; i += blockDim.x) sWo[i] = a.Wop[i];
+    // GEMM g accumulates t' W~ = 2^(14 - wexp[g]) t W (activations t' = 2^14 t, weights W 2^-wexp[g])
+    for (int i = threadIdx.x; i < a.G; i += blockDim.x) sC[i] = ldexpf(TANH_C, a.st->wexp[i] - 14);
+    for (int i = threadIdx.x; i < a.L; i += blockDim.x) sAcc[i] = i < a.G && a.st->fexp[i] >= 4;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -334,6 +334,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     need_half1(wq * 16);
                     tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
                 }
+                // the chunk loop, instantiated for the accurate-tanh layers and for the rest (a uniform
+                // branch per layer, so the common path carries no code of the other)
+                auto chunks = [&](auto EXACT) {
 #pragma unroll
                 for (int c = 0; c < KC; ++c) {
                     const int cc = c * 64 + wq * 16;
@@ -350,93 +353,55 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         }
                     } else {
                         tmem_wait_ld16(rbuf);
+                        const float cg = sC[layer - 2];   // 2 log2(e) 2^(wexp - 14): undoes the operand scales
+                        const f32x2_t C2 = pk2(cg, cg);
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
                             const float4 b4 = lds_f4(bias + cc + k);   // 2 log2(e) b
-#if CRV_FWD_F32X2 == 2
-                            const f32x2_t C2 = pk2(TANH_C, TANH_C);
                             upk2(ffma2(pk2(__uint_as_float(rbuf[k]), __uint_as_float(rbuf[k + 1])), C2, pk2(b4.x, b4.y)),
                                  v[k], v[k + 1]);
                             upk2(ffma2(pk2(__uint_as_float(rbuf[k + 2]), __uint_as_float(rbuf[k + 3])), C2, pk2(b4.z, b4.w)),
                                  v[k + 2], v[k + 3]);
-#else
-                            v[k] = fmaf(__uint_as_float(rbuf[k]), TANH_C, b4.x);
-                            v[k + 1] = fmaf(__uint_as_float(rbuf[k + 1]), TANH_C, b4.y);
-                            v[k + 2] = fmaf(__uint_as_float(rbuf[k + 2]), TANH_C, b4.z);
-                            v[k + 3] = fmaf(__uint_as_float(rbuf[k + 3]), TANH_C, b4.w);
-#endif
                         }
                         if (c + 1 < KC) {
                             need_half1(cc + 64);
                             tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
                         }
                     }
-                    // v = 2 log2(e) z (the fp32 first layer and biases arrive pre-scaled by
-                    // k_tc_refresh; the fp16 GEMM weights do not -- that was measured less accurate)
-                    // tanh(z) = 1 - 2 / (1 + 2^v) for 16 elements as a skewed pipeline:
-                    // ex2 of element i, rcp of element i-2 and the finish (t, hi/lo split, fp16 pack)
-                    // of pair (i-5, i-4) are issued together, so MUFU and ALU work interleave
+                    // v = 2 log2(e) z; tanh(z) = 1 - 2 / (1 + 2^v) for 16 elements as a skewed pipeline:
+                    // ex2 of element i, the reciprocal of element i-2 and the finish (t' = 2^14 t, hi/lo
+                    // split, fp16 pack) of pair (i-5, i-4) are issued together, so MUFU and ALU work
+                    // interleave. Even elements take the MUFU reciprocal, odd ones a Newton reciprocal on
+                    // the FMA pipe, two of them (k-2, k) per packed step (FFMA2) when k = 3 mod 4 (MUFU : ALU
+                    // balance); only the Newton elements need a finite 1 + 2^v (rcp.approx(inf) = 0).
                     uint32_t hw[8], lw[8];
-#if CRV_FWD_F32X2 == 1
-                    float r[16];   // r[k] = 1/(1 + 2^v_k), even k: negated (from rcp(-(1 + 2^v)))
-                    {
-                        // pairs (2m, 2m+1): even elements take the MUFU reciprocal, odd ones Newton on the
-                        // FMA pipe, two odd elements (of pairs m, m+1) per packed FFMA2
-                        const f32x2_t M1 = pk2(-1.0f, -1.0f), ONE = pk2(1.0f, 1.0f);
-                        float nd[16];
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) {
-                            const float e0 = ex2_v(v[2 * m]), e1 = ex2_v(fminf(v[2 * m + 1], 60.0f));
-                            upk2(ffma2(pk2(e0, e1), M1, M1), nd[2 * m], nd[2 * m + 1]);   // -(1 + 2^v)
-                            r[2 * m] = rcp_v(nd[2 * m]);
-                        }
-#pragma unroll
-                        for (int m = 0; m < 8; m += 2) {
-                            const float a = nd[2 * m + 1], b = nd[2 * m + 3];
-                            // 1/d for d = -a: bit-trick seed from a's bits, 3 Newton steps e = 1 - d R, R += R e
-                            f32x2_t R = pk2(__int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(a))),
-                                            __int_as_float((int)(0xFEF311C3u - (uint32_t)__float_as_int(b))));
-                            const f32x2_t ND = pk2(a, b);
-#pragma unroll
-                            for (int it = 0; it < 3; ++it) {
-                                const f32x2_t E = ffma2(ND, R, ONE);
-                                R = ffma2(R, E, R);
-                            }
-                            upk2(R, r[2 * m + 1], r[2 * m + 3]);
-                        }
-                        const f32x2_t TW = pk2(2.0f, -2.0f);
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) {
-                            const f32x2_t t = ffma2(pk2(r[2 * m], r[2 * m + 1]), TW, ONE);   // 1 - 2/(1 + 2^v)
-                            float t0, t1;
-                            upk2(t, t0, t1);
-                            const float h0 = __uint_as_float(__float_as_uint(t0) & 0xFFFFE000u);
-                            const float h1 = __uint_as_float(__float_as_uint(t1) & 0xFFFFE000u);
-                            float l0, l1;
-                            upk2(fsub2(t, pk2(h0, h1)), l0, l1);
-                            hw[m] = pack_half2(h0, h1);
-                            lw[m] = pack_half2(l0, l1);
-                            if (last) { v[2 * m] = t0; v[2 * m + 1] = t1; }
-                        }
-                    }
-#else
                     float e[16], r[16];
+                    if constexpr (decltype(EXACT)::value) {
+                        // accurate-tanh layer (its activations feed a GEMM with a large gain):
+                        // the formula below is accurate to ~2^-22 ABSOLUTE, which that gain would amplify
+                        // for small |t|; here |z| < 1/8 takes the odd Taylor polynomial (relative error
+                        // < 2e-9), the rest the same exp formula
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const float tb = fmaf(-2.0f, rcp_v(1.0f + ex2_v(fminf(v[k], 60.0f))), 1.0f);
+                            const float z = v[k] * (1.0f / TANH_C), z2 = z * z;
+                            const float ts = z * fmaf(z2, fmaf(z2, fmaf(z2, -17.0f / 315.0f, 2.0f / 15.0f), -1.0f / 3.0f), 1.0f);
+                            r[k] = fabsf(z) < 0.125f ? ts : tb;   // r holds t on this path
+                        }
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) finish_pair_t(r[2 * m], r[2 * m + 1], hw[m], lw[m]);
+                        if (last) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) v[k] = r[k];
+                        }
+                    } else {
 #pragma unroll
                     for (int i = 0; i < 16 + 5; ++i) {
-#if CRV_TANH_MIX && CRV_CLAMP_NEWTON_ONLY
-                        // only the Newton reciprocal needs a finite 1 + 2^v (rcp.approx(inf) = 0)
-                        if (i < 16) e[i] = ex2_v(((CRV_NEWTON_MASK >> i) & 1) ? fminf(v[i], 60.0f) : v[i]);
-#else
-                        if (i < 16) e[i] = ex2_v(fminf(v[i], 60.0f));
-#endif
-#if CRV_TANH_MIX && CRV_FWD_F32X2 == 2
-                        // odd elements take the reciprocal on the FMA pipe, two of them (k-2, k) per packed
-                        // Newton step (FFMA2) when k = 3 mod 4
+                        if (i < 16) e[i] = ex2_v((i & 1) ? fminf(v[i], 60.0f) : v[i]);
                         if (i >= 2 && i < 18) {
                             const int k = i - 2;
                             if ((k & 1) == 0) {
-                                // (CRV_NEWTON_MASK 0xEEEE: elements 2 mod 4 take a scalar Newton reciprocal too)
-                                r[k] = ((CRV_NEWTON_MASK >> k) & 1) ? rcp_newton(1.0f + e[k]) : rcp_v(1.0f + e[k]);
+                                r[k] = rcp_v(1.0f + e[k]);
                             } else if ((k & 3) == 3) {
                                 const float da = 1.0f + e[k - 2], db = 1.0f + e[k];
                                 f32x2_t R = pk2(__int_as_float(0x7EF311C3 - __float_as_int(da)),
@@ -447,23 +412,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                                 upk2(R, r[k - 2], r[k]);
                             }
                         }
-#elif CRV_TANH_MIX
-                        // odd elements take the reciprocal on the FMA pipe (MUFU : ALU balance)
-                        if (i >= 2 && i < 18)
-                            r[i - 2] = ((CRV_NEWTON_MASK >> (i - 2)) & 1) ? rcp_newton(1.0f + e[i - 2]) : rcp_v(1.0f + e[i - 2]);
-#else
-                        if (i >= 2 && i < 18) r[i - 2] = rcp_v(1.0f + e[i - 2]);
-#endif
                         if (i >= 5 && ((i - 5) & 1) == 0) {
                             const int m = (i - 5) >> 1;
                             if (m < 8) finish_pair(r[2 * m], r[2 * m + 1], hw[m], lw[m]);
                         }
                     }
-                    if (last) {
+                    if (last) {   // the output layer takes t itself (fp32)
 #pragma unroll
                         for (int k = 0; k < 16; ++k) v[k] = fmaf(-2.0f, r[k], 1.0f);
                     }
-#endif
+                    }
                     if (!last) {
                         const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
                         st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);
@@ -490,6 +448,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                         }
                     }
                 }
+                };
+                if (sAcc[layer - 1]) chunks(std::true_type{});
+                else chunks(std::false_type{});
             }
             // output layer: net = W_out t_L + b_out; u = cutoff * net (4 partial dots per row)
             sRed[(par * 4 + wq) * 128 + row] = dot;
@@ -584,6 +545,8 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 float2 t = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
+                t.x *= ACT_INV;   // stored activations are t' = 2^14 t
+                t.y *= ACT_INV;
                 const float d0 = g * wo[2 * m] * (1.0f - t.x * t.x);
                 const float d1 = g * wo[2 * m + 1] * (1.0f - t.y * t.y);
                 aw[2 * m] = fmaf(g, t.x, aw[2 * m]);
@@ -634,6 +597,8 @@ struct BwdArgs {
     float *part_dx;       // [grid][3*WP]   column sums (xy-weighted | plain)
     float *part_dw;       // [npairs][WP*WP] rows = out features
     int p0;               // first MLP point of this shard
+    const DevState *st;   // weight / Delta exponents of GEMM g
+    int g;
 };
 
 template <int WP>
@@ -764,6 +729,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) cs[k] = csx[k] = csy[k] = 0.0f;
         const int N = a.N;
+        const float kx = bwd_k(a.st, a.g), mx = kx * (ACT_INV * ACT_INV);
         int i = 0, ndx = 0;
         for (int tile = pair; tile < a.ntiles; tile += a.npairs, ++i) {
             if (i % PF != kk_pf) continue;
@@ -793,8 +759,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_bwd_layer(BwdArgs a) {
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
-                        v[8 * j + 2 * m] *= (1.0f - tf.x * tf.x);
-                        v[8 * j + 2 * m + 1] *= (1.0f - tf.y * tf.y);
+                        v[8 * j + 2 * m] *= fmaf(-mx * tf.x, tf.x, kx);
+                        v[8 * j + 2 * m + 1] *= fmaf(-mx * tf.y, tf.y, kx);
                         w[m] = pack_half2(v[8 * j + 2 * m], v[8 * j + 2 * m + 1]);
                     }
                     const int lg = ((cc & 63) >> 3) + j;
@@ -909,6 +875,7 @@ struct Bwd2Args {
     float *part_cb;       // [npairs][WP] 1^T Delta_out (CRV_B2_MMA_CS): bias gradient of theta layer g+1
     int outl_sums;        // outl: also reduce dW_out / db_L / db_out (else a side-stream k_tc_out_bwd does)
     int p0;               // first MLP point of this shard (gbar is passed offset by it)
+    int g;                // hidden GEMM index (weight / Delta exponents)
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 #ifndef CRV_B2_MMA_SLEEP
@@ -937,9 +904,6 @@ struct Bwd2Args {
 #endif
 #ifndef CRV_B2_CS_DEFER
 #define CRV_B2_CS_DEFER 1  // bwd2 bias column sums: one butterfly level per tile, the rest once at the end
-#endif
-#ifndef CRV_B2_F32X2
-#define CRV_B2_F32X2 1     // bwd2 epilogue: (1 - t^2) v in packed fp32 pairs
 #endif
 #ifndef CRV_B2_MMA_CS
 #define CRV_B2_MMA_CS 0    // bias gradients from a tensor-core 1^T Delta_out (single-buffered dX accumulator)
@@ -1245,6 +1209,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) aw[jj][e] = ab[jj][e] = 0.f;
         }
+        const float kx = bwd_k(a.st, a.g);
+        const f32x2_t K2 = pk2(kx, kx), NM2 = pk2(-kx * ACT_INV * ACT_INV, -kx * ACT_INV * ACT_INV);
         int dn = 0;
         for (int k = 0; k <= nk; ++k) {
             if (OUTL && k < nk) {
@@ -1259,6 +1225,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     if (olg == 0) ag += g[m];
                 }
                 const __half2 one2 = __floats2half2_rn(1.0f, 1.0f);
+                const __half2 tsc2 = __floats2half2_rn(ACT_INV, ACT_INV);
 #pragma unroll
                 for (int j = 0; j < KC; ++j) {
                     const int slot = (dn + j) % DS;
@@ -1281,7 +1248,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         ld_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const __half2 t = *reinterpret_cast<__half2 *>(&w[e]);
+                            const __half2 t = __hmul2(*reinterpret_cast<__half2 *>(&w[e]), tsc2);   // t' -> t
                             const __half2 d = __hmul2(__hmul2(__hfma2(__hneg2(t), t, one2), wo2[j][e]), g2[m]);
                             if (a.outl_sums && own && jj < 2) {
 #if CRV_OUTL_H2SUM
@@ -1380,18 +1347,13 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
                         const float2 tf = __half22float2(*reinterpret_cast<const __half2 *>(&tw[mm]));
-#if CRV_B2_F32X2
-                        {   // (1 - t^2) v for the pair in two packed FFMA2s
+                        {   // k (1 - t^2) v for the pair in packed FFMA2s (t' = 2^14 t)
                             const f32x2_t T = pk2(tf.x, tf.y);
                             const f32x2_t V = pk2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
-                            const f32x2_t NTV = ffma2(T, pk2(-1.0f, -1.0f) , pk2(0.0f, 0.0f));   // -t
-                            const f32x2_t G = ffma2(NTV, T, pk2(1.0f, 1.0f));                 // 1 - t^2
+                            const f32x2_t NTV = ffma2(T, NM2, pk2(0.0f, 0.0f));   // -k 2^-28 t'
+                            const f32x2_t G = ffma2(NTV, T, K2);                // k (1 - t^2)
                             upk2(ffma2(G, V, pk2(0.0f, 0.0f)), v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
                         }
-#else
-                        v[8 * j + 2 * mm] *= (1.0f - tf.x * tf.x);
-                        v[8 * j + 2 * mm + 1] *= (1.0f - tf.y * tf.y);
-#endif
                         w[4 * j + mm] = pack_half2(v[8 * j + 2 * mm], v[8 * j + 2 * mm + 1]);
                     }
                 }
@@ -1607,6 +1569,7 @@ struct BwdcArgs {
     size_t lay;           // halves per activation layer
     long long *trace;     // debug timeline: CTAs 0..7 (cluster 0), 512 slots each; nullptr normally
     int p0;               // first MLP point of this shard
+    const DevState *st;   // weight / Delta exponents per GEMM
 };
 #define CTRACE(slot) do { if (a.trace && blockIdx.x < 8 && (slot) < 1024) a.trace[blockIdx.x * 1024 + (slot)] = clock64(); } while (0)
 
@@ -1795,6 +1758,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
         const uint32_t t_lane = (uint32_t)(q * 32) << 16;
         const int N = a.N;
         float cs[2] = {0.f, 0.f}, csx[2] = {0.f, 0.f}, csy[2] = {0.f, 0.f};
+        const float kx = bwd_k(a.st, g), mx = kx * (ACT_INV * ACT_INV);
         // hand this warp's chunk of a finished tile (ring slot pgs) to the next stage. Deferred by
         // one tile: by the time the next tile's dX is drained the stores are long complete, so the
         // gpu-scope fence does not stall the epilogue.
@@ -1860,8 +1824,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
 #pragma unroll
                     for (int mm = 0; mm < 8; ++mm) {
                         const float2 tf = __half22float2(*reinterpret_cast<__half2 *>(&tw[mm]));
-                        const float d0 = __uint_as_float(r[sl][2 * mm]) * fmaf(-tf.x, tf.x, 1.0f);
-                        const float d1 = __uint_as_float(r[sl][2 * mm + 1]) * fmaf(-tf.y, tf.y, 1.0f);
+                        const float d0 = __uint_as_float(r[sl][2 * mm]) * fmaf(-mx * tf.x, tf.x, kx);
+                        const float d1 = __uint_as_float(r[sl][2 * mm + 1]) * fmaf(-mx * tf.y, tf.y, kx);
                         acc[16 * s2 + 2 * mm] = d0;
                         acc[16 * s2 + 2 * mm + 1] = d1;
                         w[mm] = pack_half2(d0, d1);
@@ -1966,40 +1930,79 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
 // ================================================================ weight re-layout
 
 
-// After each Adam step: fp16 copies of the hidden weights in the B-operand block layout
-// (forward: rows = out features; backward-dX: rows = in features), zero padded to WP.
-__global__ void k_tc_refresh(Net net, int WP, int KC, int G, int L, const float *__restrict__ theta,
-                             __half *__restrict__ Wf, __half *__restrict__ WTf, float *__restrict__ W1p,
+// Per-layer scales and fp16 copies of the hidden weights, one block per hidden GEMM g:
+// wexp[g] = ceil(log2(max|W_g| + margin)) - 14, so that |W_g 2^-wexp| <= 2^14 for the whole call
+// (margin = 4 n lr bounds what n Adam steps can add to any weight: |m^/sqrt(v^)| < 4), and
+// fexp[g] = round(log2(|W_g|_F / sqrt(fan_in))) (the typical gain of Delta through the layer, 0 for
+// Xavier weights). Then the B-operand blocks (forward: rows = out features; backward-dX: rows = in
+// features), zero padded to WP. Fixed-order block reductions: deterministic.
+__global__ void __launch_bounds__(512) k_wscale(Net net, int WP, int KC, const float *__restrict__ theta,
+                                                __half *__restrict__ Wf, __half *__restrict__ WTf, DevState *st,
+                                                float margin) {
+    __shared__ float smx[16], sss[16];
+    __shared__ int se;
+    const int g = blockIdx.x, l = g + 1;
+    const int win = net.widths[l], wout = net.widths[l + 1];
+    const float *W = theta + net.woff[l];
+    const int n = win * wout;
+    float mx = 0.0f, ss = 0.0f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float w = W[i];
+        mx = fmaxf(mx, fabsf(w));
+        ss = fmaf(w, w, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if ((threadIdx.x & 31) == 0) { smx[threadIdx.x >> 5] = mx; sss[threadIdx.x >> 5] = ss; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { mx = fmaxf(mx, smx[w]); ss += sss[w]; }
+        int e = 0, f = 0;
+        const float M = mx + margin;
+        if (M > 0.0f && isfinite(M)) {
+            int x;
+            const float m = frexpf(M, &x);             // M = m 2^x, m in [0.5, 1)
+            e = (m == 0.5f ? x - 1 : x) - 14;          // ceil(log2 M) - 14
+        } else if (!isfinite(M)) {
+            e = 100;                                   // non-finite weights: the next loss is non-finite
+        }
+        if (ss > 0.0f && isfinite(ss)) f = (int)rintf(0.5f * log2f(ss / (float)win));
+        st->wexp[g] = e;
+        st->fexp[g] = f;
+        se = e;
+    }
+    __syncthreads();
+    const int e = se;
+    for (int idx = threadIdx.x; idx < WP * WP; idx += blockDim.x) {
+        const int nn = idx / WP, k = idx % WP;     // element (row nn, K index k) of the block set
+        const float vf = (nn < wout && k < win) ? W[(long)nn * win + k] : 0.0f;   // W[nn][k]
+        const float vt = (k < wout && nn < win) ? W[(long)k * win + nn] : 0.0f;   // W^T[nn][k]
+        const size_t blk = ((size_t)g * KC + (k >> 6)) * (size_t)WP * 64;
+        const uint32_t off = (uint32_t)(nn * 64 + ((((k & 63) >> 3) ^ (nn & 7)) << 3) + (k & 7));
+        Wf[blk + off] = __float2half_rn(ldexpf(vf, -e));
+        WTf[blk + off] = __float2half_rn(ldexpf(vt, -e));
+    }
+}
+
+// fp32 operand copies: first layer and biases x 2 log2(e), output layer (zero padded to WP)
+__global__ void k_tc_refresh(Net net, int WP, int L, const float *__restrict__ theta, float *__restrict__ W1p,
                              float *__restrict__ bp, float *__restrict__ Wop) {
-    const long nW = (long)G * WP * WP;
     const long nsmall = 2L * WP + (long)L * WP + WP + 1;
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nW + nsmall; e += (long)gridDim.x * blockDim.x) {
-        if (e < nW) {
-            const int g = (int)(e / ((long)WP * WP));
-            const int rem = (int)(e % ((long)WP * WP));
-            const int n = rem / WP, k = rem % WP;     // element (row n, K index k) of the block set
-            const int l = g + 1;                      // theta layer
-            const int wout = net.widths[l + 1], win = net.widths[l];
-            const float *W = theta + net.woff[l];
-            const float vf = (n < wout && k < win) ? W[(long)n * win + k] : 0.0f;   // W[n][k]
-            const float vt = (k < wout && n < win) ? W[(long)k * win + n] : 0.0f;   // W^T[n][k]
-            const size_t blk = ((size_t)g * KC + (k >> 6)) * (size_t)WP * 64;
-            const uint32_t off = (uint32_t)(n * 64 + ((((k & 63) >> 3) ^ (n & 7)) << 3) + (k & 7));
-            Wf[blk + off] = __float2half_rn(vf);
-            WTf[blk + off] = __float2half_rn(vt);
+    for (long s = (long)blockIdx.x * blockDim.x + threadIdx.x; s < nsmall; s += (long)gridDim.x * blockDim.x) {
+        long e = s;
+        if (e < 2L * WP) {
+            const int r = (int)(e >> 1), d = (int)(e & 1);
+            W1p[e] = r < net.widths[1] ? TANH_C * theta[net.woff[0] + 2 * r + d] : 0.0f;
+        } else if ((e -= 2L * WP) < (long)L * WP) {
+            const int l = (int)(e / WP), r = (int)(e % WP);
+            bp[e] = r < net.widths[l + 1] ? TANH_C * theta[net.boff[l] + r] : 0.0f;
         } else {
-            long s = e - nW;
-            if (s < 2L * WP) {
-                const int r = (int)(s >> 1), d = (int)(s & 1);
-                W1p[s] = r < net.widths[1] ? TANH_C * theta[net.woff[0] + 2 * r + d] : 0.0f;   // fp32, pre-scaled
-            } else if ((s -= 2L * WP) < (long)L * WP) {
-                const int l = (int)(s / WP), r = (int)(s % WP);
-                bp[s] = r < net.widths[l + 1] ? TANH_C * theta[net.boff[l] + r] : 0.0f;        // fp32, pre-scaled
-            } else {
-                s -= (long)L * WP;
-                if (s < WP) Wop[s] = s < net.widths[L] ? theta[net.woff[L] + s] : 0.0f;
-                else Wop[WP] = theta[net.boff[L]];
-            }
+            e -= (long)L * WP;
+            if (e < WP) Wop[e] = e < net.widths[L] ? theta[net.woff[L] + e] : 0.0f;
+            else Wop[WP] = theta[net.boff[L]];
         }
     }
 }
@@ -2051,7 +2054,7 @@ __global__ void k_tc_adam(Net net, int WP, int KC, float *__restrict__ theta, fl
         Wop[i] = th;
     } else {
         const int gg = l - 1;
-        const __half hv = __float2half_rn(th);
+        const __half hv = __float2half_rn(ldexpf(th, -st->wexp[gg]));
         {   // Wf: row n = o, K index k = i
             const size_t blk = ((size_t)gg * KC + (i >> 6)) * (size_t)WP * 64;
             Wf[blk + (uint32_t)(o * 64 + ((((i & 63) >> 3) ^ (o & 7)) << 3) + (i & 7))] = hv;
@@ -2211,28 +2214,33 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
     int nj = 0;
     b.max_count = 0;
     b.groups = 0;
-    auto job = [&](long src, long dst, int count, int nsplit, long stride, int transposed, int cols, int ld) {
+    // lev: the Delta level of the partials (activation layer a = 1..L; Delta_a carries the scale
+    // s 2^-(fexp[a-1] + ... + fexp[G-1])), tsc: one stored activation factor t' = 2^14 t (dW)
+    auto job = [&](long src, long dst, int count, int nsplit, long stride, int transposed, int cols, int ld,
+                   int lev, int tsc) {
         RedJob &j = jobs[nj++];
         j.src = src; j.dst = dst; j.count = count; j.nsplit = nsplit; j.stride = stride;
         j.transposed = transposed; j.cols = cols; j.ld = ld; j.scaled = 1;
+        j.g_lo = lev - 1; j.g_hi = G; j.tsc = tsc;
         if (count > b.max_count) b.max_count = count;
     };
     const int nl = net.nl;
     for (int l = 0; l < nl; ++l) {
         const int win = net.widths[l], wout = net.widths[l + 1];
         if (l == nl - 1) {   // output layer: from k_tc_out_bwd (WP = 64) / the outl launch of k_tc_bwd2
-            job(b.off_ob, net.woff[l], win, b.grid_ob, 2 * WP + 1, 0, 1, 1);
-            job(b.off_ob + 2 * WP, net.boff[l], 1, b.grid_ob, 2 * WP + 1, 0, 1, 1);
+            job(b.off_ob, net.woff[l], win, b.grid_ob, 2 * WP + 1, 0, 1, 1, L, 0);
+            job(b.off_ob + 2 * WP, net.boff[l], 1, b.grid_ob, 2 * WP + 1, 0, 1, 1, L, 0);
             continue;
         }
         // bias of theta layer l <-> Delta_{l+1}: from out_bwd (l = L-1) or dx(g = l); with the chain,
         // layers l >= 1 from the tensor-core sums 1^T Delta_out of GEMM l-1
         if (b.cb_bias && l >= 1)
-            job(b.off_cb + (long)(l - 1) * b.npairs * WP, net.boff[l], wout, b.npairs, WP, 0, 1, 1);
-        else if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1);
-        else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1);
+            job(b.off_cb + (long)(l - 1) * b.npairs * WP, net.boff[l], wout, b.npairs, WP, 0, 1, 1, l + 1, 0);
+        else if (l == L - 1) job(b.off_ob + WP, net.boff[l], wout, b.grid_ob, 2 * WP + 1, 0, 1, 1, l + 1, 0);
+        else job(b.off_dx + (long)l * b.grid_dx * 3 * WP + 2 * WP, net.boff[l], wout, b.grid_dx, 3 * WP, 0, 1, 1,
+                 l + 1, 0);
         if (l == 0) {
-            if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1);
+            if (G > 0) job(b.off_dx, net.woff[0], 2 * wout, b.grid_dx, 3 * WP, 0, 1, 1, 1, 0);
         }
     }
     // hidden-layer weight jobs: with WP >= 128 and a width that is a multiple of 4 they go to the
@@ -2248,7 +2256,7 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
             const bool side = side_ok && WP >= 128 && win % 4 == 0;
             if (side != (pass == 1)) continue;
             job(b.off_dw + (long)(l - 1) * b.npairs * WP * WP, net.woff[l], wout * win, b.npairs, (long)WP * WP, 2,
-                win, WP);
+                win, WP, l + 1, 1);
             b.wside[l - 1] = side;
             b.wjobs[l - 1] = jobs[nj - 1];
         }
@@ -2304,11 +2312,11 @@ void tc_destroy(TcBufs &b) {
     if (b.side) { cudaStreamDestroy(b.side); b.side = nullptr; }
 }
 
-void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s) {
-    const long total = (long)b.G * b.WP * b.WP + 2L * b.WP + (long)b.L * b.WP + b.WP + 1;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 4096) blocks = 4096;
-    k_tc_refresh<<<blocks, 256, 0, s>>>(net, b.WP, b.KC, b.G, b.L, theta, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
+void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, DevState *st, float margin,
+                        cudaStream_t s) {
+    k_wscale<<<b.G, 512, 0, s>>>(net, b.WP, b.KC, theta, b.Wf, b.WTf, st, margin);
+    const long nsmall = 2L * b.WP + (long)b.L * b.WP + b.WP + 1;
+    k_tc_refresh<<<(unsigned)((nsmall + 255) / 256), 256, 0, s>>>(net, b.WP, b.L, theta, b.W1p, b.bp, b.Wop);
 }
 
 template <int WP>
@@ -2316,7 +2324,8 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
     static long long *trace = nullptr;
     const char *te = getenv("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
-    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0, b.tile0 * 128};
+    FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0, b.tile0 * 128,
+              b.st};
     if (te) {
         k_tc_forward<WP><<<b.grid_fwd, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
         cudaStreamSynchronize(s);
@@ -2339,7 +2348,7 @@ template <int WP>
 static void eval_launch(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s) {
     const int ntiles = (npts + 127) / 128;
     const int grid = ntiles < b.nsm ? ntiles : b.nsm;
-    FwdArgs a{net.N, ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, nullptr, out, nullptr, xy, npts, 0};
+    FwdArgs a{net.N, ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, nullptr, out, nullptr, xy, npts, 0, b.st};
     k_tc_forward<WP, true><<<grid, FWD_THREADS, fwd_smem_bytes<WP>(b.L), s>>>(a);
 }
 
@@ -2386,7 +2395,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 cfg.dynamicSmemBytes = BC<WP>::SMEM;
                 BwdcArgs a{net.N, b.ntiles, b.npairs, Sl, g0, b.delta + (size_t)(g0 + 1) * lay, b.act,
                            b.delta + (size_t)(g0 - Sl + 1) * lay, b.ring, b.WTf, b.partial + b.off_dx,
-                           b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr, p0};
+                           b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr, p0, st};
                 static long long *ctrace = nullptr;
                 const char *te = getenv("CRVPINN_CHAIN_TRACE");   // debug: clock64 timeline -> file
                 if (te && g0 == b.G - 1) {
@@ -2433,7 +2442,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
-                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1, p0};
+                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1, p0, g};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");
@@ -2467,7 +2476,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             BwdArgs a{net.N, b.ntiles, g == 0 ? 1 : 0, b.npairs, b.delta + (size_t)(g + 1) * lay,
                       b.act + (size_t)g * lay, b.delta + (size_t)g * lay, b.WTf + (size_t)g * b.KC * WP * 64,
                       b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
-                      b.partial + b.off_dw + (long)g * b.npairs * WP * WP, p0};
+                      b.partial + b.off_dw + (long)g * b.npairs * WP * WP, p0, st, g};
             k_tc_bwd_layer<WP><<<b.grid_dx, TC_THREADS, bwd_smem_bytes<WP>(), s>>>(a);
         }
     }

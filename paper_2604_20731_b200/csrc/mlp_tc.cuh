@@ -41,6 +41,7 @@ struct TcBufs {
     cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr, ev_pre = nullptr, ev_ob = nullptr;
     int outl_side = 0;                     // output-layer sums by k_tc_out_bwd<WP,false> on the side stream
     const float *theta = nullptr;
+    DevState *st = nullptr;                // the context's device state (weight / Delta exponents)
 };
 
 // tile0, ntiles: this shard's MLP tiles [tile0, tile0 + ntiles) of net.P / 128 (the whole set unsharded);
@@ -51,7 +52,10 @@ void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 // the network with cutoff at arbitrary points: out[p] = cutoff(xy[2p], xy[2p+1]) net(...), device pointers
 void tc_eval_points(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s);
 void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
-void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, cudaStream_t s);
+// fp16 copies of the hidden weights with per-layer exponents chosen for the next n Adam steps
+// (margin = 4 n lr; 0 when theta does not change), plus the fp32 operand copies
+void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, DevState *st, float margin,
+                        cudaStream_t s);
 int tc_launches(const Net &net, const TcBufs &b);
 // A8 for the tensor path: Adam + write of the updated operand copies (one launch)
 void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,

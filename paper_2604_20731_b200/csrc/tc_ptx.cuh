@@ -248,21 +248,37 @@ __device__ __forceinline__ f32x2_t fsub2(f32x2_t a, f32x2_t b) {
     return r;
 }
 
-// t = 1 - 2 r for two elements, split t = hi + lo (hi: low 13 mantissa bits cleared, exact in
-// fp16; lo = t - hi exact in fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
+// t' = 2^14 t = 2^14 - 2^15 r for two elements (the activation scale of the tensor path: |t'| < 2^14, so
+// fp16 holds t to 2^-28 before going subnormal), split t' = hi + lo with hi = fp16(t')
+// rounded to nearest (unbiased: the backward's 1 - t^2 and dW use hi) and lo = t' - hi (exact in
+// fp32), packed as fp16x2: hw = {hi0, hi1}, lw = {lo0, lo1}
 __device__ __forceinline__ void finish_pair(float r0, float r1, uint32_t &hw, uint32_t &lw) {
     asm(
-        "{\n\t.reg .f32 t0, t1, h0, h1, l0, l1;\n\t.reg .b32 b0, b1;\n\t"
-        "fma.rn.f32 t0, %2, 0fC0000000, 0f3F800000;\n\t"
-        "fma.rn.f32 t1, %3, 0fC0000000, 0f3F800000;\n\t"
-        "mov.b32 b0, t0;\n\tmov.b32 b1, t1;\n\t"
-        "and.b32 b0, b0, 0xFFFFE000;\n\tand.b32 b1, b1, 0xFFFFE000;\n\t"
-        "mov.b32 h0, b0;\n\tmov.b32 h1, b1;\n\t"
+        "{\n\t.reg .f32 t0, t1, h0, h1, l0, l1;\n\t.reg .b16 a0, a1;\n\t"
+        "fma.rn.f32 t0, %2, 0fC7000000, 0f46800000;\n\t"
+        "fma.rn.f32 t1, %3, 0fC7000000, 0f46800000;\n\t"
+        "cvt.rn.f16x2.f32 %0, t1, t0;\n\t"
+        "mov.b32 {a0, a1}, %0;\n\t"
+        "cvt.f32.f16 h0, a0;\n\tcvt.f32.f16 h1, a1;\n\t"
         "sub.f32 l0, t0, h0;\n\tsub.f32 l1, t1, h1;\n\t"
-        "cvt.rn.f16x2.f32 %0, h1, h0;\n\t"
         "cvt.rn.f16x2.f32 %1, l1, l0;\n\t}"
         : "=r"(hw), "=r"(lw)
         : "f"(r0), "f"(r1));
+}
+
+// the same split from t itself (the forward's accurate-tanh path)
+__device__ __forceinline__ void finish_pair_t(float u0, float u1, uint32_t &hw, uint32_t &lw) {
+    asm(
+        "{\n\t.reg .f32 t0, t1, h0, h1, l0, l1;\n\t.reg .b16 a0, a1;\n\t"
+        "mul.rn.f32 t0, %2, 0f46800000;\n\t"
+        "mul.rn.f32 t1, %3, 0f46800000;\n\t"
+        "cvt.rn.f16x2.f32 %0, t1, t0;\n\t"
+        "mov.b32 {a0, a1}, %0;\n\t"
+        "cvt.f32.f16 h0, a0;\n\tcvt.f32.f16 h1, a1;\n\t"
+        "sub.f32 l0, t0, h0;\n\tsub.f32 l1, t1, h1;\n\t"
+        "cvt.rn.f16x2.f32 %1, l1, l0;\n\t}"
+        : "=r"(hw), "=r"(lw)
+        : "f"(u0), "f"(u1));
 }
 
 // mbarrier wait with a suspend-time hint: the waiting thread sleeps in hardware instead of

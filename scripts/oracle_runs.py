@@ -10,11 +10,8 @@ path. Each sub-command writes one .npz under tests/golden/.
                           <iters> Adam iterations from theta0 (seed 0) or from theta0 moved by one fp32
                           ulp per entry (seed > 0, the recipe of scripts/c3_sensitivity.py)
                           -> C3_run<iters>_s<seed>.npz
-  c3 <seed> <iters> --noise SIGMA
-                          the same with a seeded Gaussian perturbation of the gradient before every
-                          Adam step, g + SIGMA (|g|_2 / sqrt(n)) xi (reading R28: the
-                          oracle driven at a given per-iteration gradient-error level)
-                          -> C3_run<iters>_s<seed>_noise<SIGMA>.npz
+  c3model <seed> <iters>  the same iteration in the 11-bit precision class (oracle/precision_model.py,
+                          DESIGN.md reading R28) -> C3_model11_run<iters>_s<seed>.npz
 """
 import os
 import sys
@@ -59,6 +56,22 @@ def c4sched():
                         threads=oracle.max_threads(), **thetas)
 
 
+def c3model(seed, iters):
+    from oracle.precision_model import PrecisionModel
+    F = W.make_fields("C3")
+    w = F.workload
+    t = time.time()
+    pm = PrecisionModel(w.N, w.widths, F.K, F.S, F.f, ulp_perturbed(F.theta0, seed), lr=w.lr, bits=11)
+    chunks = []
+    for i0 in range(0, iters, 500):
+        chunks.append(pm.train(min(500, iters - i0)))
+        print(f"C3 model11 s{seed}: it {i0 + len(chunks[-1])} loss {chunks[-1][-1]:.6e} ({time.time() - t:.0f}s)",
+              flush=True)
+    name = f"C3_model11_run{iters}_s{seed}.npz"
+    np.savez_compressed(os.path.join(OUT, name), hist=np.concatenate(chunks), seed=seed, bits=11)
+    print(f"wrote {name} ({time.time() - t:.0f}s)", flush=True)
+
+
 def c3(seed, iters, noise):
     F = W.make_fields("C3")
     w = F.workload
@@ -92,6 +105,8 @@ if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "c4sched":
         c4sched()
+    elif cmd == "c3model":
+        c3model(int(sys.argv[2]), int(sys.argv[3]))
     elif cmd == "c3":
         noise = float(sys.argv[sys.argv.index("--noise") + 1]) if "--noise" in sys.argv else 0.0
         c3(int(sys.argv[2]), int(sys.argv[3]), noise)
