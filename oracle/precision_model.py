@@ -33,16 +33,11 @@ from . import Oracle
 
 
 def round_sig(a: np.ndarray, bits: int = 11) -> np.ndarray:
-    """Round to `bits` significant bits (RNE), exponent range unlimited (one power-of-two scale per
-    array keeps every value of interest in fp16's normal range when bits = 11)."""
+    """Round to `bits` significant bits, round-to-nearest-even, at any magnitude (no exponent limits:
+    the operand scales of the class keep fp16 values in range)."""
     a = np.asarray(a, dtype=np.float64)
-    if bits != 11:
-        raise ValueError("only the 11-bit class is modelled")
-    m = np.max(np.abs(a)) if a.size else 0.0
-    if not np.isfinite(m) or m == 0.0:
-        return a.copy()
-    k = 14 - int(np.floor(np.log2(m)))             # max |a| 2^k in [2^14, 2^15)
-    return np.ldexp(np.ldexp(a, k).astype(np.float16).astype(np.float64), -k)
+    m, e = np.frexp(a)                               # a = m 2^e, |m| in [0.5, 1)
+    return np.ldexp(np.rint(np.ldexp(m, bits)), e - bits)
 
 
 class PrecisionModel:

@@ -697,3 +697,41 @@ def test_P19_saturation_step_buoyancy_and_mass():
     assert cy1 > cy0 + 1e-4, (cy0, cy1)
     m1 = o.mass_1d().sum(axis=0)
     assert abs(m1 @ S1 @ m1 - m1 @ S @ m1) <= 1e-4 * (m1 @ S @ m1)   # blob tails reach the zeroed boundary
+
+
+# ------------------------------------------------------------------ P21: the 11-bit precision-class model
+def test_P21_round_sig_is_11_bit_round_to_nearest():
+    """round_sig keeps 11 significant bits with round-to-nearest-even at any magnitude: exact on
+    11-bit values, relative error <= 2^-11 otherwise, ties to even, sign symmetric, idempotent."""
+    from oracle.precision_model import round_sig
+    rng = np.random.default_rng(3)
+    for scale in (1e-9, 1e-3, 1.0, 1e4, 1e9):
+        a = rng.standard_normal(4096) * scale
+        r = round_sig(a)
+        assert np.all(np.abs(r - a) <= 2.0 ** -11 * np.abs(a) * (1 + 1e-12))
+        np.testing.assert_array_equal(round_sig(r), r)
+        np.testing.assert_array_equal(round_sig(-a), -r)
+    m = np.ldexp(np.arange(1024, 2048, dtype=np.float64), -10)     # all 11-bit significands in [1, 2)
+    np.testing.assert_array_equal(round_sig(m), m)
+    x = np.array([2.0, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11])        # ties between 11-bit neighbours
+    np.testing.assert_array_equal(round_sig(x), [2.0, 1.0, 1.0 + 4 * 2.0 ** -11])
+
+
+def test_P21_precision_model_unrounded_is_the_oracle():
+    """With no rounding the model's iteration is the oracle's (its forward and backward are a second,
+    numpy implementation of PAPER.md:373 and the chain rule): gradient to 1e-12, 5-step history."""
+    from oracle.precision_model import PrecisionModel
+    N, widths = 16, (2, 32, 32, 32, 1)
+    K, S, f = W.random_fields(N, 17)
+    th = W.random_theta(widths, 17)
+    pm = PrecisionModel(N, widths, K, S, f, th, bits=None)
+    o = oracle.Oracle(N, widths, K, S, f, th)
+    l, g = pm.loss_grad()
+    rl, rg = o.loss_grad()
+    assert abs(l - rl) <= 1e-13 * abs(rl)
+    assert np.linalg.norm(g - rg) <= 1e-12 * np.linalg.norm(rg)
+    np.testing.assert_allclose(pm.train(5), o.train(5), rtol=1e-11)
+    pm11 = PrecisionModel(N, widths, K, S, f, th, bits=11)
+    l11, g11 = pm11.loss_grad()
+    assert l11 == l                                        # the forward is not rounded
+    assert 0 < np.linalg.norm(g11 - rg) <= 1e-2 * np.linalg.norm(rg)
