@@ -2,6 +2,7 @@
 // Product code only: nothing here is shared with oracle/ (DESIGN.md §1).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <cstdint>
 #include <cstdio>
 
@@ -65,6 +66,68 @@ __device__ __forceinline__ float red_scale(const RedJob &j, const DevState *st) 
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// A8 (Adam; reading R7) fused into the weight-gradient reductions of the tensor path:
+// the thread that finishes gradient entry e updates theta[e], m[e], v[e] and the tensor path's
+// operand copies of that parameter. on = 0: the reductions only write the gradient (loss_grad, the
+// fp32 path, whose Adam is k_adam).
+struct AdamOp {
+    int on;
+    float *theta, *m, *v;
+    DevState *st;
+    float lr, beta1, beta2, eps;
+    Net net;
+    int WP, KC;
+    __half *Wf, *WTf;                 // hidden weights, fp16, 2^-wexp scaled, B-operand block layouts
+    float *W1p, *bp, *Wop;            // first layer / biases (x 2 log2 e) and output layer, fp32
+};
+
+constexpr float ADAM_TANH_C = 2.8853900817779268f;   // 2 log2(e) (the forward's pre-scale of W1 and biases)
+
+__device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk) {
+    DevState *st = A.st;
+    if (st->nonfinite) return;
+    if (!isfinite(gk)) {
+        atomicExch(&st->nonfinite, 1);
+        return;
+    }
+    const float bc1 = (float)st->bc1, bc2 = (float)st->bc2;
+    const float mk = A.beta1 * A.m[e] + (1.0f - A.beta1) * gk;
+    const float vk = A.beta2 * A.v[e] + (1.0f - A.beta2) * gk * gk;
+    A.m[e] = mk;
+    A.v[e] = vk;
+    const float th = A.theta[e] - A.lr * (mk / bc1) / (sqrtf(vk / bc2) + A.eps);
+    A.theta[e] = th;
+    const Net &net = A.net;
+    const int nl = net.nl, L = nl - 1, WP = A.WP, KC = A.KC;
+    int l = 0;
+    while (l + 1 < nl && e >= net.woff[l + 1]) ++l;
+    const int win = net.widths[l];
+    if (e >= net.boff[l]) {   // bias of layer l
+        const int o = (int)(e - net.boff[l]);
+        if (l < L) A.bp[l * WP + o] = ADAM_TANH_C * th;
+        else A.Wop[WP] = th;
+        return;
+    }
+    const long r = e - net.woff[l];
+    const int o = (int)(r / win), i = (int)(r % win);   // W_l[o][i]
+    if (l == 0) {
+        A.W1p[2 * o + i] = ADAM_TANH_C * th;
+    } else if (l == L) {
+        A.Wop[i] = th;
+    } else {
+        const int gg = l - 1;
+        const __half hv = __float2half_rn(ldexpf(th, -st->wexp[gg]));
+        {   // Wf: row n = o, K index k = i
+            const size_t blk = ((size_t)gg * KC + (i >> 6)) * (size_t)WP * 64;
+            A.Wf[blk + (uint32_t)(o * 64 + ((((i & 63) >> 3) ^ (o & 7)) << 3) + (i & 7))] = hv;
+        }
+        {   // WTf: row n = i, K index k = o
+            const size_t blk = ((size_t)gg * KC + (o >> 6)) * (size_t)WP * 64;
+            A.WTf[blk + (uint32_t)(i * 64 + ((((o & 63) >> 3) ^ (i & 7)) << 3) + (o & 7))] = hv;
+        }
+    }
+}
+
 // Programmatic dependent launch (PDL): kernels of the iteration are launched with programmatic
 // stream serialization, so a kernel's CTAs may start (prologue: barrier init, TMEM alloc) while the
 // previous kernel drains; pdl_wait() blocks until the previous grid has completed and its memory
@@ -119,12 +182,15 @@ void launch_rhs(const float *K, const float *S, const float *f, float *b, int N,
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s);
 void launch_begin_call(DevState *st, cudaStream_t s);
+void launch_adam_op(const float *g, long np, const AdamOp &A, cudaStream_t s);
 // total_groups = reduce_groups(host copy of jobs)
 int reduce_groups(const RedJob *jobs, int njobs);
-void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int nsm,
-                        cudaStream_t s);
+// A = nullptr or A->on == 0: gradient only; max_ctas: grid cap of the split-group kernel (launches
+// with the SMs to themselves); -n: n CTAs of the one-thread-per-output kernel, no Adam (beside a GEMM)
+void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int max_ctas,
+                        cudaStream_t s, const AdamOp *A = nullptr);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
-                   const DevState *st, cudaStream_t s);
+                   const DevState *st, cudaStream_t s, const AdamOp *A = nullptr);
 // gram.cu
 struct GramConsts {
     float2 *tw = nullptr;   // FFT twiddles per stage: [hs + pos] = exp(-2 pi i pos / 2hs), 2N entries

@@ -177,6 +177,13 @@ static void launch_forward(crvpinn_ctx *ctx) {
     else simt_forward(ctx->net, ctx->theta, ctx->simt, ctx->u, s);
 }
 
+// A8 on the tensor path after the gradient all-reduce (sharded contexts with a communicator)
+static void tc_adam_after_exchange(crvpinn_ctx *ctx) {
+    const AdamOp A = tc_adam_op(ctx->net, ctx->tc, ctx->theta, ctx->m, ctx->v, ctx->st, (float)ctx->opts.lr,
+                                (float)ctx->opts.beta1, (float)ctx->opts.beta2, (float)ctx->opts.eps);
+    launch_adam_op(ctx->grad, ctx->np, A, ctx->stream);
+}
+
 // fwd = false: u is already in place (crvpinn_shard_backward); xchg: the two all-reduces
 static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool train, cudaEvent_t *ev,
                              bool fwd = true, bool xchg = true) {
@@ -193,16 +200,24 @@ static void launch_iteration(crvpinn_ctx *ctx, double *hist, int n_hist, bool tr
     launch_field_chain(ctx->u, ctx->alpha, ctx->b, ctx->res, ctx->q, gbar, ctx->gu_lat, ctx->loss_part, ctx->gram,
                        net.N, ctx->st, tc ? 1 : 0, hist, n_hist, ctx->opts.beta1, ctx->opts.beta2, train ? 1 : 0, s);
     if (ev) record(ev[2], s);
-    // A6-A7: backward and deterministic weight-gradient reduction
-    if (tc) tc_backward(net, ctx->tc, ctx->st, ctx->grad, s);
-    else simt_backward(net, ctx->plan, ctx->theta, ctx->simt, ctx->grad, s);
+    // A6-A7: backward and deterministic weight-gradient reduction; tensor path: A8 (Adam + the operand
+    // copies) fused into the reductions, unless the gradient is exchanged first (sharded)
+    const bool fuse_adam = tc && train && !ctx->comm;
+    if (tc) {
+        AdamOp A{};
+        if (fuse_adam)
+            A = tc_adam_op(net, ctx->tc, ctx->theta, ctx->m, ctx->v, ctx->st, (float)ctx->opts.lr,
+                           (float)ctx->opts.beta1, (float)ctx->opts.beta2, (float)ctx->opts.eps);
+        tc_backward(net, ctx->tc, ctx->st, ctx->grad, s, &A);
+    } else {
+        simt_backward(net, ctx->plan, ctx->theta, ctx->simt, ctx->grad, s);
+    }
     if (xchg) exchange(ctx, ctx->grad, (size_t)ctx->np);   // each shard holds its points' share
     if (ev) record(ev[3], s);
-    // A8: Adam (+ refresh of the tensor-core weight copies)
-    if (train) {
+    // A8: Adam (fp32 path; tensor path with a communicator: after the gradient exchange)
+    if (train && !fuse_adam) {
         if (tc)
-            tc_adam(net, ctx->tc, ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, (float)ctx->opts.lr,
-                    (float)ctx->opts.beta1, (float)ctx->opts.beta2, (float)ctx->opts.eps, s);
+            tc_adam_after_exchange(ctx);
         else
             launch_adam(ctx->theta, ctx->m, ctx->v, ctx->grad, ctx->np, ctx->st, ctx->st,
                         (float)ctx->opts.lr, (float)ctx->opts.beta1, (float)ctx->opts.beta2,
@@ -215,7 +230,8 @@ static int launches_per_iter(const crvpinn_ctx *ctx) {
     const bool tc = ctx->opts.precision == CRVPINN_PREC_TENSOR;
     int mlp = tc ? tc_launches(ctx->net, ctx->tc) : simt_launches_fwd(ctx->net) + simt_launches_bwd(ctx->net);
     // (sharded: + the memset of u and the two NCCL all-reduce kernels, which are not ours)
-    return mlp + 4 /*residual+DST, tridiagonal, inverse DST+loss, adjoint+loss final*/ + 1 /*adam*/;
+    const bool fused = tc && !ctx->comm;   // tensor path: Adam inside the reductions
+    return mlp + 4 /*residual+DST, tridiagonal, inverse DST+loss, adjoint+loss final*/ + (fused ? 0 : 1) /*adam*/;
 }
 
 static void drop_graphs(crvpinn_ctx *ctx) {

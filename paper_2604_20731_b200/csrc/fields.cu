@@ -72,10 +72,12 @@ __device__ __forceinline__ long red_off(const RedJob &jb, int o) {
 
 __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict__ partial, float *__restrict__ grad,
                                                         const RedJob *__restrict__ jobs, int njobs,
-                                                        const DevState *st) {
+                                                        const DevState *st, AdamOp A) {
     __shared__ float sh[RED_WARPS][33];
     pdl_wait();
     pdl_trigger();
+    // the Adam step counter: one writer (bc1/bc2 of this step were set by the field chain)
+    if (A.on && blockIdx.x == 0 && threadIdx.x == 0 && !A.st->nonfinite) A.st->t = A.st->t + 1;
     int j = 0, g = blockIdx.x;
     while (j < njobs && g >= red_groups(jobs[j])) { g -= red_groups(jobs[j]); ++j; }
     if (j >= njobs) return;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
         }
         for (; z < jb.nsplit; ++z) s += __ldg(src + (long)z * jb.stride);
         grad[jb.dst + o] = s * sc;
+        if (A.on) adam_one(A, jb.dst + o, s * sc);
         return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,18 +122,77 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
         float t = 0.0f;
         for (int w = 0; w < RED_WARPS; ++w) t += sh[w][lane];
         grad[jb.dst + o] = t * sc;
+        if (A.on) adam_one(A, jb.dst + o, t * sc);
     }
 }
 
 // One hidden-layer weight job (transposed == 2 layout with cols == ld, count % 4 == 0) with small
 // blocks and no shared memory: a 64-thread CTA fits next to a k_tc_bwd2 CTA (which leaves ~11K
 // registers and ~1.5 KB of shared memory per SM), so the reduction of GEMM g's dW partials runs on
-// a side stream underneath the backward of GEMM g-1 instead of after the last one. Each thread owns
-// four consecutive outputs (float4 loads, eight splits in flight); same summation order as k_reduce.
+// a side stream underneath the backward of GEMM g-1 instead of after the last one. A warp owns four
+// consecutive float4 outputs (lane & 3) and splits their sums over eight lane groups (lane >> 2:
+// splits sg, sg + 8, ...), all loads of a lane in flight together; the eight group sums are combined
+// by a fixed butterfly and lane group 0 keeps the result: the order depends only on nsplit.
 constexpr int RW_THREADS = 64;
 __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restrict__ partial,
                                                             float *__restrict__ grad, RedJob jb,
-                                                            const DevState *st) {
+                                                            const DevState *st, AdamOp A) {
+    const float sc = red_scale(jb, st);
+    const int n4 = jb.count >> 2;
+    const int lane = threadIdx.x & 31, og = lane & 3, sg = lane >> 2;
+    const int wpb = RW_THREADS / 32;
+    const long st4 = jb.stride >> 2;
+    for (int q0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 4; q0 < n4; q0 += gridDim.x * wpb * 4) {
+        const int q = q0 + og;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < n4) {
+            const float4 *src = reinterpret_cast<const float4 *>(partial + jb.src + red_off(jb, 4 * q));
+            int z = sg;
+            for (; z + 56 < jb.nsplit; z += 64) {   // eight loads in flight per lane
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (long)(z + 8 * u) * st4);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+            }
+            for (; z + 24 < jb.nsplit; z += 32) {
+                float4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (long)(z + 8 * u) * st4);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+            }
+            for (; z < jb.nsplit; z += 8) {
+                const float4 v = __ldg(src + (long)z * st4);
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+        }
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+            s.z += __shfl_xor_sync(0xffffffffu, s.z, off);
+            s.w += __shfl_xor_sync(0xffffffffu, s.w, off);
+        }
+        // lane group 0's sums (one summation order) to lanes (og, sg < 4): lane (og, k) finishes
+        // component k of output float4 og -- 16 lanes share the gradient stores and the Adam updates
+        const int k = sg & 3;
+        const float c0 = __shfl_sync(0xffffffffu, s.x, og), c1 = __shfl_sync(0xffffffffu, s.y, og);
+        const float c2 = __shfl_sync(0xffffffffu, s.z, og), c3 = __shfl_sync(0xffffffffu, s.w, og);
+        if (sg < 4 && q < n4) {
+            const float r = (k == 0 ? c0 : k == 1 ? c1 : k == 2 ? c2 : c3) * sc;
+            const long d = jb.dst + 4 * (long)q + k;
+            grad[d] = r;
+            if (A.on) adam_one(A, d, r);
+        }
+    }
+}
+
+// The same reduction, one thread per float4 output summing all splits in order (8 loads in flight):
+// more outputs per warp in flight, for the launches that run on one CTA per SM beside a backward GEMM
+__global__ void __launch_bounds__(RW_THREADS) k_reduce_wide_seq(const float *__restrict__ partial,
+                                                                float *__restrict__ grad, RedJob jb,
+                                                                const DevState *st) {
     const float sc = red_scale(jb, st);
     const int n4 = jb.count >> 2;
     for (int q = blockIdx.x * RW_THREADS + threadIdx.x; q < n4; q += gridDim.x * RW_THREADS) {
@@ -154,9 +216,19 @@ __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restr
     }
 }
 
-void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int nsm,
-                        cudaStream_t s) {
-    k_reduce_wide<<<nsm, RW_THREADS, 0, s>>>(partial, grad, job, st);
+void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int max_ctas,
+                        cudaStream_t s, const AdamOp *A) {
+    AdamOp a{};
+    if (A) a = *A;
+    if (max_ctas < 0) {   // beside a GEMM: one CTA per SM, no Adam
+        k_reduce_wide_seq<<<-max_ctas, RW_THREADS, 0, s>>>(partial, grad, job, st);
+        return;
+    }
+    const int n4 = job.count >> 2;
+    int grid = (n4 + 4 * (RW_THREADS / 32) - 1) / (4 * (RW_THREADS / 32));
+    if (grid > max_ctas) grid = max_ctas;
+    if (grid < 1) grid = 1;
+    k_reduce_wide<<<grid, RW_THREADS, 0, s>>>(partial, grad, job, st, a);
 }
 
 int reduce_groups(const RedJob *jobs, int njobs) {
@@ -166,8 +238,10 @@ int reduce_groups(const RedJob *jobs, int njobs) {
 }
 
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
-                   const DevState *st, cudaStream_t s) {
-    launch_pdl(k_reduce, dim3(total_groups), dim3(RED_THREADS), 0, s, 1, partial, grad, jobs, njobs, st);
+                   const DevState *st, cudaStream_t s, const AdamOp *A) {
+    AdamOp a{};
+    if (A) a = *A;
+    launch_pdl(k_reduce, dim3(total_groups), dim3(RED_THREADS), 0, s, 1, partial, grad, jobs, njobs, st, a);
 }
 
 // ---------------------------------------------------------------- A8: Adam
@@ -195,6 +269,20 @@ __global__ void k_adam(float *__restrict__ theta, float *__restrict__ m, float *
 void launch_adam(float *theta, float *m, float *v, const float *g, long np, const DevState *st,
                  DevState *st_w, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
     k_adam<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(theta, m, v, g, np, st, st_w, lr, beta1, beta2, eps);
+}
+
+// A8 with an AdamOp over a whole gradient vector (tensor path with a gradient exchange: the update
+// must follow the all-reduce, so it cannot ride on the reductions)
+__global__ void k_adam_op(const float *__restrict__ g, long np, AdamOp A) {
+    const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
+    if (e == 0 && !A.st->nonfinite) A.st->t = A.st->t + 1;
+    if (e < np) adam_one(A, e, g[e]);
+}
+
+void launch_adam_op(const float *g, long np, const AdamOp &A, cudaStream_t s) {
+    launch_pdl(k_adam_op, dim3((unsigned)((np + 255) / 256)), dim3(256), 0, s, 1, g, np, A);
 }
 
 __global__ void k_begin_call(DevState *st) {

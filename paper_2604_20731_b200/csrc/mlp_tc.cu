@@ -1935,7 +1935,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
 // (margin = 4 n lr bounds what n Adam steps can add to any weight: |m^/sqrt(v^)| < 4), and
 // fexp[g] = round(log2(|W_g|_F / sqrt(fan_in))) (the typical gain of Delta through the layer, 0 for
 // Xavier weights). Then the B-operand blocks (forward: rows = out features; backward-dX: rows = in
-// features), zero padded to WP. Fixed-order block reductions: deterministic.
+// features), zero padded to WP. Grid (G, nb): every block of layer g computes the layer's two sums
+// in the same fixed order (identical results), block (g, 0) stores the exponents, and each block
+// writes its 1/nb of the copies.
 __global__ void __launch_bounds__(512) k_wscale(Net net, int WP, int KC, const float *__restrict__ theta,
                                                 __half *__restrict__ Wf, __half *__restrict__ WTf, DevState *st,
                                                 float margin) {
@@ -1945,6 +1947,7 @@ __global__ void __launch_bounds__(512) k_wscale(Net net, int WP, int KC, const f
     const int win = net.widths[l], wout = net.widths[l + 1];
     const float *W = theta + net.woff[l];
     const int n = win * wout;
+    pdl_wait();
     float mx = 0.0f, ss = 0.0f;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const float w = W[i];
@@ -1970,13 +1973,15 @@ __global__ void __launch_bounds__(512) k_wscale(Net net, int WP, int KC, const f
             e = 100;                                   // non-finite weights: the next loss is non-finite
         }
         if (ss > 0.0f && isfinite(ss)) f = (int)rintf(0.5f * log2f(ss / (float)win));
-        st->wexp[g] = e;
-        st->fexp[g] = f;
+        if (blockIdx.y == 0) {
+            st->wexp[g] = e;
+            st->fexp[g] = f;
+        }
         se = e;
     }
     __syncthreads();
     const int e = se;
-    for (int idx = threadIdx.x; idx < WP * WP; idx += blockDim.x) {
+    for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < WP * WP; idx += gridDim.y * blockDim.x) {
         const int nn = idx / WP, k = idx % WP;     // element (row nn, K index k) of the block set
         const float vf = (nn < wout && k < win) ? W[(long)nn * win + k] : 0.0f;   // W[nn][k]
         const float vt = (k < wout && nn < win) ? W[(long)k * win + nn] : 0.0f;   // W^T[nn][k]
@@ -2007,69 +2012,32 @@ __global__ void k_tc_refresh(Net net, int WP, int L, const float *__restrict__ t
     }
 }
 
-// ================================================================ A8: Adam fused with the re-layout
-// One thread per parameter: the Adam update (as k_adam, PAPER.md:830 / reading R7) followed by the
-// write of the new value into the tensor path's operand copies (what k_tc_refresh does for the
-// whole set): hidden weights -> fp16 Wf (rows = out features) and WTf (rows = in features), first
-// layer and biases -> fp32 x 2 log2(e), output layer -> fp32. Padding entries keep the zeros of the
-// initial k_tc_refresh.
-__global__ void k_tc_adam(Net net, int WP, int KC, float *__restrict__ theta, float *__restrict__ m,
-                          float *__restrict__ v, const float *__restrict__ g, long np, DevState *st, float lr,
-                          float beta1, float beta2, float eps, __half *__restrict__ Wf, __half *__restrict__ WTf,
-                          float *__restrict__ W1p, float *__restrict__ bp, float *__restrict__ Wop) {
-    const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+// ================================================================ A8: Adam, fused into the reductions
+// (adam_one in common.cuh: the thread that finishes gradient entry e updates theta[e], m[e], v[e]
+// and the operand copies: hidden weights -> fp16 Wf / WTf with the call's exponent, first layer and
+// biases -> fp32 x 2 log2(e), output layer -> fp32; padding entries keep the refresh's zeros)
+// the hidden-layer weights only (e enumerates W_1 .. W_{L-1} in theta order)
+__global__ void k_tc_adam_hidden(const float *__restrict__ grad, long n, AdamOp A) {
+    long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
     pdl_wait();
     pdl_trigger();
-    if (st->nonfinite) return;
-    const float bc1 = (float)st->bc1, bc2 = (float)st->bc2;
-    if (e == 0) st->t = st->t + 1;   // the only writer of t; other threads read bc1/bc2 only
-    if (e >= np) return;
-    const float gk = g[e];
-    if (!isfinite(gk)) {
-        atomicExch(&st->nonfinite, 1);
-        return;
-    }
-    const float mk = beta1 * m[e] + (1.0f - beta1) * gk;
-    const float vk = beta2 * v[e] + (1.0f - beta2) * gk * gk;
-    m[e] = mk;
-    v[e] = vk;
-    const float th = theta[e] - lr * (mk / bc1) / (sqrtf(vk / bc2) + eps);
-    theta[e] = th;
-    // which layer / slot
-    const int nl = net.nl, L = nl - 1;
-    int l = 0;
-    while (l + 1 < nl && e >= net.woff[l + 1]) ++l;
-    const int win = net.widths[l];
-    if (e >= net.boff[l]) {   // bias of layer l
-        const int o = (int)(e - net.boff[l]);
-        if (l < L) bp[l * WP + o] = TANH_C * th;
-        else Wop[WP] = th;
-        return;
-    }
-    const long r = e - net.woff[l];
-    const int o = (int)(r / win), i = (int)(r % win);   // W_l[o][i]
-    if (l == 0) {
-        W1p[2 * o + i] = TANH_C * th;
-    } else if (l == L) {
-        Wop[i] = th;
-    } else {
-        const int gg = l - 1;
-        const __half hv = __float2half_rn(ldexpf(th, -st->wexp[gg]));
-        {   // Wf: row n = o, K index k = i
-            const size_t blk = ((size_t)gg * KC + (i >> 6)) * (size_t)WP * 64;
-            Wf[blk + (uint32_t)(o * 64 + ((((i & 63) >> 3) ^ (o & 7)) << 3) + (i & 7))] = hv;
-        }
-        {   // WTf: row n = i, K index k = o
-            const size_t blk = ((size_t)gg * KC + (o >> 6)) * (size_t)WP * 64;
-            WTf[blk + (uint32_t)(i * 64 + ((((o & 63) >> 3) ^ (i & 7)) << 3) + (o & 7))] = hv;
-        }
-    }
+    if (e >= n) return;
+    int l = 1;
+    long cnt = (long)A.net.widths[1] * A.net.widths[2];
+    while (e >= cnt) { e -= cnt; ++l; cnt = (long)A.net.widths[l] * A.net.widths[l + 1]; }
+    const long p = A.net.woff[l] + e;
+    adam_one(A, p, grad[p]);
 }
 
-void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
-             DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
-    launch_pdl(k_tc_adam, dim3((unsigned)((np + 255) / 256)), dim3(256), 0, s, 1, net, b.WP, b.KC, theta, m, v, g, np,
-               st, lr, beta1, beta2, eps, b.Wf, b.WTf, b.W1p, b.bp, b.Wop);
+AdamOp tc_adam_op(const Net &net, const TcBufs &b, float *theta, float *m, float *v, DevState *st, float lr,
+                  float beta1, float beta2, float eps) {
+    AdamOp A{};
+    A.on = 1;
+    A.theta = theta; A.m = m; A.v = v; A.st = st;
+    A.lr = lr; A.beta1 = beta1; A.beta2 = beta2; A.eps = eps;
+    A.net = net; A.WP = b.WP; A.KC = b.KC;
+    A.Wf = b.Wf; A.WTf = b.WTf; A.W1p = b.W1p; A.bp = b.bp; A.Wop = b.Wop;
+    return A;
 }
 
 // ================================================================ host side
@@ -2314,7 +2282,7 @@ void tc_destroy(TcBufs &b) {
 
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, DevState *st, float margin,
                         cudaStream_t s) {
-    k_wscale<<<b.G, 512, 0, s>>>(net, b.WP, b.KC, theta, b.Wf, b.WTf, st, margin);
+    launch_pdl(k_wscale, dim3(b.G, 16), dim3(512), 0, s, 1, net, b.WP, b.KC, theta, b.Wf, b.WTf, st, margin);
     const long nsmall = 2L * b.WP + (long)b.L * b.WP + b.WP + 1;
     k_tc_refresh<<<(unsigned)((nsmall + 255) / 256), 256, 0, s>>>(net, b.WP, b.L, theta, b.W1p, b.bp, b.Wop);
 }
@@ -2360,7 +2328,8 @@ void tc_eval_points(const Net &net, const TcBufs &b, const float *xy, int npts, 
 }
 
 template <int WP>
-static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
+static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s,
+                       const AdamOp *A) {
     const size_t lay = (size_t)b.ntiles * b.KC * CHUNK_HALVES;
     const int L = b.L;
     const int p0 = b.tile0 * 128;                    // this shard's first MLP point
@@ -2413,8 +2382,8 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 }
                 cudaEventRecord(b.ev_fork[g0], s);
                 cudaStreamWaitEvent(b.side, b.ev_fork[g0], 0);
-                for (int g = g0; g > g0 - Sl; --g)
-                    if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, b.nsm, b.side);
+                for (int g = g0; g > g0 - Sl; --g)   // after the chain: nothing else to share the SMs with
+                    if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, 4 * b.nsm, b.side, A);
                 g_next = g0 - Sl;
             }
             attr[0].val.clusterDim.x = NS;
@@ -2460,7 +2429,8 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             // dW of GEMM g is final: reduce it on the side stream while GEMM g-1 runs
             cudaEventRecord(b.ev_fork[g], s);
             cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
-            if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, b.nsm, b.side);
+            // (no Adam here: these CTAs share the SMs with the next GEMM; k_tc_adam_hidden after the join)
+            if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, g > 0 ? -b.nsm : 4 * b.nsm, b.side);
             if (te && g == trace_g) {
                 cudaStreamSynchronize(s);
                 static long long h[4096];
@@ -2482,18 +2452,23 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
     }
     if constexpr (WP >= 128) {
         if (b.fuse_outl && b.outl_side) cudaStreamWaitEvent(s, b.ev_ob, 0);
-        launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s);   // column sums, W1, W_out
+        launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s, A);   // column sums, W1, W_out
         cudaEventRecord(b.ev_join, b.side);
         cudaStreamWaitEvent(s, b.ev_join, 0);
+        if (!b.chain && A && A->on) {   // Adam of the hidden weights (their reductions ran beside the GEMMs)
+            long n = 0;
+            for (int l = 1; l < net.nl - 1; ++l) n += (long)net.widths[l] * net.widths[l + 1];
+            launch_pdl(k_tc_adam_hidden, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, grad, n, *A);
+        }
     } else {
-        launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s);
+        launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s, A);
     }
 }
 
-void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s) {
-    if (b.WP == 64) bwd_launch<64>(net, b, st, grad, s);
-    else if (b.WP == 128) bwd_launch<128>(net, b, st, grad, s);
-    else bwd_launch<256>(net, b, st, grad, s);
+void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s, const AdamOp *A) {
+    if (b.WP == 64) bwd_launch<64>(net, b, st, grad, s, A);
+    else if (b.WP == 128) bwd_launch<128>(net, b, st, grad, s, A);
+    else bwd_launch<256>(net, b, st, grad, s, A);
 }
 
 int tc_launches(const Net &net, const TcBufs &b) {
@@ -2510,7 +2485,7 @@ int tc_launches(const Net &net, const TcBufs &b) {
     }
     for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
     return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl || b.outl_side ? 1 : 0) /*out_bwd (sums)*/ + bwd + side +
-           1 /*reduce*/;   // Adam: crvpinn.cu
+           1 /*reduce (+ Adam when training)*/ + (b.WP >= 128 && !b.chain ? 1 : 0) /*hidden-weight Adam*/;
 }
 
 }  // namespace crv

@@ -51,14 +51,16 @@ void tc_destroy(TcBufs &b);   // device buffers, side stream, events
 void tc_forward(const Net &net, const TcBufs &b, float *u, cudaStream_t s);
 // the network with cutoff at arbitrary points: out[p] = cutoff(xy[2p], xy[2p+1]) net(...), device pointers
 void tc_eval_points(const Net &net, const TcBufs &b, const float *xy, int npts, float *out, cudaStream_t s);
-void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s);
+// A6-A7, and with A (A->on) A8: Adam fused into the reductions
+void tc_backward(const Net &net, const TcBufs &b, DevState *st, float *grad, cudaStream_t s,
+                 const AdamOp *A = nullptr);
 // fp16 copies of the hidden weights with per-layer exponents chosen for the next n Adam steps
 // (margin = 4 n lr; 0 when theta does not change), plus the fp32 operand copies
 void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, DevState *st, float margin,
                         cudaStream_t s);
 int tc_launches(const Net &net, const TcBufs &b);
-// A8 for the tensor path: Adam + write of the updated operand copies (one launch)
-void tc_adam(const Net &net, const TcBufs &b, float *theta, float *m, float *v, const float *g, long np,
-             DevState *st, float lr, float beta1, float beta2, float eps, cudaStream_t s);
+// A8 for the tensor path, as an operation of the reductions (Adam + write of the operand copies)
+AdamOp tc_adam_op(const Net &net, const TcBufs &b, float *theta, float *m, float *v, DevState *st, float lr,
+                  float beta1, float beta2, float eps);
 
 }  // namespace crv
