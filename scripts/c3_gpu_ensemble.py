@@ -1,6 +1,6 @@
-"""C3 pretraining (2000 Adam iterations) on the GPU from theta0 and from ulp-perturbed copies
-(same perturbation recipe as scripts/c3_sensitivity.py), both precisions; loss histories ->
-gpurun_out/c3_gpu_ensemble.npz. usage: python scripts/c3_gpu_ensemble.py [n_seeds]"""
+"""C3's schedule on the GPU -- pretraining (2000 Adam iterations) then 10 updates of 100 -- from theta0
+and from ulp-perturbed copies (same perturbation recipe as scripts/c3_sensitivity.py), both precisions;
+loss histories -> gpurun_out/c3_gpu_ensemble.npz. usage: python scripts/c3_gpu_ensemble.py [n_seeds]"""
 import os
 import sys
 
@@ -22,7 +22,7 @@ for prec in (1, 0):
             rng = np.random.default_rng(seed)
             t0 = np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
         g = m.Crvpinn(w.N, w.widths, F.K, F.S, F.f, t0, precision=prec, lr=w.lr)
-        out[f"p{prec}_s{seed}"] = g.pretrain(2000)
+        out[f"p{prec}_s{seed}"] = np.concatenate([g.pretrain(2000)] + [g.step(100) for _ in range(10)])
         g.close()
 np.savez(os.path.join(ROOT, "gpurun_out", "c3_gpu_ensemble.npz"), **out)
 print("done")

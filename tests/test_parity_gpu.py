@@ -175,38 +175,71 @@ def _ulp_perturbed(theta0, seed):
     return np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
 
 
+def _ensemble(pattern, n=5):
+    paths = [os.path.join(GOLDEN, pattern.format(s)) for s in range(n)]
+    missing = [p for p in paths if not os.path.exists(p)]
+    if missing:
+        pytest.skip(f"missing fixtures {missing} (scripts/oracle_runs.py)")
+    return [np.load(p)["hist"] for p in paths]
+
+
 @pytest.mark.parametrize("prec", PRECS)
-def test_c3_pretraining_2000(crv, prec):
-    """C3's pretraining phase (2000 Adam iterations; parity "after pretraining
-    for C3"). Beyond a few hundred iterations the trajectory is chaotic: the oracle itself, started
-    from theta0 moved by one fp32 ulp, leaves its unperturbed run by >2 % at iteration 388 and by up
-    to 59 % later (tests/golden/C3_traj2000_perturbed*.npz; R22). So the check is
-    (a) pointwise over the predictable first 200 iterations (the 100-step tolerance), and
-    (b) statistical afterwards: the mean loss over iterations [900, 1100) and [1800, 2000) of an
-    ensemble (theta0 + 4 ulp-perturbed starts) against the same windows of the oracle's ensemble."""
-    ref = [_golden("C3", "traj2000")["hist"]]
-    for seed in range(1, 5):
-        path = os.path.join(GOLDEN, f"C3_traj2000_perturbed{seed}.npz")
-        if os.path.exists(path):
-            ref.append(np.load(path)["hist"])
-    if len(ref) < 2:
-        pytest.skip("needs >= 1 perturbed oracle run (scripts/c3_sensitivity.py)")
+def test_c3_schedule_pretrain_and_updates(crv, prec):
+    """C3's schedule (BASELINE.json configs[2]; §6 steps 2 and 7): pretraining of
+    2000 Adam iterations, then 10 updates of 100 (fixed S), warm-started -- 3000 iterations in all.
+    After a few hundred iterations the iteration is chaotic (R22: the oracle from theta0
+    moved by one fp32 ulp leaves its own unperturbed run by > 2 % at iteration 388), so:
+    (a) pointwise over the first 200 iterations against the oracle (the 100-step tolerance);
+    (b) ensembles of 5 runs (theta0 + 4 ulp-perturbed starts) on both sides; in each window the mean
+        loss of ours must lie within 2x the reference members' spread (max deviation of a member's
+        window mean from the ensemble mean) of the reference mean. The fp32 path's reference is the
+        oracle ensemble (tests/golden/C3_run3000_s*.npz); the tensor path's is the oracle iteration
+        with an 11-bit (fp16 / TF32 class) backward (oracle/precision_model.py,
+        C3_model11_run3000_s*.npz): reading R28 -- late in C3 the gradient is a sum that cancels to
+        ~1e-3 of its terms, so any 11-bit backward follows a different, noise-driven trajectory, whose
+        window means sit 4-13 % below the exact oracle's (the model reproduces the GPU's offset)."""
     F = W.make_fields("C3")
     w = F.workload
     runs = []
     for seed in range(5):
         th = F.theta0 if seed == 0 else _ulp_perturbed(F.theta0, seed)
         g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, th, precision=prec, lr=w.lr)
-        runs.append(g.pretrain(2000))
+        runs.append(np.concatenate([g.pretrain(w.pretrain)] + [g.step(w.n_adam) for _ in range(w.n_steps)]))
         g.close()
-    hist, rhist = runs[0], ref[0]
+    assert len(runs[0]) == 3000
+    rhist = _golden("C3", "traj2000")["hist"]
+    hist = runs[0]
     assert abs(hist[0] - rhist[0]) <= TOL[prec][0] * abs(rhist[0])
     dev = np.abs(hist[:200] - rhist[:200]) / (np.abs(rhist[:200]) + 1e-3 * np.abs(rhist).max())
     assert dev.max() <= 0.02, (int(dev.argmax()), float(dev.max()))
-    for (a, b), tol in (((900, 1100), 0.10), ((1800, 2000), 0.25)):
+    ref = _ensemble("C3_run3000_s{}.npz" if prec == 1 else "C3_model11_run3000_s{}.npz")
+    for a, b in ((900, 1100), (1800, 2000), (2400, 2600), (2800, 3000)):
         ours = np.mean([r[a:b].mean() for r in runs])
-        theirs = np.mean([r[a:b].mean() for r in ref])
-        assert abs(ours - theirs) <= tol * theirs, ((a, b), ours, theirs)
+        theirs = np.array([r[a:b].mean() for r in ref])
+        spread = np.max(np.abs(theirs - theirs.mean()))
+        assert abs(ours - theirs.mean()) <= 2.0 * spread, ((a, b), ours, theirs.mean(), spread)
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_c4_schedule_10x100(crv, prec):
+    """C4's full schedule (BASELINE.json configs[3]; §6 step 7 on the current S^n):
+    10 time steps of 100 Adam iterations with warm-started weights and Adam state, the saturation
+    front S(t) advanced between steps (crvpinn_set_saturation, step A0), against the oracle's run of
+    the same schedule (tests/golden/C4_sched10x100.npz, scripts/oracle_runs.py c4sched): every
+    step's loss history within the 100-step tolerance, and the loss at the end of every step."""
+    z = _golden("C4", "sched10x100")
+    F = W.make_fields("C4")
+    w = F.workload
+    g = crv.Crvpinn(w.N, w.widths, F.K, F.S_steps[0], F.f, F.theta0, precision=prec, lr=w.lr)
+    for k in range(w.n_steps):
+        if k > 0:
+            g.set_saturation(F.S_steps[k])
+        hist = g.step(w.n_adam)
+        rh = z["hist"][k]
+        assert abs(hist[0] - rh[0]) <= 0.02 * abs(rh[0]), (k, hist[0], rh[0])
+        assert np.all(np.abs(hist - rh) <= 0.02 * np.abs(rh) + 1e-3 * np.abs(rh).max()), k
+        end = g.loss_grad(grad=False)
+        assert abs(end - z["step_end"][k]) <= 0.02 * abs(z["step_end"][k]), (k, end, z["step_end"][k])
 
 
 # ------------------------------------------------------------------ semantics and edge cases
