@@ -129,9 +129,15 @@ __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
 // the multiply in tanh was measured 3-4x less accurate in u on B200 and is not used.)
 // EVAL = true: the same network at arbitrary points a.xy (continuous evaluation, f1 / SPEC.md:493-501):
 // no activations are stored and u[p] = cutoff(x_p, y_p) net(x_p, y_p) for p < npts.
-template <int WP, bool EVAL = false>
-__global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   // 18 warps -> <= 96 regs (5 warps on SMSP 0/1)
+// EW epilogue warps: 16 (one CTA per SM; 18 warps -> <= 96 regs) or 8 (two CTAs per SM at WP <= 128, so
+// that two tiles are in flight per SM: one CTA's epilogue runs while the other's MMAs do)
+template <int EW>
+__host__ __device__ constexpr int fwd_threads() { return 64 + 32 * EW; }
+template <int WP, bool EVAL = false, int EW = FWD_EPI_WARPS>
+__global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forward(FwdArgs a) {
     constexpr int KC = WP / 64;
+    constexpr int WQ = EW / 4;      // epilogue warps per TMEM lane quarter
+    constexpr int SPW = 4 / WQ;     // 16-column slices per warp and 64-column chunk
     constexpr uint32_t WBLK = WP * 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
-        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], FWD_EPI_WARPS);
+        for (int c = 0; c < KC; ++c) mbar_init(&a_full[c], EW);
         for (int i = 0; i < 2 * NQ; ++i) mbar_init(&acc_full[i], 1);
         fence_mbar_init();
     }
@@ -268,13 +274,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
         // 16 of the 64 columns of the current chunk
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int wq = (warp - 2) >> 2;
+        const int wq = (warp - 2) >> 2;                           // slices wq, wq + WQ, ... of each chunk
         const uint32_t t_lane = tmem + ((uint32_t)(q * 32) << 16);
-        const int lg0 = 2 * wq;                                   // logical granules lg0, lg0+1
-        const int pos = (lg0 ^ (row & 7)) & ~1;                   // their 32-byte sector in the row
         const bool swap = (row & 1) != 0;
-        const uint32_t off0 = (uint32_t)(row * 128 + ((lg0 ^ (row & 7)) << 4));
-        const uint32_t off1 = (uint32_t)(row * 128 + (((lg0 + 1) ^ (row & 7)) << 4));
+        // slice sl = 16 columns = logical granules 2 sl, 2 sl + 1: shared-memory offsets and 32-byte sector
+        auto off0 = [&](int sl) { return (uint32_t)(row * 128 + (((2 * sl) ^ (row & 7)) << 4)); };
+        auto off1 = [&](int sl) { return (uint32_t)(row * 128 + (((2 * sl + 1) ^ (row & 7)) << 4)); };
+        auto pos = [&](int sl) { return ((2 * sl) ^ (row & 7)) & ~1; };
         uint32_t acc_ph = 0u;   // bit i: parity of acc_full[i]
         int gi = 0, par = 0;
         const int N = a.N;
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 }
                 const float *bias = sB + (layer - 1) * WP;
                 uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
-                                row * 128 + pos * 16;
+                                row * 128;
                 // TMEM loads run one chunk ahead of the math. t_hi of layers 1..L-1 reaches HBM by a
                 // bulk copy of the released A_hi chunk (issued by the MMA thread), so the epilogue
                 // issues no global stores there and its fence.proxy.async (a MEMBAR.ALL.CTA) does
@@ -334,12 +340,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     need_half1(wq * 16);
                     tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
                 }
+                // work items (chunk c, slice sl = wq + s WQ) in order; TMEM loads run one item ahead
                 // the chunk loop, instantiated for the accurate-tanh layers and for the rest (a uniform
                 // branch per layer, so the common path carries no code of the other)
                 auto chunks = [&](auto EXACT) {
 #pragma unroll
-                for (int c = 0; c < KC; ++c) {
-                    const int cc = c * 64 + wq * 16;
+                for (int it = 0; it < KC * SPW; ++it) {
+                    const int c = it / SPW, sp = it % SPW, sl = wq + sp * WQ;
+                    const int cc = c * 64 + sl * 16;
                     float v[16];
                     if (layer == 1) {
 #pragma unroll
@@ -363,9 +371,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                             upk2(ffma2(pk2(__uint_as_float(rbuf[k + 2]), __uint_as_float(rbuf[k + 3])), C2, pk2(b4.z, b4.w)),
                                  v[k + 2], v[k + 3]);
                         }
-                        if (c + 1 < KC) {
-                            need_half1(cc + 64);
-                            tmem_ld16_async(t_lane + acc + cc + 64, rbuf);
+                        if (it + 1 < KC * SPW) {
+                            const int nc = (it + 1) / SPW * 64 + (wq + (it + 1) % SPW * WQ) * 16;
+                            need_half1(nc);
+                            tmem_ld16_async(t_lane + acc + nc, rbuf);
                         }
                     }
                     // v = 2 log2(e) z; tanh(z) = 1 - 2 / (1 + 2^v) for 16 elements as a skewed pipeline:
@@ -424,16 +433,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                     }
                     if (!last) {
                         const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
-                        st_shared_v4(bh + off0, hw[0], hw[1], hw[2], hw[3]);
-                        st_shared_v4(bh + off1, hw[4], hw[5], hw[6], hw[7]);
-                        st_shared_v4(bl + off0, lw[0], lw[1], lw[2], lw[3]);
-                        st_shared_v4(bl + off1, lw[4], lw[5], lw[6], lw[7]);
-                        // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
-                        if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
-                        if (lane == 0) mbar_arrive(&a_full[c]);
+                        st_shared_v4(bh + off0(sl), hw[0], hw[1], hw[2], hw[3]);
+                        st_shared_v4(bh + off1(sl), hw[4], hw[5], hw[6], hw[7]);
+                        st_shared_v4(bl + off0(sl), lw[0], lw[1], lw[2], lw[3]);
+                        st_shared_v4(bl + off1(sl), lw[4], lw[5], lw[6], lw[7]);
+                        if (sp == SPW - 1) {
+                            // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
+                            fence_proxy_async_smem();
+                            __syncwarp();
+                            if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
+                            if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
+                            if (lane == 0) mbar_arrive(&a_full[c]);
+                        }
                     } else {
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
@@ -441,10 +452,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                             dot = fmaf(w4.x, v[k], fmaf(w4.y, v[k + 1], fmaf(w4.z, v[k + 2], fmaf(w4.w, v[k + 3], dot))));
                         }
                         if constexpr (!EVAL) {
+                            uint8_t *gp = grow + c * CHUNK_BYTES + pos(sl) * 16;
                             if (swap)
-                                st_global_v8(grow + c * CHUNK_BYTES, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
+                                st_global_v8(gp, hw[4], hw[5], hw[6], hw[7], hw[0], hw[1], hw[2], hw[3]);
                             else
-                                st_global_v8(grow + c * CHUNK_BYTES, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+                                st_global_v8(gp, hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
                         }
                     }
                 }
@@ -452,12 +464,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_tc_forward(FwdArgs a) {   //
                 if (sAcc[layer - 1]) chunks(std::true_type{});
                 else chunks(std::false_type{});
             }
-            // output layer: net = W_out t_L + b_out; u = cutoff * net (4 partial dots per row)
+            // output layer: net = W_out t_L + b_out; u = cutoff * net (WQ partial dots per row)
             sRed[(par * 4 + wq) * 128 + row] = dot;
-            named_bar(1, 32 * FWD_EPI_WARPS);
+            named_bar(1, 32 * EW);
             if (wq == 0) {
                 const float *r = sRed + par * 4 * 128 + row;
-                const float net = ((r[0] + r[128]) + (r[256] + r[384])) + sWo[WP];
+                const float net = (WQ == 4 ? ((r[0] + r[128]) + (r[256] + r[384])) : (r[0] + r[128])) + sWo[WP];
                 if constexpr (EVAL) {
                     if (p < a.npts) a.u[p] = cutoff(x, y) * net;
                 } else {
@@ -2044,6 +2056,8 @@ AdamOp tc_adam_op(const Net &net, const TcBufs &b, float *theta, float *m, float
 template <int WP>
 static void set_attrs(int L) {
     cudaFuncSetAttribute(k_tc_forward<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
+    if constexpr (WP <= 128)
+        cudaFuncSetAttribute(k_tc_forward<WP, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     cudaFuncSetAttribute(k_tc_forward<WP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem_bytes<WP>(L));
     if constexpr (WP >= 128) {
         cudaFuncSetAttribute(k_tc_bwd2<WP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, B2<WP, 0>::SMEM);
@@ -2107,7 +2121,9 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
     else set_attrs<256>(L);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    b.grid_fwd = b.ntiles < nsm ? b.ntiles : nsm;
+    // two CTAs (8 epilogue warps each) per SM when there are more tiles than SMs and both fit (WP = 128)
+    b.fwd_ew = (WP == 128 && b.ntiles > nsm && 2 * fwd_smem_bytes<128>(L) <= 228 * 1024) ? 8 : 16;
+    b.grid_fwd = b.ntiles < (b.fwd_ew == 8 ? 2 : 1) * nsm ? b.ntiles : (b.fwd_ew == 8 ? 2 : 1) * nsm;
     {
         // WP >= 128: clusters of NS = WP/128 CTAs (k_tc_bwd2); WP = 64: one CTA per "pair"
         const int NS = WP >= 128 ? WP / 128 : 1;
@@ -2302,6 +2318,13 @@ static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s
         FILE *f = fopen(te, "wb");
         if (f) { fwrite(h, 8, 4096, f); fclose(f); }
         return;
+    }
+    if constexpr (WP <= 128) {
+        if (b.fwd_ew == 8) {
+            launch_pdl(k_tc_forward<WP, false, 8>, dim3(b.grid_fwd), dim3(fwd_threads<8>()), fwd_smem_bytes<WP>(b.L), s,
+                       1, a);
+            return;
+        }
     }
     launch_pdl(k_tc_forward<WP>, dim3(b.grid_fwd), dim3(FWD_THREADS), fwd_smem_bytes<WP>(b.L), s, 1, a);
 }

@@ -28,6 +28,7 @@ struct TcBufs {
     float *partial = nullptr;
     long off_ob = 0, off_dx = 0, off_dw = 0, off_cb = 0;
     int grid_ob = 0, grid_dx = 0, grid_fwd = 0, grid_bwd = 0, npairs = 0;
+    int fwd_ew = 16;                       // forward epilogue warps (8: two CTAs per SM)
     RedJob *jobs = nullptr;  // device copy
     int njobs = 0, max_count = 0, groups = 0;
     int njobs_deep = 0, groups_deep = 0;   // jobs [0, njobs_deep): column sums, W1, W_out (k_reduce)
