@@ -186,7 +186,7 @@ void launch_adam_op(const float *g, long np, const AdamOp &A, cudaStream_t s);
 // total_groups = reduce_groups(host copy of jobs)
 int reduce_groups(const RedJob *jobs, int njobs);
 // A = nullptr or A->on == 0: gradient only; max_ctas: grid cap of the split-group kernel (launches
-// with the SMs to themselves); -n: n CTAs of the one-thread-per-output kernel, no Adam (beside a GEMM)
+// with the SMs to themselves); -n: n CTAs of the one-thread-per-output kernel (beside a GEMM)
 void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, const DevState *st, int max_ctas,
                         cudaStream_t s, const AdamOp *A = nullptr);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,

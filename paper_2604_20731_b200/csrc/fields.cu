@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restr
 // more outputs per warp in flight, for the launches that run on one CTA per SM beside a backward GEMM
 __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide_seq(const float *__restrict__ partial,
                                                                 float *__restrict__ grad, RedJob jb,
-                                                                const DevState *st) {
+                                                                const DevState *st, AdamOp A) {
     const float sc = red_scale(jb, st);
     const int n4 = jb.count >> 2;
     for (int q = blockIdx.x * RW_THREADS + threadIdx.x; q < n4; q += gridDim.x * RW_THREADS) {
@@ -213,6 +213,13 @@ __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide_seq(const float *__r
         }
         float *d = grad + jb.dst + 4 * q;   // dst offsets are not 16-byte aligned in theta
         d[0] = s.x * sc; d[1] = s.y * sc; d[2] = s.z * sc; d[3] = s.w * sc;
+        if (A.on) {
+            const long e = jb.dst + 4 * (long)q;
+            adam_one(A, e, s.x * sc);
+            adam_one(A, e + 1, s.y * sc);
+            adam_one(A, e + 2, s.z * sc);
+            adam_one(A, e + 3, s.w * sc);
+        }
     }
 }
 
@@ -220,8 +227,8 @@ void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, co
                         cudaStream_t s, const AdamOp *A) {
     AdamOp a{};
     if (A) a = *A;
-    if (max_ctas < 0) {   // beside a GEMM: one CTA per SM, no Adam
-        k_reduce_wide_seq<<<-max_ctas, RW_THREADS, 0, s>>>(partial, grad, job, st);
+    if (max_ctas < 0) {   // beside a GEMM: one CTA per SM
+        k_reduce_wide_seq<<<-max_ctas, RW_THREADS, 0, s>>>(partial, grad, job, st, a);
         return;
     }
     const int n4 = job.count >> 2;

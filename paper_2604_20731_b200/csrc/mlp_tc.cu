@@ -2028,19 +2028,6 @@ __global__ void k_tc_refresh(Net net, int WP, int L, const float *__restrict__ t
 // (adam_one in common.cuh: the thread that finishes gradient entry e updates theta[e], m[e], v[e]
 // and the operand copies: hidden weights -> fp16 Wf / WTf with the call's exponent, first layer and
 // biases -> fp32 x 2 log2(e), output layer -> fp32; padding entries keep the refresh's zeros)
-// the hidden-layer weights only (e enumerates W_1 .. W_{L-1} in theta order)
-__global__ void k_tc_adam_hidden(const float *__restrict__ grad, long n, AdamOp A) {
-    long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    pdl_wait();
-    pdl_trigger();
-    if (e >= n) return;
-    int l = 1;
-    long cnt = (long)A.net.widths[1] * A.net.widths[2];
-    while (e >= cnt) { e -= cnt; ++l; cnt = (long)A.net.widths[l] * A.net.widths[l + 1]; }
-    const long p = A.net.woff[l] + e;
-    adam_one(A, p, grad[p]);
-}
-
 AdamOp tc_adam_op(const Net &net, const TcBufs &b, float *theta, float *m, float *v, DevState *st, float lr,
                   float beta1, float beta2, float eps) {
     AdamOp A{};
@@ -2452,8 +2439,8 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             // dW of GEMM g is final: reduce it on the side stream while GEMM g-1 runs
             cudaEventRecord(b.ev_fork[g], s);
             cudaStreamWaitEvent(b.side, b.ev_fork[g], 0);
-            // (no Adam here: these CTAs share the SMs with the next GEMM; k_tc_adam_hidden after the join)
-            if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, g > 0 ? -b.nsm : 4 * b.nsm, b.side);
+            // (g > 0: beside the next GEMM, one small CTA per SM; g = 0: the SMs are free)
+            if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, g > 0 ? -b.nsm : 4 * b.nsm, b.side, A);
             if (te && g == trace_g) {
                 cudaStreamSynchronize(s);
                 static long long h[4096];
@@ -2478,11 +2465,6 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s, A);   // column sums, W1, W_out
         cudaEventRecord(b.ev_join, b.side);
         cudaStreamWaitEvent(s, b.ev_join, 0);
-        if (!b.chain && A && A->on) {   // Adam of the hidden weights (their reductions ran beside the GEMMs)
-            long n = 0;
-            for (int l = 1; l < net.nl - 1; ++l) n += (long)net.widths[l] * net.widths[l + 1];
-            launch_pdl(k_tc_adam_hidden, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, grad, n, *A);
-        }
     } else {
         launch_reduce(b.partial, grad, b.jobs, b.njobs, b.groups, st, s, A);
     }
@@ -2508,7 +2490,7 @@ int tc_launches(const Net &net, const TcBufs &b) {
     }
     for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
     return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl || b.outl_side ? 1 : 0) /*out_bwd (sums)*/ + bwd + side +
-           1 /*reduce (+ Adam when training)*/ + (b.WP >= 128 && !b.chain ? 1 : 0) /*hidden-weight Adam*/;
+           1 /*reduce (+ Adam when training)*/;
 }
 
 }  // namespace crv
