@@ -114,9 +114,12 @@ __device__ __forceinline__ float bwd_k(const DevState *st, int g) { return ldexp
 constexpr int FWD_EPI_WARPS = 16;                       // 4 per TMEM lane quarter
 constexpr int FWD_THREADS = 64 + 32 * FWD_EPI_WARPS;     // producer warp + MMA warp + epilogue
 
+// the forward keeps its activations (A operands) in TMEM; shared memory holds the weight ring
+template <int WP>
+__host__ __device__ constexpr int fwd_nstw() { return WP == 256 ? 4 : (WP == 128 ? 4 : 2); }
 template <int WP>
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int L) {
-    return 1024 + 2 * (WP / 64) * CHUNK_BYTES + NST_W * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128 + 2 * L) * 4 +
+    return 1024 + (WP / 64) * CHUNK_BYTES + fwd_nstw<WP>() * WP * 128 + (2 * WP + L * WP + WP + 1 + 2 * 4 * 128 + 2 * L) * 4 +
            40 * 8 + 16;
 }
 
@@ -141,24 +144,24 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
     constexpr uint32_t WBLK = WP * 128;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *A_hi = smem;
-    uint8_t *A_lo = A_hi + KC * CHUNK_BYTES;
-    uint8_t *Wr = A_lo + KC * CHUNK_BYTES;
-    float *sW1 = (float *)(Wr + NST_W * WBLK);
+    constexpr int NSW = fwd_nstw<WP>();
+    uint8_t *Th = smem;                  // [KC] chunks: t'_hi staging for the bulk copies to HBM
+    uint8_t *Wr = Th + KC * CHUNK_BYTES;
+    float *sW1 = (float *)(Wr + NSW * WBLK);
     float *sB = sW1 + 2 * WP;
     float *sWo = sB + a.L * WP;          // WP + 1 (bias last)
     float *sRed = sWo + WP + 1;          // [2 parity][4][128]
     float *sC = sRed + 2 * 4 * 128;      // [G] epilogue factor of GEMM g: 2 log2(e) 2^(wexp[g] - 14)
     int *sAcc = (int *)(sC + a.L);       // [L] layer l's tanh must be accurate for small |t| (next GEMM's gain >= 16)
     uint64_t *bars = (uint64_t *)(((uintptr_t)(sAcc + a.L) + 7) & ~(uintptr_t)7);
-    uint64_t *w_full = bars, *w_empty = bars + NST_W;
-    uint64_t *a_full = bars + 2 * NST_W;          // [KC]
+    uint64_t *w_full = bars, *w_empty = bars + NSW;
+    uint64_t *a_full = bars + 2 * NSW;            // [KC]
     uint64_t *acc_full = a_full + KC;             // [2 accumulators][NQ N-parts]
     uint32_t *tmem_slot = (uint32_t *)(acc_full + 2 * NQ);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NST_W; ++s) {
+        for (int s = 0; s < NSW; ++s) {
             mbar_init(&w_full[s], 1);
             mbar_init(&w_empty[s], 1);
         }
@@ -194,84 +197,88 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                         mbar_arrive_expect_tx(&w_full[stage], WBLK);
                         bulk_g2s(Wr + stage * WBLK, (const uint8_t *)a.Wf + (size_t)(g * KC + c) * WBLK, WBLK,
                                  &w_full[stage]);
-                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                        if (++stage == NSW) { stage = 0; ph ^= 1; }
                     }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (one thread)
+        // ---------------- MMA issuer (one thread). GEMM gi accumulates into TMEM region (gi & 1) and
+        // takes its A operand (hi/lo activations) from region ((gi + 1) & 1), where the epilogue wrote it
+        // in place of the accumulator it read (16-feature slice k of chunk c: hi in the slice's first 8
+        // columns, lo in the next 8)
         if (lane == 0 && a.G > 0) {
             constexpr uint32_t idesc = idesc_f16(128, WP, 0, 0);
             constexpr uint32_t idesc_h = idesc_f16(128, WP / NQ, 0, 0);
             int stage = 0;
             uint32_t ph = 0, aph = 0;
-            int gi = 0;   // running GEMM counter -> accumulator gi & 1
-            const uint32_t ahi = smem_u32(A_hi), alo = smem_u32(A_lo), wr = smem_u32(Wr);
+            uint32_t dph = 0u;   // bit i: parity of acc_full[i] as seen by this thread
+            int gi = 0;          // running GEMM counter
+            const uint32_t wr = smem_u32(Wr);
             for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
                 for (int g = 0; g < a.G; ++g, ++gi) {
                     const uint32_t acc = tmem + (uint32_t)((gi & 1) * WP);
+                    const uint32_t asrc = tmem + (uint32_t)(((gi + 1) & 1) * WP);
+                    // region (gi & 1) held GEMM gi-1's A operand: its MMAs must be complete before the
+                    // first MMA of GEMM gi overwrites it
+                    if (gi > 0) {
+                        const int pb = ((gi - 1) & 1) * NQ + NQ - 1;
+                        FWD_MMA_WAIT(&acc_full[pb], (dph >> pb) & 1u);
+                    }
+                    if (gi > 0) {
+                        const int pb0 = ((gi - 1) & 1) * NQ;
+                        for (int hh = 0; hh < NQ; ++hh) dph ^= 1u << (pb0 + hh);
+                    }
                     for (int c = 0; c < KC; ++c) {
                         FWD_MMA_WAIT(&a_full[c], aph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 0);
-                        // t_hi chunk c of layer g+1 -> HBM (the backward's operand)
-                        if constexpr (!EVAL) {
+                        if constexpr (!EVAL) {   // t'_hi chunk c of layer g+1 -> HBM
                             bulk_s2g(a.act + ((size_t)g * a.ntiles + tile) * (KC * CHUNK_HALVES) + c * CHUNK_HALVES,
-                                     A_hi + c * CHUNK_BYTES, CHUNK_BYTES);
+                                     Th + c * CHUNK_BYTES, CHUNK_BYTES);
                             bulk_commit();
                         }
                         FWD_MMA_WAIT(&w_full[stage], ph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
-                        if (c + 1 < KC) {
+                        if (c + 1 < KC || !CRV_FWD_NSPLIT) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
-                                uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
-                                uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
-                                mma_f16(acc, dl, bd, idesc, 1u);
+                                const uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
+                                const uint32_t ah = asrc + (uint32_t)(c * 64 + kk * 16);
+                                mma_f16_ts(acc, ah, bd, idesc, (c | kk) != 0);
+                                mma_f16_ts(acc, ah + 8, bd, idesc, 1u);
                             }
-                        } else if (!CRV_FWD_NSPLIT) {
-                            bulk_wait_read0();
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
-                                uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                mma_f16(acc, dh, bd, idesc, (c | kk) != 0);
-                                mma_f16(acc, dl, bd, idesc, 1u);
+                            if (c + 1 == KC) {
+                                if constexpr (!EVAL) bulk_wait_read0();
+                                for (int hh = 0; hh < NQ; ++hh) mma_commit(&acc_full[(gi & 1) * NQ + hh]);
                             }
-                            for (int hh = 0; hh < NQ; ++hh) mma_commit(&acc_full[(gi & 1) * NQ + hh]);
                         } else {
-                            // last K chunk in two N halves, each committed on its own barrier: the
-                            // next epilogue starts on output features [0, WP/2) while the MMAs for
-                            // [WP/2, WP) still run (shortens the per-layer MMA tail by half a chunk)
-                            // -- the HBM copies of this GEMM's A chunks must have been read out
-                            // before the epilogue overwrites A_hi
-                            bulk_wait_read0();
+                            // last K chunk in N parts, each committed on its own barrier: the next
+                            // epilogue starts on the first part while the MMAs for the rest still run
+                            // -- and rewrites the staging chunks, so their HBM copies must have read them
+                            if constexpr (!EVAL) bulk_wait_read0();
 #pragma unroll
                             for (int hh = 0; hh < NQ; ++hh) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk) {
-                                    uint64_t bd = sdesc_sw128(wr + stage * WBLK + hh * (WP / NQ) * 128 + kk * 32, 16, 1024);
-                                    uint64_t dh = sdesc_sw128(ahi + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                    uint64_t dl = sdesc_sw128(alo + c * CHUNK_BYTES + kk * 32, 16, 1024);
-                                    mma_f16(acc + hh * (WP / NQ), dh, bd, idesc_h, (c | kk) != 0);
-                                    mma_f16(acc + hh * (WP / NQ), dl, bd, idesc_h, 1u);
+                                    const uint64_t bd =
+                                        sdesc_sw128(wr + stage * WBLK + hh * (WP / NQ) * 128 + kk * 32, 16, 1024);
+                                    const uint32_t ah = asrc + (uint32_t)(c * 64 + kk * 16);
+                                    mma_f16_ts(acc + hh * (WP / NQ), ah, bd, idesc_h, (c | kk) != 0);
+                                    mma_f16_ts(acc + hh * (WP / NQ), ah + 8, bd, idesc_h, 1u);
                                 }
                                 mma_commit(&acc_full[(gi & 1) * NQ + hh]);
                             }
                         }
                         FTRACE(2048 + (gi * KC + c) * 4 + 2);
                         mma_commit(&w_empty[stage]);
-                        if (++stage == NST_W) { stage = 0; ph ^= 1; }
+                        if (++stage == NSW) { stage = 0; ph ^= 1; }
                     }
                     aph ^= 1;
                 }
             bulk_wait0();
         }
     } else {
-        // ---------------- epilogue: 16 warps; warp % 4 = TMEM lane quarter (rows), wq = which
-        // 16 of the 64 columns of the current chunk
+        // ---------------- epilogue: EW warps; warp % 4 = TMEM lane quarter (rows), wq = which
+        // 16-column slices of each 64-column chunk
         const int q = warp & 3;
         const int row = q * 32 + lane;
         const int wq = (warp - 2) >> 2;                           // slices wq, wq + WQ, ... of each chunk
@@ -301,6 +308,10 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
             for (int layer = 1; layer <= a.L; ++layer) {
                 const bool last = layer == a.L;
                 uint32_t acc = 0;
+                // where this layer's activations go (the A operand of GEMM gi', the next one): region
+                // ((gi' + 1) & 1) -- for layer 1 (gi' = gi) the previous GEMM's region, for layer > 1
+                // (gi' = gi + 1 after the wait) the accumulator region read here, in place
+                uint32_t aout = (uint32_t)(((gi + 1) & 1) * WP);
                 int ab = 0;          // first acc_full barrier of this layer's accumulator
                 uint32_t got = ~0u;  // bit p: output part [p WP/NQ, (p+1) WP/NQ) available
                 if (layer > 1) {
@@ -312,6 +323,7 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                     if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1)) * 16 + (warp - 2));
                     acc_ph ^= 1u << ab;
                     acc = (uint32_t)(ai * WP);
+                    aout = acc;
                     got = 1u;
                     ++gi;
                     tc_fence_after();
@@ -319,10 +331,8 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                 const float *bias = sB + (layer - 1) * WP;
                 uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
                                 row * 128;
-                // TMEM loads run one chunk ahead of the math. t_hi of layers 1..L-1 reaches HBM by a
-                // bulk copy of the released A_hi chunk (issued by the MMA thread), so the epilogue
-                // issues no global stores there and its fence.proxy.async (a MEMBAR.ALL.CTA) does
-                // not wait on any; the last layer stores t_hi from registers.
+                // TMEM loads run one slice ahead of the math; every layer stores t'_hi to HBM from
+                // registers (there is no shared-memory A operand any more, hence no proxy fence).
                 uint32_t rbuf[16];
                 auto need_half1 = [&](int col) {   // wait for the N-part holding column col
                     const int pp = col / (WP / NQ);
@@ -432,14 +442,21 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                     }
                     }
                     if (!last) {
-                        const uint32_t bh = smem_u32(A_hi) + c * CHUNK_BYTES, bl = smem_u32(A_lo) + c * CHUNK_BYTES;
-                        st_shared_v4(bh + off0(sl), hw[0], hw[1], hw[2], hw[3]);
-                        st_shared_v4(bh + off1(sl), hw[4], hw[5], hw[6], hw[7]);
-                        st_shared_v4(bl + off0(sl), lw[0], lw[1], lw[2], lw[3]);
-                        st_shared_v4(bl + off1(sl), lw[4], lw[5], lw[6], lw[7]);
+                        // the next GEMM's A operand, in place of the accumulator slice just read; t'_hi
+                        // also into the staging chunk that the MMA thread bulk-copies to HBM (the
+                        // backward's operand: stores from the epilogue's registers cost ~20 % of the
+                        // forward, the TMA engine does them for free)
+                        tmem_st16(t_lane + aout + (uint32_t)cc, hw, lw);
+                        if constexpr (!EVAL) {
+                            const uint32_t bh = smem_u32(Th) + c * CHUNK_BYTES;
+                            st_shared_v4(bh + off0(sl), hw[0], hw[1], hw[2], hw[3]);
+                            st_shared_v4(bh + off1(sl), hw[4], hw[5], hw[6], hw[7]);
+                        }
                         if (sp == SPW - 1) {
                             // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
-                            fence_proxy_async_smem();
+                            if constexpr (!EVAL) fence_proxy_async_smem();
+                            tmem_wait_st();
+                            tc_fence_before();
                             __syncwarp();
                             if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
                             if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
