@@ -56,6 +56,12 @@ struct RedJob {
     int g_lo, g_hi, tsc;
 };
 
+// several reduction jobs in one launch (kernel parameter)
+struct RedJobSet {
+    RedJob j[CRV_MAX_LAYERS];
+    int n;
+};
+
 // unscale factor of a reduction job (RedJob::scaled)
 __device__ __forceinline__ float red_scale(const RedJob &j, const DevState *st) {
     if (!j.scaled) return 1.0f;
@@ -191,6 +197,9 @@ void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, co
                         cudaStream_t s, const AdamOp *A = nullptr);
 void launch_reduce(const float *partial, float *grad, const RedJob *jobs, int njobs, int total_groups,
                    const DevState *st, cudaStream_t s, const AdamOp *A = nullptr);
+// the split-group kernel over several jobs at once (grid rows = jobs), up to max_ctas CTAs in all
+void launch_reduce_wide_set(const float *partial, float *grad, const RedJobSet &js, const DevState *st,
+                            int max_ctas, cudaStream_t s, const AdamOp *A = nullptr);
 // gram.cu
 struct GramConsts {
     float2 *tw = nullptr;   // FFT twiddles per stage: [hs + pos] = exp(-2 pi i pos / 2hs), 2N entries

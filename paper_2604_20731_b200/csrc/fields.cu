@@ -135,8 +135,9 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
 // by a fixed butterfly and lane group 0 keeps the result: the order depends only on nsplit.
 constexpr int RW_THREADS = 64;
 __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restrict__ partial,
-                                                            float *__restrict__ grad, RedJob jb,
+                                                            float *__restrict__ grad, RedJobSet js,
                                                             const DevState *st, AdamOp A) {
+    const RedJob jb = js.j[blockIdx.y];   // one job per grid row: the jobs of a launch run concurrently
     const float sc = red_scale(jb, st);
     const int n4 = jb.count >> 2;
     const int lane = threadIdx.x & 31, og = lane & 3, sg = lane >> 2;
@@ -231,11 +232,23 @@ void launch_reduce_wide(const float *partial, float *grad, const RedJob &job, co
         k_reduce_wide_seq<<<-max_ctas, RW_THREADS, 0, s>>>(partial, grad, job, st, a);
         return;
     }
-    const int n4 = job.count >> 2;
+    RedJobSet js{};
+    js.j[0] = job;
+    js.n = 1;
+    launch_reduce_wide_set(partial, grad, js, st, max_ctas, s, A);
+}
+
+void launch_reduce_wide_set(const float *partial, float *grad, const RedJobSet &js, const DevState *st,
+                            int max_ctas, cudaStream_t s, const AdamOp *A) {
+    if (js.n < 1) return;
+    AdamOp a{};
+    if (A) a = *A;
+    int n4 = 0;
+    for (int k = 0; k < js.n; ++k) n4 = js.j[k].count / 4 > n4 ? js.j[k].count / 4 : n4;
     int grid = (n4 + 4 * (RW_THREADS / 32) - 1) / (4 * (RW_THREADS / 32));
-    if (grid > max_ctas) grid = max_ctas;
+    if (grid * js.n > max_ctas) grid = max_ctas / js.n;
     if (grid < 1) grid = 1;
-    k_reduce_wide<<<grid, RW_THREADS, 0, s>>>(partial, grad, job, st, a);
+    k_reduce_wide<<<dim3(grid, js.n), RW_THREADS, 0, s>>>(partial, grad, js, st, a);
 }
 
 int reduce_groups(const RedJob *jobs, int njobs) {

@@ -2409,8 +2409,11 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                 }
                 cudaEventRecord(b.ev_fork[g0], s);
                 cudaStreamWaitEvent(b.side, b.ev_fork[g0], 0);
-                for (int g = g0; g > g0 - Sl; --g)   // after the chain: nothing else to share the SMs with
-                    if (b.wside[g]) launch_reduce_wide(b.partial, grad, b.wjobs[g], st, 4 * b.nsm, b.side, A);
+                // after the chain, nothing else shares the SMs: every layer's dW reduction in one launch
+                RedJobSet js{};
+                for (int g = g0; g > g0 - Sl; --g)
+                    if (b.wside[g]) js.j[js.n++] = b.wjobs[g];
+                launch_reduce_wide_set(b.partial, grad, js, st, 8 * b.nsm, b.side, A);
                 g_next = g0 - Sl;
             }
             attr[0].val.clusterDim.x = NS;
@@ -2507,6 +2510,7 @@ int tc_launches(const Net &net, const TcBufs &b) {
         }
     }
     for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
+    if (b.chain) side = bwd;   // one batched reduction launch per chain launch
     return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl || b.outl_side ? 1 : 0) /*out_bwd (sums)*/ + bwd + side +
            1 /*reduce (+ Adam when training)*/;
 }
