@@ -34,7 +34,8 @@ from . import Oracle
 
 def round_sig(a: np.ndarray, bits: int = 11) -> np.ndarray:
     """Round to `bits` significant bits, round-to-nearest-even, at any magnitude (no exponent limits:
-    the operand scales of the class keep fp16 values in range)."""
+    the operand scales of the class keep fp16 values in range, DESIGN.md §6). bits = 11: fp16 / TF32;
+    bits = 24: fp32."""
     a = np.asarray(a, dtype=np.float64)
     m, e = np.frexp(a)                               # a = m 2^e, |m| in [0.5, 1)
     return np.ldexp(np.rint(np.ldexp(m, bits)), e - bits)

@@ -10,8 +10,10 @@ path. Each sub-command writes one .npz under tests/golden/.
                           <iters> Adam iterations from theta0 (seed 0) or from theta0 moved by one fp32
                           ulp per entry (seed > 0, the recipe of scripts/c3_sensitivity.py)
                           -> C3_run<iters>_s<seed>.npz
-  c3model <seed> <iters>  the same iteration in the 11-bit precision class (oracle/precision_model.py,
-                          DESIGN.md reading R28) -> C3_model11_run<iters>_s<seed>.npz
+  c3model <seed> <iters> [--bits B]
+                          the same iteration in the B-bit precision class (default 11: fp16 / TF32;
+                          24: fp32) (oracle/precision_model.py, reading R28)
+                          -> C3_model<B>_run<iters>_s<seed>.npz
 """
 import os
 import sys
@@ -56,19 +58,19 @@ def c4sched():
                         threads=oracle.max_threads(), **thetas)
 
 
-def c3model(seed, iters):
+def c3model(seed, iters, bits=11):
     from oracle.precision_model import PrecisionModel
     F = W.make_fields("C3")
     w = F.workload
     t = time.time()
-    pm = PrecisionModel(w.N, w.widths, F.K, F.S, F.f, ulp_perturbed(F.theta0, seed), lr=w.lr, bits=11)
+    pm = PrecisionModel(w.N, w.widths, F.K, F.S, F.f, ulp_perturbed(F.theta0, seed), lr=w.lr, bits=bits)
     chunks = []
     for i0 in range(0, iters, 500):
         chunks.append(pm.train(min(500, iters - i0)))
-        print(f"C3 model11 s{seed}: it {i0 + len(chunks[-1])} loss {chunks[-1][-1]:.6e} ({time.time() - t:.0f}s)",
+        print(f"C3 model{bits} s{seed}: it {i0 + len(chunks[-1])} loss {chunks[-1][-1]:.6e} ({time.time() - t:.0f}s)",
               flush=True)
-    name = f"C3_model11_run{iters}_s{seed}.npz"
-    np.savez_compressed(os.path.join(OUT, name), hist=np.concatenate(chunks), seed=seed, bits=11)
+    name = f"C3_model{bits}_run{iters}_s{seed}.npz"
+    np.savez_compressed(os.path.join(OUT, name), hist=np.concatenate(chunks), seed=seed, bits=bits)
     print(f"wrote {name} ({time.time() - t:.0f}s)", flush=True)
 
 
@@ -106,7 +108,8 @@ if __name__ == "__main__":
     if cmd == "c4sched":
         c4sched()
     elif cmd == "c3model":
-        c3model(int(sys.argv[2]), int(sys.argv[3]))
+        bits = int(sys.argv[sys.argv.index("--bits") + 1]) if "--bits" in sys.argv else 11
+        c3model(int(sys.argv[2]), int(sys.argv[3]), bits)
     elif cmd == "c3":
         noise = float(sys.argv[sys.argv.index("--noise") + 1]) if "--noise" in sys.argv else 0.0
         c3(int(sys.argv[2]), int(sys.argv[3]), noise)
