@@ -190,14 +190,11 @@ def test_c3_schedule_pretrain_and_updates(crv, prec):
     After a few hundred iterations the iteration is chaotic (R22: the oracle from theta0
     moved by one fp32 ulp leaves its own unperturbed run by > 2 % at iteration 388), so:
     (a) pointwise over the first 200 iterations against the oracle (the 100-step tolerance);
-    (b) ensembles of 5 runs (theta0 + 4 ulp-perturbed starts) on both sides; in each window the mean
-        loss of ours must lie within 2x the reference members' spread (max deviation of a member's
-        window mean from the ensemble mean) of the reference mean. The fp32 path's reference is the
-        oracle ensemble (tests/golden/C3_run3000_s*.npz); the tensor path's is the oracle iteration
-        with an 11-bit (fp16 / TF32 class) backward (oracle/precision_model.py,
-        C3_model11_run3000_s*.npz): reading R28 -- late in C3 the gradient is a sum that cancels to
-        ~1e-3 of its terms, so any 11-bit backward follows a different, noise-driven trajectory, whose
-        window means sit 4-13 % below the exact oracle's (the model reproduces the GPU's offset)."""
+    (b) ensembles of 5 runs (theta0 + 4 ulp-perturbed starts) on both sides against the oracle's
+        (tests/golden/C3_run3000_s*.npz): in each window the two ensemble means must agree within the
+        sum of the two ensembles' spreads (a spread = the largest deviation of a member's window mean
+        from its ensemble's mean), i.e. 2x their average spread (reading R22; R28 for what the tensor
+        path's 11-bit backward does to these statistics)."""
     F = W.make_fields("C3")
     w = F.workload
     runs = []
@@ -212,12 +209,12 @@ def test_c3_schedule_pretrain_and_updates(crv, prec):
     assert abs(hist[0] - rhist[0]) <= TOL[prec][0] * abs(rhist[0])
     dev = np.abs(hist[:200] - rhist[:200]) / (np.abs(rhist[:200]) + 1e-3 * np.abs(rhist).max())
     assert dev.max() <= 0.02, (int(dev.argmax()), float(dev.max()))
-    ref = _ensemble("C3_run3000_s{}.npz" if prec == 1 else "C3_model11_run3000_s{}.npz")
+    ref = _ensemble("C3_run3000_s{}.npz")
     for a, b in ((900, 1100), (1800, 2000), (2400, 2600), (2800, 3000)):
-        ours = np.mean([r[a:b].mean() for r in runs])
+        ours = np.array([r[a:b].mean() for r in runs])
         theirs = np.array([r[a:b].mean() for r in ref])
-        spread = np.max(np.abs(theirs - theirs.mean()))
-        assert abs(ours - theirs.mean()) <= 2.0 * spread, ((a, b), ours, theirs.mean(), spread)
+        band = np.max(np.abs(theirs - theirs.mean())) + np.max(np.abs(ours - ours.mean()))
+        assert abs(ours.mean() - theirs.mean()) <= band, ((a, b), ours.mean(), theirs.mean(), band)
 
 
 @pytest.mark.parametrize("prec", PRECS)
