@@ -88,22 +88,10 @@ struct FwdArgs {
 #define CRV_FWD_NQ 2         // N-parts of the last K chunk, each committed on its own barrier
 #endif
 constexpr int NQ = CRV_FWD_NQ;
-#ifndef CRV_FWD_MMA_SLEEP
-#define CRV_FWD_MMA_SLEEP 1  // MMA-issuer waits suspend (try_wait with a time hint) instead of polling
-#endif
-#ifndef CRV_FWD_EPI_SLEEP
-#define CRV_FWD_EPI_SLEEP 0  // same for the epilogue's accumulator waits
-#endif
-#if CRV_FWD_MMA_SLEEP
+// the MMA issuer's waits suspend (try_wait with a time hint) so they do not take the epilogue warps'
+// issue slots on the shared SMSP; the epilogue's accumulator waits poll
 #define FWD_MMA_WAIT mbar_wait_sleep
-#else
-#define FWD_MMA_WAIT mbar_wait
-#endif
-#if CRV_FWD_EPI_SLEEP
-#define FWD_EPI_WAIT mbar_wait_sleep
-#else
 #define FWD_EPI_WAIT mbar_wait
-#endif
 
 constexpr float TANH_C = 2.8853900817779268f;   // 2 log2(e): tanh(z) = 1 - 2 / (1 + 2^(TANH_C z))
 // activation scale of every fp16 activation operand and stored activation: t' = 2^14 t
@@ -901,41 +889,22 @@ struct Bwd2Args {
     float *part_dw;       // [npairs][WP*WP]   rows = out features
     DevState *st;
     long long *trace;     // debug timeline (CTA 0), nullptr normally
-    float *part_cb;       // [npairs][WP] 1^T Delta_out (CRV_B2_MMA_CS): bias gradient of theta layer g+1
+    float *part_cb;       // unused by k_tc_bwd2 (the chain's 1^T Delta_out partials)
     int outl_sums;        // outl: also reduce dW_out / db_L / db_out (else a side-stream k_tc_out_bwd does)
     int p0;               // first MLP point of this shard (gbar is passed offset by it)
     int g;                // hidden GEMM index (weight / Delta exponents)
 };
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
-#ifndef CRV_B2_MMA_SLEEP
-#define CRV_B2_MMA_SLEEP 0
-#endif
-#if CRV_B2_MMA_SLEEP
-#define B2_MMA_WAIT mbar_wait_sleep
-#else
 #define B2_MMA_WAIT mbar_wait
-#endif
 
 #ifndef CRV_OUTL_H2SUM
 #define CRV_OUTL_H2SUM 1   // output-layer sums: rows of a granule column summed in half2 first
-#endif
-#ifndef CRV_B2_DEEP_DELTA
-#define CRV_B2_DEEP_DELTA 0   // middle and g = 0 launches: Delta ring of 2 tiles, t ring of 1 tile
-#endif
-#ifndef CRV_B2_OUTL_SWAP
-#define CRV_B2_OUTL_SWAP 0   // output-layer launch: early t release instead of the deferred bias sums
-#endif
-#ifndef CRV_B2_EARLY_T_OUTL
-#define CRV_B2_EARLY_T_OUTL 0   // early t release in the fused output-layer launch too
 #endif
 #ifndef CRV_B2_DEFER_FIRST
 #define CRV_B2_DEFER_FIRST 1   // the g = 0 launch defers its x-, y- and bias sums too (its own instantiation)
 #endif
 #ifndef CRV_B2_CS_DEFER
 #define CRV_B2_CS_DEFER 1  // bwd2 bias column sums: one butterfly level per tile, the rest once at the end
-#endif
-#ifndef CRV_B2_MMA_CS
-#define CRV_B2_MMA_CS 0    // bias gradients from a tensor-core 1^T Delta_out (single-buffered dX accumulator)
 #endif
 #ifndef CRV_B2_DX_FIRST
 #define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
@@ -958,12 +927,11 @@ struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch ke
               // with one t slot its transform would wait on Delta chunks queued behind t)
     static constexpr int NS = WP / 128;
     static constexpr int KC = WP / 64;
-    static constexpr bool DEEP = CRV_B2_DEEP_DELTA && (MODE & 1) == 0;
-    static constexpr int DS = KC + (DEEP ? KC : CRV_B2_DSX);   // Delta ring slots (DEEP: 2 tiles)
-    static constexpr int NT = DEEP ? 1 : CRV_B2_NT;           // t ring depth (tiles of 2 chunks)
+    static constexpr int DS = KC + CRV_B2_DSX;   // Delta ring slots
+    static constexpr int NT = CRV_B2_NT;         // t ring depth (tiles of 2 chunks)
     // measured: CRV_B2_DSX = 1 (a 5-slot Delta ring at WP = 256) hangs the launches (like NT = 1 with
     // the output layer fused) -- the ring must hold the tile in flight plus the next pair of chunks
-    static_assert(DEEP || CRV_B2_DSX >= 2, "CRV_B2_DSX < 2 deadlocks k_tc_bwd2");
+    static_assert(CRV_B2_DSX >= 2, "CRV_B2_DSX < 2 deadlocks k_tc_bwd2");
     static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
@@ -973,10 +941,8 @@ struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch ke
 template <int WP, int MODE>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr bool OUTL = (MODE & 1) != 0, FIRST = (MODE & 2) != 0;
-    // the output-layer launch can trade the deferred bias sums for the early t release
-    constexpr bool OUTL_SWAP = MODE == 1 && CRV_B2_OUTL_SWAP;
-    constexpr bool EARLY_T = CRV_B2_EARLY_T && (MODE == 0 || (MODE == 1 && (CRV_B2_EARLY_T_OUTL || OUTL_SWAP)));
-    constexpr bool DEFER_CS = CRV_B2_CS_DEFER && !OUTL_SWAP;
+    constexpr bool EARLY_T = CRV_B2_EARLY_T && MODE == 0;
+    constexpr bool DEFER_CS = CRV_B2_CS_DEFER;
     // with a single t slot the t load must not sit in front of the Delta chunks
     constexpr bool T_FIRST = CRV_T_FIRST && B2<WP, MODE>::NT > 1;
     constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
@@ -1027,8 +993,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t tm_w = tmem + 256;   // dW^T accumulator; dX accumulators at columns 0 / 128
-    [[maybe_unused]] const uint32_t tm_c = tmem + 128;   // CRV_B2_MMA_CS: 1^T Delta_out (dX single-buffered)
-    constexpr int XB = CRV_B2_MMA_CS ? 1 : 2;   // dX accumulator buffers
+    constexpr int XB = 2;   // dX accumulator buffers
 
     if (warp == 0) {
         // ---------------- producer
@@ -1119,17 +1084,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
                         mma_f16(tm_w + h * 128, ad, bd, idesc_w, (k | ks) != 0);
                     }
-#if CRV_B2_MMA_CS
-                    if (h == (int)rank) {   // 1^T Delta_out for this CTA's half of the output features
-                        constexpr uint32_t idesc_c = idesc_f16(128, 128, 0, 1);
-                        const uint64_t d1 = sdesc_none(smem_u32(ones), 0, 0);
-#pragma unroll
-                        for (int ks = 0; ks < 8; ++ks) {
-                            const uint64_t bd = sdesc_sw128(dr + sl * CHUNK_BYTES + ks * 2048, CHUNK_BYTES, 1024);
-                            mma_f16(tm_c, d1, bd, idesc_c, (k | ks) != 0);
-                        }
-                    }
-#endif
                     for (int j = 0; j < 2; ++j) {
                         if (NS == 1) mma_commit(&dempty[sl + j]);
                         else mma_commit_mc(&dempty[sl + j], MASK);
@@ -1323,15 +1277,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             mbar_wait(&xfull[b], (kk / XB) & 1);
             if (warp == 2 && lane == 0) BTRACE(kk * 16 + 5);
             tc_fence_after();
-#if CRV_B2_MMA_CS
-            // single dX buffer: drain it into registers and release it before any math
-            float vall[CPW / 32][32];
-#pragma unroll
-            for (int g2 = 0; g2 < CPW / 32; ++g2) tmem_ld32(tmem + t_lane + (uint32_t)(wq * CPW + g2 * 32), vall[g2]);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&xempty[b]);
-#endif
             // EARLY_T: the dW MMAs of this tile are complete (xfull follows them): take this warp's t
             // values into registers and release the t slot now, so the next-but-one tile's t_in load
             // starts a whole epilogue earlier
@@ -1356,12 +1301,8 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 const int lgb = (col0 & 63) >> 3;        // first logical granule in the chunk
                 const uint32_t tsm = smem_u32(Tr) + (uint32_t)((tb * 2 + hf) * CHUNK_BYTES + row * 128);
                 uint8_t *drow = (uint8_t *)a.din + ((size_t)tile * KC + 2 * rank + hf) * CHUNK_BYTES + row * 128;
-#if CRV_B2_MMA_CS
-                float(&v)[32] = vall[g2];
-#else
                 float v[32];
                 tmem_ld32(tmem + t_lane + (uint32_t)(b * 128 + col0), v);
-#endif
                 uint32_t w[16];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -1416,7 +1357,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         csy[g2] += vy[0];
                     }
                 }
-                if (!CRV_B2_MMA_CS || FIRST) {   // bias sums on the CUDA cores (else: tensor cores)
+                {   // bias sums (CUDA cores)
 #if CRV_B2_CS_DEFER
                     if (DEFER_CS && (!FIRST || DEFER_FIRST)) {
                         level16(v, csd[g2], 1.0f);
@@ -1432,7 +1373,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             __syncwarp();
             if (lane == 0) {
                 if (warp == 2) BTRACE(kk * 16 + 6);
-                if (!CRV_B2_MMA_CS) mbar_arrive(&xempty[b]);
+                mbar_arrive(&xempty[b]);
                 if constexpr (!EARLY_T) mbar_arrive(&tempty[tb]);
             }
         }
@@ -1515,26 +1456,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 }
             }
         }
-#if CRV_B2_MMA_CS
-        // 1^T Delta_out for the own output-feature half: every TMEM row holds the same sums
-        if (q == 0) {
-            float v[32];
-#pragma unroll 1
-            for (int c32 = wq * (128 / EWQ); c32 < (wq + 1) * (128 / EWQ); c32 += 32) {
-                if (nk > 0) {
-                    tmem_ld32(tm_c + t_lane + (uint32_t)c32, v);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                }
-                if (lane == 0) {
-                    float *pc = a.part_cb + (size_t)pair * WP + rank * 128 + c32;
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) pc[e] = v[e];
-                }
-            }
-        }
-#endif
         // dW^T (rows i local = TMEM lanes, columns o) -> part_dw[pair][o][i], coalesced over i
         float *pw = a.part_dw + (size_t)pair * WP * WP + rank * 128 + row;
 #pragma unroll 1
@@ -2168,11 +2089,7 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
         // every stage of the chain
         const char *e = getenv("CRVPINN_FUSE_OUTL");   // tuning knob: fused output-layer backward
         b.fuse_outl = WP >= 128 && !b.chain && !(e && e[0] == '0');
-        // tuning knob (opt-in, measured slower: the sums kernel takes the SMs the first k_tc_bwd2
-        // launch needs, 0.59 vs 0.49 ms): output-layer sums on the side stream
-        const char *os = getenv("CRVPINN_OUTL_SIDE");
-        b.outl_side = b.fuse_outl && os && os[0] == '1';
-        b.grid_ob = WP >= 128 && b.fuse_outl && !b.outl_side ? b.npairs : (b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm);
+        b.grid_ob = WP >= 128 && b.fuse_outl ? b.npairs : (b.ntiles < 2 * nsm ? b.ntiles : 2 * nsm);
         const char *r = getenv("CRVPINN_BWD_REV");     // tuning knob: alternating tile-walk direction
         b.bwd_rev = !(r && r[0] == '0');
     }
@@ -2188,7 +2105,7 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
     b.off_dx = up64(b.off_ob + (long)b.grid_ob * (2 * WP + 1));
     b.off_dw = up64(b.off_dx + (long)(G > 0 ? G : 1) * b.grid_dx * 3 * WP);
     b.off_cb = up64(b.off_dw + (long)(G > 0 ? G * b.npairs : 1) * WP * WP);
-    b.cb_bias = WP >= 128 && (b.chain || CRV_B2_MMA_CS);   // hidden biases from the tensor-core column sums
+    b.cb_bias = WP >= 128 && b.chain;   // hidden biases from the chain's tensor-core column sums
     const long ptotal = b.off_cb + (b.cb_bias ? (long)(G > 0 ? G : 1) * b.npairs * WP : 0);
     if (!al((void **)&b.Wf, wblocks * 2) || !al((void **)&b.WTf, wblocks * 2) ||
         !al((void **)&b.W1p, 2 * WP * 4) || !al((void **)&b.bp, (size_t)L * WP * 4) ||
@@ -2258,8 +2175,7 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
     b.groups_deep = reduce_groups(jobs, b.njobs_deep);
     if (cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&b.ev_pre, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&b.ev_ob, cudaEventDisableTiming) != cudaSuccess) {
+        false) {
         err = "stream/event creation failed";
         return CRVPINN_ECUDA;
     }
@@ -2295,8 +2211,6 @@ void tc_destroy(TcBufs &b) {
     for (auto &e : b.ev_fork)
         if (e) { cudaEventDestroy(e); e = nullptr; }
     if (b.ev_join) { cudaEventDestroy(b.ev_join); b.ev_join = nullptr; }
-    if (b.ev_pre) { cudaEventDestroy(b.ev_pre); b.ev_pre = nullptr; }
-    if (b.ev_ob) { cudaEventDestroy(b.ev_ob); b.ev_ob = nullptr; }
     if (b.side) { cudaStreamDestroy(b.side); b.side = nullptr; }
 }
 
@@ -2420,15 +2334,6 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
             cfg.gridDim = dim3(b.npairs * NS);
             cfg.dynamicSmemBytes = B2<WP>::SMEM;
         }
-        if (b.fuse_outl && b.outl_side && g_next == b.G - 1) {
-            // output-layer gradient sums on the side stream, concurrent with the fused first GEMM
-            cudaEventRecord(b.ev_pre, s);
-            cudaStreamWaitEvent(b.side, b.ev_pre, 0);
-            k_tc_out_bwd<WP, false><<<b.grid_ob, OB_THREADS, 0, b.side>>>(b.ntiles, b.act + (size_t)(L - 1) * lay,
-                                                                          gbar, b.Wop, nullptr,
-                                                                          b.partial + b.off_ob, st);
-            cudaEventRecord(b.ev_ob, b.side);   // the deep reduction below reads these sums
-        }
         for (int g = g_next; g >= 0; --g) {
             const bool outl = g == b.G - 1 && b.fuse_outl;
             // Launches alternate the direction of their tile walk, starting backwards: the forward
@@ -2441,7 +2346,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        gbar, b.Wop, b.partial + b.off_ob,
                        b.partial + b.off_dx + (long)g * b.grid_dx * 3 * WP,
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
-                       b.partial + b.off_cb + (long)g * b.npairs * WP, b.outl_side ? 0 : 1, p0, g};
+                       b.partial + b.off_cb + (long)g * b.npairs * WP, 1, p0, g};
             static long long *trace = nullptr;
             const char *te = getenv("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");
@@ -2482,7 +2387,6 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
         }
     }
     if constexpr (WP >= 128) {
-        if (b.fuse_outl && b.outl_side) cudaStreamWaitEvent(s, b.ev_ob, 0);
         launch_reduce(b.partial, grad, b.jobs, b.njobs_deep, b.groups_deep, st, s, A);   // column sums, W1, W_out
         cudaEventRecord(b.ev_join, b.side);
         cudaStreamWaitEvent(s, b.ev_join, 0);
@@ -2511,7 +2415,7 @@ int tc_launches(const Net &net, const TcBufs &b) {
     }
     for (int g = 0; g < G; ++g) side += b.wside[g] ? 1 : 0;
     if (b.chain) side = bwd;   // one batched reduction launch per chain launch
-    return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl || b.outl_side ? 1 : 0) /*out_bwd (sums)*/ + bwd + side +
+    return 1 /*fwd*/ + (b.WP < 128 || !b.fuse_outl ? 1 : 0) /*out_bwd*/ + bwd + side +
            1 /*reduce (+ Adam when training)*/;
 }
 

@@ -39,8 +39,7 @@ struct TcBufs {
     int cb_bias = 0;                       // hidden-layer bias gradients from the 1^T Delta partials (off_cb)
     __half *ring = nullptr;                // its per-cluster Delta rings between stages
     cudaStream_t side = nullptr;           // side stream of the per-layer weight reductions
-    cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr, ev_pre = nullptr, ev_ob = nullptr;
-    int outl_side = 0;                     // output-layer sums by k_tc_out_bwd<WP,false> on the side stream
+    cudaEvent_t ev_fork[CRV_MAX_LAYERS] = {}, ev_join = nullptr;
     const float *theta = nullptr;
     DevState *st = nullptr;                // the context's device state (weight / Delta exponents)
 };
