@@ -163,7 +163,10 @@ int crvpinn_direct_solve(crvpinn_ctx *ctx, double rtol, int max_iter, float *u_o
 int crvpinn_loss_grad(crvpinn_ctx *ctx, double *loss, float *grad);
 
 /* Intermediates of the last crvpinn_loss_grad (test hook, host float32; each nullable):
- * u (N+1)^2 lattice, res (N-1)^2, q (N-1)^2, gu (N+1)^2 lattice = dLOSS/du (0 on boundary). */
+ * u (N+1)^2 lattice, res (N-1)^2, q (N-1)^2, gu (N+1)^2 lattice = dLOSS/du (0 on boundary).
+ * On a sharded context without a communicator (caller exchange) they are those of the last
+ * crvpinn_shard_forward / _backward: u as this rank's forward left it (its own points only)
+ * unless _backward has since received the summed u. Never fails on a valid ctx. */
 int crvpinn_get_intermediates(crvpinn_ctx *ctx, float *u, float *res, float *q, float *gu);
 
 size_t crvpinn_num_params(const crvpinn_ctx *ctx);
