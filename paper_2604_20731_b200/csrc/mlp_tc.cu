@@ -1199,6 +1199,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             if (OUTL && k < nk) {
                 // Delta_L = s gbar W_out (.) (1 - t_L^2), in place in this CTA's copy of the ring
                 const int tile = pair + (a.rev ? nk - 1 - k : k) * a.npairs;
+                if (warp == 2 && lane == 0) BTRACE(k * 16 + 12);
                 float g[ORM];
                 __half2 g2[ORM];
 #pragma unroll
@@ -1263,7 +1264,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 #endif
                     fence_proxy_async_smem();
                     mbar_arrive(&dready[slot]);   // count = B2_EPI_THREADS
+                    if (warp == 2 && lane == 0 && j == 0) BTRACE(k * 16 + 13);
                 }
+                if (warp == 2 && lane == 0) BTRACE(k * 16 + 14);
                 dn += KC;
             }
             if (k == 0) continue;
