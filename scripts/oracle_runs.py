@@ -6,6 +6,8 @@ path. Each sub-command writes one .npz under tests/golden/.
   c4sched                 C4's full schedule (§6 step 7; BASELINE.json configs[3]):
                           10 time steps x 100 Adam iterations, warm-started weights and Adam state,
                           S advanced between steps (S_steps[k] for step k) -> C4_sched10x100.npz
+  c5sched [steps]         the same for C5 (configs[4]), the first [steps] time steps (the fixture is
+                          rewritten after every step: steps_done) -> C5_sched.npz
   c3 <seed> <iters>       C3's pretraining + updates with fixed S (configs[2]):
                           <iters> Adam iterations from theta0 (seed 0) or from theta0 moved by one fp32
                           ulp per entry (seed > 0, the recipe of scripts/c3_sensitivity.py)
@@ -37,25 +39,30 @@ def ulp_perturbed(theta0, seed):
     return np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
 
 
-def c4sched():
-    F = W.make_fields("C4")
+def sched(name="C4", max_steps=None):
+    """name's schedule (C4: all 10 steps -> C4_sched10x100.npz; C5: the first max_steps of its 10,
+    rewritten after every step so a partial run is usable -> C5_sched.npz with steps_done)"""
+    F = W.make_fields(name)
     w = F.workload
+    n = w.n_steps if max_steps is None else min(max_steps, w.n_steps)
     t = time.time()
     o = oracle.Oracle(w.N, w.widths, F.K, F.S_steps[0], F.f, F.theta0, lr=w.lr)
-    hist = np.zeros((w.n_steps, w.n_adam))
-    step_end = np.zeros(w.n_steps)
+    hist = np.zeros((n, w.n_adam))
+    step_end = np.zeros(n)
     thetas = {}
-    for k in range(w.n_steps):
+    fname = "C4_sched10x100.npz" if name == "C4" else f"{name}_sched.npz"
+    for k in range(n):
         if k > 0:
             o.set_saturation(F.S_steps[k])
         hist[k] = o.train(w.n_adam)
         step_end[k] = o.loss_grad()[0]      # LOSS(theta after step k) on S_steps[k]
         if k in (0, w.n_steps - 1):
             thetas[f"theta_step{k + 1}"] = o.theta.astype(np.float32)
-        print(f"C4 step {k + 1}: {hist[k, 0]:.6e} -> {hist[k, -1]:.6e} end {step_end[k]:.6e} "
+        print(f"{name} step {k + 1}: {hist[k, 0]:.6e} -> {hist[k, -1]:.6e} end {step_end[k]:.6e} "
               f"({time.time() - t:.0f}s)", flush=True)
-    np.savez_compressed(os.path.join(OUT, "C4_sched10x100.npz"), hist=hist, step_end=step_end,
-                        threads=oracle.max_threads(), **thetas)
+        if name != "C4" or k == n - 1:
+            np.savez_compressed(os.path.join(OUT, fname), hist=hist[:k + 1], step_end=step_end[:k + 1],
+                                steps_done=k + 1, threads=oracle.max_threads(), **thetas)
 
 
 def c3model(seed, iters, bits=11):
@@ -106,7 +113,9 @@ def c3(seed, iters, noise):
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "c4sched":
-        c4sched()
+        sched("C4")
+    elif cmd == "c5sched":
+        sched("C5", int(sys.argv[2]) if len(sys.argv) > 2 else None)
     elif cmd == "c3model":
         bits = int(sys.argv[sys.argv.index("--bits") + 1]) if "--bits" in sys.argv else 11
         c3model(int(sys.argv[2]), int(sys.argv[3]), bits)

@@ -239,6 +239,28 @@ def test_c4_schedule_10x100(crv, prec):
         assert abs(end - z["step_end"][k]) <= 0.02 * abs(z["step_end"][k]), (k, end, z["step_end"][k])
 
 
+@pytest.mark.parametrize("prec", PRECS)
+def test_c5_schedule(crv, prec):
+    """C5's schedule (BASELINE.json configs[4]: 10 time steps of 100 Adam iterations on the fixed
+    S of the t = 10 front; §6 step 7 with warm-started weights and Adam state),
+    the time steps the oracle fixture holds (tests/golden/C5_sched.npz, scripts/oracle_runs.py
+    c5sched: ~1 h of 8-core fp64 per step, `steps_done` of the 10): the same per-step bounds as
+    C4's schedule test."""
+    z = _golden("C5", "sched")
+    F = W.make_fields("C5")
+    w = F.workload
+    n = int(z["steps_done"])
+    assert n >= 2, n
+    g = crv.Crvpinn(w.N, w.widths, F.K, F.S, F.f, F.theta0, precision=prec, lr=w.lr)
+    for k in range(n):
+        hist = g.step(w.n_adam)
+        rh = z["hist"][k]
+        assert abs(hist[0] - rh[0]) <= 0.02 * abs(rh[0]), (k, hist[0], rh[0])
+        assert np.all(np.abs(hist - rh) <= 0.02 * np.abs(rh) + 1e-3 * np.abs(rh).max()), k
+        end = g.loss_grad(grad=False)
+        assert abs(end - z["step_end"][k]) <= 0.02 * abs(z["step_end"][k]), (k, end, z["step_end"][k])
+
+
 # ------------------------------------------------------------------ semantics and edge cases
 def test_step_composition_and_determinism(crv):
     """step(30)+step(70) == step(100) bitwise (Adam state persists, R8); runs are deterministic."""
