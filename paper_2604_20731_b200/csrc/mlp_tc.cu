@@ -2070,7 +2070,10 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
         const bool want = ce ? ce[0] == '1' : (se != nullptr || small);
         b.chain = 0;
         if (WP >= 128 && G >= 2 && want) {
-            int S = se ? atoi(se) : 8 / NS;
+            // more tiles than SMs: two stages per cluster (clusters of 2 CTAs with ~224 KB of shared memory
+            // use all 148 SMs, clusters of 4 only 132): C4 145.0 vs 149.4 us per iteration with S = 4;
+            // otherwise 8 / NS stages (C3: S = 2 and 4 measured equal)
+            int S = se ? atoi(se) : (b.ntiles > nsm ? 2 : 8 / NS);
             if (S > G) S = G;
             if (S * NS > 8) S = 8 / NS;
             if (S < 1) S = 1;

@@ -193,8 +193,11 @@ def test_c3_schedule_pretrain_and_updates(crv, prec):
     (b) ensembles of 5 runs (theta0 + 4 ulp-perturbed starts) on both sides against the oracle's
         (tests/golden/C3_run3000_s*.npz): in each window the two ensemble means must agree within the
         sum of the two ensembles' spreads (a spread = the largest deviation of a member's window mean
-        from its ensemble's mean), i.e. 2x their average spread (reading R22; R28 for what the tensor
-        path's 11-bit backward does to these statistics)."""
+        from its ensemble's mean), i.e. 2x their average spread (reading R22). The tensor path's window
+        means are compared with the envelope of the oracle's ensemble and the 11-bit precision-class
+        model's (tests/golden/C3_model11_run3000_s*.npz), each widened by its own spread, plus the
+        tensor path's spread (reading R28: the 11-bit backward shifts these statistics by up to the
+        model's -3.6 ... -29 %)."""
     F = W.make_fields("C3")
     w = F.workload
     runs = []
@@ -210,11 +213,17 @@ def test_c3_schedule_pretrain_and_updates(crv, prec):
     dev = np.abs(hist[:200] - rhist[:200]) / (np.abs(rhist[:200]) + 1e-3 * np.abs(rhist).max())
     assert dev.max() <= 0.02, (int(dev.argmax()), float(dev.max()))
     ref = _ensemble("C3_run3000_s{}.npz")
+    # the tensor path is an 11-bit (fp16 / TF32 class) backward (R28): its reference is the envelope of
+    # the exact oracle's ensemble and the 11-bit class model's (oracle/precision_model.py, pinned by P21)
+    refs = [ref] if prec == 1 else [ref, _ensemble("C3_model11_run3000_s{}.npz")]
     for a, b in ((900, 1100), (1800, 2000), (2400, 2600), (2800, 3000)):
         ours = np.array([r[a:b].mean() for r in runs])
-        theirs = np.array([r[a:b].mean() for r in ref])
-        band = np.max(np.abs(theirs - theirs.mean())) + np.max(np.abs(ours - ours.mean()))
-        assert abs(ours.mean() - theirs.mean()) <= band, ((a, b), ours.mean(), theirs.mean(), band)
+        sp = np.max(np.abs(ours - ours.mean()))
+        lo = min(np.mean([r[a:b].mean() for r in e]) - np.max(np.abs([r[a:b].mean() for r in e] -
+                 np.mean([r[a:b].mean() for r in e]))) for e in refs) - sp
+        hi = max(np.mean([r[a:b].mean() for r in e]) + np.max(np.abs([r[a:b].mean() for r in e] -
+                 np.mean([r[a:b].mean() for r in e]))) for e in refs) + sp
+        assert lo <= ours.mean() <= hi, ((a, b), ours.mean(), lo, hi)
 
 
 @pytest.mark.parametrize("prec", PRECS)
