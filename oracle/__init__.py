@@ -19,6 +19,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "crvpinn_oracle.c")
 _SRC_IGA = os.path.join(_HERE, "iga_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_SRC_ABI = os.path.join(_HERE, "crvpinn_abi.c")
+LIB_ABI = os.path.join(_HERE, "liboracle_abi.so")   # the oracle behind the product's C ABI (tests only)
 
 MOBILITY_RATIO = 25.35 / 3.95   # Table 1
 DENSITY_RATIO = 479.0 / 1045.0   # rho_g / rho_w, Table 1
@@ -29,6 +31,10 @@ def build(force: bool = False) -> str:
     if (force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC)
             or os.path.getmtime(_LIB) < os.path.getmtime(_SRC_IGA)):
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, _SRC_IGA, "-lm"])
+    if (force or not os.path.exists(LIB_ABI) or os.path.getmtime(LIB_ABI) < os.path.getmtime(_SRC)
+            or os.path.getmtime(LIB_ABI) < os.path.getmtime(_SRC_ABI)):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-fvisibility=default", "-o", LIB_ABI,
+                               _SRC, _SRC_ABI, "-lm"])
     return _LIB
 
 

@@ -290,6 +290,9 @@ void orc_set_theta(orc_ctx *c, const double *th) { memcpy(c->theta, th, sizeof(d
 void orc_get_adam(const orc_ctx *c, double *m, double *v, long *t) {
     memcpy(m, c->m, sizeof(double) * c->np); memcpy(v, c->v, sizeof(double) * c->np); *t = c->t;
 }
+void orc_set_adam(orc_ctx *c, const double *m, const double *v, long t) {
+    memcpy(c->m, m, sizeof(double) * c->np); memcpy(c->v, v, sizeof(double) * c->np); c->t = t;
+}
 void orc_get_alpha(const orc_ctx *c, double *a) {
     memcpy(a, c->alpha, sizeof(double) * (c->N + 1) * (c->N + 1));
 }
