@@ -23,12 +23,6 @@
 #include <math.h>
 #include <cstdlib>
 #include <type_traits>
-#ifndef CRV_B2_DSX
-#define CRV_B2_DSX 2
-#endif
-#ifndef CRV_B2_NT
-#define CRV_B2_NT 2
-#endif
 
 namespace crv {
 
@@ -81,13 +75,7 @@ struct FwdArgs {
 
 
 
-#ifndef CRV_FWD_NSPLIT
-#define CRV_FWD_NSPLIT 1     // last K chunk of each GEMM issued and committed in two N halves
-#endif
-#ifndef CRV_FWD_NQ
-#define CRV_FWD_NQ 2         // N-parts of the last K chunk, each committed on its own barrier
-#endif
-constexpr int NQ = CRV_FWD_NQ;
+constexpr int NQ = 2;   // N-parts of the last K chunk of each GEMM, each committed on its own barrier
 // the MMA issuer's waits suspend (try_wait with a time hint) so they do not take the epilogue warps'
 // issue slots on the shared SMSP; the epilogue's accumulator waits poll
 #define FWD_MMA_WAIT mbar_wait_sleep
@@ -226,7 +214,7 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                         FWD_MMA_WAIT(&w_full[stage], ph);
                         FTRACE(2048 + (gi * KC + c) * 4 + 1);
                         tc_fence_after();
-                        if (c + 1 < KC || !CRV_FWD_NSPLIT) {
+                        if (c + 1 < KC) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 const uint64_t bd = sdesc_sw128(wr + stage * WBLK + kk * 32, 16, 1024);
@@ -897,28 +885,7 @@ struct Bwd2Args {
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
 #define B2_MMA_WAIT mbar_wait
 
-#ifndef CRV_OUTL_H2SUM
-#define CRV_OUTL_H2SUM 1   // output-layer sums: rows of a granule column summed in half2 first
-#endif
-#ifndef CRV_B2_DEFER_FIRST
-#define CRV_B2_DEFER_FIRST 1   // the g = 0 launch defers its x-, y- and bias sums too (its own instantiation)
-#endif
-#ifndef CRV_B2_CS_DEFER
-#define CRV_B2_CS_DEFER 1  // bwd2 bias column sums: one butterfly level per tile, the rest once at the end
-#endif
-#ifndef CRV_B2_DX_FIRST
-#define CRV_B2_DX_FIRST 1  // bwd2 MMA order: all dX chunk pairs, commit, then the dW halves
-#endif
-#ifndef CRV_B2_EARLY_T
-#define CRV_B2_EARLY_T 1   // bwd2 (middle GEMMs only) releases the t slot right after xfull (t values in registers)
-#endif
-#ifndef CRV_T_FIRST
-#define CRV_T_FIRST 1   // backward producers issue a tile's t_in load before its Delta chunks
-#endif
-#ifndef CRV_B2_EPI_WARPS
-#define CRV_B2_EPI_WARPS 8
-#endif
-constexpr int B2_EPI_WARPS = CRV_B2_EPI_WARPS;    // 8 or 16 (4 per TMEM lane quarter)
+constexpr int B2_EPI_WARPS = 8;    // 2 per TMEM lane quarter
 constexpr int B2_EPI_THREADS = 32 * B2_EPI_WARPS;
 constexpr int B2_THREADS = 64 + B2_EPI_THREADS;
 
@@ -927,11 +894,10 @@ struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch ke
               // with one t slot its transform would wait on Delta chunks queued behind t)
     static constexpr int NS = WP / 128;
     static constexpr int KC = WP / 64;
-    static constexpr int DS = KC + CRV_B2_DSX;   // Delta ring slots
-    static constexpr int NT = CRV_B2_NT;         // t ring depth (tiles of 2 chunks)
-    // measured: CRV_B2_DSX = 1 (a 5-slot Delta ring at WP = 256) hangs the launches (like NT = 1 with
-    // the output layer fused) -- the ring must hold the tile in flight plus the next pair of chunks
-    static_assert(CRV_B2_DSX >= 2, "CRV_B2_DSX < 2 deadlocks k_tc_bwd2");
+    // Delta ring slots: a tile in flight plus the next pair of chunks (measured: one slot fewer -- 5 at
+    // WP = 256 -- hangs the launches, like a single t slot with the output layer fused)
+    static constexpr int DS = KC + 2;
+    static constexpr int NT = 2;                 // t ring depth (tiles of 2 chunks)
     static constexpr uint32_t SMEM = 1024 + (uint32_t)(KC + DS + 2 * NT) * CHUNK_BYTES + 256 + 64 * 8;   // + ones
 };
 
@@ -941,11 +907,14 @@ struct B2 {   // ring geometry; MODE as in k_tc_bwd2 (the output-layer launch ke
 template <int WP, int MODE>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
     constexpr bool OUTL = (MODE & 1) != 0, FIRST = (MODE & 2) != 0;
-    constexpr bool EARLY_T = CRV_B2_EARLY_T && MODE == 0;
-    constexpr bool DEFER_CS = CRV_B2_CS_DEFER;
-    // with a single t slot the t load must not sit in front of the Delta chunks
-    constexpr bool T_FIRST = CRV_T_FIRST && B2<WP, MODE>::NT > 1;
-    constexpr bool DEFER_FIRST = CRV_B2_CS_DEFER && CRV_B2_DEFER_FIRST && FIRST;
+    // middle GEMMs release the t slot right after xfull (t values in registers); bias column sums:
+    // one butterfly level per tile, the rest once at the end (the g = 0 launch also defers its x-
+    // and y-sums); a tile's t_in load goes out before its Delta chunks (with a single t slot it
+    // must not sit in front of them)
+    constexpr bool EARLY_T = MODE == 0;
+    constexpr bool DEFER_CS = true;
+    constexpr bool T_FIRST = B2<WP, MODE>::NT > 1;
+    constexpr bool DEFER_FIRST = FIRST;
     constexpr int NS = B2<WP, MODE>::NS, KC = B2<WP, MODE>::KC, DS = B2<WP, MODE>::DS, NT = B2<WP, MODE>::NT;
     constexpr uint16_t MASK = (uint16_t)((1u << NS) - 1u);
     extern __shared__ uint8_t smem_raw[];
@@ -1089,18 +1058,10 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                         else mma_commit_mc(&dempty[sl + j], MASK);
                     }
                 };
-#if CRV_B2_DX_FIRST
                 // all of dX first, committed before the dW MMAs: the epilogue drains it while dW runs
                 for (int h = 0; h < KC / 2; ++h) dx_pair(h);
                 mma_commit(&xfull[b]);
                 for (int h = 0; h < KC / 2; ++h) dw_half(h);
-#else
-                for (int h = 0; h < KC / 2; ++h) {
-                    dx_pair(h);
-                    dw_half(h);
-                }
-                mma_commit(&xfull[b]);
-#endif
                 BTRACE(k * 16 + 3);
                 mma_commit(&tempty[tb]);
                 dn += KC;
@@ -1120,7 +1081,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
         const uint32_t t_lane = (uint32_t)(q * 32) << 16;
         const int N = a.N;
         float cs[CPW / 32], csx[CPW / 32], csy[CPW / 32];
-#if CRV_B2_CS_DEFER
         // column sums after the first butterfly level (lanes l, l^16), accumulated over all tiles;
         // the other four levels run once at the end (csdx/csdy: the g = 0 launch's x- and y-sums)
         float csd[CPW / 32][16], csdx[CPW / 32][16], csdy[CPW / 32][16];
@@ -1150,7 +1110,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
             }
             return acc[0];
         };
-#endif
 #pragma unroll
         for (int g2 = 0; g2 < CPW / 32; ++g2) cs[g2] = csx[g2] = csy[g2] = 0.f;
         // output-layer transform state (outl). Thread -> granule lg (8 features) of every chunk,
@@ -1217,13 +1176,11 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     const uint32_t blk = smem_u32(Dr + slot * CHUNK_BYTES);
                     const bool own = NS == 1 || (j >> 1) == (int)rank;
                     const int jj = NS == 1 ? j : (j & 1);
-#if CRV_OUTL_H2SUM
                     // the ORM rows of a granule column are first summed in half2 (g t and Delta_L are
                     // fp16 values already), then added to the fp32 sums once
                     __half2 haw[4], hab[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) haw[e] = hab[e] = __floats2half2_rn(0.0f, 0.0f);
-#endif
 #pragma unroll
                     for (int m = 0; m < ORM; ++m) {
                         const int r = orr + ORG * m;
@@ -1235,22 +1192,13 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                             const __half2 t = __hmul2(*reinterpret_cast<__half2 *>(&w[e]), tsc2);   // t' -> t
                             const __half2 d = __hmul2(__hmul2(__hfma2(__hneg2(t), t, one2), wo2[j][e]), g2[m]);
                             if (a.outl_sums && own && jj < 2) {
-#if CRV_OUTL_H2SUM
                                 haw[e] = __hfma2(g2[m], t, haw[e]);
                                 hab[e] = __hadd2(hab[e], d);
-#else
-                                const float2 tf = __half22float2(t), df = __half22float2(d);
-                                aw[jj][2 * e] = fmaf(g[m], tf.x, aw[jj][2 * e]);
-                                aw[jj][2 * e + 1] = fmaf(g[m], tf.y, aw[jj][2 * e + 1]);
-                                ab[jj][2 * e] += df.x;
-                                ab[jj][2 * e + 1] += df.y;
-#endif
                             }
                             w[e] = *reinterpret_cast<const uint32_t *>(&d);
                         }
                         st_shared_v4(blk + off, w[0], w[1], w[2], w[3]);
                     }
-#if CRV_OUTL_H2SUM
                     if (a.outl_sums && own && jj < 2) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
@@ -1261,7 +1209,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                             ab[jj][2 * e + 1] += fb.y;
                         }
                     }
-#endif
                     fence_proxy_async_smem();
                     mbar_arrive(&dready[slot]);   // count = B2_EPI_THREADS
                     if (warp == 2 && lane == 0 && j == 0) BTRACE(k * 16 + 13);
@@ -1344,12 +1291,10 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
                 }
                 if (FIRST) {
-#if CRV_B2_CS_DEFER
                     if constexpr (DEFER_FIRST) {
                         level16(v, csdx[g2], x);
                         level16(v, csdy[g2], y);
                     } else
-#endif
                     {
                         float vx[32], vy[32];
 #pragma unroll
@@ -1361,11 +1306,9 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                     }
                 }
                 {   // bias sums (CUDA cores)
-#if CRV_B2_CS_DEFER
                     if (DEFER_CS && (!FIRST || DEFER_FIRST)) {
                         level16(v, csd[g2], 1.0f);
                     } else
-#endif
                     {
                         warp_reduce_scatter32(v, lane);
                         cs[g2] += v[0];
@@ -1380,7 +1323,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 if constexpr (!EARLY_T) mbar_arrive(&tempty[tb]);
             }
         }
-#if CRV_B2_CS_DEFER
         // remaining butterfly levels (8, 4, 2, 1) of the deferred column sums: column = lane
         if (DEFER_CS && (!FIRST || DEFER_FIRST)) {
 #pragma unroll
@@ -1393,7 +1335,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
                 csy[g2] = finish16(csdy[g2]);
             }
         }
-#endif
         // ---- end: all MMAs done -> the rings are free for the reductions
         if (nk > 0) mbar_wait(wdone, 0);
         tc_fence_after();
@@ -1498,13 +1439,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwd2(Bwd2Args a) {
 // own output on the CUDA cores (bias and first-layer weights). The dX accumulator is single
 // buffered to make room (its commit is issued before the second dW half, so the epilogue drains
 // it under the remaining MMAs). The output-layer backward runs before the chain (k_tc_out_bwd).
-#ifndef CRV_BC_FENCE
-#define CRV_BC_FENCE 1     // ring hand-off: 1 = cluster-scope acq_rel fence per lane, 2 = gpu-scope sc fence
-#endif
-#ifndef CRV_BC_RS
-#define CRV_BC_RS 3
-#endif
-constexpr int BC_RS = CRV_BC_RS;   // global ring slots (tiles) per stage boundary
+constexpr int BC_RS = 3;   // global ring slots (tiles) per stage boundary
 template <int WP>
 struct BC {
     static constexpr uint32_t SMEM = B2<WP>::SMEM;   // includes the all-ones core matrix
@@ -1619,7 +1554,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
                 const int tile = cid + k * a.nclus;
                 const int gs = k % RS;
                 prefetch(k + PD);
-                if (CRV_T_FIRST) load_t(k, tile);
+                load_t(k, tile);   // a tile's t_in before its Delta chunks
                 for (int j = 0; j < KC; ++j, ++dn) {
                     const int slot = dn % DS;
                     mbar_wait_sleep(&dempty[slot], ((dn / DS) & 1) ^ 1);
@@ -1638,7 +1573,6 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
                     if (NS == 1) bulk_g2s(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot]);
                     else bulk_g2s_mc(Dr + slot * CHUNK_BYTES, src, CHUNK_BYTES, &dfull[slot], smask);
                 }
-                if (!CRV_T_FIRST) load_t(k, tile);
             }
         }
     } else if (warp == 1) {
@@ -1719,11 +1653,7 @@ __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
         auto handoff = [&]() {
             if (pgs < 0) return;
             fence_proxy_async_global();
-#if CRV_BC_FENCE == 2
-            __threadfence();
-#elif CRV_BC_FENCE == 1
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
-#endif
             __syncwarp();
             if (lane == 0) {
                 const int j = 2 * (int)rank + wq;   // global chunk index within the tile
