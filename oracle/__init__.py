@@ -60,6 +60,7 @@ def lib():
         L.orc_get_theta.argtypes = [P, D]
         L.orc_set_theta.argtypes = [P, D]
         L.orc_get_adam.argtypes = [P, D, D, ctypes.POINTER(ctypes.c_long)]
+        L.orc_set_adam.argtypes = [P, D, D, ctypes.c_long]
         L.orc_get_alpha.argtypes = [P, D]
         L.orc_get_b.argtypes = [P, D]
         L.orc_direct_solve.restype = ctypes.c_int
@@ -154,6 +155,11 @@ class Oracle:
         m, v, t = np.empty(self.np), np.empty(self.np), ctypes.c_long(0)
         lib().orc_get_adam(self._h, _dp(m), _dp(v), ctypes.byref(t))
         return m, v, int(t.value)
+
+    def set_adam_state(self, m, v, t: int):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        lib().orc_set_adam(self._h, _dp(m), _dp(v), int(t))
 
     def alpha(self) -> np.ndarray:
         out = np.empty((self.N + 1) ** 2)

@@ -6,7 +6,7 @@ path. Each sub-command writes one .npz under tests/golden/.
   c4sched                 C4's full schedule (§6 step 7; BASELINE.json configs[3]):
                           10 time steps x 100 Adam iterations, warm-started weights and Adam state,
                           S advanced between steps (S_steps[k] for step k) -> C4_sched10x100.npz
-  c5sched [steps]         the same for C5 (configs[4]), the first [steps] time steps (the fixture is
+  c5sched [steps] [--resume]  the same for C5 (configs[4]), the first [steps] time steps (the fixture is
                           rewritten after every step: steps_done) -> C5_sched.npz
   c3 <seed> <iters>       C3's pretraining + updates with fixed S (configs[2]):
                           <iters> Adam iterations from theta0 (seed 0) or from theta0 moved by one fp32
@@ -39,9 +39,11 @@ def ulp_perturbed(theta0, seed):
     return np.nextafter(t0, np.where(rng.random(t0.shape) < 0.5, -np.inf, np.inf).astype(np.float32))
 
 
-def sched(name="C4", max_steps=None):
+def sched(name="C4", max_steps=None, resume=False):
     """name's schedule (C4: all 10 steps -> C4_sched10x100.npz; C5: the first max_steps of its 10,
-    rewritten after every step so a partial run is usable -> C5_sched.npz with steps_done)"""
+    rewritten after every step so a partial run is usable -> C5_sched.npz with steps_done, plus the
+    fp64 state after the last step (theta, m, v, t) so that `resume` continues the run exactly).
+    S_steps[k] is the saturation of time step k; a workload with one S (C5) keeps it."""
     F = W.make_fields(name)
     w = F.workload
     n = w.n_steps if max_steps is None else min(max_steps, w.n_steps)
@@ -51,18 +53,30 @@ def sched(name="C4", max_steps=None):
     step_end = np.zeros(n)
     thetas = {}
     fname = "C4_sched10x100.npz" if name == "C4" else f"{name}_sched.npz"
-    for k in range(n):
-        if k > 0:
+    k0 = 0
+    if resume:
+        z = np.load(os.path.join(OUT, fname))
+        k0 = int(z["steps_done"])
+        hist[:k0], step_end[:k0] = z["hist"][:k0], z["step_end"][:k0]
+        thetas = {key: z[key] for key in z.files if key.startswith("theta_step")}
+        o.theta = z["state_theta"]
+        o.set_adam_state(z["state_m"], z["state_v"], int(z["state_t"]))
+        if k0 < len(F.S_steps) and k0 > 0:
+            o.set_saturation(F.S_steps[k0 - 1])
+    for k in range(k0, n):
+        if 0 < k < len(F.S_steps):
             o.set_saturation(F.S_steps[k])
         hist[k] = o.train(w.n_adam)
-        step_end[k] = o.loss_grad()[0]      # LOSS(theta after step k) on S_steps[k]
+        step_end[k] = o.loss_grad()[0]      # LOSS(theta after step k) on the step's S
         if k in (0, w.n_steps - 1):
             thetas[f"theta_step{k + 1}"] = o.theta.astype(np.float32)
         print(f"{name} step {k + 1}: {hist[k, 0]:.6e} -> {hist[k, -1]:.6e} end {step_end[k]:.6e} "
               f"({time.time() - t:.0f}s)", flush=True)
         if name != "C4" or k == n - 1:
+            m, v, tt = o.adam_state()
             np.savez_compressed(os.path.join(OUT, fname), hist=hist[:k + 1], step_end=step_end[:k + 1],
-                                steps_done=k + 1, threads=oracle.max_threads(), **thetas)
+                                steps_done=k + 1, threads=oracle.max_threads(), state_theta=o.theta,
+                                state_m=m, state_v=v, state_t=tt, **thetas)
 
 
 def c3model(seed, iters, bits=11):
@@ -115,7 +129,7 @@ if __name__ == "__main__":
     if cmd == "c4sched":
         sched("C4")
     elif cmd == "c5sched":
-        sched("C5", int(sys.argv[2]) if len(sys.argv) > 2 else None)
+        sched("C5", int(sys.argv[2]) if len(sys.argv) > 2 else None, resume="--resume" in sys.argv)
     elif cmd == "c3model":
         bits = int(sys.argv[sys.argv.index("--bits") + 1]) if "--bits" in sys.argv else 11
         c3model(int(sys.argv[2]), int(sys.argv[3]), bits)

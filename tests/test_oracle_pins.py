@@ -735,3 +735,23 @@ def test_P21_precision_model_unrounded_is_the_oracle():
     l11, g11 = pm11.loss_grad()
     assert l11 == l                                        # the forward is not rounded
     assert 0 < np.linalg.norm(g11 - rg) <= 1e-2 * np.linalg.norm(rg)
+
+
+def test_oracle_state_resume_is_exact():
+    """scripts/oracle_runs.py resumes long fixture runs (C5's schedule) from the saved fp64 state:
+    theta + Adam (m, v, t) restored into a fresh oracle continue the iteration bit for bit."""
+    N, widths = 16, (2, 32, 32, 1)
+    K, S, f = W.random_fields(N, 71)
+    th = W.random_theta(widths, 71)
+    a = oracle.Oracle(N, widths, K, S, f, th)
+    full = a.train(6)
+    b = oracle.Oracle(N, widths, K, S, f, th)
+    first = b.train(3)
+    m, v, t = b.adam_state()
+    c = oracle.Oracle(N, widths, K, S, f, th)
+    c.theta = b.theta
+    c.set_adam_state(m, v, t)
+    rest = c.train(3)
+    np.testing.assert_array_equal(np.concatenate([first, rest]), full)
+    np.testing.assert_array_equal(c.theta, a.theta)
+    assert c.adam_state()[2] == 6
