@@ -508,13 +508,26 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
     constexpr int KC = WP / 64;
     constexpr int NRG = OB_THREADS / (8 * KC);   // row groups
     constexpr int RPT = 128 / NRG;               // rows per thread per tile
-    __shared__ float sg[128];
     __shared__ float sred[2][NRG][WP];
     __shared__ float sgsum[NRG];
     __shared__ float swo;
     const int T = threadIdx.x;
     const int lg = T & 7, c = (T >> 3) % KC, rg = T / (8 * KC);
     const int f0 = c * 64 + lg * 8;
+    // a thread's RPT rows of one tile: t_L granules and gbar, loaded together (every input is complete
+    // at launch); the next tile's are in flight while this one is transformed
+    uint4 raw[RPT];
+    float gr[RPT];
+    auto fetch = [&](int tl) {
+        const uint8_t *src = (const uint8_t *)actL + ((size_t)tl * KC + c) * CHUNK_BYTES;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+            const int r = rg + k * NRG;
+            raw[k] = __ldg((const uint4 *)(src + (uint32_t)(r * 128 + ((lg ^ (r & 7)) << 4))));
+            gr[k] = __ldg(gbar + tl * 128 + r);
+        }
+    };
+    if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
     if (T < 32) {   // max |W_out| (order-independent: every block gets the same value)
         float m = 0.0f;
         for (int f = T; f < WP; f += 32) m = fmaxf(m, fabsf(Wop[f]));
@@ -533,20 +546,19 @@ __global__ void __launch_bounds__(OB_THREADS) k_tc_out_bwd(int ntiles, const __h
     for (int e = 0; e < 8; ++e) { wo[e] = Wop[f0 + e]; aw[e] = 0.0f; ab[e] = 0.0f; }
     float ag = 0.0f;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
-        if (T < 128) sg[T] = gbar[tile * 128 + T] * s;
-        __syncthreads();
-        const size_t base = ((size_t)tile * KC + c) * CHUNK_BYTES;
-        const uint8_t *src = (const uint8_t *)actL + base;
-        uint8_t *dst = (uint8_t *)deltaL + base;
-#pragma unroll 4
+        uint4 cur[RPT];
+        float gc[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) { cur[k] = raw[k]; gc[k] = gr[k]; }
+        if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
+        uint8_t *dst = (uint8_t *)deltaL + ((size_t)tile * KC + c) * CHUNK_BYTES;
+#pragma unroll
         for (int k = 0; k < RPT; ++k) {
             const int r = rg + k * NRG;
             const uint32_t off = (uint32_t)(r * 128 + ((lg ^ (r & 7)) << 4));
-            uint4 raw = *(const uint4 *)(src + off);
-            const float g = sg[r];
+            const float g = gc[k] * s;
             ag += g;
-            uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+            uint32_t w[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 float2 t = __half22float2(*reinterpret_cast<__half2 *>(&w[m]));
