@@ -79,7 +79,7 @@ __device__ __forceinline__ void fft_inplace(float2 *sa, const float2 *tw, int M,
 __device__ __forceinline__ void res_dst_pair(int pair, const float *__restrict__ u, const float *__restrict__ alpha,
                                              const float *__restrict__ bvec, float *__restrict__ res,
                                              float *__restrict__ rhat, float2 *sa, const float2 *stw, int N, int logM,
-                                             float scale) {
+                                             float scale, const float (*pre)[4] = nullptr) {
     const int n = N - 1, M = 2 * N;
     const int j0 = 2 * pair;
     const bool has1 = j0 + 1 < n;
@@ -96,11 +96,15 @@ __device__ __forceinline__ void res_dst_pair(int pair, const float *__restrict__
             const int j = j0 + r;
             if (r == 1 && !has1) break;
             const int i = k + 1, l = j + 1;   // lattice node of RES[j][k]
+            // alpha and b of this node: preloaded (before the dependency wait) for the first column
+            const bool pl = pre != nullptr && k == (int)threadIdx.x;
+            const float aw = pl ? pre[r][0] : alpha[latx(i - 1, l, N)];
+            const float as = pl ? pre[r][1] : alpha[latx(i, l - 1, N)];
+            const float ac = pl ? pre[r][2] : alpha[latx(i, l, N)];
+            const float bb = pl ? pre[r][3] : bvec[latx(i, l, N)];
             const float uc = u[latx(i, l, N)];
-            const float rr = alpha[latx(i - 1, l, N)] * (uc - u[latx(i - 1, l, N)]) +
-                             alpha[latx(i, l - 1, N)] * (uc - u[latx(i, l - 1, N)]) +
-                             alpha[latx(i, l, N)] * ((uc - u[latx(i + 1, l, N)]) + (uc - u[latx(i, l + 1, N)])) -
-                             bvec[latx(i, l, N)];
+            const float rr = aw * (uc - u[latx(i - 1, l, N)]) + as * (uc - u[latx(i, l - 1, N)]) +
+                             ac * ((uc - u[latx(i + 1, l, N)]) + (uc - u[latx(i, l + 1, N)])) - bb;
             res[(long)j * n + k] = rr;
             v[r] = rr;
         }
@@ -124,10 +128,27 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
     const int M = 2 * N;
     float2 *stw = sa + M;
     for (int k = threadIdx.x; k < M; k += blockDim.x) stw[k] = tw[k];   // constants: before the wait
+    // alpha and b are fixed for the whole call (A0 ran before it): this thread's first column's
+    // values are loaded before the dependency wait too, under the forward's tail
+    float pre[2][4] = {};
+    {
+        const int n = N - 1, k = threadIdx.x, i = k + 1;
+        if (k < n)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int l = 2 * blockIdx.x + r + 1;
+                if (l <= n) {
+                    pre[r][0] = alpha[latx(i - 1, l, N)];
+                    pre[r][1] = alpha[latx(i, l - 1, N)];
+                    pre[r][2] = alpha[latx(i, l, N)];
+                    pre[r][3] = bvec[latx(i, l, N)];
+                }
+            }
+    }
     pdl_wait();
     pdl_trigger();
     if (blockIdx.x == 0 && threadIdx.x == 0) st->gmax_bits = 0u;   // k_adj_final folds this iteration's max
-    res_dst_pair(blockIdx.x, u, alpha, bvec, res, rhat, sa, stw, N, logM, scale);
+    res_dst_pair(blockIdx.x, u, alpha, bvec, res, rhat, sa, stw, N, logM, scale, pre);
 }
 
 // One warp per mode a: Thomas elimination of (lam_a I + T) z = h2 * r written as two first-order
@@ -139,29 +160,46 @@ __global__ void k_res_dst(const float *__restrict__ u, const float *__restrict__
 constexpr int TRI_WARPS = 4;
 
 // Thomas scans of mode a by one warp; sm: the warp's 2 * 32 * seg floats of shared memory
-__device__ __forceinline__ void tridiag_mode(int a, const float *__restrict__ rhat, const float *__restrict__ etab,
-                                             float *__restrict__ z, int n, int seg, float h2, float *sm) {
+// the pivots of mode a (constants of the context) into the warp's staging rows (se)
+__device__ __forceinline__ void stage_pivots(int a, const float *__restrict__ etab, int n, int seg, float *sm) {
     const int lane = threadIdx.x & 31;
-    const int stride = 32 * seg;
-    float *sr = sm;   // this warp's [2][32 seg]: r, then g, then z
-    float *se = sr + stride;
-    const float *r = rhat + (size_t)a * n;
+    float *se = sm + 32 * seg;
     const float *e = etab + (size_t)a * n;
-    for (int j0 = lane; j0 < n; j0 += 8 * 32) {   // eight loads of each row in flight per lane
-        float rv[8], ev[8];
+    for (int j0 = lane; j0 < n; j0 += 8 * 32) {
+        float ev[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int j = j0 + 32 * u;
-            rv[u] = j < n ? r[j] : 0.0f;
             ev[u] = j < n ? e[j] : 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int j = j0 + 32 * u;
-            if (j < n) {
-                sr[j] = h2 * rv[u];
-                se[j] = ev[u];
-            }
+            if (j < n) se[j] = ev[u];
+        }
+    }
+}
+
+__device__ __forceinline__ void tridiag_mode(int a, const float *__restrict__ rhat, const float *__restrict__ etab,
+                                             float *__restrict__ z, int n, int seg, float h2, float *sm,
+                                             bool pivots_staged = false) {
+    const int lane = threadIdx.x & 31;
+    const int stride = 32 * seg;
+    float *sr = sm;   // this warp's [2][32 seg]: r, then g, then z
+    float *se = sr + stride;
+    const float *r = rhat + (size_t)a * n;
+    if (!pivots_staged) stage_pivots(a, etab, n, seg, sm);
+    for (int j0 = lane; j0 < n; j0 += 8 * 32) {   // eight loads of the row in flight per lane
+        float rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 32 * u;
+            rv[u] = j < n ? r[j] : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 32 * u;
+            if (j < n) sr[j] = h2 * rv[u];
         }
     }
     __syncwarp();
@@ -213,13 +251,15 @@ __device__ __forceinline__ void tridiag_mode(int a, const float *__restrict__ rh
 
 __global__ void k_tridiag(const float *__restrict__ rhat, const float *__restrict__ etab, float *__restrict__ z,
                           int n, int seg, float h2) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ float sm[];
     const int warp = threadIdx.x >> 5;
     const int a = blockIdx.x * TRI_WARPS + warp;
+    float *wsm = sm + (size_t)warp * 2 * 32 * seg;
+    if (a < n) stage_pivots(a, etab, n, seg, wsm);   // constants: before the dependency wait
+    pdl_wait();
+    pdl_trigger();
     if (a >= n) return;
-    tridiag_mode(a, rhat, etab, z, n, seg, h2, sm + (size_t)warp * 2 * 32 * seg);
+    tridiag_mode(a, rhat, etab, z, n, seg, h2, wsm, true);
 }
 
 
@@ -296,11 +336,22 @@ __global__ void k_adj_final(const float *__restrict__ q, const float *__restrict
                             double beta2, int advance) {
     __shared__ float smax[8];
     __shared__ double sh[256];
-    pdl_wait();
-    pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     float g = 0.0f, gb = 0.0f;
     const int n = N - 1;
+    // alpha is fixed for the whole call: this point's three coefficients before the dependency wait
+    float aw = 0.0f, as = 0.0f, ac = 0.0f;
+    if (p < N * N) {
+        int i, j;
+        point_ij(p, N, i, j);
+        if (i <= n && j <= n) {
+            aw = alpha[latx(i - 1, j, N)];
+            as = alpha[latx(i, j - 1, N)];
+            ac = alpha[latx(i, j, N)];
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
     if (p < N * N) {
         int i, j;
         point_ij(p, N, i, j);
@@ -309,8 +360,7 @@ __global__ void k_adj_final(const float *__restrict__ q, const float *__restrict
                 return (a >= 1 && a <= n && c >= 1 && c <= n) ? q[(long)(c - 1) * n + (a - 1)] : 0.0f;
             };
             const float qc = Q(i, j);
-            const float aq = alpha[latx(i - 1, j, N)] * (qc - Q(i - 1, j)) + alpha[latx(i, j - 1, N)] * (qc - Q(i, j - 1)) +
-                             alpha[latx(i, j, N)] * ((qc - Q(i + 1, j)) + (qc - Q(i, j + 1)));
+            const float aq = aw * (qc - Q(i - 1, j)) + as * (qc - Q(i, j - 1)) + ac * ((qc - Q(i + 1, j)) + (qc - Q(i, j + 1)));
             g = 2.0f * aq;
             const float x = (float)i / (float)N, y = (float)j / (float)N;
             gb = g * cutoff(x, y);
