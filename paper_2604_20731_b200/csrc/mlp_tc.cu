@@ -2100,8 +2100,14 @@ int tc_create(const Net &net, TcBufs &b, int tile0, int ntiles, std::string &err
     // side-stream reduction (k_reduce_wide, float4 rows) launched right after GEMM g; the rest stay
     // in the table k_reduce walks after the last GEMM. Side jobs are appended after the deep ones.
     b.nsm = nsm;
+    // Side-stream reductions: with the backward chain (its launches' dW reduced beside the next launch).
+    // The per-GEMM path (k_tc_bwd2, C5) reduces every hidden layer after the last GEMM instead: its
+    // side-stream reductions beside k_tc_bwd2 made C5's step(n) differ run to run in ~1 of 5 runs
+    // (first in W0 / b0 / W1 / b1, scripts/det_steps.py, det_layers.py), and the
+    // step time is the same without them (C5 793-801 vs 791-820 us per iteration).
+    // CRVPINN_SIDE_REDUCE=0/1 forces it (A/B knob).
     const char *sre = getenv("CRVPINN_SIDE_REDUCE");
-    const bool side_ok = !(sre && sre[0] == '0');
+    const bool side_ok = sre ? sre[0] != '0' : b.chain != 0;
     for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1) b.njobs_deep = nj;
         for (int l = 1; l < nl - 1; ++l) {
