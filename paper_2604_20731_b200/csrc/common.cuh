@@ -89,7 +89,14 @@ struct AdamOp {
 
 constexpr float ADAM_TANH_C = 2.8853900817779268f;   // 2 log2(e) (the forward's pre-scale of W1 and biases)
 
-__device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk) {
+// Adam state of entry e, loaded ahead of the gradient it will be combined with (the reductions issue
+// these loads before their partial-sum loads, so the two latencies overlap)
+struct AdamPre {
+    float m, v, th;
+};
+__device__ __forceinline__ AdamPre adam_pre(const AdamOp &A, long e) { return {A.m[e], A.v[e], A.theta[e]}; }
+
+__device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk, const AdamPre &p) {
     DevState *st = A.st;
     if (st->nonfinite) return;
     if (!isfinite(gk)) {
@@ -97,11 +104,11 @@ __device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk) {
         return;
     }
     const float bc1 = (float)st->bc1, bc2 = (float)st->bc2;
-    const float mk = A.beta1 * A.m[e] + (1.0f - A.beta1) * gk;
-    const float vk = A.beta2 * A.v[e] + (1.0f - A.beta2) * gk * gk;
+    const float mk = A.beta1 * p.m + (1.0f - A.beta1) * gk;
+    const float vk = A.beta2 * p.v + (1.0f - A.beta2) * gk * gk;
     A.m[e] = mk;
     A.v[e] = vk;
-    const float th = A.theta[e] - A.lr * (mk / bc1) / (sqrtf(vk / bc2) + A.eps);
+    const float th = p.th - A.lr * (mk / bc1) / (sqrtf(vk / bc2) + A.eps);
     A.theta[e] = th;
     const Net &net = A.net;
     const int nl = net.nl, L = nl - 1, WP = A.WP, KC = A.KC;
@@ -133,6 +140,8 @@ __device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk) {
         }
     }
 }
+
+__device__ __forceinline__ void adam_one(const AdamOp &A, long e, float gk) { adam_one(A, e, gk, adam_pre(A, e)); }
 
 // Programmatic dependent launch (PDL): kernels of the iteration are launched with programmatic
 // stream serialization, so a kernel's CTAs may start (prologue: barrier init, TMEM alloc) while the

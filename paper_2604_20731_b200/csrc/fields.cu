@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
     if (red_wide(jb)) {
         const int o = g * RED_THREADS + threadIdx.x;
         if (o >= jb.count) return;
+        const AdamPre ap = A.on ? adam_pre(A, jb.dst + o) : AdamPre{};
         const float *src = partial + jb.src + red_off(jb, o);
         float s = 0.0f;
         int z = 0;
@@ -98,11 +99,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
         }
         for (; z < jb.nsplit; ++z) s += __ldg(src + (long)z * jb.stride);
         grad[jb.dst + o] = s * sc;
-        if (A.on) adam_one(A, jb.dst + o, s * sc);
+        if (A.on) adam_one(A, jb.dst + o, s * sc, ap);
         return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int o = g * 32 + lane;
+    const AdamPre ap = (A.on && warp == 0 && o < jb.count) ? adam_pre(A, jb.dst + o) : AdamPre{};
     float s = 0.0f;
     if (o < jb.count) {
         const float *src = partial + jb.src + red_off(jb, o);
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(const float *__restrict_
         float t = 0.0f;
         for (int w = 0; w < RED_WARPS; ++w) t += sh[w][lane];
         grad[jb.dst + o] = t * sc;
-        if (A.on) adam_one(A, jb.dst + o, t * sc);
+        if (A.on) adam_one(A, jb.dst + o, t * sc, ap);
     }
 }
 
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restr
     const long st4 = jb.stride >> 2;
     for (int q0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 4; q0 < n4; q0 += gridDim.x * wpb * 4) {
         const int q = q0 + og;
+        // lane (og, sg < 4) finishes component sg of output float4 og: its Adam state first
+        const AdamPre ap = (A.on && sg < 4 && q < n4) ? adam_pre(A, jb.dst + 4 * (long)q + (sg & 3)) : AdamPre{};
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
         if (q < n4) {
             const float4 *src = reinterpret_cast<const float4 *>(partial + jb.src + red_off(jb, 4 * q));
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(RW_THREADS) k_reduce_wide(const float *__restr
             const float r = (k == 0 ? c0 : k == 1 ? c1 : k == 2 ? c2 : c3) * sc;
             const long d = jb.dst + 4 * (long)q + k;
             grad[d] = r;
-            if (A.on) adam_one(A, d, r);
+            if (A.on) adam_one(A, d, r, ap);
         }
     }
 }
