@@ -321,6 +321,10 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     stage_ms, prof_iters = g.profile(reset=True)
     g.set_profiling(False)
+    # leaving profiling mode drops the captured graphs: re-capture the step graph here (one untimed
+    # step) so that the end-to-end loop below times steady-state steps, not a graph instantiation
+    g.step(ITERS_PER_STEP, history=True)
+    torch.cuda.synchronize()
     red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"   # where the max-over-ranks reductions run
     t = torch.tensor([t_ms], dtype=torch.float64, device=red_dev)
     if dist:
