@@ -71,7 +71,29 @@ struct FwdArgs {
     int p0;                // first MLP point of this shard (tile0 * 128); 0 unsharded
     const DevState *st;    // per-GEMM weight exponents (wexp, written by k_wscale)
 };
+// clock64 timelines (FTRACE / BTRACE / CTRACE, the CRVPINN_*_TRACE debug paths) are compiled in only with
+// -DCRV_TRACE=1 (scripts/ab_build_tc.sh trace -DCRV_TRACE=1): their run-time checks sit in the hot loops
+#ifndef CRV_TRACE
+#define CRV_TRACE 0
+#endif
+// the trace file name from the environment; a library built without CRV_TRACE says so instead of writing zeros
+static inline const char *trace_env(const char *name) {
+    const char *e = getenv(name);
+#if !CRV_TRACE
+    if (e) {
+        static bool warned = false;
+        if (!warned) fprintf(stderr, "crvpinn: %s ignored: this library was built without -DCRV_TRACE=1\n", name);
+        warned = true;
+        return nullptr;
+    }
+#endif
+    return e;
+}
+#if CRV_TRACE
 #define FTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
+#else
+#define FTRACE(slot) do { } while (0)
+#endif
 
 
 
@@ -305,6 +327,8 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                     tc_fence_after();
                 }
                 const float *bias = sB + (layer - 1) * WP;
+                // 2 log2(e) 2^(wexp - 14): undoes the operand scales (one shared-memory load per layer)
+                const float cg = layer > 1 ? lds_f32(sC + layer - 2) : 0.0f;
                 uint8_t *grow = (uint8_t *)(a.act + ((size_t)(layer - 1) * a.ntiles + tile) * (KC * CHUNK_HALVES)) +
                                 row * 128;
                 // TMEM loads run one slice ahead of the math; every layer stores t'_hi to HBM from
@@ -326,6 +350,16 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                     need_half1(wq * 16);
                     tmem_ld16_async(t_lane + acc + wq * 16, rbuf);
                 }
+                // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
+                auto release = [&](int c) {
+                    if constexpr (!EVAL) fence_proxy_async_smem();
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
+                    if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
+                    if (lane == 0) mbar_arrive(&a_full[c]);
+                };
                 // work items (chunk c, slice sl = wq + s WQ) in order; TMEM loads run one item ahead
                 // the chunk loop, instantiated for the accurate-tanh layers and for the rest (a uniform
                 // branch per layer, so the common path carries no code of the other)
@@ -347,7 +381,6 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                         }
                     } else {
                         tmem_wait_ld16(rbuf);
-                        const float cg = sC[layer - 2];   // 2 log2(e) 2^(wexp - 14): undoes the operand scales
                         const f32x2_t C2 = pk2(cg, cg);
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
@@ -428,16 +461,7 @@ __global__ void __launch_bounds__(fwd_threads<EW>(), EW == 8 ? 2 : 1) k_tc_forwa
                             st_shared_v4(bh + off0(sl), hw[0], hw[1], hw[2], hw[3]);
                             st_shared_v4(bh + off1(sl), hw[4], hw[5], hw[6], hw[7]);
                         }
-                        if (sp == SPW - 1) {
-                            // release chunk c to the next GEMM (and its HBM copy); one arrival per warp
-                            if constexpr (!EVAL) fence_proxy_async_smem();
-                            tmem_wait_st();
-                            tc_fence_before();
-                            __syncwarp();
-                            if (warp == 2 && lane == 0) FTRACE(gi * 16 + 2 + c);
-                            if (lane == 0 && gi < 12) FTRACE(1024 + (gi * (KC + 1) + 1 + c) * 16 + (warp - 2));
-                            if (lane == 0) mbar_arrive(&a_full[c]);
-                        }
+                        if (sp == SPW - 1) release(c);
                     } else {
 #pragma unroll
                         for (int k = 0; k < 16; k += 4) {
@@ -894,7 +918,11 @@ struct Bwd2Args {
     int p0;               // first MLP point of this shard (gbar is passed offset by it)
     int g;                // hidden GEMM index (weight / Delta exponents)
 };
+#if CRV_TRACE
 #define BTRACE(slot) do { if (a.trace && blockIdx.x == 0 && (slot) < 4096) a.trace[(slot)] = clock64(); } while (0)
+#else
+#define BTRACE(slot) do { } while (0)
+#endif
 #define B2_MMA_WAIT mbar_wait
 
 constexpr int B2_EPI_WARPS = 8;    // 2 per TMEM lane quarter
@@ -1471,7 +1499,11 @@ struct BwdcArgs {
     int p0;               // first MLP point of this shard
     const DevState *st;   // weight / Delta exponents per GEMM
 };
+#if CRV_TRACE
 #define CTRACE(slot) do { if (a.trace && blockIdx.x < 8 && (slot) < 1024) a.trace[blockIdx.x * 1024 + (slot)] = clock64(); } while (0)
+#else
+#define CTRACE(slot) do { } while (0)
+#endif
 
 template <int WP>
 __global__ void __launch_bounds__(B2_THREADS, 1) k_tc_bwdc(BwdcArgs a) {
@@ -2178,7 +2210,7 @@ void tc_refresh_weights(const Net &net, const TcBufs &b, const float *theta, Dev
 template <int WP>
 static void fwd_launch(const Net &net, const TcBufs &b, float *u, cudaStream_t s) {
     static long long *trace = nullptr;
-    const char *te = getenv("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
+    const char *te = trace_env("CRVPINN_FWD_TRACE");   // debug: clock64 timeline of CTA 0 -> file
     if (te && !trace) { cudaMalloc(&trace, 4096 * 8); cudaMemset(trace, 0, 4096 * 8); }
     FwdArgs a{net.N, b.ntiles, b.L, b.G, b.Wf, b.W1p, b.bp, b.Wop, b.act, u, te ? trace : nullptr, nullptr, 0, b.tile0 * 128,
               b.st};
@@ -2261,7 +2293,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                            b.delta + (size_t)(g0 - Sl + 1) * lay, b.ring, b.WTf, b.partial + b.off_dx,
                            b.partial + b.off_dw, b.partial + b.off_cb, lay, nullptr, p0, st};
                 static long long *ctrace = nullptr;
-                const char *te = getenv("CRVPINN_CHAIN_TRACE");   // debug: clock64 timeline -> file
+                const char *te = trace_env("CRVPINN_CHAIN_TRACE");   // debug: clock64 timeline -> file
                 if (te && g0 == b.G - 1) {
                     if (!ctrace) cudaMalloc(&ctrace, 8 * 1024 * 8);
                     cudaMemset(ctrace, 0, 8 * 1024 * 8);
@@ -2302,7 +2334,7 @@ static void bwd_launch(const Net &net, const TcBufs &b, DevState *st, float *gra
                        b.partial + b.off_dw + (long)g * b.npairs * WP * WP, st, nullptr,
                        b.partial + b.off_cb + (long)g * b.npairs * WP, 1, p0, g};
             static long long *trace = nullptr;
-            const char *te = getenv("CRVPINN_BWD_TRACE");
+            const char *te = trace_env("CRVPINN_BWD_TRACE");
             const char *tg = getenv("CRVPINN_BWD_TRACE_G");
             const int trace_g = tg ? atoi(tg) : b.G - 1;
             if (te && g == trace_g) {

@@ -1,7 +1,10 @@
 """Per-tile breakdown of a k_tc_bwd2 trace (CRVPINN_BWD_TRACE, CTA 0; slots per tile: 0/1 producer
 t wait, 2 MMA tfull, 7 MMA xempty, 8-11 MMA chunk j data, 3 MMA done, 4/5 epilogue xfull wait,
 6 epilogue done; output-layer launch: 12/13/14 Delta_L transform start, chunk 0 released, end).
-usage: python scripts/bwd2_report.py file"""
+usage: python scripts/bwd2_report.py file
+Needs a library built with the timeline macros: scripts/ab_build_tc.sh trace -DCRV_TRACE=1, then
+CRVPINN_LIB=build/ab/trace/libcrvpinn.so (the default build compiles them out of the hot loops).
+"""
 import sys
 
 import numpy as np

@@ -1,5 +1,8 @@
 """Backward-chain clock64 timeline (CRVPINN_CHAIN_TRACE) of cluster 0 on C5: one eager loss_grad.
-usage: python scripts/chain_trace.py [C5] ; report: python scripts/chain_trace.py --report file"""
+usage: python scripts/chain_trace.py [C5] ; report: python scripts/chain_trace.py --report file
+Needs a library built with the timeline macros: scripts/ab_build_tc.sh trace -DCRV_TRACE=1, then
+CRVPINN_LIB=build/ab/trace/libcrvpinn.so (the default build compiles them out of the hot loops).
+"""
 import os
 import sys
 

@@ -1,5 +1,8 @@
 """clock64 timeline of the forward kernel's CTA 0 (debug build path, env CRVPINN_FWD_TRACE).
-usage: python scripts/fwd_trace.py [C5] [out.bin] ; analysed by scripts/fwd_trace_report.py"""
+usage: python scripts/fwd_trace.py [C5] [out.bin] ; analysed by scripts/fwd_trace_report.py
+Needs a library built with the timeline macros: scripts/ab_build_tc.sh trace -DCRV_TRACE=1, then
+CRVPINN_LIB=build/ab/trace/libcrvpinn.so (the default build compiles them out of the hot loops).
+"""
 import os
 import sys
 
