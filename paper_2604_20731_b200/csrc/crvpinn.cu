@@ -142,7 +142,9 @@ static int dalloc(crvpinn_ctx *ctx, T **p, size_t count) {
         ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
         return e == cudaErrorMemoryAllocation ? CRVPINN_ENOMEM : CRVPINN_ECUDA;
     }
-    cudaMemset(q, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+    // zero-filled on the context stream: a cudaMemset on the legacy stream is not ordered with the
+    // (non-blocking) context stream and could land after a later copy or kernel there wrote the buffer
+    cudaMemsetAsync(q, 0, count * sizeof(T) > 0 ? count * sizeof(T) : 16, ctx->stream);
     ctx->allocs.push_back(q);
     *p = (T *)q;
     return CRVPINN_OK;
@@ -446,6 +448,9 @@ static int create_impl(crvpinn_ctx *ctx, int N, int n_widths, const int *widths,
             for (int k = 0; k < fout; ++k) th[net.boff[l] + k] = 0.0f;
         }
     }
+    // the legacy-stream work of the set-up above (tc_create's and the Gram constants' zero fills and
+    // table copies) is complete before anything on the context stream touches those buffers
+    CK(cudaDeviceSynchronize());
     // pageable sources: the copies are staged and ordered on the context stream, ahead of the
     // kernels that read them (a plain cudaMemcpy runs on the legacy stream, which a non-blocking
     // context stream does not wait for)
