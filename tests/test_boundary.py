@@ -107,3 +107,15 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).lower().replace("oracle/", ""), fn
+
+
+def test_context_code_has_no_legacy_stream_fills_or_uploads():
+    """crvpinn.cu works on a non-blocking context stream, which does not wait for the legacy stream:
+    a bare cudaMemset / host-to-device cudaMemcpy there can land after later context-stream work
+    (round 2: the fp32 path's reduction-job table was zeroed after its copy). Zero fills and uploads
+    in the context code must be stream-ordered (…Async on ctx->stream)."""
+    text = open(os.path.join(ROOT, "paper_2604_20731_b200", "csrc", "crvpinn.cu")).read()
+    code = re.sub(r"//.*", "", text)
+    assert not re.search(r"\bcudaMemset\s*\(", code)
+    for m in re.finditer(r"\bcudaMemcpy\s*\(([^;]*);", code):
+        assert "cudaMemcpyDeviceToHost" in m.group(1), m.group(0)
